@@ -1,0 +1,71 @@
+/*
+ * gvx_c.h — C facade of the graphvx-b200 graph API (in libgraphvx.so), for
+ * FFI hosts (ctypes / cgo / JNI).  It drives the same public C++ entry
+ * points a C++ user calls (verify, expand, optimize, run_plan, run_naive,
+ * DeviceSession), so measurements through it are measurements of the API.
+ *
+ * Reference interfaces these wrap (ref = /root/reference/proj):
+ *   gvxc_graph_*          Context / AppGraph / add_node / add_custom
+ *                         (include/graphvx/graph.hpp:87-201, registry.hpp:48-64)
+ *   gvxc_*_verify / plan  verify -> expand -> verify -> optimize
+ *                         (verify.hpp:74, registry.hpp:70, optimize.hpp:109)
+ *   gvxc_*_run_host       run_plan / run_naive (execute.hpp:60-65)
+ *   gvxc_session_*        additive device-resident execution (device.hpp)
+ * Status: 0 = ok, else gvx::ErrorCode + 1 (1..20) or 100+ for runtime
+ * failures; gvxc_last_error() holds the message.
+ */
+#ifndef GVX_C_H_
+#define GVX_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gvxc_graph_s* gvxc_graph;
+typedef struct gvxc_session_s* gvxc_session;
+
+const char* gvxc_last_error(void);
+int gvxc_device_count(void);
+
+/* ---- the five BASELINE configurations (config_graphs.hpp) ---------------- */
+/* cfg 1..5; virtual_mid = 1 uses virtual intermediates (the fusible form). */
+int gvxc_config_create(int cfg, int width, int height, int virtual_mid, gvxc_graph* out);
+int gvxc_graph_destroy(gvxc_graph g);
+/* Device program summary (naive = 1: per-node program, else the plan's). */
+int gvxc_graph_describe(gvxc_graph g, int naive, char* buf, size_t cap);
+/* PassStats of the optimized plan: {nodes_before, nodes_alive, removed,
+ * transfers_naive, transfers_optimized, fused_groups, launches_before,
+ * launches_after}. */
+int gvxc_graph_pass_stats(gvxc_graph g, long long stats[8]);
+
+/* Host-buffer execution through run_plan (naive = 0) / run_naive (1).
+ * `in` = packed U8 input.  Outputs by config: cfg1/5 S16 plane, cfg2/3 U8
+ * plane into `out`; cfg4 hist[256] + stats {mean, stddev}.  counters gets
+ * {kernel_launches, pixels_read, pixels_written, transfers_executed}. */
+int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, long long* hist, double* stats,
+                        long long counters[4]);
+
+/* ---- device-resident sessions ---------------------------------------------- */
+int gvxc_session_create(gvxc_graph g, int naive, int frames, gvxc_session* out);
+int gvxc_session_destroy(gvxc_session s);
+/* slot 0 = the input image; slot k >= 1 = config output k-1. */
+int gvxc_session_bind(gvxc_session s, int slot, void* dptr, int64_t pitch, int64_t frame_stride);
+int gvxc_session_set_stream(gvxc_session s, void* cuda_stream);
+int gvxc_session_launch(gvxc_session s);
+int gvxc_session_sync(gvxc_session s);
+int gvxc_session_launches(gvxc_session s);
+/* Host copies of one frame of slot 0 (upload) / output slot (download). */
+int gvxc_session_upload_input(gvxc_session s, int frame, const uint8_t* in);
+int gvxc_session_download(gvxc_session s, int slot, int frame, void* out, long long* hist, double* stats);
+
+/* Reference-identical synthetic input (random_buffer, U8). */
+int gvxc_random_u8(int width, int height, unsigned long long seed, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GVX_C_H_ */

@@ -1,0 +1,131 @@
+"""ORACLE — test infrastructure only.
+
+Python access to the CPU checkers:
+  * ``ref``  : the unmodified reference engine (oracle/_ref/liboracle_ref.so,
+               built from /root/reference by oracle/Makefile with
+               -Dgvx=gvxref) — run_naive on the five configurations;
+  * ``port`` : the plain-C restatement oracle/gvx_oracle.c
+               (oracle/build/libgvx_oracle.so).
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline /
+--impl reference legs may import this package; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import subprocess
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+REF_LIB = HERE / "_ref" / "liboracle_ref.so"
+PORT_LIB = HERE / "build" / "libgvx_oracle.so"
+REFERENCE_SRC = pathlib.Path("/root/reference/proj")
+
+_ref = None
+_port = None
+
+
+def build() -> None:
+    """Build the port always; the reference oracle only where /root/reference exists."""
+    subprocess.run(["make", "-C", str(HERE), "oracle"], check=True, capture_output=True)
+    if REFERENCE_SRC.exists():
+        subprocess.run(["make", "-j8", "-C", str(HERE), "ref"], check=True, capture_output=True)
+
+
+def have_ref() -> bool:
+    return REF_LIB.exists()
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not REF_LIB.exists():
+            raise FileNotFoundError(f"{REF_LIB} not built (needs /root/reference; see oracle/Makefile)")
+        lib = ctypes.CDLL(str(REF_LIB))
+        lib.oref_last_error.restype = ctypes.c_char_p
+        lib.oref_random_image.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_void_p]
+        lib.oref_run_config.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p] * 2 + [
+            ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        lib.oref_config_counters.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)]
+        _ref = lib
+    return _ref
+
+
+def port():
+    global _port
+    if _port is None:
+        if not PORT_LIB.exists():
+            build()
+        lib = ctypes.CDLL(str(PORT_LIB))
+        V = ctypes.c_void_p
+        lib.gvxo_edge.argtypes = [V, ctypes.c_int, ctypes.c_int, V]
+        lib.gvxo_harris.argtypes = [V, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, V, V]
+        lib.gvxo_unsharp.argtypes = [V, ctypes.c_int, ctypes.c_int, V]
+        lib.gvxo_conv_stats.argtypes = [V, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        _port = lib
+    return _port
+
+
+HARRIS_K = 0.04
+HARRIS_T = 1.0e9
+
+
+def ref_random_u8(w: int, h: int, seed: int) -> np.ndarray:
+    out = np.empty((h, w), np.uint8)
+    if ref().oref_random_image(w, h, 0, seed, out.ctypes.data) != 0:
+        raise RuntimeError(ref().oref_last_error().decode())
+    return out
+
+
+def ref_run(cfg: int, img: np.ndarray):
+    """Reference run_naive on config `cfg`; returns (result, seconds)."""
+    h, w = img.shape
+    img = np.ascontiguousarray(img, np.uint8)
+    hist = (ctypes.c_longlong * 256)()
+    stats = (ctypes.c_double * 2)()
+    secs = ctypes.c_double()
+    out = None
+    if cfg in (1, 5):
+        out = np.empty((h, w), np.int16)
+    elif cfg in (2, 3):
+        out = np.empty((h, w), np.uint8)
+    rc = ref().oref_run_config(cfg, w, h, img.ctypes.data, None if out is None else out.ctypes.data, hist, stats,
+                               ctypes.byref(secs))
+    if rc != 0:
+        raise RuntimeError(ref().oref_last_error().decode())
+    if cfg == 4:
+        return (np.array(list(hist), np.int64), stats[0], stats[1]), secs.value
+    return out, secs.value
+
+
+def ref_counters(cfg: int, img: np.ndarray) -> dict:
+    h, w = img.shape
+    c = (ctypes.c_longlong * 4)()
+    if ref().oref_config_counters(cfg, w, h, np.ascontiguousarray(img, np.uint8).ctypes.data, c) != 0:
+        raise RuntimeError(ref().oref_last_error().decode())
+    return dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(c)))
+
+
+def port_run(cfg: int, img: np.ndarray):
+    """The C restatement on config `cfg`."""
+    lib = port()
+    h, w = img.shape
+    img = np.ascontiguousarray(img, np.uint8)
+    if cfg in (1, 5):
+        out = np.empty((h, w), np.int16)
+        lib.gvxo_edge(img.ctypes.data, w, h, out.ctypes.data)
+        return out
+    if cfg == 2:
+        out = np.empty((h, w), np.uint8)
+        lib.gvxo_harris(img.ctypes.data, w, h, HARRIS_K, HARRIS_T, out.ctypes.data, None)
+        return out
+    if cfg == 3:
+        out = np.empty((h, w), np.uint8)
+        lib.gvxo_unsharp(img.ctypes.data, w, h, out.ctypes.data)
+        return out
+    hist = (ctypes.c_longlong * 256)()
+    m, s = ctypes.c_double(), ctypes.c_double()
+    lib.gvxo_conv_stats(img.ctypes.data, w, h, hist, ctypes.byref(m), ctypes.byref(s))
+    return np.array(list(hist), np.int64), m.value, s.value

@@ -1,0 +1,319 @@
+"""graphvx-b200: B200-native execution backend for the OpenVX graph path of
+HipaccVX (arXiv:2008.11476).
+
+The product is native code: the C++ graph API (``include/graphvx``, in
+``lib/libgraphvx.so``) over the sm_100a device runtime (``include/gvxb.h``,
+``lib/libgvx_cuda.so``).  This module only loads those libraries with
+ctypes and mirrors the C facade (``include/gvx_c.h``) for Python hosts
+(tests, ``bench.py``).  There is no Python or host compute path: on a
+machine without a CUDA device every execution call raises ``GraphvxError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+import subprocess
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+REPO = ROOT.parent
+LIB_DIR = ROOT / "lib"
+LIB_CUDA = LIB_DIR / "libgvx_cuda.so"
+LIB_GRAPH = LIB_DIR / "libgraphvx.so"
+
+# gvx::ErrorCode names, index = status - 1 (include/graphvx/error.hpp)
+ERROR_CODES = [
+    "ZeroDimension", "BadFormat", "BadKernel", "AccessDenied", "UnknownObject", "UnknownKernel",
+    "CrossGraphVirtual", "MultipleWriters", "CycleDetected", "UnstampedGraph", "MissingInput",
+    "ShapeMismatch", "DivByZero", "TypeMismatch", "MissingCast", "OffsetOutOfWindow", "UnsupportedKind",
+    "NonStreamable", "IoError", "SchemaError",
+]
+
+# exact output formats of the five configurations
+CONFIG_OUTPUT = {1: np.int16, 2: np.uint8, 3: np.uint8, 4: None, 5: np.int16}
+CONFIG_SEED = {1: 1, 2: 2, 3: 3, 4: 4, 5: 5}
+CONFIG_SIZE = {1: (1920, 1080), 2: (3840, 2160), 3: (7680, 4320), 4: (3840, 2160), 5: (16384, 16384)}
+CONFIG_FRAMES = {1: 1, 2: 1, 3: 1, 4: 64, 5: 1}
+
+
+class GraphvxError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        name = ERROR_CODES[status - 1] if 1 <= status <= len(ERROR_CODES) else f"status{status}"
+        super().__init__(f"{name}: {message}")
+        self.status = status
+        self.code = name
+
+
+def build(verbose: bool = False) -> None:
+    """Compile the native libraries in-tree (make)."""
+    out = subprocess.run(["make", "-j8", "-C", str(REPO)], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("native build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+    if verbose:
+        print(out.stdout[-2000:])
+
+
+_cuda = None
+_graph = None
+
+
+def _load():
+    global _cuda, _graph
+    if _graph is not None:
+        return _cuda, _graph
+    if not LIB_GRAPH.exists() or not LIB_CUDA.exists():
+        raise ImportError(f"graphvx-b200 native libraries missing in {LIB_DIR}; run build()")
+    _cuda = ctypes.CDLL(str(LIB_CUDA), mode=ctypes.RTLD_GLOBAL)
+    _graph = ctypes.CDLL(str(LIB_GRAPH), mode=ctypes.RTLD_GLOBAL)
+    _declare(_cuda, _graph)
+    return _cuda, _graph
+
+
+def _declare(c, g):
+    P, I, L, D, U8P = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p
+    c.gvxb_last_error.restype = ctypes.c_char_p
+    c.gvxb_device_count.argtypes = [ctypes.POINTER(I)]
+    c.gvxb_ctx_create.argtypes = [I, ctypes.POINTER(P)]
+    c.gvxb_ctx_destroy.argtypes = [P]
+    c.gvxb_ctx_stream.argtypes = [P]
+    c.gvxb_ctx_stream.restype = P
+    c.gvxb_ctx_set_stream.argtypes = [P, P]
+    c.gvxb_sync.argtypes = [P]
+    c.gvxb_alloc.argtypes = [P, ctypes.c_size_t, ctypes.POINTER(P)]
+    c.gvxb_free.argtypes = [P, P]
+    c.gvxb_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(P)]
+    c.gvxb_host_free.argtypes = [P]
+    c.gvxb_memset.argtypes = [P, P, I, ctypes.c_size_t]
+    c.gvxb_upload_2d.argtypes = [P, P, ctypes.c_size_t, P, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t]
+    c.gvxb_download_2d.argtypes = [P, P, ctypes.c_size_t, P, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t]
+    c.gvxb_event_create.argtypes = [ctypes.POINTER(P)]
+    c.gvxb_event_destroy.argtypes = [P]
+    c.gvxb_event_record.argtypes = [P, P]
+    c.gvxb_event_elapsed_ms.argtypes = [P, P, ctypes.POINTER(ctypes.c_float)]
+    c.gvxb_launch_count.argtypes = [P]
+    c.gvxb_launch_count.restype = ctypes.c_int64
+    c.gvxb_band_rows.argtypes = [ctypes.c_int32] * 3 + [ctypes.POINTER(ctypes.c_int32)] * 2
+    g.gvxc_last_error.restype = ctypes.c_char_p
+    g.gvxc_config_create.argtypes = [I, I, I, I, ctypes.POINTER(P)]
+    g.gvxc_graph_destroy.argtypes = [P]
+    g.gvxc_graph_describe.argtypes = [P, I, ctypes.c_char_p, ctypes.c_size_t]
+    g.gvxc_graph_pass_stats.argtypes = [P, ctypes.POINTER(L)]
+    g.gvxc_graph_run_host.argtypes = [P, I, U8P, P, ctypes.POINTER(L), ctypes.POINTER(D), ctypes.POINTER(L)]
+    g.gvxc_session_create.argtypes = [P, I, I, ctypes.POINTER(P)]
+    g.gvxc_session_destroy.argtypes = [P]
+    g.gvxc_session_bind.argtypes = [P, I, P, ctypes.c_int64, ctypes.c_int64]
+    g.gvxc_session_set_stream.argtypes = [P, P]
+    g.gvxc_session_launch.argtypes = [P]
+    g.gvxc_session_sync.argtypes = [P]
+    g.gvxc_session_launches.argtypes = [P]
+    g.gvxc_session_upload_input.argtypes = [P, I, U8P]
+    g.gvxc_session_download.argtypes = [P, I, I, P, ctypes.POINTER(L), ctypes.POINTER(D)]
+    g.gvxc_random_u8.argtypes = [I, I, ctypes.c_ulonglong, U8P]
+
+
+def _check_graph(rc: int):
+    if rc != 0:
+        raise GraphvxError(rc, _graph.gvxc_last_error().decode(errors="replace"))
+
+
+def _check_cuda(rc: int):
+    if rc != 0:
+        raise GraphvxError(rc, _cuda.gvxb_last_error().decode(errors="replace"))
+
+
+def libraries():
+    return _load()
+
+
+def device_count() -> int:
+    c, _ = _load()
+    n = ctypes.c_int(0)
+    c.gvxb_device_count(ctypes.byref(n))
+    return n.value
+
+
+def random_u8(width: int, height: int, seed: int) -> np.ndarray:
+    """Reference-identical synthetic U8 image (random_buffer, mt19937_64)."""
+    _, g = _load()
+    out = np.empty((height, width), np.uint8)
+    _check_graph(g.gvxc_random_u8(width, height, seed, out.ctypes.data))
+    return out
+
+
+class ConfigGraph:
+    """One BASELINE configuration built through the public API (verify ->
+    expand -> verify -> optimize)."""
+
+    def __init__(self, cfg: int, width: int, height: int, virtual_mid: bool = True):
+        _, g = _load()
+        self.cfg, self.width, self.height = cfg, width, height
+        h = ctypes.c_void_p()
+        _check_graph(g.gvxc_config_create(cfg, width, height, int(virtual_mid), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _graph.gvxc_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def describe(self, naive: bool = False) -> str:
+        buf = ctypes.create_string_buffer(8192)
+        _check_graph(_graph.gvxc_graph_describe(self._h, int(naive), buf, len(buf)))
+        return buf.value.decode()
+
+    def pass_stats(self) -> dict:
+        st = (ctypes.c_longlong * 8)()
+        _graph.gvxc_graph_pass_stats(self._h, st)
+        keys = ["nodes_before", "nodes_alive", "nodes_removed", "transfers_naive", "transfers_optimized",
+                "fused_groups", "launches_before", "launches_after"]
+        return dict(zip(keys, list(st)))
+
+    def output_array(self):
+        dt = CONFIG_OUTPUT[self.cfg]
+        return None if dt is None else np.empty((self.height, self.width), dt)
+
+    def run_host(self, image: np.ndarray, naive: bool = False):
+        """run_plan / run_naive with host buffers.  Returns (result, counters)
+        where result is the output plane, or (hist, mean, stddev) for cfg4."""
+        img = np.ascontiguousarray(image, dtype=np.uint8)
+        assert img.shape == (self.height, self.width)
+        out = self.output_array()
+        hist = (ctypes.c_longlong * 256)()
+        stats = (ctypes.c_double * 2)()
+        counters = (ctypes.c_longlong * 4)()
+        _check_graph(_graph.gvxc_graph_run_host(self._h, int(naive), img.ctypes.data,
+                                                None if out is None else out.ctypes.data, hist, stats, counters))
+        cnt = dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(counters)))
+        if self.cfg == 4:
+            return (np.array(list(hist), np.int64), stats[0], stats[1]), cnt
+        return out, cnt
+
+
+class Session:
+    """Device-resident execution of a ConfigGraph over `frames` frames."""
+
+    def __init__(self, graph: ConfigGraph, frames: int = 1, naive: bool = False):
+        self.graph, self.frames = graph, frames
+        h = ctypes.c_void_p()
+        _check_graph(_graph.gvxc_session_create(graph.handle, int(naive), frames, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _graph.gvxc_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bind(self, slot: int, dptr: int, pitch: int, frame_stride: int = 0):
+        _check_graph(_graph.gvxc_session_bind(self._h, slot, ctypes.c_void_p(dptr), pitch, frame_stride))
+
+    def set_stream(self, stream: int | None):
+        _check_graph(_graph.gvxc_session_set_stream(self._h, ctypes.c_void_p(stream or 0)))
+
+    def launch(self):
+        _check_graph(_graph.gvxc_session_launch(self._h))
+
+    def sync(self):
+        _check_graph(_graph.gvxc_session_sync(self._h))
+
+    def launches(self) -> int:
+        return _graph.gvxc_session_launches(self._h)
+
+    def upload(self, frame: int, image: np.ndarray):
+        img = np.ascontiguousarray(image, dtype=np.uint8)
+        _check_graph(_graph.gvxc_session_upload_input(self._h, frame, img.ctypes.data))
+
+    def download(self, frame: int = 0, slot: int = 1):
+        out = self.graph.output_array()
+        hist = (ctypes.c_longlong * 256)()
+        stats = (ctypes.c_double * 2)()
+        _check_graph(_graph.gvxc_session_download(self._h, slot, frame, None if out is None else out.ctypes.data,
+                                                  hist, stats))
+        if self.graph.cfg == 4:
+            return np.array(list(hist), np.int64), stats[0], stats[1]
+        return out
+
+
+class Device:
+    """Thin wrapper over a gvxb context (device memory, events, stream)."""
+
+    def __init__(self, device: int = 0):
+        c, _ = _load()
+        self.c = c
+        h = ctypes.c_void_p()
+        _check_cuda(c.gvxb_ctx_create(device, ctypes.byref(h)))
+        self.h = h
+
+    @property
+    def stream(self) -> int:
+        return self.c.gvxb_ctx_stream(self.h) or 0
+
+    def alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        _check_cuda(self.c.gvxb_alloc(self.h, nbytes, ctypes.byref(p)))
+        return p.value
+
+    def free(self, ptr: int):
+        self.c.gvxb_free(self.h, ctypes.c_void_p(ptr))
+
+    def upload(self, dptr: int, dpitch: int, arr: np.ndarray):
+        a = np.ascontiguousarray(arr)
+        row = a.shape[-1] * a.itemsize
+        rows = a.size * a.itemsize // row
+        _check_cuda(self.c.gvxb_upload_2d(self.h, ctypes.c_void_p(dptr), dpitch, a.ctypes.data, row, row, rows))
+
+    def download(self, arr: np.ndarray, dptr: int, dpitch: int):
+        row = arr.shape[-1] * arr.itemsize
+        rows = arr.size * arr.itemsize // row
+        _check_cuda(self.c.gvxb_download_2d(self.h, arr.ctypes.data, row, ctypes.c_void_p(dptr), dpitch, row, rows))
+        self.sync()
+
+    def memset(self, dptr: int, value: int, nbytes: int):
+        _check_cuda(self.c.gvxb_memset(self.h, ctypes.c_void_p(dptr), value, nbytes))
+
+    def sync(self):
+        _check_cuda(self.c.gvxb_sync(self.h))
+
+    def event(self) -> int:
+        e = ctypes.c_void_p()
+        _check_cuda(self.c.gvxb_event_create(ctypes.byref(e)))
+        return e.value
+
+    def record(self, ev: int):
+        _check_cuda(self.c.gvxb_event_record(self.h, ctypes.c_void_p(ev)))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = ctypes.c_float()
+        _check_cuda(self.c.gvxb_event_elapsed_ms(ctypes.c_void_p(a), ctypes.c_void_p(b), ctypes.byref(ms)))
+        return ms.value
+
+    def launch_count(self) -> int:
+        return int(self.c.gvxb_launch_count(self.h))
+
+
+def band_rows(height: int, world: int, rank: int):
+    c, _ = _load()
+    r0, r1 = ctypes.c_int32(), ctypes.c_int32()
+    _check_cuda(c.gvxb_band_rows(height, world, rank, ctypes.byref(r0), ctypes.byref(r1)))
+    return r0.value, r1.value
+
+
+__all__ = ["GraphvxError", "ConfigGraph", "Session", "Device", "build", "device_count", "random_u8",
+           "band_rows", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]

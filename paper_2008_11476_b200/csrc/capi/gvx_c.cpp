@@ -1,0 +1,208 @@
+// C facade over the public C++ API (include/gvx_c.h).
+#include "gvx_c.h"
+
+#include "../configs/config_graphs.hpp"
+#include "graphvx/device.hpp"
+#include "graphvx/optimize.hpp"
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail_from(const std::exception& e) {
+    g_err = e.what();
+    if (auto* ge = dynamic_cast<const gvx::Error*>(&e)) return static_cast<int>(ge->code()) + 1;
+    return 100;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_from(e);
+    }
+}
+
+} // namespace
+
+struct gvxc_graph_s {
+    int cfg = 0;
+    int width = 0, height = 0;
+    gvx::Context ctx;
+    gvx_configs::ConfigGraph cg;
+    gvx::VerifiedGraph impl;
+    gvx::OptimizedPlan plan;
+};
+
+struct gvxc_session_s {
+    gvxc_graph g = nullptr;
+    std::unique_ptr<gvx::DeviceSession> s;
+};
+
+extern "C" {
+
+const char* gvxc_last_error(void) { return g_err.c_str(); }
+int gvxc_device_count(void) { return gvx::device_count(); }
+
+int gvxc_config_create(int cfg, int w, int h, int virtual_mid, gvxc_graph* out) {
+    return guarded([&] {
+        auto g = std::make_unique<gvxc_graph_s>();
+        g->cfg = cfg;
+        g->width = w;
+        g->height = h;
+        g->cg = gvx_configs::build_config(g->ctx, cfg, w, h, virtual_mid != 0);
+        g->impl = gvx_configs::verified_impl(g->ctx, *g->cg.graph);
+        g->plan = gvx::optimize(g->impl, g->ctx);
+        *out = g.release();
+    });
+}
+
+int gvxc_graph_destroy(gvxc_graph g) {
+    delete g;
+    return 0;
+}
+
+int gvxc_graph_describe(gvxc_graph g, int naive, char* buf, size_t cap) {
+    return guarded([&] {
+        std::string d = naive ? gvx::DeviceSession(g->impl).describe() : gvx::DeviceSession(g->plan).describe();
+        if (cap) {
+            std::strncpy(buf, d.c_str(), cap - 1);
+            buf[cap - 1] = '\0';
+        }
+    });
+}
+
+int gvxc_graph_pass_stats(gvxc_graph g, long long st[8]) {
+    const gvx::PassStats& p = g->plan.stats;
+    const long long v[8] = {p.nodes_before, p.nodes_alive, p.nodes_removed, p.transfers_naive,
+                            p.transfers_optimized, p.fused_groups, p.launches_before, p.launches_after};
+    std::memcpy(st, v, sizeof(v));
+    return 0;
+}
+
+namespace {
+
+void copy_outputs(gvxc_graph g, const std::map<gvx::ObjectId, gvx::Buffer>& outs, void* out, long long* hist,
+                  double* stats) {
+    if (g->cfg == 4) {
+        const gvx::Buffer& hb = outs.at(g->cg.outputs[0]);
+        if (hist)
+            for (std::size_t i = 0; i < hb.dist.counts.size(); ++i) hist[i] = hb.dist.counts[i];
+        if (stats) {
+            stats[0] = outs.at(g->cg.outputs[1]).scalar.as_real();
+            stats[1] = outs.at(g->cg.outputs[2]).scalar.as_real();
+        }
+        return;
+    }
+    const gvx::Buffer& b = outs.at(g->cg.outputs[0]);
+    if (out) std::memcpy(out, b.bytes.data(), b.bytes.size());
+}
+
+gvx::Buffer input_buffer(gvxc_graph g, const uint8_t* in) {
+    gvx::ResolvedDesc d;
+    d.kind = gvx::ObjKind::Image;
+    d.width = g->width;
+    d.height = g->height;
+    d.format = gvx::ImageFormat::U8;
+    gvx::Buffer b = gvx::Buffer::image(d);
+    std::memcpy(b.bytes.data(), in, b.bytes.size());
+    return b;
+}
+
+} // namespace
+
+int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, long long* hist, double* stats,
+                        long long counters[4]) {
+    return guarded([&] {
+        gvx::InputMap inputs;
+        inputs[g->cg.input] = input_buffer(g, in);
+        gvx::ExecutionReport r = naive ? gvx::run_naive(g->impl, inputs) : gvx::run_plan(g->plan, inputs);
+        copy_outputs(g, r.outputs, out, hist, stats);
+        if (counters) {
+            counters[0] = r.counters.kernel_launches;
+            counters[1] = r.counters.pixels_read;
+            counters[2] = r.counters.pixels_written;
+            counters[3] = r.counters.transfers_executed;
+        }
+    });
+}
+
+int gvxc_session_create(gvxc_graph g, int naive, int frames, gvxc_session* out) {
+    return guarded([&] {
+        auto s = std::make_unique<gvxc_session_s>();
+        s->g = g;
+        s->s = naive ? std::make_unique<gvx::DeviceSession>(g->impl, frames)
+                     : std::make_unique<gvx::DeviceSession>(g->plan, frames);
+        *out = s.release();
+    });
+}
+
+int gvxc_session_destroy(gvxc_session s) {
+    delete s;
+    return 0;
+}
+
+namespace {
+gvx::ObjectId slot_object(gvxc_session s, int slot) {
+    if (slot == 0) return s->g->cg.input;
+    const auto& outs = s->g->cg.outputs;
+    if (slot < 1 || slot > static_cast<int>(outs.size())) throw gvx::Error(gvx::ErrorCode::UnknownObject, "bad slot");
+    return outs[static_cast<std::size_t>(slot - 1)];
+}
+} // namespace
+
+int gvxc_session_bind(gvxc_session s, int slot, void* dptr, int64_t pitch, int64_t fstride) {
+    return guarded([&] { s->s->bind(slot_object(s, slot), gvx::DeviceTensor{dptr, pitch, fstride}); });
+}
+
+int gvxc_session_set_stream(gvxc_session s, void* stream) {
+    return guarded([&] { s->s->set_stream(stream); });
+}
+
+int gvxc_session_launch(gvxc_session s) {
+    return guarded([&] { s->s->launch(); });
+}
+
+int gvxc_session_sync(gvxc_session s) {
+    return guarded([&] { s->s->synchronize(); });
+}
+
+int gvxc_session_launches(gvxc_session s) { return s->s->launches_per_run(); }
+
+int gvxc_session_upload_input(gvxc_session s, int frame, const uint8_t* in) {
+    return guarded([&] { s->s->upload(s->g->cg.input, input_buffer(s->g, in), frame); });
+}
+
+int gvxc_session_download(gvxc_session s, int slot, int frame, void* out, long long* hist, double* stats) {
+    return guarded([&] {
+        gvxc_graph g = s->g;
+        std::map<gvx::ObjectId, gvx::Buffer> outs;
+        if (g->cfg == 4) {
+            for (gvx::ObjectId id : g->cg.outputs) outs[id] = s->s->download(id, frame);
+        } else {
+            const gvx::ObjectId id = slot_object(s, slot < 1 ? 1 : slot);
+            outs[g->cg.outputs[0]] = s->s->download(id, frame);
+        }
+        copy_outputs(g, outs, out, hist, stats);
+    });
+}
+
+int gvxc_random_u8(int w, int h, unsigned long long seed, uint8_t* out) {
+    return guarded([&] {
+        gvx::ResolvedDesc d;
+        d.kind = gvx::ObjKind::Image;
+        d.width = w;
+        d.height = h;
+        d.format = gvx::ImageFormat::U8;
+        gvx::Buffer b = gvx::random_buffer(d, seed);
+        std::memcpy(out, b.bytes.data(), b.bytes.size());
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,126 @@
+// Shared pieces of the sm_100a kernels: context layout, exact integer
+// rounding helpers matching the reference's cast semantics, TMA/mbarrier
+// wrappers, and the tile loader that reproduces Clamp borders in shared
+// memory.
+#pragma once
+
+#include "gvxb.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+struct gvxb_ctx_s {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    unsigned* status = nullptr;            // GVXB_STATUS_* bits
+    unsigned long long* counter = nullptr; // pixel-read events of generated kernels
+    int64_t launches = 0;
+};
+
+namespace gvxb_impl {
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int check_launch(gvxb_ctx ctx, const char* what);
+} // namespace gvxb_impl
+
+namespace gvxd {
+
+__host__ __device__ __forceinline__ int clampi(int v, int lo, int hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+
+/// round-half-away-from-zero of s / d for d > 0 (llround semantics of the
+/// reference's `cast_value(Saturate, s * (1.0 / d))` when that product is
+/// exact enough; callers prove that per use).
+__device__ __forceinline__ int round_div_away(int s, int d) {
+    int a = s < 0 ? -s : s;
+    int q = (2 * a + d) / (2 * d);
+    return s < 0 ? -q : q;
+}
+
+__device__ __forceinline__ int sat_s16(int v) { return clampi(v, -32768, 32767); }
+__device__ __forceinline__ int sat_u8(int v) { return clampi(v, 0, 255); }
+
+/// round(sqrt(n)) with half away from zero, exact for 0 <= n < 2^24:
+/// fp32 estimate then integer correction (k = largest integer with
+/// k*k - k < n).  Matches llround(sqrt((double)n)) of the reference
+/// (Magnitude, ref:src/registry.cpp:567-570).
+__device__ __forceinline__ int round_sqrt_exact(int n) {
+    float s = sqrtf(__int2float_rn(n));
+    int k = __float2int_rd(s + 0.4995f);
+    k += (n > k * k + k) ? 1 : 0;
+    return k;
+}
+
+// ---- mbarrier + TMA (cp.async.bulk.tensor) --------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+
+} // namespace gvxd
+
+namespace gvxb_impl {
+
+/// Encodes a 3D (x, y, frame) U8 tensor map for a gvxb_image with the given
+/// box; OOB elements are zero-filled (kernels patch Clamp borders after).
+int make_u8_tensor_map(CUtensorMap* map, const gvxb_image& img, int box_w, int box_h);
+
+/// Shared-memory tile of U8 source pixels covering image columns
+/// [x_org, x_org + tw) and rows [y_org, y_org + th) of a frame, loaded by TMA
+/// and patched so out-of-image positions hold the clamped (replicated)
+/// pixel: exactly the reference's Clamp window reads
+/// (NodeEnv::window, ref:src/execute.cpp:233-248).
+struct TileGeom {
+    int x_org, y_org; // image coordinates of smem (0, 0)
+    int tw, th;       // tile extent in smem (tw multiple of 16)
+};
+
+} // namespace gvxb_impl

@@ -1,0 +1,361 @@
+// Device runtime behind the C-ABI (include/gvxb.h): contexts, streams,
+// memory, copies, events, status word, NVRTC JIT and peer access.
+//
+// Driver-API symbols (module loading, launches) are resolved at run time via
+// cudaGetDriverEntryPoint so this library loads on a machine without a GPU
+// driver (the CPU test suite checks the exported symbols there).
+#include "common.cuh"
+
+#include <cuda.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace gvxb_impl {
+
+thread_local std::string g_last_error;
+thread_local std::string g_jit_log;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(GVXB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int check_launch(gvxb_ctx ctx, const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    ++ctx->launches;
+    return GVXB_OK;
+}
+
+} // namespace gvxb_impl
+
+using namespace gvxb_impl;
+
+struct gvxb_module_s {
+    CUmodule module = nullptr;
+    std::vector<CUfunction> functions;
+};
+
+namespace {
+
+struct DriverApi {
+    CUresult (*module_load_data)(CUmodule*, const void*) = nullptr;
+    CUresult (*module_unload)(CUmodule) = nullptr;
+    CUresult (*module_get_function)(CUfunction*, CUmodule, const char*) = nullptr;
+    CUresult (*launch_kernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                              unsigned, CUstream, void**, void**) = nullptr;
+    CUresult (*func_set_attribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    bool ok = false;
+};
+
+DriverApi& driver() {
+    static DriverApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn != nullptr;
+        };
+        api.ok = get("cuModuleLoadData", reinterpret_cast<void**>(&api.module_load_data)) &&
+                 get("cuModuleUnload", reinterpret_cast<void**>(&api.module_unload)) &&
+                 get("cuModuleGetFunction", reinterpret_cast<void**>(&api.module_get_function)) &&
+                 get("cuLaunchKernel", reinterpret_cast<void**>(&api.launch_kernel)) &&
+                 get("cuFuncSetAttribute", reinterpret_cast<void**>(&api.func_set_attribute));
+    });
+    return api;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* gvxb_last_error(void) { return g_last_error.c_str(); }
+int gvxb_abi_version(void) { return GVXB_ABI_VERSION; }
+
+int gvxb_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *count = 0;
+        return fail(GVXB_ERR_NO_DEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    *count = n;
+    return GVXB_OK;
+}
+
+int gvxb_ctx_create(int device, gvxb_ctx* out) {
+    int n = 0;
+    if (int rc = gvxb_device_count(&n)) return rc;
+    if (device < 0 || device >= n) return fail(GVXB_ERR_NO_DEVICE, "device index out of range");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    auto* c = new gvxb_ctx_s();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    c->stream = c->own_stream;
+    e = cudaMalloc(&c->status, sizeof(unsigned) + sizeof(unsigned long long) * 2);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(c->own_stream);
+        delete c;
+        return cuda_fail(e, "cudaMalloc(status)");
+    }
+    c->counter = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c->status) + 8);
+    cudaMemset(c->status, 0, sizeof(unsigned) + sizeof(unsigned long long) * 2);
+    *out = c;
+    return GVXB_OK;
+}
+
+int gvxb_ctx_destroy(gvxb_ctx ctx) {
+    if (!ctx) return GVXB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->status);
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return GVXB_OK;
+}
+
+int gvxb_ctx_set_stream(gvxb_ctx ctx, void* s) {
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    return GVXB_OK;
+}
+
+void* gvxb_ctx_stream(gvxb_ctx ctx) { return ctx->stream; }
+int gvxb_ctx_device(gvxb_ctx ctx) { return ctx->device; }
+int gvxb_ctx_sm_count(gvxb_ctx ctx) { return ctx->sm_count; }
+int64_t gvxb_launch_count(gvxb_ctx ctx) { return ctx->launches; }
+
+int gvxb_sync(gvxb_ctx ctx) {
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaStreamSynchronize");
+}
+
+int gvxb_alloc(gvxb_ctx ctx, size_t bytes, void** p) {
+    cudaSetDevice(ctx->device);
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMalloc");
+}
+
+int gvxb_free(gvxb_ctx ctx, void* p) {
+    cudaSetDevice(ctx->device);
+    cudaError_t e = cudaFree(p);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaFree");
+}
+
+int gvxb_host_alloc(size_t bytes, void** p) {
+    cudaError_t e = cudaHostAlloc(p, bytes ? bytes : 16, cudaHostAllocPortable);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaHostAlloc");
+}
+
+int gvxb_host_free(void* p) {
+    cudaError_t e = cudaFreeHost(p);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaFreeHost");
+}
+
+int gvxb_memset(gvxb_ctx ctx, void* p, int v, size_t bytes) {
+    cudaError_t e = cudaMemsetAsync(p, v, bytes, ctx->stream);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemsetAsync");
+}
+
+int gvxb_upload_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
+                   size_t row_bytes, size_t rows) {
+    if (!rows || !row_bytes) return GVXB_OK;
+    cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyHostToDevice,
+                                      ctx->stream);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemcpy2DAsync(H2D)");
+}
+
+int gvxb_download_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
+                     size_t row_bytes, size_t rows) {
+    if (!rows || !row_bytes) return GVXB_OK;
+    cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyDeviceToHost,
+                                      ctx->stream);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemcpy2DAsync(D2H)");
+}
+
+int gvxb_copy_d2d(gvxb_ctx ctx, void* dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemcpyAsync(D2D)");
+}
+
+int gvxb_event_create(void** ev) {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    *ev = e;
+    return r == cudaSuccess ? GVXB_OK : cuda_fail(r, "cudaEventCreate");
+}
+
+int gvxb_event_destroy(void* ev) {
+    cudaEventDestroy(static_cast<cudaEvent_t>(ev));
+    return GVXB_OK;
+}
+
+int gvxb_event_record(gvxb_ctx ctx, void* ev) {
+    cudaError_t r = cudaEventRecord(static_cast<cudaEvent_t>(ev), ctx->stream);
+    return r == cudaSuccess ? GVXB_OK : cuda_fail(r, "cudaEventRecord");
+}
+
+int gvxb_event_elapsed_ms(void* a, void* b, float* ms) {
+    cudaError_t r = cudaEventSynchronize(static_cast<cudaEvent_t>(b));
+    if (r != cudaSuccess) return cuda_fail(r, "cudaEventSynchronize");
+    r = cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b));
+    return r == cudaSuccess ? GVXB_OK : cuda_fail(r, "cudaEventElapsedTime");
+}
+
+int gvxb_status_reset(gvxb_ctx ctx) {
+    cudaError_t e = cudaMemsetAsync(ctx->status, 0, sizeof(unsigned) + 2 * sizeof(unsigned long long),
+                                    ctx->stream);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "status reset");
+}
+
+int gvxb_status_read(gvxb_ctx ctx, uint32_t* status) {
+    unsigned v = 0;
+    cudaError_t e = cudaMemcpyAsync(&v, ctx->status, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "status read");
+    *status = v;
+    return GVXB_OK;
+}
+
+int gvxb_status_ptr(gvxb_ctx ctx, uint32_t** p) {
+    *p = ctx->status;
+    return GVXB_OK;
+}
+
+int gvxb_counter_ptr(gvxb_ctx ctx, unsigned long long** p) {
+    *p = ctx->counter;
+    return GVXB_OK;
+}
+
+int gvxb_counter_read(gvxb_ctx ctx, long long* reads) {
+    unsigned long long v = 0;
+    cudaError_t e = cudaMemcpyAsync(&v, ctx->counter, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "counter read");
+    *reads = static_cast<long long>(v);
+    return GVXB_OK;
+}
+
+// ---------------------------------------------------------------------- JIT
+
+const char* gvxb_jit_log(void) { return g_jit_log.c_str(); }
+
+int gvxb_jit_build(gvxb_ctx ctx, const char* source, const char* const* names, int n, gvxb_module* out) {
+    DriverApi& drv = driver();
+    if (!drv.ok) return fail(GVXB_ERR_NO_DEVICE, "CUDA driver entry points unavailable");
+    cudaSetDevice(ctx->device);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, ctx->device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, ctx->device);
+    if (major != 10) return fail(GVXB_ERR_UNSUPPORTED, "graphvx-b200 kernels target sm_100a (B200)");
+
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, source, "gvx_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+        return fail(GVXB_ERR_NVRTC, "nvrtcCreateProgram failed");
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
+                          "--device-as-default-execution-space", "-lineinfo"};
+    nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+    size_t log_size = 0;
+    nvrtcGetProgramLogSize(prog, &log_size);
+    g_jit_log.assign(log_size, '\0');
+    if (log_size) nvrtcGetProgramLog(prog, &g_jit_log[0]);
+    if (r != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return fail(GVXB_ERR_NVRTC, std::string("NVRTC compile failed: ") + g_jit_log.substr(0, 2000));
+    }
+    size_t cubin_size = 0;
+    nvrtcGetCUBINSize(prog, &cubin_size);
+    std::vector<char> cubin(cubin_size);
+    nvrtcGetCUBIN(prog, cubin.data());
+    std::vector<std::string> lowered(names, names + n); // extern "C" kernels: unmangled
+    nvrtcDestroyProgram(&prog);
+
+    auto* m = new gvxb_module_s();
+    if (drv.module_load_data(&m->module, cubin.data()) != CUDA_SUCCESS) {
+        delete m;
+        return fail(GVXB_ERR_CUDA, "cuModuleLoadData failed");
+    }
+    for (const std::string& ln : lowered) {
+        CUfunction f = nullptr;
+        if (drv.module_get_function(&f, m->module, ln.c_str()) != CUDA_SUCCESS) {
+            drv.module_unload(m->module);
+            delete m;
+            return fail(GVXB_ERR_CUDA, "cuModuleGetFunction(" + ln + ") failed");
+        }
+        drv.func_set_attribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024);
+        m->functions.push_back(f);
+    }
+    *out = m;
+    return GVXB_OK;
+}
+
+int gvxb_jit_free(gvxb_module m) {
+    if (!m) return GVXB_OK;
+    if (driver().ok && m->module) driver().module_unload(m->module);
+    delete m;
+    return GVXB_OK;
+}
+
+int gvxb_jit_launch(gvxb_ctx ctx, gvxb_module m, int k, const unsigned grid[3], const unsigned block[3],
+                    size_t smem, void** args) {
+    if (k < 0 || k >= static_cast<int>(m->functions.size())) return fail(GVXB_ERR_INVALID, "bad kernel index");
+    if (grid[0] == 0 || grid[1] == 0 || grid[2] == 0) return GVXB_OK;
+    CUresult r = driver().launch_kernel(m->functions[static_cast<std::size_t>(k)], grid[0], grid[1], grid[2],
+                                        block[0], block[1], block[2], static_cast<unsigned>(smem),
+                                        static_cast<CUstream>(ctx->stream), args, nullptr);
+    if (r != CUDA_SUCCESS) return fail(GVXB_ERR_CUDA, "cuLaunchKernel failed (" + std::to_string(r) + ")");
+    ++ctx->launches;
+    return GVXB_OK;
+}
+
+// --------------------------------------------------------------- row bands
+
+int gvxb_band_rows(int32_t h, int32_t world, int32_t rank, int32_t* row0, int32_t* row1) {
+    if (world < 1 || rank < 0 || rank >= world || h < 0) return fail(GVXB_ERR_INVALID, "bad band query");
+    const int64_t base = h / world, extra = h % world;
+    *row0 = static_cast<int32_t>(rank * base + (rank < extra ? rank : extra));
+    *row1 = static_cast<int32_t>(*row0 + base + (rank < extra ? 1 : 0));
+    return GVXB_OK;
+}
+
+int gvxb_enable_peer(gvxb_ctx ctx, int peer) {
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, ctx->device, peer);
+    if (!can) return fail(GVXB_ERR_UNSUPPORTED, "peer access not possible");
+    cudaSetDevice(ctx->device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return GVXB_OK;
+    }
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
+}
+
+int gvxb_copy_peer_rows(gvxb_ctx ctx, void* dst, size_t dpitch, int dst_dev, const void* src, size_t spitch,
+                        int src_dev, size_t row_bytes, size_t rows) {
+    for (size_t r = 0; r < rows; ++r) {
+        cudaError_t e = cudaMemcpyPeerAsync(static_cast<char*>(dst) + r * dpitch, dst_dev,
+                                            static_cast<const char*>(src) + r * spitch, src_dev, row_bytes,
+                                            ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyPeerAsync");
+    }
+    return GVXB_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,1123 @@
+// vxProcessGraph on the B200: Buffers, device programs, sessions and the
+// run_naive / run_plan entry points.
+//
+// Host contract kept from ref:src/execute.cpp:
+//   Buffer layout, load/store, byte_equal     :14-123
+//   random_buffer (mt19937_64 streams)        :125-167
+//   input binding rules and errors            :300-346
+//   outputs = every produced non-virtual obj  :862-876
+//   transfers_executed                        :880-897
+// Everything per pixel runs on the device through include/gvxb.h.
+#include "graphvx/device.hpp"
+#include "program.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <future>
+#include <random>
+#include <sstream>
+#include <unordered_map>
+
+namespace gvx {
+
+// ================================================================== Buffer
+
+namespace {
+std::size_t packed_bytes(const ResolvedDesc& d) {
+    return static_cast<std::size_t>(d.width) * static_cast<std::size_t>(d.height) *
+           static_cast<std::size_t>(bytes_per_pixel(d.format));
+}
+} // namespace
+
+Buffer Buffer::image(const ResolvedDesc& d) {
+    Buffer b;
+    b.desc = d;
+    b.bytes.assign(packed_bytes(d), 0);
+    return b;
+}
+
+Buffer Buffer::scalar_value(ScalarType t, Value v) {
+    Buffer b;
+    b.desc.kind = ObjKind::Scalar;
+    b.desc.element_type = t;
+    b.scalar = v;
+    return b;
+}
+
+Value Buffer::load(int x, int y, Channel ch) const {
+    const std::size_t i = static_cast<std::size_t>(y) * static_cast<std::size_t>(desc.width) + x;
+    const std::uint8_t* p = bytes.data();
+    switch (desc.format) {
+    case ImageFormat::U8: return Value::of_int(p[i]);
+    case ImageFormat::U16: {
+        std::uint16_t v;
+        std::memcpy(&v, p + 2 * i, 2);
+        return Value::of_int(v);
+    }
+    case ImageFormat::S16: {
+        std::int16_t v;
+        std::memcpy(&v, p + 2 * i, 2);
+        return Value::of_int(v);
+    }
+    case ImageFormat::S32: {
+        std::int32_t v;
+        std::memcpy(&v, p + 4 * i, 4);
+        return Value::of_int(v);
+    }
+    case ImageFormat::F32: {
+        float v;
+        std::memcpy(&v, p + 4 * i, 4);
+        return Value::of_real(v);
+    }
+    case ImageFormat::RGB: return Value::of_int(p[3 * i + (ch == Channel::G ? 1 : ch == Channel::B ? 2 : 0)]);
+    case ImageFormat::UYVY: {
+        const std::size_t row = static_cast<std::size_t>(y) * desc.width * 2;
+        if (ch == Channel::U) return Value::of_int(p[row + 4 * (x / 2)]);
+        if (ch == Channel::V) return Value::of_int(p[row + 4 * (x / 2) + 2]);
+        return Value::of_int(p[row + 2 * x + 1]);
+    }
+    case ImageFormat::UNRESOLVED: break;
+    }
+    throw Error(ErrorCode::BadFormat, "load from unresolved image");
+}
+
+void Buffer::store(int x, int y, Channel ch, const Value& v) {
+    const std::size_t i = static_cast<std::size_t>(y) * static_cast<std::size_t>(desc.width) + x;
+    std::uint8_t* p = bytes.data();
+    switch (desc.format) {
+    case ImageFormat::U8: p[i] = static_cast<std::uint8_t>(v.i); return;
+    case ImageFormat::U16: {
+        auto s = static_cast<std::uint16_t>(v.i);
+        std::memcpy(p + 2 * i, &s, 2);
+        return;
+    }
+    case ImageFormat::S16: {
+        auto s = static_cast<std::int16_t>(v.i);
+        std::memcpy(p + 2 * i, &s, 2);
+        return;
+    }
+    case ImageFormat::S32: {
+        auto s = static_cast<std::int32_t>(v.i);
+        std::memcpy(p + 4 * i, &s, 4);
+        return;
+    }
+    case ImageFormat::F32: {
+        auto s = static_cast<float>(v.as_real());
+        std::memcpy(p + 4 * i, &s, 4);
+        return;
+    }
+    case ImageFormat::RGB: p[3 * i + (ch == Channel::G ? 1 : ch == Channel::B ? 2 : 0)] = static_cast<std::uint8_t>(v.i); return;
+    default: break;
+    }
+    throw Error(ErrorCode::BadFormat, "store into unsupported format");
+}
+
+bool Buffer::byte_equal(const Buffer& o) const {
+    if (desc.kind != o.desc.kind) return false;
+    switch (desc.kind) {
+    case ObjKind::Image: return bytes == o.bytes;
+    case ObjKind::Scalar: return scalar == o.scalar;
+    case ObjKind::Array:
+        if (has_dist != o.has_dist) return false;
+        return has_dist ? dist.counts == o.dist.counts : elements == o.elements;
+    case ObjKind::Matrix: return elements == o.elements;
+    }
+    return false;
+}
+
+Buffer random_buffer(const ResolvedDesc& desc, std::uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    Buffer b;
+    b.desc = desc;
+    if (desc.kind == ObjKind::Image) {
+        b = Buffer::image(desc);
+        const std::size_t n = b.bytes.size();
+        std::uint8_t* p = b.bytes.data();
+        switch (desc.format) {
+        case ImageFormat::F32: {
+            std::uniform_real_distribution<float> d(0.0f, 255.0f);
+            for (std::size_t i = 0; i < n / 4; ++i) {
+                float v = d(rng);
+                std::memcpy(p + 4 * i, &v, 4);
+            }
+            break;
+        }
+        case ImageFormat::S16: {
+            std::uniform_int_distribution<int> d(-32768, 32767);
+            for (std::size_t i = 0; i < n / 2; ++i) {
+                auto v = static_cast<std::int16_t>(d(rng));
+                std::memcpy(p + 2 * i, &v, 2);
+            }
+            break;
+        }
+        case ImageFormat::U16: {
+            std::uniform_int_distribution<int> d(0, 65535);
+            for (std::size_t i = 0; i < n / 2; ++i) {
+                auto v = static_cast<std::uint16_t>(d(rng));
+                std::memcpy(p + 2 * i, &v, 2);
+            }
+            break;
+        }
+        case ImageFormat::S32: {
+            std::uniform_int_distribution<std::int32_t> d(-100000, 100000);
+            for (std::size_t i = 0; i < n / 4; ++i) {
+                std::int32_t v = d(rng);
+                std::memcpy(p + 4 * i, &v, 4);
+            }
+            break;
+        }
+        default: {
+            std::uniform_int_distribution<int> d(0, 255);
+            for (std::size_t i = 0; i < n; ++i) p[i] = static_cast<std::uint8_t>(d(rng));
+            break;
+        }
+        }
+        return b;
+    }
+    if (desc.kind == ObjKind::Scalar) {
+        std::uniform_int_distribution<int> d(0, 255);
+        const int v = d(rng);
+        b.scalar = is_float(desc.element_type) ? Value::of_real(static_cast<double>(v)) : Value::of_int(v);
+        return b;
+    }
+    std::uniform_int_distribution<int> d(-8, 8);
+    const std::int64_t n = desc.kind == ObjKind::Array ? desc.capacity
+                                                       : static_cast<std::int64_t>(desc.rows) * desc.cols;
+    for (std::int64_t i = 0; i < n; ++i) {
+        const int v = d(rng);
+        b.elements.push_back(is_float(desc.element_type) ? Value::of_real(v) : Value::of_int(v));
+    }
+    return b;
+}
+
+// ============================================================ device layer
+
+namespace dev {
+
+void check(int status, const char* what) {
+    if (status == GVXB_OK) return;
+    const std::string msg = std::string(what) + ": " + gvxb_last_error();
+    if (status >= 1 && status <= 20) throw Error(static_cast<ErrorCode>(status - 1), msg);
+    if (status == GVXB_ERR_INVALID) throw Error(ErrorCode::BadKernel, msg);
+    throw Error(ErrorCode::UnsupportedKind, msg);
+}
+
+gvxb_ctx context() {
+    static std::mutex m;
+    static gvxb_ctx ctx = nullptr;
+    std::lock_guard<std::mutex> lock(m);
+    if (ctx) return ctx;
+    int n = 0;
+    if (gvxb_device_count(&n) != GVXB_OK || n == 0)
+        throw Error(ErrorCode::UnsupportedKind,
+                    "no CUDA device: graphvx-b200 executes graphs only on the GPU (no host fallback)");
+    int dev = 0;
+    if (const char* e = std::getenv("GVX_DEVICE")) dev = std::atoi(e);
+    check(gvxb_ctx_create(dev, &ctx), "gvxb_ctx_create");
+    return ctx;
+}
+
+namespace {
+
+// ------------------------------------------------------------ JIT modules
+
+std::mutex g_module_mu;
+// process-lifetime caches are intentionally leaked: tearing down device
+// objects from static destructors races the CUDA runtime's own teardown
+std::unordered_map<std::string, gvxb_module>& module_cache() {
+    static auto* cache = new std::unordered_map<std::string, gvxb_module>();
+    return *cache;
+}
+
+gvxb_module compile(const jit::NodeProgram& prog) {
+    const std::string& src = prog.kernels.at(0).source;
+    std::string key = src;
+    for (const auto& k : prog.kernels) key += "|" + k.name;
+    {
+        std::lock_guard<std::mutex> lock(g_module_mu);
+        auto it = module_cache().find(key);
+        if (it != module_cache().end()) return it->second;
+    }
+    std::vector<const char*> names;
+    for (const auto& k : prog.kernels) names.push_back(k.name.c_str());
+    gvxb_module m = nullptr;
+    const int rc = gvxb_jit_build(context(), src.c_str(), names.data(), static_cast<int>(names.size()), &m);
+    if (rc != GVXB_OK)
+        throw Error(ErrorCode::UnsupportedKind, std::string("device code generation failed: ") + gvxb_last_error());
+    std::lock_guard<std::mutex> lock(g_module_mu);
+    auto [it, fresh] = module_cache().emplace(key, m);
+    if (!fresh) gvxb_jit_free(m);
+    return it->second;
+}
+
+jit::SlotInfo slot_of(const VerifiedGraph& vg, ObjectId id) {
+    jit::SlotInfo s;
+    if (id == kInvalidId) return s;
+    s.desc = vg.desc(id);
+    switch (s.desc.kind) {
+    case ObjKind::Image: s.kind = jit::SlotKind::Image; break;
+    case ObjKind::Scalar: s.kind = jit::SlotKind::Scalar; break;
+    case ObjKind::Array: s.kind = jit::SlotKind::Array; break;
+    case ObjKind::Matrix: s.kind = jit::SlotKind::Matrix; break;
+    }
+    return s;
+}
+
+std::vector<Value> matrix_for(const Unit& u, const Context& ctx,
+                              const std::map<ObjectId, std::vector<Value>>& matrices) {
+    for (ObjectId id : u.in_ids) {
+        if (id == kInvalidId) continue;
+        const DataObject* o = ctx.find(id);
+        if (!o || o->kind != ObjKind::Matrix) continue;
+        auto it = matrices.find(id);
+        return it != matrices.end() ? it->second : o->matrix_values;
+    }
+    return {};
+}
+
+Unit jit_unit(const OperatorNode& n, const VerifiedGraph& vg,
+              const std::map<ObjectId, std::vector<Value>>& matrices) {
+    if (!n.abstraction)
+        throw Error(ErrorCode::UnknownKernel, "node '" + n.kernel + "' has no abstraction kernel (expand first)");
+    Unit u;
+    u.kind = Unit::Kind::Jit;
+    u.k = n.abstraction;
+    u.label = n.label.empty() ? n.kernel : n.label;
+    u.covers = {n.id};
+    const auto& ps = u.k->signature.params;
+    for (std::size_t i = 0; i < ps.size(); ++i) {
+        const Binding* b = n.binding_for(static_cast<int>(i));
+        const ObjectId id = b ? b->object : kInvalidId;
+        if (ps[i].direction == Direction::Input) {
+            u.in_ids.push_back(id);
+            u.in_slots.push_back(slot_of(vg, id));
+            if (id != kInvalidId) u.reads.push_back(id);
+        } else {
+            u.out_ids.push_back(id);
+            u.out_slots.push_back(slot_of(vg, id));
+            if (id != kInvalidId) u.writes.push_back(id);
+        }
+    }
+    u.prog = jit::lower_node(*u.k, u.in_slots, u.out_slots, matrix_for(u, vg.context(), matrices));
+    const ResolvedDesc* d = nullptr;
+    if (u.prog.dims_from >= 0 && u.prog.dims_from < static_cast<int>(u.in_slots.size()))
+        d = &u.in_slots[static_cast<std::size_t>(u.prog.dims_from)].desc;
+    else if (!u.out_slots.empty() && u.out_slots[0].kind != jit::SlotKind::None)
+        d = &u.out_slots[0].desc;
+    if (d) {
+        u.width = d->width;
+        u.height = d->height;
+    }
+    std::int64_t r = 0, w = 0;
+    const bool stat = static_counts(n, vg, r, w);
+    u.static_writes = w;
+    u.device_counts_reads = u.prog.counts_reads;
+    u.static_reads = u.prog.counts_reads ? 0 : r;
+    (void)stat;
+    return u;
+}
+
+void record_objects(Program& p, const VerifiedGraph& vg) {
+    const Context& ctx = vg.context();
+    for (const Unit& u : p.units) {
+        auto touch = [&](ObjectId id, bool produced) {
+            if (id == kInvalidId) return;
+            ObjInfo& oi = p.objects[id];
+            oi.id = id;
+            oi.desc = vg.desc(id);
+            const DataObject* o = ctx.find(id);
+            oi.is_virtual = o && o->is_virtual;
+            oi.produced = oi.produced || produced;
+            if (oi.desc.kind == ObjKind::Array) oi.length = static_cast<int>(std::max<std::int64_t>(oi.desc.capacity, 0));
+            if (oi.desc.kind == ObjKind::Matrix) oi.length = oi.desc.rows * oi.desc.cols;
+        };
+        for (ObjectId id : u.reads) touch(id, false);
+        for (ObjectId id : u.writes) touch(id, true);
+    }
+    // array roles from producers
+    for (const Unit& u : p.units) {
+        auto set_role = [&](ObjectId id, ArrayRole role, int len) {
+            if (id == kInvalidId) return;
+            ObjInfo& oi = p.objects[id];
+            oi.role = role;
+            oi.length = std::max(oi.length, len);
+        };
+        if (u.kind == Unit::Kind::Jit) {
+            switch (u.k->kind) {
+            case AbstractionKind::Histogram: {
+                const HistogramKernel& hk = u.k->histogram();
+                set_role(u.out_ids[0], ArrayRole::Distribution, hk.bins);
+                ObjInfo& oi = p.objects[u.out_ids[0]];
+                oi.bins = hk.bins;
+                oi.offset = hk.offset;
+                oi.range = hk.range;
+                break;
+            }
+            case AbstractionKind::Reduce:
+                if (u.out_ids.size() > 1 && u.out_ids[1] != kInvalidId) set_role(u.out_ids[1], ArrayRole::Location, 2);
+                break;
+            case AbstractionKind::Table: {
+                int n = 256;
+                if (!u.in_ids.empty() && p.objects.count(u.in_ids[0])) n = std::max(n, p.objects[u.in_ids[0]].length);
+                set_role(u.out_ids[0], ArrayRole::Table, n);
+                break;
+            }
+            default: break;
+            }
+        } else if (u.kind == Unit::Kind::ConvStats && u.out[1] != kInvalidId) {
+            set_role(u.out[1], ArrayRole::Distribution, u.bins);
+            ObjInfo& oi = p.objects[u.out[1]];
+            oi.bins = u.bins;
+            oi.offset = u.offset;
+            oi.range = u.range;
+        }
+    }
+}
+
+/// Orders units so every object is written before it is read.
+void order_units(Program& p) {
+    const std::size_t n = p.units.size();
+    std::map<ObjectId, std::size_t> writer;
+    for (std::size_t i = 0; i < n; ++i)
+        for (ObjectId w : p.units[i].writes) writer[w] = i;
+    std::vector<std::set<std::size_t>> succ(n);
+    std::vector<int> indeg(n, 0);
+    for (std::size_t i = 0; i < n; ++i)
+        for (ObjectId r : p.units[i].reads) {
+            auto it = writer.find(r);
+            if (it != writer.end() && it->second != i && succ[it->second].insert(i).second) ++indeg[i];
+        }
+    std::vector<std::size_t> order;
+    std::vector<bool> done(n, false);
+    for (std::size_t round = 0; round < n; ++round)
+        for (std::size_t i = 0; i < n; ++i) {
+            if (done[i] || indeg[i] != 0) continue;
+            done[i] = true;
+            order.push_back(i);
+            for (std::size_t s : succ[i]) --indeg[s];
+            break;
+        }
+    if (order.size() != n) throw Error(ErrorCode::CycleDetected, "device program has a cyclic dependency");
+    std::vector<Unit> sorted;
+    for (std::size_t i : order) sorted.push_back(std::move(p.units[i]));
+    p.units = std::move(sorted);
+}
+
+void compile_all(Program& p) {
+    std::vector<std::future<gvxb_module>> jobs;
+    context();
+    for (Unit& u : p.units)
+        if (u.kind == Unit::Kind::Jit) jobs.push_back(std::async(std::launch::async, [&u] { return compile(u.prog); }));
+    std::size_t j = 0;
+    for (Unit& u : p.units)
+        if (u.kind == Unit::Kind::Jit) u.module = jobs[j++].get();
+}
+
+} // namespace
+
+std::string Program::describe() const {
+    std::ostringstream os;
+    os << (naive ? "naive" : "plan") << " program, " << units.size() << " units:";
+    for (const Unit& u : units) {
+        os << "\n  " << u.label << " [";
+        switch (u.kind) {
+        case Unit::Kind::Jit: os << "nvrtc " << u.prog.kernels.size() << " kernel(s)"; break;
+        case Unit::Kind::Edge: os << "sm_100a fused edge" << (u.with_gauss ? " (+gauss)" : ""); break;
+        case Unit::Kind::Harris: os << "sm_100a fused harris"; break;
+        case Unit::Kind::Stencil: os << "sm_100a fused stencil k=" << u.ksize << " mode=" << u.mode; break;
+        case Unit::Kind::ConvStats: os << "sm_100a fused conv+stats k=" << u.ksize; break;
+        }
+        os << "] covers " << u.covers.size() << " node(s)";
+    }
+    return os.str();
+}
+
+int Program::launches_per_run() const {
+    int n = 0;
+    for (const Unit& u : units) {
+        if (u.kind == Unit::Kind::Jit) n += static_cast<int>(u.prog.kernels.size());
+        else if (u.kind == Unit::Kind::ConvStats) n += (u.out[2] != kInvalidId || u.out[3] != kInvalidId) ? 2 : 1;
+        else n += 1;
+    }
+    return n;
+}
+
+std::shared_ptr<Program> build_naive(const VerifiedGraph& vg, const std::map<ObjectId, std::vector<Value>>& matrices) {
+    auto p = std::make_shared<Program>();
+    p->naive = true;
+    const AppGraph& g = vg.graph();
+    for (ObjectId nid : g.topo_sort()) p->units.push_back(jit_unit(*g.node(nid), vg, matrices));
+    record_objects(*p, vg);
+    compile_all(*p);
+    return p;
+}
+
+std::shared_ptr<Program> build_plan(const OptimizedPlan& plan, const std::map<ObjectId, std::vector<Value>>& matrices) {
+    auto p = std::make_shared<Program>();
+    const VerifiedGraph& base = plan.base;
+    const VerifiedGraph& fused = plan.fused;
+    const AppGraph& bg = base.graph();
+    const AppGraph& fg = fused.graph();
+
+    GraphView view;
+    view.vg = &base;
+    view.ctx = &base.context();
+    view.matrices = &matrices;
+    std::set<ObjectId> alive_nodes;
+    for (ObjectId nid : plan.filtered.alive_nodes()) {
+        const OperatorNode* n = bg.node(nid);
+        if (!n || !n->abstraction) continue;
+        view.nodes.push_back(n);
+        alive_nodes.insert(nid);
+        std::set<ObjectId> seen;
+        for (const Binding& b : n->bindings) {
+            if (b.direction == Direction::Input) {
+                if (seen.insert(b.object).second) view.readers[b.object].push_back(nid);
+            } else {
+                view.writer[b.object] = nid;
+            }
+        }
+    }
+    std::vector<Unit> aot = match_fused_groups(view);
+
+    // base members of every executed (fused-graph) node
+    std::map<ObjectId, std::vector<ObjectId>> members;
+    for (const FusedKernel& fk : plan.groups) members[fk.fused_node] = fk.members;
+    for (const OperatorNode& fnode : fg.nodes()) {
+        if (members.count(fnode.id)) continue;
+        for (const OperatorNode* bn : view.nodes)
+            if (bn->abstraction == fnode.abstraction && bn->bindings.size() == fnode.bindings.size() &&
+                std::equal(bn->bindings.begin(), bn->bindings.end(), fnode.bindings.begin(),
+                           [](const Binding& a, const Binding& b) {
+                               return a.param == b.param && a.object == b.object && a.direction == b.direction;
+                           })) {
+                members[fnode.id] = {bn->id};
+                break;
+            }
+    }
+
+    // keep only groups that cover whole executed nodes with static counters
+    std::set<ObjectId> covered_fused;
+    for (bool changed = true; changed;) {
+        changed = false;
+        covered_fused.clear();
+        for (std::size_t gi = 0; gi < aot.size(); ++gi) {
+            Unit& u = aot[gi];
+            std::set<ObjectId> cov(u.covers.begin(), u.covers.end());
+            bool ok = true;
+            std::vector<ObjectId> fnodes;
+            std::int64_t reads = 0, writes = 0;
+            for (const OperatorNode& fnode : fg.nodes()) {
+                auto it = members.find(fnode.id);
+                if (it == members.end()) continue;
+                std::size_t inside = 0;
+                for (ObjectId m : it->second) inside += cov.count(m);
+                if (inside == 0) continue;
+                if (inside != it->second.size()) {
+                    ok = false;
+                    break;
+                }
+                std::int64_t r = 0, w = 0;
+                if (!static_counts(fnode, fused, r, w)) {
+                    ok = false;
+                    break;
+                }
+                reads += r;
+                writes += w;
+                fnodes.push_back(fnode.id);
+            }
+            std::size_t member_total = 0;
+            for (ObjectId f : fnodes) member_total += members[f].size();
+            if (ok && member_total != cov.size()) ok = false; // group must be exactly a union of executed nodes
+            if (!ok) {
+                aot.erase(aot.begin() + static_cast<std::ptrdiff_t>(gi));
+                changed = true;
+                break;
+            }
+            u.static_reads = reads;
+            u.static_writes = writes;
+            u.covers = fnodes;
+            covered_fused.insert(fnodes.begin(), fnodes.end());
+        }
+    }
+    for (Unit& u : aot) p->units.push_back(std::move(u));
+    for (ObjectId nid : fg.topo_sort())
+        if (!covered_fused.count(nid)) p->units.push_back(jit_unit(*fg.node(nid), fused, matrices));
+    order_units(*p);
+    record_objects(*p, base);
+    compile_all(*p);
+    return p;
+}
+
+} // namespace dev
+
+// ============================================================== sessions
+
+struct DeviceSession::Impl {
+    std::shared_ptr<dev::Program> prog;
+    const VerifiedGraph* exec_graph = nullptr; ///< graph whose outputs are reported
+    VerifiedGraph exec_copy;
+    int frames = 1;
+    gvxb_ctx ctx = nullptr;
+    void* stream = nullptr;
+
+    struct Store {
+        void* ptr = nullptr;
+        std::int64_t pitch = 0;
+        std::int64_t fstride = 0;
+        bool owned = false;
+        int length = 0; ///< arrays: live Value slots for bounds checks
+    };
+    std::map<ObjectId, Store> store;
+    std::vector<void*> scratch; ///< per unit (JIT reduce scratch, conv sums)
+
+    ~Impl() {
+        if (!ctx) return;
+        gvxb_sync(ctx);
+        for (auto& kv : store)
+            if (kv.second.owned) gvxb_free(ctx, kv.second.ptr);
+        for (void* s : scratch)
+            if (s) gvxb_free(ctx, s);
+    }
+
+    static std::int64_t row_pitch(const ResolvedDesc& d) {
+        const std::int64_t row = static_cast<std::int64_t>(d.width) * bytes_per_pixel(d.format);
+        return std::max<std::int64_t>(128, (row + 127) / 128 * 128);
+    }
+
+    Store& ensure(ObjectId id) {
+        auto it = store.find(id);
+        if (it != store.end()) return it->second;
+        const dev::ObjInfo& oi = prog->objects.at(id);
+        Store s;
+        s.owned = true;
+        std::size_t bytes = 0;
+        if (oi.desc.kind == ObjKind::Image) {
+            s.pitch = row_pitch(oi.desc);
+            s.fstride = s.pitch * oi.desc.height;
+            bytes = static_cast<std::size_t>(s.fstride) * frames;
+        } else {
+            const int n = oi.desc.kind == ObjKind::Scalar ? 1 : std::max(oi.length, 1);
+            s.length = oi.desc.kind == ObjKind::Scalar ? 1 : oi.length;
+            s.fstride = static_cast<std::int64_t>(n) * 16;
+            bytes = static_cast<std::size_t>(s.fstride) * frames;
+        }
+        dev::check(gvxb_alloc(ctx, bytes, &s.ptr), "device allocation");
+        dev::check(gvxb_memset(ctx, s.ptr, 0, bytes), "device clear");
+        return store.emplace(id, s).first->second;
+    }
+
+    gvxb_image image(ObjectId id) {
+        gvxb_image im{};
+        if (id == kInvalidId) return im;
+        Store& s = ensure(id);
+        const ResolvedDesc& d = prog->objects.at(id).desc;
+        im.data = s.ptr;
+        im.pitch = s.pitch;
+        im.width = d.width;
+        im.height = d.height;
+        im.format = static_cast<int32_t>(d.format);
+        im.frames = frames;
+        im.frame_stride = s.fstride;
+        return im;
+    }
+
+    gvxb_value* values(ObjectId id) { return id == kInvalidId ? nullptr : static_cast<gvxb_value*>(ensure(id).ptr); }
+
+    void prepare() {
+        for (auto& kv : prog->objects) ensure(kv.first);
+        scratch.assign(prog->units.size(), nullptr);
+        for (std::size_t i = 0; i < prog->units.size(); ++i) {
+            const dev::Unit& u = prog->units[i];
+            std::size_t bytes = 0;
+            if (u.kind == dev::Unit::Kind::Jit) bytes = u.prog.scratch_bytes_per_frame * frames;
+            if (u.kind == dev::Unit::Kind::ConvStats) bytes = 16 * static_cast<std::size_t>(frames);
+            if (bytes) dev::check(gvxb_alloc(ctx, bytes, &scratch[i]), "scratch allocation");
+        }
+    }
+
+    void launch_unit(std::size_t idx) {
+        const dev::Unit& u = prog->units[idx];
+        const gvxb_band full{0, 0, 0, 0, 0};
+        (void)full;
+        switch (u.kind) {
+        case dev::Unit::Kind::Jit: launch_jit(u, scratch[idx]); return;
+        case dev::Unit::Kind::Edge: {
+            gvxb_edge_args a{};
+            a.src = image(u.src);
+            a.gx = image(u.out[0]);
+            a.gy = image(u.out[1]);
+            a.mag = image(u.out[2]);
+            a.with_gauss = u.with_gauss ? 1 : 0;
+            a.band = gvxb_band{0, a.src.height, a.src.height, 0, 0};
+            dev::check(gvxb_edge(ctx, &a), "gvxb_edge");
+            return;
+        }
+        case dev::Unit::Kind::Harris: {
+            gvxb_harris_args a{};
+            a.src = image(u.src);
+            a.mask = image(u.out[0]);
+            a.response = image(u.out[1]);
+            a.k = u.k_param;
+            a.threshold = u.threshold;
+            a.band = gvxb_band{0, a.src.height, a.src.height, 0, 0};
+            dev::check(gvxb_harris(ctx, &a), "gvxb_harris");
+            return;
+        }
+        case dev::Unit::Kind::Stencil: {
+            gvxb_stencil_args a{};
+            a.src = image(u.src);
+            a.dst = image(u.out[0]);
+            a.ksize = u.ksize;
+            std::memcpy(a.mask, u.mask, sizeof(a.mask));
+            a.div_num = 1;
+            a.div_den = u.divisor;
+            a.mode = u.mode;
+            a.band = gvxb_band{0, a.src.height, a.src.height, 0, 0};
+            dev::check(gvxb_stencil_point(ctx, &a), "gvxb_stencil_point");
+            return;
+        }
+        case dev::Unit::Kind::ConvStats: {
+            gvxb_conv_stats_args a{};
+            a.src = image(u.src);
+            a.converted = image(u.out[0]);
+            a.ksize = u.ksize;
+            std::memcpy(a.mask, u.mask, sizeof(a.mask));
+            a.scale = u.divisor;
+            a.conv_format = u.conv_format;
+            a.shift = u.shift;
+            a.wrap = u.wrap;
+            a.bins = u.bins;
+            a.offset = u.offset;
+            a.range = u.range;
+            a.hist = values(u.out[1]);
+            a.sum = static_cast<int64_t*>(scratch[idx]);
+            a.sumsq = static_cast<int64_t*>(scratch[idx]) + frames;
+            a.mean = values(u.out[2]);
+            a.stddev = values(u.out[3]);
+            dev::check(gvxb_conv_stats(ctx, &a), "gvxb_conv_stats");
+            return;
+        }
+        }
+    }
+
+    void launch_jit(const dev::Unit& u, void* scr) {
+        const jit::NodeProgram& np = u.prog;
+        std::vector<std::uint64_t> f(static_cast<std::size_t>(np.fields()), 0);
+        unsigned long long* counter = nullptr;
+        std::uint32_t* status = nullptr;
+        gvxb_counter_ptr(ctx, &counter);
+        gvxb_status_ptr(ctx, &status);
+        f[0] = reinterpret_cast<std::uint64_t>(status);
+        f[1] = reinterpret_cast<std::uint64_t>(counter);
+        f[2] = static_cast<std::uint64_t>(u.width);
+        f[3] = static_cast<std::uint64_t>(u.height);
+        f[4] = static_cast<std::uint64_t>(frames);
+        auto put = [&](int slot, ObjectId id) {
+            const std::size_t b = static_cast<std::size_t>(5 + 3 * slot);
+            if (id == kInvalidId) return;
+            Store& s = ensure(id);
+            f[b] = reinterpret_cast<std::uint64_t>(s.ptr);
+            const dev::ObjInfo& oi = prog->objects.at(id);
+            f[b + 1] = oi.desc.kind == ObjKind::Image ? static_cast<std::uint64_t>(s.pitch)
+                                                      : static_cast<std::uint64_t>(s.length);
+            f[b + 2] = static_cast<std::uint64_t>(s.fstride);
+        };
+        for (std::size_t i = 0; i < u.in_ids.size(); ++i) put(static_cast<int>(i), u.in_ids[i]);
+        for (std::size_t o = 0; o < u.out_ids.size(); ++o) put(static_cast<int>(u.in_ids.size() + o), u.out_ids[o]);
+        f[f.size() - 2] = reinterpret_cast<std::uint64_t>(scr);
+        f[f.size() - 1] = np.scratch_bytes_per_frame;
+        void* args[] = {f.data()};
+        for (std::size_t ki = 0; ki < np.kernels.size(); ++ki) {
+            const jit::KernelSpec& ks = np.kernels[ki];
+            unsigned grid[3] = {1, 1, static_cast<unsigned>(frames)};
+            unsigned block[3] = {static_cast<unsigned>(ks.block_x), static_cast<unsigned>(ks.block_y), 1};
+            switch (ks.grid) {
+            case jit::KernelSpec::Grid::Pixels:
+            case jit::KernelSpec::Grid::OutPixels:
+                grid[0] = static_cast<unsigned>((u.width + ks.block_x - 1) / ks.block_x);
+                grid[1] = static_cast<unsigned>((u.height + ks.block_y - 1) / ks.block_y);
+                break;
+            case jit::KernelSpec::Grid::Single: block[1] = 1; break;
+            case jit::KernelSpec::Grid::Rows: grid[0] = static_cast<unsigned>((u.height + 127) / 128); break;
+            case jit::KernelSpec::Grid::Cols: grid[0] = static_cast<unsigned>((u.width + 127) / 128); break;
+            }
+            dev::check(gvxb_jit_launch(ctx, u.module, static_cast<int>(ki), grid, block, 0, args), "generated kernel launch");
+        }
+    }
+
+    void upload(ObjectId id, const Buffer& b, int frame) {
+        const dev::ObjInfo& oi = prog->objects.at(id);
+        Store& s = ensure(id);
+        char* base = static_cast<char*>(s.ptr) + static_cast<std::int64_t>(frame) * s.fstride;
+        if (oi.desc.kind == ObjKind::Image) {
+            const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
+            if (b.bytes.size() < row * oi.desc.height) throw Error(ErrorCode::ShapeMismatch, "image payload too small", id);
+            dev::check(gvxb_upload_2d(ctx, base, static_cast<std::size_t>(s.pitch), b.bytes.data(), row, row,
+                                      static_cast<std::size_t>(oi.desc.height)),
+                       "image upload");
+            return;
+        }
+        std::vector<gvxb_value> vals;
+        auto push = [&](const Value& v) {
+            gvxb_value g;
+            g.real = v.real ? 1 : 0;
+            if (v.real) std::memcpy(&g.bits, &v.f, 8);
+            else g.bits = v.i;
+            vals.push_back(g);
+        };
+        if (oi.desc.kind == ObjKind::Scalar) {
+            push(b.scalar);
+        } else if (b.has_dist) {
+            for (std::int64_t c : b.dist.counts) push(Value::of_int(c));
+        } else {
+            for (const Value& v : b.elements) push(v);
+        }
+        const int cap = static_cast<int>(s.fstride / 16);
+        if (static_cast<int>(vals.size()) > cap) {
+            if (!s.owned) throw Error(ErrorCode::ShapeMismatch, "array payload exceeds bound storage", id);
+            gvxb_sync(ctx);
+            gvxb_free(ctx, s.ptr);
+            s.fstride = static_cast<std::int64_t>(vals.size()) * 16;
+            dev::check(gvxb_alloc(ctx, static_cast<std::size_t>(s.fstride) * frames, &s.ptr), "device allocation");
+            base = static_cast<char*>(s.ptr) + static_cast<std::int64_t>(frame) * s.fstride;
+        }
+        if (oi.desc.kind != ObjKind::Scalar) s.length = static_cast<int>(vals.size());
+        if (!vals.empty())
+            dev::check(gvxb_upload_2d(ctx, base, vals.size() * 16, vals.data(), vals.size() * 16, vals.size() * 16, 1),
+                       "value upload");
+    }
+
+    Buffer download(ObjectId id, int frame) {
+        const dev::ObjInfo& oi = prog->objects.at(id);
+        Store& s = ensure(id);
+        const char* base = static_cast<const char*>(s.ptr) + static_cast<std::int64_t>(frame) * s.fstride;
+        Buffer b;
+        b.id = id;
+        b.desc = exec_graph->resolved().count(id) ? exec_graph->desc(id) : oi.desc;
+        if (oi.desc.kind == ObjKind::Image) {
+            b = Buffer::image(b.desc);
+            b.id = id;
+            const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
+            dev::check(gvxb_download_2d(ctx, b.bytes.data(), row, base, static_cast<std::size_t>(s.pitch), row,
+                                        static_cast<std::size_t>(oi.desc.height)),
+                       "image download");
+            dev::check(gvxb_sync(ctx), "download sync");
+            return b;
+        }
+        int n = oi.desc.kind == ObjKind::Scalar ? 1 : oi.length;
+        if (oi.role == dev::ArrayRole::Distribution) n = oi.bins;
+        if (oi.role == dev::ArrayRole::Location) n = 2;
+        std::vector<gvxb_value> vals(static_cast<std::size_t>(std::max(n, 0)));
+        if (!vals.empty())
+            dev::check(gvxb_download_2d(ctx, vals.data(), vals.size() * 16, base, vals.size() * 16, vals.size() * 16, 1),
+                       "value download");
+        dev::check(gvxb_sync(ctx), "download sync");
+        auto value = [](const gvxb_value& g) {
+            if (!g.real) return Value::of_int(g.bits);
+            double d;
+            std::memcpy(&d, &g.bits, 8);
+            return Value::of_real(d);
+        };
+        if (oi.desc.kind == ObjKind::Scalar) {
+            b.scalar = value(vals[0]);
+        } else if (oi.role == dev::ArrayRole::Distribution) {
+            b.has_dist = true;
+            b.dist.bins = oi.bins;
+            b.dist.offset = oi.offset;
+            b.dist.range = oi.range;
+            for (const gvxb_value& g : vals) b.dist.counts.push_back(g.bits);
+        } else {
+            for (const gvxb_value& g : vals) b.elements.push_back(value(g));
+        }
+        return b;
+    }
+
+    void run_all() {
+        for (std::size_t i = 0; i < prog->units.size(); ++i) launch_unit(i);
+    }
+};
+
+namespace {
+
+std::map<ObjectId, std::vector<Value>> matrix_inputs(const VerifiedGraph& vg, const InputMap* inputs) {
+    std::map<ObjectId, std::vector<Value>> m;
+    const Context& ctx = vg.context();
+    for (ObjectId id : vg.graph().data()) {
+        const DataObject* o = ctx.find(id);
+        if (!o || o->kind != ObjKind::Matrix) continue;
+        if (inputs) {
+            auto it = inputs->find(id);
+            if (it != inputs->end()) {
+                m[id] = it->second.elements;
+                continue;
+            }
+        }
+        m[id] = o->matrix_values;
+    }
+    return m;
+}
+
+std::string program_key(std::uint64_t stamp, bool naive, const std::map<ObjectId, std::vector<Value>>& mats) {
+    std::ostringstream os;
+    os << (naive ? "n" : "p") << stamp;
+    for (const auto& [id, vals] : mats) {
+        os << "|" << id << ":";
+        for (const Value& v : vals) os << (v.real ? "r" : "i") << (v.real ? v.f : static_cast<double>(v.i)) << ",";
+    }
+    return os.str();
+}
+
+std::mutex g_prog_mu;
+std::map<std::string, std::shared_ptr<dev::Program>>& program_cache() {
+    static auto* c = new std::map<std::string, std::shared_ptr<dev::Program>>();
+    return *c;
+}
+
+std::shared_ptr<dev::Program> cached_program(const std::string& key, const std::function<std::shared_ptr<dev::Program>()>& make) {
+    {
+        std::lock_guard<std::mutex> lock(g_prog_mu);
+        auto it = program_cache().find(key);
+        if (it != program_cache().end()) return it->second;
+    }
+    auto p = make();
+    std::lock_guard<std::mutex> lock(g_prog_mu);
+    if (program_cache().size() > 256) program_cache().clear();
+    return program_cache().emplace(key, p).first->second;
+}
+
+std::shared_ptr<dev::Program> naive_program(const VerifiedGraph& g, const InputMap* inputs) {
+    auto mats = matrix_inputs(g, inputs);
+    return cached_program(program_key(g.stamp(), true, mats), [&] { return dev::build_naive(g, mats); });
+}
+
+std::shared_ptr<dev::Program> plan_program(const OptimizedPlan& plan, const InputMap* inputs) {
+    auto mats = matrix_inputs(plan.fused, inputs);
+    auto base_mats = matrix_inputs(plan.base, inputs);
+    mats.insert(base_mats.begin(), base_mats.end());
+    return cached_program(program_key(plan.fused.stamp(), false, mats), [&] { return dev::build_plan(plan, mats); });
+}
+
+/// The reference's input binding rules (ref:src/execute.cpp:300-346).
+std::map<ObjectId, const Buffer*> bind_inputs(const VerifiedGraph& vg, const InputMap& inputs,
+                                               std::map<ObjectId, Buffer>& defaults) {
+    const AppGraph& g = vg.graph();
+    const Context& ctx = vg.context();
+    for (const auto& [id, buf] : inputs) {
+        const DataObject* o = ctx.find(id);
+        if (!o) throw Error(ErrorCode::UnknownObject, "input #" + std::to_string(id), id);
+        if (o->is_virtual)
+            throw Error(ErrorCode::AccessDenied, "virtual object '" + o->name + "' cannot be written from the host", id);
+    }
+    std::map<ObjectId, const Buffer*> bound;
+    for (ObjectId id : g.data()) {
+        const DataObject* o = ctx.find(id);
+        if (!o || o->is_virtual || g.producer(id) != kInvalidId) continue;
+        auto it = inputs.find(id);
+        if (it != inputs.end()) {
+            const ResolvedDesc& want = vg.desc(id);
+            const Buffer& got = it->second;
+            if (want.kind != got.desc.kind ||
+                (want.kind == ObjKind::Image &&
+                 (want.width != got.desc.width || want.height != got.desc.height || want.format != got.desc.format)))
+                throw Error(ErrorCode::ShapeMismatch, "input '" + o->name + "' does not match its declaration", id);
+            bound[id] = &got;
+            continue;
+        }
+        if (o->kind == ObjKind::Scalar && o->scalar_value) {
+            Buffer b = Buffer::scalar_value(o->element_type, *o->scalar_value);
+            b.id = id;
+            b.desc = vg.desc(id);
+            bound[id] = &(defaults[id] = b);
+            continue;
+        }
+        if (o->kind == ObjKind::Matrix && !o->matrix_values.empty()) {
+            Buffer b;
+            b.id = id;
+            b.desc = vg.desc(id);
+            b.elements = o->matrix_values;
+            bound[id] = &(defaults[id] = b);
+            continue;
+        }
+        if (!g.consumers(id).empty())
+            throw Error(ErrorCode::MissingInput, "no buffer for input '" + o->name + "'", id);
+    }
+    return bound;
+}
+
+struct HostSession {
+    std::mutex mu;
+    DeviceSession::Impl impl;
+};
+
+/// Device storage is kept per program between synchronous host runs (the
+/// reference allocates per run; reusing it keeps run_plan at copy speed).
+std::shared_ptr<HostSession> host_session(const std::shared_ptr<dev::Program>& prog) {
+    static std::mutex mu;
+    static auto& cache =
+        *new std::map<const dev::Program*, std::pair<std::weak_ptr<dev::Program>, std::shared_ptr<HostSession>>>();
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto it = cache.begin(); it != cache.end();)
+        it = it->second.first.expired() ? cache.erase(it) : std::next(it);
+    auto& slot = cache[prog.get()];
+    if (!slot.second) {
+        slot.first = prog;
+        slot.second = std::make_shared<HostSession>();
+        slot.second->impl.prog = prog;
+        slot.second->impl.frames = 1;
+        slot.second->impl.ctx = dev::context();
+    }
+    return slot.second;
+}
+
+ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const VerifiedGraph& vg, const InputMap& inputs) {
+    std::map<ObjectId, Buffer> defaults;
+    auto bound = bind_inputs(vg, inputs, defaults);
+
+    std::shared_ptr<HostSession> hs = host_session(prog);
+    std::lock_guard<std::mutex> lock(hs->mu);
+    DeviceSession::Impl& s = hs->impl;
+    s.exec_graph = &vg;
+    gvxb_ctx_set_stream(s.ctx, nullptr);
+    if (s.scratch.size() != prog->units.size()) s.prepare();
+    for (const auto& [id, b] : bound)
+        if (prog->objects.count(id)) s.upload(id, *b, 0);
+    dev::check(gvxb_status_reset(s.ctx), "status reset");
+    const std::int64_t launches0 = gvxb_launch_count(s.ctx);
+    s.run_all();
+    std::uint32_t status = 0;
+    dev::check(gvxb_status_read(s.ctx, &status), "device status");
+    if (status & GVXB_STATUS_DIV_BY_ZERO) throw Error(ErrorCode::DivByZero, "division by zero");
+    if (status & GVXB_STATUS_INDEX_RANGE) throw Error(ErrorCode::ShapeMismatch, "array index out of range");
+    long long dyn_reads = 0;
+    dev::check(gvxb_counter_read(s.ctx, &dyn_reads), "counter read");
+
+    ExecutionReport report;
+    report.counters.kernel_launches = gvxb_launch_count(s.ctx) - launches0;
+    report.counters.pixels_read = dyn_reads;
+    for (const dev::Unit& u : prog->units) {
+        report.counters.pixels_read += u.static_reads;
+        report.counters.pixels_written += u.static_writes;
+    }
+    const AppGraph& g = vg.graph();
+    const Context& ctx = vg.context();
+    for (ObjectId id : g.data()) {
+        const DataObject* o = ctx.find(id);
+        if (!o || o->is_virtual || g.producer(id) == kInvalidId) continue;
+        if (!prog->objects.count(id)) continue;
+        report.outputs[id] = s.download(id, 0);
+    }
+    return report;
+}
+
+} // namespace
+
+ExecutionReport run_naive(const VerifiedGraph& g, const InputMap& inputs) {
+    if (!g.stamped()) throw Error(ErrorCode::UnstampedGraph, "execution needs a verified graph");
+    auto prog = naive_program(g, &inputs);
+    ExecutionReport r = execute(prog, g, inputs);
+    r.counters.transfers_executed = static_cast<std::int64_t>(g.graph().nodes().size()) * 2;
+    return r;
+}
+
+ExecutionReport run_plan(const OptimizedPlan& plan, const InputMap& inputs) {
+    if (!plan.fused.stamped()) throw Error(ErrorCode::UnstampedGraph, "plan execution needs a verified fused graph");
+    auto prog = plan_program(plan, &inputs);
+    ExecutionReport r = execute(prog, plan.fused, inputs);
+    r.counters.transfers_executed = plan.transfers.optimized_count();
+    return r;
+}
+
+// ------------------------------------------------------------ DeviceSession
+
+DeviceSession::DeviceSession(const OptimizedPlan& plan, int frames) : impl_(std::make_unique<Impl>()) {
+    if (!plan.fused.stamped()) throw Error(ErrorCode::UnstampedGraph, "plan execution needs a verified fused graph");
+    impl_->prog = plan_program(plan, nullptr);
+    impl_->exec_copy = plan.fused;
+    impl_->exec_graph = &impl_->exec_copy;
+    impl_->frames = std::max(1, frames);
+    impl_->ctx = dev::context();
+}
+
+DeviceSession::DeviceSession(const VerifiedGraph& g, int frames) : impl_(std::make_unique<Impl>()) {
+    if (!g.stamped()) throw Error(ErrorCode::UnstampedGraph, "execution needs a verified graph");
+    impl_->prog = naive_program(g, nullptr);
+    impl_->exec_copy = g;
+    impl_->exec_graph = &impl_->exec_copy;
+    impl_->frames = std::max(1, frames);
+    impl_->ctx = dev::context();
+}
+
+DeviceSession::~DeviceSession() = default;
+
+void DeviceSession::bind(ObjectId id, DeviceTensor t) {
+    auto it = impl_->prog->objects.find(id);
+    if (it == impl_->prog->objects.end()) return; // not touched by the program
+    if (it->second.is_virtual) throw Error(ErrorCode::AccessDenied, "virtual objects are program-internal", id);
+    Impl::Store s;
+    s.ptr = t.data;
+    s.pitch = t.pitch;
+    const ResolvedDesc& d = it->second.desc;
+    if (d.kind == ObjKind::Image) {
+        if (t.pitch % 16 != 0) throw Error(ErrorCode::ShapeMismatch, "device image pitch must be a multiple of 16", id);
+        s.fstride = t.frame_stride ? t.frame_stride : t.pitch * d.height;
+    } else {
+        s.length = d.kind == ObjKind::Scalar ? 1 : std::max(it->second.length, 1);
+        s.fstride = t.frame_stride ? t.frame_stride : static_cast<std::int64_t>(s.length) * 16;
+    }
+    auto old = impl_->store.find(id);
+    if (old != impl_->store.end() && old->second.owned) gvxb_free(impl_->ctx, old->second.ptr);
+    impl_->store[id] = s;
+}
+
+DeviceTensor DeviceSession::tensor(ObjectId id) {
+    Impl::Store& s = impl_->ensure(id);
+    return DeviceTensor{s.ptr, s.pitch, s.fstride};
+}
+
+void DeviceSession::set_stream(void* s) { impl_->stream = s; }
+
+void DeviceSession::launch() {
+    if (impl_->scratch.size() != impl_->prog->units.size()) impl_->prepare();
+    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
+    impl_->run_all();
+    gvxb_ctx_set_stream(impl_->ctx, nullptr);
+}
+
+void DeviceSession::synchronize() {
+    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
+    std::uint32_t status = 0;
+    const int rc = gvxb_status_read(impl_->ctx, &status);
+    gvxb_ctx_set_stream(impl_->ctx, nullptr);
+    dev::check(rc, "device status");
+    if (status & GVXB_STATUS_DIV_BY_ZERO) throw Error(ErrorCode::DivByZero, "division by zero");
+    if (status & GVXB_STATUS_INDEX_RANGE) throw Error(ErrorCode::ShapeMismatch, "array index out of range");
+}
+
+void DeviceSession::upload(ObjectId id, const Buffer& b, int frame) {
+    if (!impl_->prog->objects.count(id)) return;
+    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
+    impl_->upload(id, b, frame);
+    gvxb_ctx_set_stream(impl_->ctx, nullptr);
+}
+
+Buffer DeviceSession::download(ObjectId id, int frame) {
+    if (!impl_->prog->objects.count(id)) throw Error(ErrorCode::UnknownObject, "object not produced on the device", id);
+    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
+    Buffer b = impl_->download(id, frame);
+    gvxb_ctx_set_stream(impl_->ctx, nullptr);
+    return b;
+}
+
+int DeviceSession::frames() const { return impl_->frames; }
+int DeviceSession::launches_per_run() const { return impl_->prog->launches_per_run(); }
+std::string DeviceSession::describe() const { return impl_->prog->describe(); }
+
+int device_count() {
+    int n = 0;
+    return gvxb_device_count(&n) == GVXB_OK ? n : 0;
+}
+
+} // namespace gvx

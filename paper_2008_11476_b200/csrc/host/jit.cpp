@@ -1,0 +1,773 @@
+// CUDA C generator for single abstraction nodes (generic device path).
+// See jit.hpp.  Semantics mirrored (file:line in /root/reference/proj):
+//   Value arithmetic / casts        src/expr.cpp:8-43, 351-399
+//   pixel loads / stores per format src/execute.cpp:36-109
+//   window reads, borders, masks    src/execute.cpp:233-254, 550-555
+//   point / local / median          src/execute.cpp:421-622
+//   reduce (row-major fold, arg)    src/execute.cpp:624-696
+//   histogram                       src/execute.cpp:698-727
+//   scan / scale / table            src/execute.cpp:729-843
+#include "jit.hpp"
+
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <sstream>
+
+namespace gvx::jit {
+
+namespace {
+
+// ------------------------------------------------------------------ prelude
+
+const char* kPrelude = R"CUDA(
+typedef long long i64;
+typedef unsigned long long u64;
+struct V { int r; i64 i; double f; };
+struct P { u64 f[NFIELDS]; };
+__device__ __forceinline__ V vi(i64 x) { V v; v.r = 0; v.i = x; v.f = 0.0; return v; }
+__device__ __forceinline__ V vf(double x) { V v; v.r = 1; v.i = 0; v.f = x; return v; }
+__device__ __forceinline__ double vd(V a) { return a.r ? a.f : __ll2double_rn(a.i); }
+__device__ __forceinline__ i64 vl(V a) { return a.r ? (i64)a.f : a.i; }
+__device__ __forceinline__ void raise_st(const P& p, unsigned bit) { atomicOr((unsigned*)p.f[0], bit); }
+__device__ __forceinline__ V v_add(V a, V b) { return (a.r | b.r) ? vf(__dadd_rn(vd(a), vd(b))) : vi((i64)((u64)a.i + (u64)b.i)); }
+__device__ __forceinline__ V v_sub(V a, V b) { return (a.r | b.r) ? vf(__dsub_rn(vd(a), vd(b))) : vi((i64)((u64)a.i - (u64)b.i)); }
+__device__ __forceinline__ V v_mul(V a, V b) { return (a.r | b.r) ? vf(__dmul_rn(vd(a), vd(b))) : vi((i64)((u64)a.i * (u64)b.i)); }
+__device__ __forceinline__ V v_div(const P& p, V a, V b) {
+  if (a.r | b.r) { double d = vd(b); if (d == 0.0) { raise_st(p, 1u); return vf(0.0); } return vf(__ddiv_rn(vd(a), d)); }
+  if (b.i == 0) { raise_st(p, 1u); return vi(0); }
+  if (b.i == -1) return vi((i64)(0ull - (u64)a.i));
+  return vi(a.i / b.i);
+}
+__device__ __forceinline__ V v_min(V a, V b) {
+  if (a.r | b.r) { double x = vd(a), y = vd(b); return vf(y < x ? y : x); }
+  return vi(b.i < a.i ? b.i : a.i);
+}
+__device__ __forceinline__ V v_max(V a, V b) {
+  if (a.r | b.r) { double x = vd(a), y = vd(b); return vf(x < y ? y : x); }
+  return vi(a.i < b.i ? b.i : a.i);
+}
+__device__ __forceinline__ i64 shcnt(i64 s) { return s < 0 ? 0 : (s > 63 ? 63 : s); }
+__device__ __forceinline__ V v_and(V a, V b) { return vi(a.i & b.i); }
+__device__ __forceinline__ V v_or(V a, V b) { return vi(a.i | b.i); }
+__device__ __forceinline__ V v_xor(V a, V b) { return vi(a.i ^ b.i); }
+__device__ __forceinline__ V v_shl(V a, V b) { return vi((i64)((u64)a.i << shcnt(b.i))); }
+__device__ __forceinline__ V v_shr(V a, V b) { return vi(a.i >> shcnt(b.i)); }
+__device__ __forceinline__ V v_lt(V a, V b) { return vi((a.r | b.r) ? (vd(a) < vd(b)) : (a.i < b.i)); }
+__device__ __forceinline__ V v_gt(V a, V b) { return vi((a.r | b.r) ? (vd(a) > vd(b)) : (a.i > b.i)); }
+__device__ __forceinline__ V v_eq(V a, V b) { return vi((a.r | b.r) ? (vd(a) == vd(b)) : (a.i == b.i)); }
+__device__ __forceinline__ V v_atan2(V a, V b) { return vf(atan2(vd(a), vd(b))); }
+__device__ __forceinline__ V v_not(V a) { return vi(~a.i); }
+__device__ __forceinline__ V v_neg(V a) { return a.r ? vf(-a.f) : vi((i64)(0ull - (u64)a.i)); }
+__device__ __forceinline__ V v_abs(V a) { return a.r ? vf(fabs(a.f)) : vi(a.i < 0 ? (i64)(0ull - (u64)a.i) : a.i); }
+__device__ __forceinline__ V v_sqrt(V a) { return vf(__dsqrt_rn(vd(a))); }
+// cast_value: T = 0 U8, 1 U16, 2 S16, 3 S32, 4 F32, 5 I64, 6 F64; pol 0 saturate, 1 wrap
+__device__ __forceinline__ V v_cast(V a, int t, int pol) {
+  if (t == 6) return vf(vd(a));
+  if (t == 4) return vf((double)__double2float_rn(vd(a)));
+  if (t == 5) return vi(vl(a));
+  i64 lo, hi;
+  if (t == 0) { lo = 0; hi = 255; } else if (t == 1) { lo = 0; hi = 65535; }
+  else if (t == 2) { lo = -32768; hi = 32767; } else { lo = -2147483648ll; hi = 2147483647ll; }
+  i64 x = a.i;
+  if (a.r) {
+    double r = a.f;
+    if (r != r) return vi(0);
+    if (pol == 0) {
+      if (r >= (double)hi) return vi(hi);
+      if (r <= (double)lo) return vi(lo);
+      x = llround(r);
+    } else {
+      x = (i64)fmod(trunc(r), 18446744073709551616.0);
+    }
+  }
+  if (pol == 0) return vi(x < lo ? lo : (x > hi ? hi : x));
+  u64 width = (u64)(hi - lo) + 1ull;
+  u64 low = (u64)x & (width - 1ull);
+  if (lo < 0 && low > (u64)hi) return vi((i64)low - (i64)width);
+  return vi((i64)low);
+}
+__device__ __forceinline__ V ld_val(const i64* slot) {
+  // device Value slot: [0] real flag, [1] payload (int64 or double bits)
+  return slot[0] ? vf(__longlong_as_double(slot[1])) : vi(slot[1]);
+}
+__device__ __forceinline__ void st_val(i64* slot, V v) {
+  slot[0] = v.r; slot[1] = v.r ? __double_as_longlong(v.f) : v.i;
+}
+__device__ __forceinline__ void flush_reads(const P& p, u64 rd) {
+  for (int o = 16; o > 0; o >>= 1) rd += __shfl_xor_sync(0xffffffffu, rd, o);
+  if ((threadIdx.x & 31) == 0 && threadIdx.y == 0 && rd) atomicAdd((u64*)p.f[1], rd);
+}
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+)CUDA";
+
+std::string hex_i64(std::int64_t v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "vi((i64)0x%llxull)", static_cast<unsigned long long>(v));
+    return buf;
+}
+
+std::string hex_f64(double d) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &d, 8);
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "vf(__longlong_as_double((i64)0x%llxull))", static_cast<unsigned long long>(bits));
+    return buf;
+}
+
+std::string lit(const Value& v) { return v.real ? hex_f64(v.f) : hex_i64(v.i); }
+
+int type_code(ScalarType t) { return static_cast<int>(t); }
+
+int field_in(int k) { return 5 + 3 * k; }
+
+// ------------------------------------------------------------ node emitter
+
+struct Emitter {
+    const std::vector<SlotInfo>& ins;
+    const std::vector<SlotInfo>& outs;
+    int n_in;
+
+    enum class Mode { Point, Tap, Post, Combine, Finalize, BinOf };
+    Mode mode = Mode::Point;
+    int tdx = 0, tdy = 0;
+    const LocalKernel* local = nullptr;
+    const std::vector<Value>* mask = nullptr;
+    std::ostringstream helpers; // per-slot load functions
+    std::vector<std::string> defined;
+
+    Emitter(const std::vector<SlotInfo>& i, const std::vector<SlotInfo>& o)
+        : ins(i), outs(o), n_in(static_cast<int>(i.size())) {}
+
+    std::string in_base(int slot) const {
+        std::ostringstream s;
+        s << "((const unsigned char*)p.f[" << field_in(slot) << "] + (u64)fr * p.f[" << field_in(slot) + 2 << "])";
+        return s.str();
+    }
+
+    /// Image load function name for (slot, channel, clamp flavour); emitted once.
+    std::string image_loader(int slot, Channel ch) {
+        const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
+        std::string name = "ld" + std::to_string(slot) + "_" + std::to_string(static_cast<int>(ch));
+        for (const std::string& d : defined)
+            if (d == name) return name;
+        defined.push_back(name);
+        std::ostringstream f;
+        f << "__device__ __forceinline__ V " << name << "(const P& p, int fr, int x, int y, u64& rd) {\n"
+          << "  rd++;\n  const unsigned char* row = " << in_base(slot) << " + (u64)y * p.f[" << field_in(slot) + 1
+          << "];\n";
+        switch (s.desc.format) {
+        case ImageFormat::U8: f << "  return vi(row[x]);\n"; break;
+        case ImageFormat::U16: f << "  return vi(((const unsigned short*)row)[x]);\n"; break;
+        case ImageFormat::S16: f << "  return vi(((const short*)row)[x]);\n"; break;
+        case ImageFormat::S32: f << "  return vi(((const int*)row)[x]);\n"; break;
+        case ImageFormat::F32: f << "  return vf((double)((const float*)row)[x]);\n"; break;
+        case ImageFormat::RGB: {
+            int c = ch == Channel::G ? 1 : ch == Channel::B ? 2 : 0;
+            f << "  return vi(row[3 * x + " << c << "]);\n";
+            break;
+        }
+        case ImageFormat::UYVY:
+            if (ch == Channel::U) f << "  return vi(row[4 * (x / 2)]);\n";
+            else if (ch == Channel::V) f << "  return vi(row[4 * (x / 2) + 2]);\n";
+            else f << "  return vi(row[2 * x + 1]);\n";
+            break;
+        default: throw Error(ErrorCode::BadFormat, "load from unresolved image");
+        }
+        f << "}\n";
+        helpers << f.str();
+        return name;
+    }
+
+    std::string scalar_load(int slot) const {
+        std::ostringstream s;
+        s << "ld_val((const i64*)((const unsigned char*)p.f[" << field_in(slot) << "] + (u64)fr * p.f["
+          << field_in(slot) + 2 << "]))";
+        return s.str();
+    }
+
+    /// Pointwise read of kernel slot `slot` at (x, y) expressions.
+    std::string pointwise(int slot, Channel ch, const std::string& x, const std::string& y) {
+        if (slot < 0 || slot >= n_in) throw Error(ErrorCode::TypeMismatch, "input index out of range");
+        const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
+        switch (s.kind) {
+        case SlotKind::Scalar: return scalar_load(slot);
+        case SlotKind::Image: return image_loader(slot, ch) + "(p, fr, " + x + ", " + y + ", rd)";
+        case SlotKind::None: throw Error(ErrorCode::MissingInput, "read of an unbound input slot");
+        default: throw Error(ErrorCode::TypeMismatch, "pointwise read from non-image input");
+        }
+    }
+
+    std::string array_read(int slot, const std::string& idx) {
+        if (slot < 0 || slot >= n_in) throw Error(ErrorCode::TypeMismatch, "array index out of range");
+        const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
+        if (s.kind != SlotKind::Array && s.kind != SlotKind::Matrix)
+            return "(raise_st(p, 2u), vi(0))";
+        std::ostringstream o;
+        o << "[&]() -> V { i64 at = vl(" << idx << "); u64 n = p.f[" << field_in(slot) + 1
+          << "]; if (at < 0 || (u64)at >= n) { raise_st(p, 2u); return vi(0); } return ld_val((const i64*)((const "
+             "unsigned char*)p.f["
+          << field_in(slot) << "] + (u64)fr * p.f[" << field_in(slot) + 2 << "]) + 2 * at); }()";
+        return o.str();
+    }
+
+    std::string window(const Expr& e) {
+        const int slot = e.input;
+        if (slot < 0 || slot >= n_in || ins[static_cast<std::size_t>(slot)].kind != SlotKind::Image)
+            throw Error(ErrorCode::TypeMismatch, "window read from non-image input");
+        const int ox = tdx + e.dx, oy = tdy + e.dy;
+        std::ostringstream x, y;
+        x << "(px + (" << ox << "))";
+        y << "(py + (" << oy << "))";
+        const std::string ld = image_loader(slot, e.channel);
+        std::ostringstream o;
+        if (local->boundary == BoundaryMode::Constant) {
+            o << "([&]() -> V { int xx = " << x.str() << ", yy = " << y.str()
+              << "; if (xx < 0 || yy < 0 || xx >= W || yy >= H) return " << lit(local->boundary_value)
+              << "; return " << ld << "(p, fr, xx, yy, rd); }())";
+        } else {
+            o << ld << "(p, fr, clampi(" << x.str() << ", 0, W - 1), clampi(" << y.str() << ", 0, H - 1), rd)";
+        }
+        return o.str();
+    }
+
+    std::string mask_coef(const Expr& e) const {
+        const int mw = local->window_w, mh = local->window_h;
+        const int ix = std::min(std::max(tdx + e.dx + mw / 2, 0), mw - 1);
+        const int iy = std::min(std::max(tdy + e.dy + mh / 2, 0), mh - 1);
+        const std::size_t at = static_cast<std::size_t>(iy * mw + ix);
+        if (!mask || at >= mask->size()) return "(raise_st(p, 2u), vi(0))";
+        return lit((*mask)[at]);
+    }
+
+    std::string input(const Expr& e) {
+        switch (mode) {
+        case Mode::Point:
+        case Mode::Tap:
+        case Mode::BinOf: return pointwise(e.input, e.channel, "px", "py");
+        case Mode::Post: return e.input == 0 ? "cmb" : pointwise(e.input, e.channel, "px", "py");
+        case Mode::Combine: return e.input == 0 ? "acc" : "pix";
+        case Mode::Finalize:
+            if (e.input == 0) return "acc";
+            if (e.input == 1) return "vi(cnt)";
+            return pointwise(e.input - 1, e.channel, "0", "0");
+        }
+        return "vi(0)";
+    }
+
+    int array_slot(int k) const { return mode == Mode::Finalize ? k - 1 : k; }
+
+    std::string emit(const Expr& e) {
+        switch (e.op) {
+        case ExprOp::ConstI: return hex_i64(e.ival);
+        case ExprOp::ConstF: return hex_f64(e.fval);
+        case ExprOp::InputPixel: return input(e);
+        case ExprOp::WindowPixel:
+            if (mode != Mode::Tap) throw Error(ErrorCode::TypeMismatch, "window read outside a tap body");
+            return window(e);
+        case ExprOp::MaskCoef:
+            if (mode != Mode::Tap) throw Error(ErrorCode::TypeMismatch, "mask read outside a tap body");
+            return mask_coef(e);
+        case ExprOp::ArrayAt: return array_read(array_slot(e.input), emit(*e.a));
+        case ExprOp::Select:
+            return "((" + emit(*e.a) + ").i != 0 ? (" + emit(*e.b) + ") : (" + emit(*e.c) + "))";
+        case ExprOp::Cast:
+            return "v_cast(" + emit(*e.a) + ", " + std::to_string(type_code(e.cast_to)) + ", " +
+                   std::to_string(e.policy == CastPolicy::Wrap ? 1 : 0) + ")";
+        case ExprOp::Div: return "v_div(p, " + emit(*e.a) + ", " + emit(*e.b) + ")";
+        default: break;
+        }
+        static const char* const bin[] = {"v_add", "v_sub", "v_mul", "",      "v_min", "v_max", "v_and", "v_or",
+                                          "v_xor", "v_shl", "v_shr", "v_lt",  "v_gt",  "v_eq",  "v_atan2"};
+        if (is_binary(e.op)) {
+            const int i = static_cast<int>(e.op) - static_cast<int>(ExprOp::Add);
+            return std::string(bin[i]) + "(" + emit(*e.a) + ", " + emit(*e.b) + ")";
+        }
+        static const char* const un[] = {"v_not", "v_neg", "v_abs", "v_sqrt"};
+        const int i = static_cast<int>(e.op) - static_cast<int>(ExprOp::Not);
+        return std::string(un[i]) + "(" + emit(*e.a) + ")";
+    }
+
+    /// Store statement of V `val` into output slot `o`, channel c (RGB).
+    std::string store(int o, const std::string& val, int channel, const std::string& x, const std::string& y) const {
+        const SlotInfo& s = outs[static_cast<std::size_t>(o)];
+        const int f = field_in(n_in + o);
+        std::ostringstream r;
+        r << "{ unsigned char* row = (unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2 << "] + (u64)(" << y
+          << ") * p.f[" << f + 1 << "]; V sv = " << val << "; ";
+        switch (s.desc.format) {
+        case ImageFormat::U8: r << "row[" << x << "] = (unsigned char)sv.i;"; break;
+        case ImageFormat::U16: r << "((unsigned short*)row)[" << x << "] = (unsigned short)sv.i;"; break;
+        case ImageFormat::S16: r << "((short*)row)[" << x << "] = (short)sv.i;"; break;
+        case ImageFormat::S32: r << "((int*)row)[" << x << "] = (int)sv.i;"; break;
+        case ImageFormat::F32: r << "((float*)row)[" << x << "] = (float)vd(sv);"; break;
+        case ImageFormat::RGB: r << "row[3 * (" << x << ") + " << channel << "] = (unsigned char)sv.i;"; break;
+        default: throw Error(ErrorCode::BadFormat, "store into unsupported format");
+        }
+        r << " }\n";
+        return r.str();
+    }
+
+    std::string out_slot_ptr(int o) const {
+        const int f = field_in(n_in + o);
+        return "((i64*)((unsigned char*)p.f[" + std::to_string(f) + "] + (u64)fr * p.f[" + std::to_string(f + 2) +
+               "]))";
+    }
+};
+
+std::string assemble(const Emitter& em, const std::string& body, int nfields) {
+    std::string pre = kPrelude;
+    const std::string key = "NFIELDS";
+    pre.replace(pre.find(key), key.size(), std::to_string(nfields));
+    return pre + em.helpers.str() + body;
+}
+
+const char* kPixelHead = R"CUDA(
+  const int W = (int)p.f[2], H = (int)p.f[3];
+  const int px = blockIdx.x * blockDim.x + threadIdx.x;
+  const int py = blockIdx.y * blockDim.y + threadIdx.y;
+  const int fr = blockIdx.z;
+  u64 rd = 0;
+  const bool live = px < W && py < H;
+)CUDA";
+
+// ----------------------------------------------------------------- point
+
+NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                        const std::vector<SlotInfo>& outs) {
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    for (std::size_t i = 0; i < ins.size(); ++i)
+        if (ins[i].kind == SlotKind::Image) {
+            prog.dims_from = static_cast<int>(i);
+            break;
+        }
+    Emitter em(ins, outs);
+    em.mode = Emitter::Mode::Point;
+    std::ostringstream b;
+    const PointKernel& pk = k.point();
+    for (std::size_t o = 0; o < pk.outputs.size() && o < outs.size(); ++o) {
+        if (outs[o].kind != SlotKind::Image) continue;
+        const auto& bodies = pk.outputs[o].channel_bodies;
+        if (bodies.size() == 3 && outs[o].desc.format == ImageFormat::RGB) {
+            for (int c = 0; c < 3; ++c) b << "  " << em.store(static_cast<int>(o), em.emit(*bodies[static_cast<std::size_t>(c)]), c, "px", "py");
+        } else {
+            b << "  " << em.store(static_cast<int>(o), em.emit(*bodies[0]), 0, "px", "py");
+        }
+    }
+    KernelSpec ks;
+    ks.name = "gvx_point";
+    std::ostringstream src;
+    src << "extern \"C\" __global__ void gvx_point(const P p) {" << kPixelHead << "  if (live) {\n"
+        << b.str() << "  }\n  flush_reads(p, rd);\n}\n";
+    ks.source = assemble(em, src.str(), prog.fields());
+    prog.kernels.push_back(std::move(ks));
+    return prog;
+}
+
+// ----------------------------------------------------------------- local
+
+NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                        const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values) {
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = -1; // output 0 dims (exec_local iterates the output)
+    const LocalKernel& lk = k.local();
+    Emitter em(ins, outs);
+    em.local = &lk;
+    em.mask = lk.mask.empty() ? &matrix_values : &lk.mask;
+    const int hw = lk.window_w / 2, hh = lk.window_h / 2;
+    const ScalarType out_t = scalar_of(outs.at(0).desc.format);
+
+    std::ostringstream b;
+    if (lk.boundary == BoundaryMode::Undefined) {
+        b << "    if (px < " << hw << " || py < " << hh << " || px >= W - " << hw << " || py >= H - " << hh << ") {\n"
+          << "      " << em.store(0, "v_cast(vi(0), " + std::to_string(type_code(out_t)) + ", 0)", 0, "px", "py")
+          << "      goto done;\n    }\n";
+    }
+    em.mode = Emitter::Mode::Tap;
+    if (lk.median3x3) {
+        b << "    V t[9];\n";
+        int idx = 0;
+        for (int dy = -hh; dy <= hh; ++dy)
+            for (int dx = -hw; dx <= hw; ++dx) {
+                em.tdx = dx;
+                em.tdy = dy;
+                b << "    t[" << idx++ << "] = " << em.emit(*lk.tap_body) << ";\n";
+            }
+        b << "    {\n      auto s2 = [](V& a, V& c) { bool sw = (a.r | c.r) ? vd(a) > vd(c) : a.i > c.i; if (sw) { V "
+             "tmp = a; a = c; c = tmp; } };\n"
+             "      s2(t[1], t[2]); s2(t[4], t[5]); s2(t[7], t[8]); s2(t[0], t[1]); s2(t[3], t[4]); s2(t[6], t[7]);\n"
+             "      s2(t[1], t[2]); s2(t[4], t[5]); s2(t[7], t[8]); s2(t[0], t[3]); s2(t[5], t[8]); s2(t[4], t[7]);\n"
+             "      s2(t[3], t[6]); s2(t[1], t[4]); s2(t[2], t[5]); s2(t[4], t[7]); s2(t[4], t[2]); s2(t[6], t[4]);\n"
+             "      s2(t[4], t[2]);\n    }\n    V cmb = t[4];\n";
+    } else {
+        const char* comb = lk.combine == CombineMode::Sum ? "v_add" : lk.combine == CombineMode::Min ? "v_min" : "v_max";
+        bool first = true;
+        for (int dy = -hh; dy <= hh; ++dy)
+            for (int dx = -hw; dx <= hw; ++dx) {
+                em.tdx = dx;
+                em.tdy = dy;
+                const std::string v = em.emit(*lk.tap_body);
+                if (first) {
+                    b << "    V cmb = " << v << ";\n";
+                    first = false;
+                } else {
+                    b << "    cmb = " << comb << "(cmb, " << v << ");\n";
+                }
+            }
+    }
+    em.tdx = em.tdy = 0;
+    if (lk.post_body) {
+        em.mode = Emitter::Mode::Post;
+        b << "    " << em.store(0, em.emit(*lk.post_body), 0, "px", "py");
+    } else {
+        b << "    " << em.store(0, "cmb", 0, "px", "py");
+    }
+    KernelSpec ks;
+    ks.name = "gvx_local";
+    std::ostringstream src;
+    src << "extern \"C\" __global__ void gvx_local(const P p) {" << kPixelHead << "  if (live) {\n"
+        << b.str() << "  }\n" << (lk.boundary == BoundaryMode::Undefined ? "done:\n" : "")
+        << "  flush_reads(p, rd);\n}\n";
+    ks.source = assemble(em, src.str(), prog.fields());
+    prog.kernels.push_back(std::move(ks));
+    return prog;
+}
+
+// ---------------------------------------------------------------- reduce
+
+bool refs_slot(const Expr& e, int slot) {
+    if (e.op == ExprOp::InputPixel && e.input == slot) return true;
+    for (const ExprPtr* c : {&e.a, &e.b, &e.c})
+        if (*c && refs_slot(**c, slot)) return true;
+    return false;
+}
+
+bool has_real(const Expr& e) {
+    if (e.op == ExprOp::ConstF || e.op == ExprOp::Sqrt || e.op == ExprOp::Atan2) return true;
+    if (e.op == ExprOp::Cast && (e.cast_to == ScalarType::F32 || e.cast_to == ScalarType::F64)) return true;
+    for (const ExprPtr* c : {&e.a, &e.b, &e.c})
+        if (*c && has_real(**c)) return true;
+    return false;
+}
+
+bool has_select_or_div(const Expr& e) {
+    if (e.op == ExprOp::Select || e.op == ExprOp::Div || e.op == ExprOp::ArrayAt) return true;
+    for (const ExprPtr* c : {&e.a, &e.b, &e.c})
+        if (*c && has_select_or_div(**c)) return true;
+    return false;
+}
+
+NodeProgram lower_reduce(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                         const std::vector<SlotInfo>& outs) {
+    const ReduceKernel& rk = k.reduce();
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = 0;
+    if (ins.empty() || ins[0].kind != SlotKind::Image) throw Error(ErrorCode::TypeMismatch, "reduce needs an image");
+    const bool pixel_real = ins[0].desc.format == ImageFormat::F32;
+    Emitter em(ins, outs);
+    const std::string ldpix = em.image_loader(0, Channel::C0);
+
+    // Parallel forms (exact): integer sum of f(pixel) with init, and
+    // seeded min/max (optionally tracking the first arg).
+    const Expr& c = *rk.combine;
+    bool par_sum = false, par_min = false, par_max = false;
+    const Expr* term = nullptr;
+    if (!rk.seed_first && !rk.init.real && !pixel_real && c.op == ExprOp::Add && rk.track == ReduceKernel::Track::None) {
+        const Expr *l = c.a.get(), *r = c.b.get();
+        if (l->op == ExprOp::InputPixel && l->input == 0 && !refs_slot(*r, 0) && !has_real(*r) && !has_select_or_div(*r))
+            term = r;
+        else if (r->op == ExprOp::InputPixel && r->input == 0 && !refs_slot(*l, 0) && !has_real(*l) &&
+                 !has_select_or_div(*l))
+            term = l;
+        par_sum = term != nullptr;
+    }
+    if (rk.seed_first && !pixel_real && (c.op == ExprOp::Min || c.op == ExprOp::Max)) {
+        const Expr *l = c.a.get(), *r = c.b.get();
+        const bool args = l->op == ExprOp::InputPixel && r->op == ExprOp::InputPixel &&
+                          ((l->input == 0 && r->input == 1) || (l->input == 1 && r->input == 0));
+        if (args) {
+            if (c.op == ExprOp::Min && rk.track != ReduceKernel::Track::ArgMax) par_min = true;
+            if (c.op == ExprOp::Max && rk.track != ReduceKernel::Track::ArgMin) par_max = true;
+        }
+    }
+    // scratch per frame: [0..1] acc Value, [2] packed key / flag, [3] arg index
+    prog.scratch_bytes_per_frame = 64;
+    const std::string scratch = "((i64*)((unsigned char*)p.f[" + std::to_string(prog.fields() - 2) +
+                                "] + (u64)fr * p.f[" + std::to_string(prog.fields() - 1) + "]))";
+
+    std::ostringstream src;
+    if (par_sum) {
+        em.mode = Emitter::Mode::Combine;
+        std::string t = em.emit(*term);
+        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {" << kPixelHead
+            << "  i64 part = 0;\n  if (live) { V pix = " << ldpix << "(p, fr, px, py, rd); V acc = vi(0); (void)acc; part = vl("
+            << t << "); }\n"
+            << "  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);\n"
+            << "  if ((threadIdx.x & 31) == 0 && part) atomicAdd((u64*)(" << scratch << " + 1), (u64)part);\n"
+            << "  flush_reads(p, rd);\n}\n";
+    } else if (par_min || par_max) {
+        // key: (biased value, linear index) packed so that atomicMin picks the
+        // extreme value and, among equals, the first row-major position
+        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {" << kPixelHead
+            << "  u64 key = ~0ull;\n  if (live) { V pix = " << ldpix
+            << "(p, fr, px, py, rd); u64 b = (u64)(pix.i + 2147483648ll);\n"
+            << (par_min ? "    u64 kv = b;\n" : "    u64 kv = 0xFFFFFFFFull - b;\n")
+            << "    key = (kv << 32) | (u64)(py * (u64)W + px); }\n"
+            << "  for (int o = 16; o > 0; o >>= 1) { u64 q = __shfl_xor_sync(0xffffffffu, key, o); key = q < key ? q : "
+               "key; }\n"
+            << "  if ((threadIdx.x & 31) == 0 && key != ~0ull) atomicMin((u64*)(" << scratch << " + 2), key);\n"
+            << "  flush_reads(p, rd);\n}\n";
+    } else {
+        // exact row-major fold on one thread (general user combine bodies)
+        em.mode = Emitter::Mode::Combine;
+        std::string body = em.emit(c);
+        const char* cmp = rk.track == ReduceKernel::Track::ArgMin ? "<" : ">";
+        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {\n"
+            << "  const int W = (int)p.f[2], H = (int)p.f[3]; const int fr = blockIdx.z; u64 rd = 0;\n"
+            << "  if (threadIdx.x != 0 || threadIdx.y != 0) return;\n"
+            << "  V acc = " << lit(rk.init) << "; bool seeded = " << (rk.seed_first ? "false" : "true")
+            << "; int ax = 0, ay = 0;\n"
+            << "  for (int py = 0; py < H; ++py) for (int px = 0; px < W; ++px) {\n"
+            << "    V pix = " << ldpix << "(p, fr, px, py, rd);\n"
+            << "    if (!seeded) { acc = pix; seeded = true; ax = px; ay = py; continue; }\n";
+        if (rk.track != ReduceKernel::Track::None)
+            src << "    { bool better = (pix.r | acc.r) ? vd(pix) " << cmp << " vd(acc) : pix.i " << cmp
+                << " acc.i; if (better) { ax = px; ay = py; } }\n";
+        src << "    acc = " << body << ";\n  }\n"
+            << "  st_val(" << scratch << ", acc); " << scratch << "[2] = ax; " << scratch << "[3] = ay;\n"
+            << "  atomicAdd((u64*)p.f[1], rd);\n}\n";
+    }
+
+    // finalize: one thread per frame
+    std::ostringstream fin;
+    fin << "extern \"C\" __global__ void gvx_reduce_final(const P p) {\n"
+        << "  const int W = (int)p.f[2], H = (int)p.f[3]; const int fr = blockIdx.z; u64 rd = 0; (void)rd;\n"
+        << "  if (threadIdx.x != 0) return;\n  const i64 cnt = (i64)W * H;\n  const int px = 0, py = 0; (void)px; (void)py;\n"
+        << "  V acc; int ax = 0, ay = 0;\n";
+    if (par_sum) {
+        fin << "  acc = vi((i64)((u64)" << rk.init.i << "ll + (u64)" << scratch << "[1]));\n";
+    } else if (par_min || par_max) {
+        fin << "  { u64 key = (u64)" << scratch << "[2]; u64 kv = key >> 32; i64 v = "
+            << (par_min ? "(i64)kv" : "(i64)(0xFFFFFFFFull - kv)") << " - 2147483648ll; u64 li = key & 0xFFFFFFFFull;\n"
+            << "    if (key == ~0ull) { v = 0; li = 0; }\n"
+            << "    acc = vi(v); ax = (int)(li % (u64)W); ay = (int)(li / (u64)W); }\n";
+    } else {
+        fin << "  acc = ld_val(" << scratch << "); ax = (int)" << scratch << "[2]; ay = (int)" << scratch << "[3];\n";
+    }
+    if (rk.finalize) {
+        em.mode = Emitter::Mode::Finalize;
+        fin << "  V res = " << em.emit(*rk.finalize) << ";\n";
+    } else {
+        fin << "  V res = acc;\n";
+    }
+    fin << "  if (p.f[" << field_in(prog.n_inputs) << "]) st_val(" << em.out_slot_ptr(0) << ", res);\n";
+    if (outs.size() > 1 && rk.track != ReduceKernel::Track::None)
+        fin << "  if (p.f[" << field_in(prog.n_inputs + 1) << "]) { i64* l = " << em.out_slot_ptr(1)
+            << "; st_val(l, vi(ax)); st_val(l + 2, vi(ay)); }\n";
+    fin << "  if (rd) atomicAdd((u64*)p.f[1], rd);\n}\n";
+
+    // init kernel: clear scratch (sum / key) per frame
+    std::ostringstream init;
+    init << "extern \"C\" __global__ void gvx_reduce_init(const P p) {\n  const int fr = blockIdx.z;\n"
+         << "  if (threadIdx.x == 0) { i64* s = " << scratch << "; s[0] = 0; s[1] = 0; s[2] = -1; s[3] = 0; }\n}\n";
+
+    KernelSpec k0, k1, k2;
+    k0.name = "gvx_reduce_init";
+    k0.grid = KernelSpec::Grid::Single;
+    k1.name = "gvx_reduce_part";
+    k1.grid = (par_sum || par_min || par_max) ? KernelSpec::Grid::Pixels : KernelSpec::Grid::Single;
+    k2.name = "gvx_reduce_final";
+    k2.grid = KernelSpec::Grid::Single;
+    const std::string all = assemble(em, init.str() + src.str() + fin.str(), prog.fields());
+    k0.source = all;
+    prog.kernels = {k0, k1, k2};
+    return prog;
+}
+
+// -------------------------------------------------------------- histogram
+
+NodeProgram lower_histogram(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                            const std::vector<SlotInfo>& outs) {
+    const HistogramKernel& hk = k.histogram();
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = 0;
+    Emitter em(ins, outs);
+    em.mode = Emitter::Mode::BinOf;
+    const std::string bin = em.emit(*hk.bin_of);
+    std::ostringstream src;
+    src << "extern \"C\" __global__ void gvx_hist_clear(const P p) {\n  const int fr = blockIdx.z;\n"
+        << "  i64* o = " << em.out_slot_ptr(0) << ";\n  for (int b = threadIdx.x; b < " << hk.bins
+        << "; b += blockDim.x) { o[2 * b] = 0; o[2 * b + 1] = 0; }\n}\n"
+        << "extern \"C\" __global__ void gvx_hist(const P p) {" << kPixelHead
+        << "  if (live) { i64 b = vl(" << bin << "); if (b >= 0 && b < " << hk.bins << ") atomicAdd((u64*)(" << em.out_slot_ptr(0)
+        << " + 2 * b + 1), 1ull); }\n  flush_reads(p, rd);\n}\n";
+    KernelSpec k0, k1;
+    k0.name = "gvx_hist_clear";
+    k0.grid = KernelSpec::Grid::Single;
+    k0.block_x = 256;
+    k1.name = "gvx_hist";
+    k0.source = assemble(em, src.str(), prog.fields());
+    prog.kernels = {k0, k1};
+    return prog;
+}
+
+// ------------------------------------------------------------------ scan
+
+NodeProgram lower_scan(const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs) {
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = 0;
+    prog.counts_reads = false;
+    Emitter em(ins, outs);
+    const long long px = static_cast<long long>(ins.at(0).desc.width) * ins.at(0).desc.height;
+    const bool parallel = px * 255 <= 2147483647LL; // no S32 saturation possible
+    const std::string inb = em.in_base(0);
+    const int of = field_in(prog.n_inputs);
+    std::ostringstream src;
+    src << "__device__ __forceinline__ int* orow(const P& p, int fr, int y) { return (int*)((unsigned char*)p.f[" << of
+        << "] + (u64)fr * p.f[" << of + 2 << "] + (u64)y * p.f[" << of + 1 << "]); }\n"
+        << "__device__ __forceinline__ int irow(const P& p, int fr, int y, int x) { return (" << inb
+        << " + (u64)y * p.f[" << field_in(0) + 1 << "])[x]; }\n";
+    if (parallel) {
+        src << "extern \"C\" __global__ void gvx_scan_rows(const P p) {\n"
+            << "  const int W = (int)p.f[2], H = (int)p.f[3]; const int fr = blockIdx.z;\n"
+            << "  const int y = blockIdx.x * blockDim.x + threadIdx.x; if (y >= H) return;\n"
+            << "  int s = 0; int* o = orow(p, fr, y); for (int x = 0; x < W; ++x) { s += irow(p, fr, y, x); o[x] = s; }\n}\n"
+            << "extern \"C\" __global__ void gvx_scan_cols(const P p) {\n"
+            << "  const int W = (int)p.f[2], H = (int)p.f[3]; const int fr = blockIdx.z;\n"
+            << "  const int x = blockIdx.x * blockDim.x + threadIdx.x; if (x >= W) return;\n"
+            << "  int s = 0; for (int y = 0; y < H; ++y) { int* o = orow(p, fr, y); s += o[x]; o[x] = s; }\n}\n";
+        KernelSpec a, b;
+        a.name = "gvx_scan_rows";
+        a.grid = KernelSpec::Grid::Rows;
+        a.block_x = 128;
+        a.block_y = 1;
+        b.name = "gvx_scan_cols";
+        b.grid = KernelSpec::Grid::Cols;
+        b.block_x = 128;
+        b.block_y = 1;
+        a.source = assemble(em, src.str(), prog.fields());
+        prog.kernels = {a, b};
+    } else {
+        // the reference recurrence with S32 saturation at every step
+        src << "extern \"C\" __global__ void gvx_scan_seq(const P p) {\n"
+            << "  const int W = (int)p.f[2], H = (int)p.f[3]; const int fr = blockIdx.z; if (threadIdx.x) return;\n"
+            << "  for (int y = 0; y < H; ++y) for (int x = 0; x < W; ++x) {\n"
+            << "    i64 v = irow(p, fr, y, x);\n"
+            << "    if (x > 0) v += orow(p, fr, y)[x - 1];\n    if (y > 0) v += orow(p, fr, y - 1)[x];\n"
+            << "    if (x > 0 && y > 0) v -= orow(p, fr, y - 1)[x - 1];\n"
+            << "    orow(p, fr, y)[x] = (int)(v < -2147483648ll ? -2147483648ll : (v > 2147483647ll ? 2147483647ll : v));\n"
+            << "  }\n}\n";
+        KernelSpec a;
+        a.name = "gvx_scan_seq";
+        a.grid = KernelSpec::Grid::Single;
+        a.source = assemble(em, src.str(), prog.fields());
+        prog.kernels = {a};
+    }
+    return prog;
+}
+
+// ----------------------------------------------------------------- scale
+
+NodeProgram lower_scale(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                        const std::vector<SlotInfo>& outs) {
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = -1; // output dims
+    prog.counts_reads = false;
+    Emitter em(ins, outs);
+    const std::string ld = em.image_loader(0, Channel::C0);
+    const ResolvedDesc& sd = ins.at(0).desc;
+    const ScalarType t = scalar_of(outs.at(0).desc.format);
+    std::ostringstream src;
+    src << "extern \"C\" __global__ void gvx_scale(const P p) {" << kPixelHead
+        << "  const int sw = " << sd.width << ", sh = " << sd.height << ";\n"
+        << "  if (live) {\n"
+        << "    double yin = __dsub_rn(__ddiv_rn(__dmul_rn((double)py + 0.5, (double)sh), (double)H), 0.5);\n"
+        << "    double xin = __dsub_rn(__ddiv_rn(__dmul_rn((double)px + 0.5, (double)sw), (double)W), 0.5);\n"
+        << "    V v;\n";
+    if (k.scale().interp == InterpMode::Nearest) {
+        src << "    int xi = clampi((int)floor(__dadd_rn(xin, 0.5)), 0, sw - 1);\n"
+            << "    int yi = clampi((int)floor(__dadd_rn(yin, 0.5)), 0, sh - 1);\n"
+            << "    v = " << ld << "(p, fr, xi, yi, rd);\n";
+    } else {
+        src << "    int x0 = clampi((int)floor(xin), 0, sw - 1), y0 = clampi((int)floor(yin), 0, sh - 1);\n"
+            << "    int x1 = min(x0 + 1, sw - 1), y1 = min(y0 + 1, sh - 1);\n"
+            << "    double fx = fmin(fmax(__dsub_rn(xin, (double)x0), 0.0), 1.0);\n"
+            << "    double fy = fmin(fmax(__dsub_rn(yin, (double)y0), 0.0), 1.0);\n"
+            << "    double p00 = vd(" << ld << "(p, fr, x0, y0, rd)), p10 = vd(" << ld << "(p, fr, x1, y0, rd));\n"
+            << "    double p01 = vd(" << ld << "(p, fr, x0, y1, rd)), p11 = vd(" << ld << "(p, fr, x1, y1, rd));\n"
+            << "    double gx = __dsub_rn(1.0, fx), gy = __dsub_rn(1.0, fy);\n"
+            << "    double r = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(p00, gx), gy), "
+               "__dmul_rn(__dmul_rn(p10, fx), gy)), __dmul_rn(__dmul_rn(p01, gx), fy)), __dmul_rn(__dmul_rn(p11, fx), fy));\n"
+            << "    v = vf(r);\n";
+    }
+    src << "    " << em.store(0, "v_cast(v, " + std::to_string(type_code(t)) + ", 0)", 0, "px", "py") << "  }\n}\n";
+    KernelSpec ks;
+    ks.name = "gvx_scale";
+    ks.grid = KernelSpec::Grid::OutPixels;
+    ks.source = assemble(em, src.str(), prog.fields());
+    prog.kernels = {ks};
+    return prog;
+}
+
+// ----------------------------------------------------------------- table
+
+NodeProgram lower_table(const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs) {
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.counts_reads = false;
+    Emitter em(ins, outs);
+    std::ostringstream src;
+    src << "extern \"C\" __global__ void gvx_table(const P p) {\n  const int fr = blockIdx.z; if (threadIdx.x) return;\n"
+        << "  const i64* h = (const i64*)((const unsigned char*)p.f[" << field_in(0) << "] + (u64)fr * p.f[" << field_in(0) + 2
+        << "]);\n  const int n = (int)p.f[" << field_in(0) + 1 << "];\n"
+        << "  i64* o = " << em.out_slot_ptr(0) << ";\n"
+        << "  i64 total = 0; for (int i = 0; i < n; ++i) total += h[2 * i + 1];\n"
+        << "  i64 run = 0, cmin = 0; bool found = false;\n"
+        << "  for (int i = 0; i < n; ++i) { run += h[2 * i + 1]; if (!found && h[2 * i + 1] > 0) { cmin = run; found = true; } }\n"
+        << "  run = 0;\n"
+        << "  for (int i = 0; i < n; ++i) {\n    run += h[2 * i + 1]; i64 v;\n"
+        << "    if (!found || total == cmin) v = i;\n"
+        << "    else v = llround(__ddiv_rn(__dmul_rn(255.0, __ll2double_rn(run - cmin)), __ll2double_rn(total - cmin)));\n"
+        << "    v = v < 0 ? 0 : (v > 255 ? 255 : v);\n    st_val(o + 2 * i, vi(v));\n  }\n}\n";
+    KernelSpec ks;
+    ks.name = "gvx_table";
+    ks.grid = KernelSpec::Grid::Single;
+    ks.source = assemble(em, src.str(), prog.fields());
+    prog.kernels = {ks};
+    return prog;
+}
+
+} // namespace
+
+NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                       const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values) {
+    NodeProgram p;
+    switch (k.kind) {
+    case AbstractionKind::Point: p = lower_point(k, ins, outs); break;
+    case AbstractionKind::Local: p = lower_local(k, ins, outs, matrix_values); break;
+    case AbstractionKind::Reduce: p = lower_reduce(k, ins, outs); break;
+    case AbstractionKind::Histogram: p = lower_histogram(k, ins, outs); break;
+    case AbstractionKind::Scan: p = lower_scan(ins, outs); break;
+    case AbstractionKind::Scale: p = lower_scale(k, ins, outs); break;
+    case AbstractionKind::Table: p = lower_table(ins, outs); break;
+    }
+    // every kernel of a node shares one source (one NVRTC module)
+    for (std::size_t i = 1; i < p.kernels.size(); ++i)
+        if (p.kernels[i].source.empty()) p.kernels[i].source = p.kernels[0].source;
+    return p;
+}
+
+} // namespace gvx::jit

@@ -1,0 +1,62 @@
+// Generic device path: CUDA C emitted from the expression IR of one
+// abstraction node and compiled with NVRTC for sm_100a (gvxb_jit_*).
+//
+// Replaces the reference's per-pixel stack VM (CompiledExpr::run,
+// ref:src/expr.cpp:486-519) and the Engine::exec_* loops
+// (ref:src/execute.cpp:421-760) for every node that the hand-written fused
+// kernels do not cover, and for run_naive.  The emitted code evaluates the
+// same tagged int64/double Value semantics (Select stays lazy, casts follow
+// cast_value, no FMA contraction: NVRTC runs with --fmad=false), and counts
+// pixel-read events exactly like NodeEnv does.
+#pragma once
+
+#include "graphvx/kernel.hpp"
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace gvx::jit {
+
+/// What a kernel slot is bound to at run time.
+enum class SlotKind : std::uint8_t { Image, Scalar, Array, Matrix, None };
+
+struct SlotInfo {
+    SlotKind kind = SlotKind::None;
+    ResolvedDesc desc;
+    bool is_dist = false; ///< array holding a histogram distribution
+};
+
+/// One device kernel to launch: NVRTC source + launch geometry.  The single
+/// kernel argument is a struct of `nfields` 8-byte fields laid out as the
+/// host Binder fills them (see execute.cpp).
+struct KernelSpec {
+    std::string name;
+    std::string source;
+    enum class Grid : std::uint8_t { Pixels, OutPixels, Single, Rows, Cols } grid = Grid::Pixels;
+    int block_x = 32, block_y = 8;
+};
+
+/// A node lowered to one or more generated kernels.
+struct NodeProgram {
+    std::vector<KernelSpec> kernels;
+    // field layout of the parameter block:
+    //  [0] status*  [1] read counter*  [2] W  [3] H  [4] frame count
+    //  then per input slot k: 3 fields (ptr, pitch/len, frame stride)
+    //  then per output slot o: 3 fields
+    //  then scratch fields (scratch pointer, scratch stride)
+    int n_inputs = 0;
+    int n_outputs = 0;
+    std::size_t scratch_bytes_per_frame = 0; ///< device scratch needed
+    bool counts_reads = true;
+    int dims_from = -1; ///< input slot giving W/H (-1 = output 0)
+    int fields() const { return 5 + 3 * (n_inputs + n_outputs) + 2; }
+};
+
+/// Lowers one abstraction node.  `ins` / `outs` describe the bound objects
+/// per INPUT / OUTPUT parameter (None when unbound).  Mask values of a
+/// matrix-driven local are taken from `matrix_values` (baked as constants).
+NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                       const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values);
+
+} // namespace gvx::jit
