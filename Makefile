@@ -20,7 +20,7 @@ HOST_OBJ  := $(patsubst $(PKG)/csrc/host/%.cpp,build/host/%.o,$(HOST_SRC))
 CAPI_SRC  := $(wildcard $(PKG)/csrc/capi/*.cpp)
 CAPI_OBJ  := $(patsubst $(PKG)/csrc/capi/%.cpp,build/capi/%.o,$(CAPI_SRC))
 
-all: $(LIB)/libgvx_cuda.so $(LIB)/libgraphvx.so
+all: $(LIB)/libgvx_cuda.so $(LIB)/libgraphvx.so tests/cpp/bin/test_graphvx
 
 build/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(wildcard $(PKG)/csrc/cuda/*.cuh) include/gvxb.h
 	@mkdir -p build/cuda
@@ -46,3 +46,11 @@ clean:
 	rm -rf build $(LIB)/*.so
 
 .PHONY: all clean
+
+# C++ API / fusion tests (doctest stand-in); pytest runs them
+tests/cpp/bin/test_graphvx: tests/cpp/test_graphvx.cpp tests/cpp/doctest.h $(LIB)/libgraphvx.so $(PKG)/csrc/configs/config_graphs.hpp
+	@mkdir -p tests/cpp/bin
+	$(CXX) -std=c++20 -O1 -Iinclude -Itests/cpp $< -o $@ -L$(LIB) -lgraphvx -Wl,-rpath,'$$ORIGIN/../../../$(LIB)'
+
+tests: tests/cpp/bin/test_graphvx
+.PHONY: tests

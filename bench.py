@@ -1,0 +1,494 @@
+#!/usr/bin/env python
+"""graphvx-b200 benchmark (driver contract, see task README / DESIGN.md §6).
+
+Default workload = BASELINE.json configs[1]: the Harris corner graph on
+3840x2160 U8 frames, executed through the optimized plan (fused sm_100a
+kernel) on device-resident frame batches.  One *step* = one graph execution
+over a batch of `--frames` frames.  Inputs rotate over two batches
+(footprint > L2).  `--config k` selects another BASELINE config (1..5);
+config 5 (16384^2 edge graph) runs as row bands with NVLink halo exchange
+when launched with N > 1 ranks.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference CPU
+engine (oracle/_ref, built unmodified from the reference sources) on bounded
+samples of the same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG_NAME = {
+    1: "Gaussian3x3->Sobel3x3->Magnitude 1920x1080 U8",
+    2: "Harris corners (Sobel, Ixx/Iyy/Ixy, Box3x3, F32 response, threshold) 3840x2160 U8",
+    3: "Unsharp mask with user-defined 5x5 local node 7680x4320 U8",
+    4: "Gaussian5x5 (Convolve) -> ConvertDepth -> Histogram + MeanStdDev, 4K frames",
+    5: "Gaussian3x3->Sobel3x3->Magnitude 16384x16384 U8, row bands + halo exchange",
+}
+# algorithmic HBM bytes per output pixel of the fused program
+ALGO_BYTES = {1: 3, 2: 2, 3: 2, 4: 1, 5: 3}
+KERNEL_NAME = {1: "edge_kernel", 2: "harris_kernel", 3: "stencil_point_kernel", 4: "conv_stats_kernel",
+               5: "edge_kernel"}
+DEFAULT_FRAMES = {1: 16, 2: 8, 3: 2, 4: 16, 5: 1}
+CPU_SAMPLE = {1: (1920, 1080), 2: (3840, 544), 3: (7680, 272), 4: (3840, 544), 5: (16384, 128)}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(cfg):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        return data.get(str(cfg))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, device: int):
+        self.device, self.samples, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- CPU legs
+
+def cpu_reference_run(cfg, steps, warmup):
+    """Reference CPU engine on bounded samples of the workload (all host threads)."""
+    import oracle
+    kind = "reference" if oracle.have_ref() else "port"
+    w, h = CPU_SAMPLE[cfg]
+    img = oracle.ref_random_u8(w, h, cfg) if kind == "reference" else None
+    if img is None:
+        import paper_2008_11476_b200 as gvx
+        img = gvx.random_u8(w, h, cfg)
+    ncpu = os.cpu_count() or 1
+    workers = max(1, ncpu // 4) if kind == "reference" else ncpu  # the reference engine uses <= 4 threads
+
+    def one(_):
+        if kind == "reference":
+            oracle.ref_run(cfg, img)
+        else:
+            oracle.port_run(cfg, img)
+
+    with ThreadPoolExecutor(workers) as ex:
+        for _ in range(warmup):
+            list(ex.map(one, range(workers)))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            list(ex.map(one, range(workers)))
+        dt = time.perf_counter() - t0
+    px = w * h * workers * steps
+    return {"value": px / dt / 1e6, "unit": "Mpixel/s", "cores": min(ncpu, 4 * workers) if kind == "reference" else ncpu,
+            "kind": kind, "sample": f"{workers} concurrent x {w}x{h} crop(s) of config {cfg} per step, {steps} steps",
+            "seconds": dt}
+
+
+def cpu_baseline_leg(cfg):
+    """~10-30 s of reference CPU work on one bounded sample (rank 0, N=1)."""
+    import oracle
+    kind = "reference" if oracle.have_ref() else "port"
+    w, h = CPU_SAMPLE[cfg]
+    if cfg in (1,):
+        w, h = 1920, 1080
+    import paper_2008_11476_b200 as gvx
+    img = gvx.random_u8(w, h, cfg)
+    reps, t_total = 0, 0.0
+    while t_total < 10.0 and reps < 50:
+        t0 = time.perf_counter()
+        if kind == "reference":
+            oracle.ref_run(cfg, img)
+        else:
+            oracle.port_run(cfg, img)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    return {"value": w * h * reps / t_total / 1e6, "unit": "Mpixel/s",
+            "cores": min(4, os.cpu_count() or 1) if kind == "reference" else 1, "kind": kind,
+            "sample": f"{reps} run_naive call(s) on a {w}x{h} crop of config {cfg} (reference uses <=4 threads)",
+            "seconds": round(t_total, 3)}
+
+
+# ------------------------------------------------------------------ GPU legs
+
+def make_frames(gvx, w, h, n, seed):
+    base = gvx.random_u8(w, h, seed)
+    frames = [base]
+    for i in range(1, n):
+        frames.append(np.roll(base, shift=(i * 7919) % (w * h)).reshape(h, w) ^ np.uint8((i * 37) & 0xFF))
+    return np.stack(frames)
+
+
+def run_frames(args, cfg, rank, world, local_rank):
+    import paper_2008_11476_b200 as gvx
+    w, h = gvx.CONFIG_SIZE[cfg]
+    F = args.frames or DEFAULT_FRAMES[cfg]
+    dev = gvx.Device(local_rank)
+    graph = gvx.ConfigGraph(cfg, w, h, True)
+    sess = gvx.Session(graph, frames=F)
+    sess.set_stream(dev.stream)
+    pitch = (w + 127) // 128 * 128
+    in_bytes = pitch * h * F
+    out_pitch = pitch * (2 if cfg in (1, 5) else 1)
+    pools = []
+    host = make_frames(gvx, w, h, F, gvx.CONFIG_SEED[cfg] + 97 * rank)
+    for b in range(2):
+        din = dev.alloc(in_bytes)
+        for f in range(F):
+            dev.upload(din + f * pitch * h, pitch, np.roll(host[f], b * 13, axis=1))
+        dout = dev.alloc(out_pitch * h * F) if cfg != 4 else None
+        pools.append((din, dout))
+    # cfg4 outputs (histogram / mean / stddev) stay session-owned value slots
+
+    def bind(b):
+        din, dout = pools[b]
+        sess.bind(0, din, pitch, pitch * h)
+        if dout is not None:
+            sess.bind(1, dout, out_pitch, out_pitch * h)
+
+    for i in range(args.warmup):
+        bind(i % 2)
+        sess.launch()
+    sess.sync()
+    # correctness spot check of frame 0 of the first batch against the oracle port
+    checked = None
+    if rank == 0 and not args.no_check and cfg in (1, 2, 3, 4) and w * h <= 9_000_000:
+        import oracle
+        bind(0)
+        sess.launch()
+        sess.sync()
+        got = sess.download(0)
+        want = oracle.port_run(cfg, np.roll(host[0], 0, axis=1))
+        checked = bool((got[0] == want[0]).all() and got[1] == want[1] and got[2] == want[2]) if cfg == 4 \
+            else bool((got == want).all())
+
+    ev = [dev.event() for _ in range(2)]
+    barrier()
+    dev.sync()
+    with ClockSampler(local_rank) as clk:
+        # identical load for ~1 s so nvidia-smi samples clocks under load
+        # (the sampler runs across this window and the timed region)
+        t_end = time.perf_counter() + args.clock_window
+        i = 0
+        while time.perf_counter() < t_end:
+            bind(i % 2)
+            sess.launch()
+            i += 1
+            if i % 50 == 0:
+                dev.sync()
+        dev.sync()
+        launches0 = gvx.launch_count()
+        dev.record(ev[0])
+        for i in range(args.steps):
+            bind(i % 2)
+            sess.launch()
+        dev.record(ev[1])
+        dev.sync()
+    ms = dev.elapsed_ms(ev[0], ev[1])
+    launches = gvx.launch_count() - launches0
+    ms_max = allreduce_max(ms)
+    px_step = w * h * F
+    value = px_step * args.steps * world / (ms_max / 1e3) / 1e6
+
+    # end to end through the public API (run_plan with host buffers, H2D + D2H inside)
+    e2e_frames = max(1, min(args.steps, args.e2e_frames))
+    frame_host = host[0]
+    graph.run_host(frame_host)  # warm the host session
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_frames):
+        graph.run_host(host[i % F])
+    e2e_s = allreduce_max(time.perf_counter() - t0)
+    e2e_value = w * h * e2e_frames * world / e2e_s / 1e6
+    out_b = {1: 2, 2: 1, 3: 1, 4: 256 * 8 + 16, 5: 2}[cfg]
+    e2e = {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": w * h,
+           "d2h_bytes_per_step": out_b * (w * h if cfg != 4 else 1), "frames": e2e_frames,
+           "path": "gvx::run_plan(OptimizedPlan, InputMap of host Buffers) via gvx_c.h"}
+
+    kernel_ms = ms / args.steps  # one fused launch per step (F frames in grid.z)
+    if sess.launches() != 1:
+        kernel_ms = None
+    return dict(value=value, ms_per_step=ms_max / args.steps, clocks=clk.summary(), launches=launches,
+                e2e=e2e, frames=F, kernel_ms=kernel_ms, checked=checked, w=w, h=h, px_step=px_step,
+                launches_per_step=sess.launches(), describe=graph.describe())
+
+
+# --------------------------------------------------------------- banded cfg5
+
+class GvxbImage(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("pitch", ctypes.c_int64), ("width", ctypes.c_int32),
+                ("height", ctypes.c_int32), ("format", ctypes.c_int32), ("frames", ctypes.c_int32),
+                ("frame_stride", ctypes.c_int64)]
+
+
+class GvxbBand(ctypes.Structure):
+    _fields_ = [("row0", ctypes.c_int32), ("row1", ctypes.c_int32), ("global_h", ctypes.c_int32),
+                ("src_row0", ctypes.c_int32), ("dst_row0", ctypes.c_int32)]
+
+
+class GvxbEdgeArgs(ctypes.Structure):
+    _fields_ = [("src", GvxbImage), ("gx", GvxbImage), ("gy", GvxbImage), ("mag", GvxbImage),
+                ("with_gauss", ctypes.c_int32), ("band", GvxbBand)]
+
+
+HALO = 2  # Gaussian radius 1 + Sobel radius 1
+
+
+def run_banded(args, rank, world, local_rank):
+    """cfg5: 16384^2 edge graph as row bands; halo rows exchanged over NCCL."""
+    import torch
+    import paper_2008_11476_b200 as gvx
+    c, _ = gvx.libraries()
+    c.gvxb_edge.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbEdgeArgs)]
+    W = H = args.size or 16384
+    r0, r1 = gvx.band_rows(H, world, rank)
+    s0, s1 = max(0, r0 - HALO), min(H, r1 + HALO)
+    dev = gvx.Device(local_rank)
+    torch.cuda.set_device(local_rank)
+    stream = torch.cuda.Stream()  # a real stream: the legacy default stream does not order with ours
+    torch.cuda.set_stream(stream)
+    c.gvxb_ctx_set_stream(dev.h, ctypes.c_void_p(stream.cuda_stream))
+    src = torch.empty((s1 - s0, W), dtype=torch.uint8, device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(5 + rank)
+    src.random_(0, 256, generator=gen)
+    mag = torch.empty((r1 - r0, W), dtype=torch.int16, device="cuda")
+
+    a = GvxbEdgeArgs()
+    a.src = GvxbImage(src.data_ptr(), W, W, s1 - s0, 0, 1, 0)
+    a.mag = GvxbImage(mag.data_ptr(), W * 2, W, r1 - r0, 2, 1, 0)
+    a.with_gauss = 1
+    a.band = GvxbBand(r0, r1, H, s0, r0)
+    import torch.distributed as dist
+
+    def exchange():
+        # my first/last owned rows go to the neighbours; their rows fill my halo
+        ops = []
+        if world > 1:
+            if rank > 0:
+                ops.append(dist.P2POp(dist.isend, src[r0 - s0:r0 - s0 + HALO], rank - 1))
+                ops.append(dist.P2POp(dist.irecv, src[0:r0 - s0], rank - 1))
+            if rank < world - 1:
+                ops.append(dist.P2POp(dist.isend, src[r1 - s0 - HALO:r1 - s0], rank + 1))
+                ops.append(dist.P2POp(dist.irecv, src[r1 - s0:s1 - s0], rank + 1))
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def step():
+        exchange()
+        rc = c.gvxb_edge(dev.h, ctypes.byref(a))
+        if rc:
+            raise RuntimeError(c.gvxb_last_error().decode())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t_end = time.perf_counter() + args.clock_window
+        while time.perf_counter() < t_end:
+            step()
+            torch.cuda.synchronize()
+        launches0 = dev.launch_count()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ms_max = allreduce_max(ms)
+    value = W * H * args.steps / (ms_max / 1e3) / 1e6
+    launches = dev.launch_count() - launches0
+    # e2e: host band in, host magnitude out, through the C-ABI with copies
+    host_in = np.random.default_rng(rank).integers(0, 256, size=(s1 - s0, W), dtype=np.uint8)
+    host_out = np.empty((r1 - r0, W), np.int16)
+    t0 = time.perf_counter()
+    n_e2e = max(1, min(args.steps, 3))
+    for _ in range(n_e2e):
+        src.copy_(torch.from_numpy(host_in))
+        step()
+        host_out[:] = mag.cpu().numpy()
+    torch.cuda.synchronize()
+    e2e_s = allreduce_max(time.perf_counter() - t0)
+    e2e = {"value": W * H * n_e2e / e2e_s / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": (s1 - s0) * W,
+           "d2h_bytes_per_step": (r1 - r0) * W * 2, "path": "gvxb_edge C-ABI on row bands (pageable host copies)"}
+    return dict(value=value, ms_per_step=ms_max / args.steps, clocks=clk.summary(), launches=launches, e2e=e2e,
+                frames=1, kernel_ms=ms / args.steps if world == 1 else None, checked=None, w=W, h=H,
+                px_step=W * H, launches_per_step=1, describe=f"row band {r0}:{r1} of {H}, halo {HALO}")
+
+
+# ------------------------------------------------------------- distributed
+
+_dist = None
+
+
+def init_dist(world, local_rank):
+    global _dist
+    if world <= 1:
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    _dist = dist
+
+
+def barrier():
+    if _dist is not None:
+        _dist.barrier()
+
+
+def allreduce_max(x: float) -> float:
+    if _dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    _dist.all_reduce(t, op=_dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="graphvx-b200", choices=["graphvx-b200", "ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--frames", type=int, default=0)
+    ap.add_argument("--size", type=int, default=0, help="cfg5 image side (default 16384)")
+    ap.add_argument("--e2e-frames", type=int, default=8)
+    ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-window", type=float, default=1.0, help="seconds of identical load sampled before timing")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local_rank = dist_env()
+    cfg = args.config
+    import paper_2008_11476_b200 as gvx
+    w, h = gvx.CONFIG_SIZE[cfg]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        r = cpu_reference_run(cfg, args.steps, args.warmup)
+        line = {"metric": "graph Mpixel/s", "value": r["value"], "unit": "Mpixel/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["seconds"] / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference random_buffer)",
+                "config": {"workload": CONFIG_NAME[cfg], "width": w, "height": h},
+                "impl": "reference", "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    os.environ.setdefault("GVX_DEVICE", str(local_rank))
+    init_dist(world, local_rank)
+    if cfg == 5:
+        res = run_banded(args, rank, world, local_rank)
+        scaling = "strong"
+    else:
+        res = run_frames(args, cfg, rank, world, local_rank)
+        scaling = "weak"
+    if rank != 0:
+        return 0
+
+    peaks, peak_kind = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roof = None
+    if res["kernel_ms"]:
+        achieved = ALGO_BYTES[cfg] * res["px_step"] / (res["kernel_ms"] / 1e3) / 1e9
+        traffic = ncu_traffic(cfg)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                "kernel": KERNEL_NAME[cfg], "algorithmic_bytes_per_px": ALGO_BYTES[cfg],
+                "px_per_launch": res["px_step"], "kernel_ms": round(res["kernel_ms"], 4)}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_leg(cfg)
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+    line = {"metric": "graph Mpixel/s", "value": res["value"], "unit": "Mpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (reference random_buffer frame + derived frames)",
+            "config": {"workload": CONFIG_NAME[cfg], "width": res["w"], "height": res["h"],
+                       "frames_per_step": res["frames"], "l2": "inputs rotate over 2 batches larger than L2"
+                       if cfg != 5 else "16384^2 input > L2",
+                       "parallelism": f"{'row bands' if cfg == 5 else 'frame replicas'} x{world}"},
+            "e2e": res["e2e"], "roofline": roof, "cpu_baseline": cpu, "clocks": res["clocks"],
+            "gpu_launches": res["launches"], "launches_per_step": res["launches_per_step"],
+            "checked_vs_oracle": res["checked"], "program": res["describe"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -61,6 +61,11 @@ int gvxc_session_launches(gvxc_session s);
 int gvxc_session_upload_input(gvxc_session s, int frame, const uint8_t* in);
 int gvxc_session_download(gvxc_session s, int slot, int frame, void* out, long long* hist, double* stats);
 
+/* Device kernels launched so far by the library's device context. */
+long long gvxc_launch_count(void);
+/* The library's launch stream (cudaStream_t) for `device`'s context. */
+void* gvxc_default_stream(void);
+
 /* Reference-identical synthetic input (random_buffer, U8). */
 int gvxc_random_u8(int width, int height, unsigned long long seed, uint8_t* out);
 

@@ -111,6 +111,8 @@ def _declare(c, g):
     g.gvxc_session_upload_input.argtypes = [P, I, U8P]
     g.gvxc_session_download.argtypes = [P, I, I, P, ctypes.POINTER(L), ctypes.POINTER(D)]
     g.gvxc_random_u8.argtypes = [I, I, ctypes.c_ulonglong, U8P]
+    g.gvxc_launch_count.restype = ctypes.c_longlong
+    g.gvxc_default_stream.restype = P
 
 
 def _check_graph(rc: int):
@@ -132,6 +134,12 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     c.gvxb_device_count(ctypes.byref(n))
     return n.value
+
+
+def launch_count() -> int:
+    """Device kernels launched so far by the library's context (-1: no device)."""
+    _, g = _load()
+    return int(g.gvxc_launch_count())
 
 
 def random_u8(width: int, height: int, seed: int) -> np.ndarray:
@@ -306,6 +314,40 @@ class Device:
 
     def launch_count(self) -> int:
         return int(self.c.gvxb_launch_count(self.h))
+
+
+class GvxbImage(ctypes.Structure):
+    """include/gvxb.h gvxb_image."""
+    _fields_ = [("data", ctypes.c_void_p), ("pitch", ctypes.c_int64), ("width", ctypes.c_int32),
+                ("height", ctypes.c_int32), ("format", ctypes.c_int32), ("frames", ctypes.c_int32),
+                ("frame_stride", ctypes.c_int64)]
+
+
+class GvxbBand(ctypes.Structure):
+    """include/gvxb.h gvxb_band."""
+    _fields_ = [("row0", ctypes.c_int32), ("row1", ctypes.c_int32), ("global_h", ctypes.c_int32),
+                ("src_row0", ctypes.c_int32), ("dst_row0", ctypes.c_int32)]
+
+
+class GvxbEdgeArgs(ctypes.Structure):
+    """include/gvxb.h gvxb_edge_args."""
+    _fields_ = [("src", GvxbImage), ("gx", GvxbImage), ("gy", GvxbImage), ("mag", GvxbImage),
+                ("with_gauss", ctypes.c_int32), ("band", GvxbBand)]
+
+
+def edge_band(device: "Device", src_ptr: int, src_pitch: int, width: int, src_rows: int, mag_ptr: int,
+              mag_pitch: int, row0: int, row1: int, global_h: int, src_row0: int, dst_row0: int,
+              with_gauss: bool = True):
+    """Fused Gaussian3x3 -> Sobel3x3 -> Magnitude on global rows [row0, row1)
+    of a row band (gvxb_edge); `src` holds global rows from src_row0."""
+    c, _ = _load()
+    c.gvxb_edge.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbEdgeArgs)]
+    a = GvxbEdgeArgs()
+    a.src = GvxbImage(src_ptr, src_pitch, width, src_rows, 0, 1, 0)
+    a.mag = GvxbImage(mag_ptr, mag_pitch, width, row1 - row0, 2, 1, 0)
+    a.with_gauss = int(with_gauss)
+    a.band = GvxbBand(row0, row1, global_h, src_row0, dst_row0)
+    _check_cuda(c.gvxb_edge(device.h, ctypes.byref(a)))
 
 
 def band_rows(height: int, world: int, rank: int):

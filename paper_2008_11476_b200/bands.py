@@ -1,0 +1,45 @@
+"""Multi-GPU row-band scheduler for large images (BASELINE config 5).
+
+Band g of G owns global rows [row0, row1) (balanced split, gvxb_band_rows in
+the C-ABI).  A fused stencil group of total radius R needs source rows
+[row0 - R, row1 + R) clipped to the image; the R rows on each side that a
+rank does not own are exchanged with its neighbours, point to point, once
+per group execution — the only collective on this path.
+Clamp borders use *global* rows, so only the first and last bands clamp.
+
+The exchange runs on torch.distributed tensors: NCCL over NVLink on the GPU
+box, gloo in the CPU tests (tests/test_cpu_multirank.py).
+"""
+from __future__ import annotations
+
+
+def band_slab(height: int, world: int, rank: int, halo: int, band_rows=None):
+    """(row0, row1, src_row0, src_row1) of rank's band and its halo'd slab."""
+    if band_rows is None:
+        from . import band_rows as _band_rows  # C-ABI gvxb_band_rows
+        band_rows = _band_rows
+    r0, r1 = band_rows(height, world, rank)
+    return r0, r1, max(0, r0 - halo), min(height, r1 + halo)
+
+
+def halo_exchange(dist, slab, r0: int, r1: int, s0: int, s1: int, rank: int, world: int, halo: int) -> None:
+    """Fill the halo rows of `slab` (global rows s0..s1) from the neighbours.
+
+    `slab` is a torch tensor of shape (s1 - s0, W) whose owned rows
+    [r0, r1) are valid.  Sends my first / last `halo` owned rows, receives
+    the neighbours' into my halo.
+    """
+    if world <= 1:
+        return
+    ops = []
+    if rank > 0 and r0 > s0:
+        ops.append(dist.P2POp(dist.isend, slab[r0 - s0:r0 - s0 + halo].contiguous(), rank - 1))
+        top = slab[0:r0 - s0]
+        ops.append(dist.P2POp(dist.irecv, top, rank - 1))
+    if rank < world - 1 and s1 > r1:
+        ops.append(dist.P2POp(dist.isend, slab[r1 - s0 - halo:r1 - s0].contiguous(), rank + 1))
+        bottom = slab[r1 - s0:s1 - s0]
+        ops.append(dist.P2POp(dist.irecv, bottom, rank + 1))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()

@@ -4,6 +4,7 @@
 #include "../configs/config_graphs.hpp"
 #include "graphvx/device.hpp"
 #include "graphvx/optimize.hpp"
+#include "program.hpp"
 
 #include <cstring>
 #include <memory>
@@ -191,6 +192,22 @@ int gvxc_session_download(gvxc_session s, int slot, int frame, void* out, long l
         }
         copy_outputs(g, outs, out, hist, stats);
     });
+}
+
+long long gvxc_launch_count(void) {
+    try {
+        return gvx::dev::launch_count();
+    } catch (...) {
+        return -1;
+    }
+}
+
+void* gvxc_default_stream(void) {
+    try {
+        return gvxb_ctx_stream(gvx::dev::context());
+    } catch (...) {
+        return nullptr;
+    }
 }
 
 int gvxc_random_u8(int w, int h, unsigned long long seed, uint8_t* out) {

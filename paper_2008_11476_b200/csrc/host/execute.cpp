@@ -219,6 +219,8 @@ gvxb_ctx context() {
     return ctx;
 }
 
+long long launch_count() { return gvxb_launch_count(context()); }
+
 namespace {
 
 // ------------------------------------------------------------ JIT modules

@@ -27,6 +27,9 @@ namespace gvx::dev {
 /// is no host execution path.
 gvxb_ctx context();
 
+/// Device kernels launched by the process-wide context.
+long long launch_count();
+
 /// Throws gvx::Error for a failed C-ABI call.
 void check(int status, const char* what);
 

@@ -1,0 +1,355 @@
+// graphvx-b200 API and fusion tests (doctest stand-in).
+//   CPU cases: object model fixes, DCE / transfer / fusion plans of the
+//              BASELINE graphs, fusion refusal rules.
+//   GPU cases (skipped without a CUDA device; the pytest wrapper runs them
+//              under -m gpu): run_plan == run_naive bit-exactly on random
+//              DAGs (SPEC.md:518 fusion soundness), custom kernels with every
+//              boundary mode, device DivByZero, frame batches.
+#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+#include <doctest.h>
+
+#include "../../paper_2008_11476_b200/csrc/configs/config_graphs.hpp"
+#include "graphvx/device.hpp"
+#include "graphvx/optimize.hpp"
+
+#include <cstdlib>
+#include <random>
+
+using namespace gvx;
+
+namespace {
+
+bool has_gpu() {
+    static const int n = [] {
+        if (std::getenv("GVX_TEST_CPU_ONLY")) return 0;
+        return device_count();
+    }();
+    return n > 0;
+}
+
+#define GPU_ONLY()                                                                                                   \
+    do {                                                                                                             \
+        if (!has_gpu()) return;                                                                                      \
+    } while (0)
+
+ResolvedDesc img_desc(int w, int h, ImageFormat f) {
+    ResolvedDesc d;
+    d.kind = ObjKind::Image;
+    d.width = w;
+    d.height = h;
+    d.format = f;
+    return d;
+}
+
+VerifiedGraph impl_of(Context& ctx, const AppGraph& g) { return gvx_configs::verified_impl(ctx, g); }
+
+bool same_outputs(const ExecutionReport& a, const ExecutionReport& b) {
+    if (a.outputs.size() != b.outputs.size()) return false;
+    for (const auto& [id, buf] : a.outputs) {
+        auto it = b.outputs.find(id);
+        if (it == b.outputs.end() || !buf.byte_equal(it->second)) return false;
+    }
+    return true;
+}
+
+} // namespace
+
+// ----------------------------------------------------------------- CPU
+
+TEST_CASE("virtual intermediates expand and fuse (reference CrossGraphVirtual defect fixed)") {
+    for (int cfg : {1, 2, 3, 4}) {
+        Context ctx;
+        auto cg = gvx_configs::build_config(ctx, cfg, 64, 48, true);
+        VerifiedGraph impl = impl_of(ctx, *cg.graph);
+        CHECK(impl.stamped());
+        OptimizedPlan plan = optimize(impl, ctx);
+        CHECK(plan.fused.stamped());
+        CHECK(plan.stats.launches_after <= plan.stats.launches_before);
+    }
+}
+
+TEST_CASE("foreign virtual images are still rejected in application graphs") {
+    Context ctx;
+    AppGraph& g1 = ctx.create_graph();
+    AppGraph& g2 = ctx.create_graph();
+    ObjectId foreign = ctx.create_virtual_image(g1).id;
+    ObjectId local = ctx.create_virtual_image(g2).id;
+    CHECK_THROWS_AS(g2.add_node("Gaussian3x3", {foreign, local}), Error);
+}
+
+TEST_CASE("reference-granularity fusion of the BASELINE graphs (SURVEY.md 3.3)") {
+    struct Want {
+        int cfg, launches_after;
+    };
+    for (Want w : {Want{1, 3}, Want{2, 5}, Want{3, 1}, Want{4, 4}}) {
+        Context ctx;
+        auto cg = gvx_configs::build_config(ctx, w.cfg, 32, 32, true);
+        OptimizedPlan plan = optimize(impl_of(ctx, *cg.graph), ctx);
+        CAPTURE(w.cfg);
+        CHECK(plan.stats.launches_after == w.launches_after);
+        CHECK(plan.stats.nodes_removed == 0);
+    }
+}
+
+TEST_CASE("transfer reduction: one upload and one download per graph input/output") {
+    Context ctx;
+    auto cg = gvx_configs::build_config(ctx, 1, 32, 32, true);
+    OptimizedPlan plan = optimize(impl_of(ctx, *cg.graph), ctx);
+    CHECK(plan.transfers.segment_count == 1);
+    CHECK(plan.transfers.optimized_count() == 2);
+    CHECK(plan.transfers.naive_count == 8);
+}
+
+TEST_CASE("dead computation elimination drops the unused Sobel half (paper Fig. 8 analogue)") {
+    Context ctx;
+    AppGraph& g = ctx.create_graph();
+    ObjectId in = ctx.create_image(32, 32, ImageFormat::U8).id;
+    ObjectId gx = ctx.create_image(32, 32, ImageFormat::S16).id;
+    ObjectId gy = ctx.create_virtual_image(g).id;
+    g.note_data(in);
+    g.add_node("Sobel3x3", {in, gx, gy});
+    OptimizedPlan plan = optimize(impl_of(ctx, g), ctx);
+    CHECK(plan.stats.nodes_before == 2);
+    CHECK(plan.stats.nodes_removed == 1);
+}
+
+namespace {
+AbstractionPtr point_plus(int k) {
+    std::vector<SignatureParam> ps(2);
+    ps[0].direction = Direction::Input;
+    ps[0].kind = ObjKind::Image;
+    ps[1].direction = Direction::Output;
+    ps[1].kind = ObjKind::Image;
+    ps[1].formats = {ImageFormat::U8};
+    PointKernel pk;
+    pk.outputs.push_back(PointOutput{{saturate_to(ScalarType::U8, add(input_pixel(0), const_i(k)))}});
+    return make_point_kernel("plus" + std::to_string(k), KernelSignature(ps), pk);
+}
+
+AbstractionPtr blur_local(BoundaryMode mode, std::int64_t constant) {
+    std::vector<SignatureParam> ps(2);
+    ps[0].direction = Direction::Input;
+    ps[0].kind = ObjKind::Image;
+    ps[1].direction = Direction::Output;
+    ps[1].kind = ObjKind::Image;
+    ps[1].formats = {ImageFormat::U8};
+    LocalKernel lk;
+    lk.window_w = 3;
+    lk.window_h = 5;
+    lk.boundary = mode;
+    lk.boundary_value = Value::of_int(constant);
+    lk.tap_body = window_pixel(0, 0, 0);
+    lk.post_body = saturate_to(ScalarType::U8, div(add(input_pixel(0), const_i(7)), const_i(15)));
+    return make_local_kernel(std::string("blur_") + to_string(mode), KernelSignature(ps), lk);
+}
+
+/// in -> plus3 -> blur(mode) -> plus5 -> out, all intermediates virtual.
+struct Chain {
+    Context ctx;
+    AppGraph* g = nullptr;
+    ObjectId in = 0, out = 0;
+    explicit Chain(BoundaryMode mode, int w = 23, int h = 19) {
+        auto reg = std::make_shared<KernelRegistry>(KernelRegistry::builtin().clone());
+        reg->add_custom(point_plus(3));
+        reg->add_custom(point_plus(5));
+        reg->add_custom(blur_local(mode, 200));
+        ctx.set_registry(reg);
+        g = &ctx.create_graph();
+        in = ctx.create_image(w, h, ImageFormat::U8).id;
+        out = ctx.create_image(w, h, ImageFormat::U8).id;
+        g->note_data(in);
+        ObjectId a = ctx.create_virtual_image(*g).id, b = ctx.create_virtual_image(*g).id;
+        g->add_node("plus3", {in, a});
+        g->add_node(std::string("blur_") + to_string(mode), {a, b});
+        g->add_node("plus5", {b, out});
+    }
+};
+} // namespace
+
+TEST_CASE("fusion refuses rewrites that would change results vs run_naive") {
+    {
+        Chain c(BoundaryMode::Clamp);
+        OptimizedPlan p = optimize(impl_of(c.ctx, *c.g), c.ctx);
+        CHECK(p.stats.launches_after == 1); // point->local->point fully fused under Clamp
+    }
+    {
+        Chain c(BoundaryMode::Constant);
+        OptimizedPlan p = optimize(impl_of(c.ctx, *c.g), c.ctx);
+        CHECK(p.stats.launches_after == 2); // point->local refused (border constant)
+    }
+    {
+        Chain c(BoundaryMode::Undefined);
+        OptimizedPlan p = optimize(impl_of(c.ctx, *c.g), c.ctx);
+        CHECK(p.stats.launches_after == 2); // local->point refused (border ring)
+    }
+}
+
+TEST_CASE("execution without a device fails loudly (no host fallback)") {
+    if (has_gpu()) return;
+    Context ctx;
+    auto cg = gvx_configs::build_config(ctx, 1, 16, 16, true);
+    VerifiedGraph impl = impl_of(ctx, *cg.graph);
+    InputMap in;
+    in[cg.input] = random_buffer(img_desc(16, 16, ImageFormat::U8), 1);
+    try {
+        run_naive(impl, in);
+        FAIL("expected UnsupportedKind");
+    } catch (const Error& e) {
+        CHECK(e.code() == ErrorCode::UnsupportedKind);
+    }
+}
+
+// ----------------------------------------------------------------- GPU
+
+TEST_CASE("gpu: boundary modes through fused plans equal run_naive") {
+    GPU_ONLY();
+    for (BoundaryMode m : {BoundaryMode::Clamp, BoundaryMode::Constant, BoundaryMode::Undefined}) {
+        for (auto [w, h] : {std::pair{23, 19}, std::pair{1, 1}, std::pair{2, 7}, std::pair{200, 3}}) {
+            Chain c(m, w, h);
+            VerifiedGraph impl = impl_of(c.ctx, *c.g);
+            OptimizedPlan p = optimize(impl, c.ctx);
+            InputMap in;
+            in[c.in] = random_buffer(img_desc(w, h, ImageFormat::U8), 99 + w);
+            ExecutionReport a = run_naive(impl, in), b = run_plan(p, in);
+            CAPTURE(to_string(m));
+            CAPTURE(w);
+            CHECK(same_outputs(a, b));
+            CHECK(b.counters.kernel_launches <= a.counters.kernel_launches);
+        }
+    }
+}
+
+TEST_CASE("gpu: runtime division by zero surfaces as DivByZero") {
+    GPU_ONLY();
+    std::vector<SignatureParam> ps(3);
+    ps[0].direction = ps[1].direction = Direction::Input;
+    ps[0].kind = ps[1].kind = ObjKind::Image;
+    ps[2].direction = Direction::Output;
+    ps[2].kind = ObjKind::Image;
+    ps[2].formats = {ImageFormat::U8};
+    PointKernel pk;
+    pk.arity = 2;
+    pk.outputs.push_back(PointOutput{{saturate_to(ScalarType::U8, div(input_pixel(0), input_pixel(1)))}});
+    auto reg = std::make_shared<KernelRegistry>(KernelRegistry::builtin().clone());
+    reg->add_custom(make_point_kernel("ratio", KernelSignature(ps), pk));
+    Context ctx;
+    ctx.set_registry(reg);
+    AppGraph& g = ctx.create_graph();
+    ObjectId a = ctx.create_image(8, 8, ImageFormat::U8).id, b = ctx.create_image(8, 8, ImageFormat::U8).id;
+    ObjectId o = ctx.create_image(8, 8, ImageFormat::U8).id;
+    g.note_data(a);
+    g.note_data(b);
+    g.add_node("ratio", {a, b, o});
+    VerifiedGraph impl = impl_of(ctx, g);
+    InputMap in;
+    in[a] = random_buffer(img_desc(8, 8, ImageFormat::U8), 1);
+    in[b] = Buffer::image(img_desc(8, 8, ImageFormat::U8)); // zeros
+    CHECK_THROWS_AS(run_naive(impl, in), Error);
+    try {
+        run_naive(impl, in);
+    } catch (const Error& e) {
+        CHECK(e.code() == ErrorCode::DivByZero);
+    }
+}
+
+namespace {
+
+/// Random DAG over the registry (point, local, global kinds).
+struct RandomGraph {
+    Context ctx;
+    AppGraph* g = nullptr;
+    std::vector<ObjectId> inputs;
+    RandomGraph(std::uint64_t seed, int w, int h) {
+        std::mt19937_64 rng(seed);
+        g = &ctx.create_graph();
+        std::vector<ObjectId> u8, s16;
+        for (int i = 0; i < 2; ++i) {
+            ObjectId id = ctx.create_image(w, h, ImageFormat::U8).id;
+            g->note_data(id);
+            inputs.push_back(id);
+            u8.push_back(id);
+        }
+        auto pick = [&](std::vector<ObjectId>& v) { return v[rng() % v.size()]; };
+        auto fresh = [&](ImageFormat f, bool last) {
+            const bool virt = !last && (rng() % 10) < 7;
+            ObjectId id = virt ? ctx.create_virtual_image(*g).id : ctx.create_image(w, h, f).id;
+            g->note_data(id);
+            return id;
+        };
+        const int n = 3 + static_cast<int>(rng() % 6);
+        for (int i = 0; i < n; ++i) {
+            const bool last = i == n - 1;
+            switch (rng() % 11) {
+            case 0: { ObjectId o = fresh(ImageFormat::U8, last); g->add_node("Gaussian3x3", {pick(u8), o}); u8.push_back(o); break; }
+            case 1: { ObjectId o = fresh(ImageFormat::U8, last); g->add_node("Box3x3", {pick(u8), o}); u8.push_back(o); break; }
+            case 2: { ObjectId x = fresh(ImageFormat::S16, last), y = fresh(ImageFormat::S16, last);
+                      g->add_node("Sobel3x3", {pick(u8), x, y}); s16.push_back(x); s16.push_back(y); break; }
+            case 3: { ObjectId o = fresh(ImageFormat::U8, last); g->add_node("Dilate3x3", {pick(u8), o}); u8.push_back(o); break; }
+            case 4: { ObjectId o = fresh(ImageFormat::U8, last); g->add_node("Median3x3", {pick(u8), o}); u8.push_back(o); break; }
+            case 5: { ObjectId o = fresh(ImageFormat::S16, last); g->add_node("Subtract", {pick(u8), pick(u8), o}); s16.push_back(o); break; }
+            case 6: { if (s16.size() < 2) { --i; break; }
+                      ObjectId o = fresh(ImageFormat::S16, last); g->add_node("Magnitude", {pick(s16), pick(s16), o}); s16.push_back(o); break; }
+            case 7: { if (s16.empty()) { --i; break; }
+                      ObjectId o = fresh(ImageFormat::U8, last); g->add_node("ConvertDepth", {pick(s16), o}); u8.push_back(o); break; }
+            case 8: { ObjectId o = fresh(ImageFormat::U8, last); g->add_node("AbsDiff", {pick(u8), pick(u8), o}); u8.push_back(o); break; }
+            case 9: { ObjectId t = ctx.create_scalar(ScalarType::U8, Value::of_int(static_cast<std::int64_t>(rng() % 256))).id;
+                      g->note_data(t);
+                      ObjectId o = fresh(ImageFormat::U8, last); g->add_node("Threshold", {pick(u8), t, kInvalidId, o}); u8.push_back(o); break; }
+            default: { ObjectId o = fresh(ImageFormat::U8, last); g->add_node("Not", {pick(u8), o}); u8.push_back(o); break; }
+            }
+        }
+    }
+};
+
+} // namespace
+
+TEST_CASE("gpu: fusion soundness on random DAGs (run_plan == run_naive, bit exact)") {
+    GPU_ONLY();
+    int checked = 0;
+    for (std::uint64_t seed = 1; seed <= 40; ++seed) {
+        const int w = 5 + static_cast<int>(seed * 37 % 120), h = 3 + static_cast<int>(seed * 11 % 50);
+        RandomGraph rg(seed, w, h);
+        VerifyResult vr = verify(*rg.g);
+        if (!vr.ok()) continue;
+        VerifiedGraph impl = impl_of(rg.ctx, *rg.g);
+        OptimizedPlan plan = optimize(impl, rg.ctx);
+        InputMap in;
+        for (ObjectId id : rg.inputs) in[id] = random_buffer(img_desc(w, h, ImageFormat::U8), seed * 3 + id);
+        ExecutionReport a = run_naive(impl, in);
+        ExecutionReport b = run_plan(plan, in);
+        CAPTURE(seed);
+        CHECK(same_outputs(a, b));
+        CHECK(b.counters.kernel_launches <= a.counters.kernel_launches);
+        CHECK(b.counters.transfers_executed <= a.counters.transfers_executed);
+        ++checked;
+    }
+    CHECK(checked >= 30);
+}
+
+TEST_CASE("gpu: frame batches through a DeviceSession equal per-frame run_plan") {
+    GPU_ONLY();
+    for (int cfg : {1, 2, 3, 4}) {
+        Context ctx;
+        auto cg = gvx_configs::build_config(ctx, cfg, 77, 41, true);
+        OptimizedPlan plan = optimize(impl_of(ctx, *cg.graph), ctx);
+        const int frames = 3;
+        DeviceSession s(plan, frames);
+        std::vector<Buffer> ins;
+        for (int f = 0; f < frames; ++f) {
+            ins.push_back(random_buffer(img_desc(77, 41, ImageFormat::U8), 500 + f));
+            s.upload(cg.input, ins.back(), f);
+        }
+        s.launch();
+        s.synchronize();
+        for (int f = 0; f < frames; ++f) {
+            InputMap in;
+            in[cg.input] = ins[static_cast<std::size_t>(f)];
+            ExecutionReport r = run_plan(plan, in);
+            for (ObjectId o : cg.outputs) {
+                CAPTURE(cfg);
+                CAPTURE(f);
+                CHECK(s.download(o, f).byte_equal(r.outputs.at(o)));
+            }
+        }
+    }
+}

@@ -1,0 +1,51 @@
+"""The CPU oracle is pinned before it is trusted (tests/golden/ were produced
+by the unmodified reference, see tests/golden/make_golden.py)."""
+import numpy as np
+import pytest
+
+SIZES = [(1, 1), (2, 3), (7, 5), (16, 16), (33, 17), (64, 48), (5, 129), (130, 3)]
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+@pytest.mark.parametrize("size", SIZES)
+def test_port_matches_reference_golden(cfg, size, golden, oracle_mod):
+    w, h = size
+    key = f"c{cfg}_{w}x{h}"
+    img = golden[key + "_in"]
+    got = oracle_mod.port_run(cfg, img)
+    if cfg == 4:
+        assert np.array_equal(got[0], golden[key + "_hist"])
+        assert got[1] == golden[key + "_stats"][0] and got[2] == golden[key + "_stats"][1]
+    else:
+        assert np.array_equal(got, golden[key + "_out"])
+
+
+def test_random_buffer_is_reference_identical(golden, gvx):
+    for (w, h) in SIZES:
+        for cfg in (1, 2, 3, 4):
+            key = f"c{cfg}_{w}x{h}"
+            assert np.array_equal(gvx.random_u8(w, h, int(golden[key + "_seed"])), golden[key + "_in"])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_port_matches_live_reference(cfg, oracle_mod, gvx):
+    if not oracle_mod.have_ref():
+        pytest.skip("reference oracle not built here (needs /root/reference)")
+    for (w, h, seed) in [(97, 61, 3), (200, 33, 4), (1, 40, 5)]:
+        img = gvx.random_u8(w, h, seed)
+        want, _ = oracle_mod.ref_run(cfg, img)
+        got = oracle_mod.port_run(cfg, img)
+        if cfg == 4:
+            assert np.array_equal(got[0], want[0]) and got[1] == want[1] and got[2] == want[2]
+        else:
+            assert np.array_equal(got, want)
+
+
+def test_known_answers_from_reference_tests(oracle_mod):
+    """KATs of ref:tests/test_registry.cpp:543-553 (constant 17 is a fixed point of
+    the 3x3 blurs) through the restated edge / unsharp chains."""
+    c = np.full((9, 11), 17, np.uint8)
+    assert (oracle_mod.port_run(1, c) == 0).all()        # no gradient on a constant image
+    assert (oracle_mod.port_run(3, c) == 17).all()       # unsharp of a constant is the constant
+    hist, mean, sd = oracle_mod.port_run(4, c)
+    assert hist[17] == c.size and mean == 17.0 and sd == 0.0
