@@ -96,7 +96,7 @@ __device__ __forceinline__ void st_val(i64* slot, V v) {
 }
 __device__ __forceinline__ void flush_reads(const P& p, u64 rd) {
   for (int o = 16; o > 0; o >>= 1) rd += __shfl_xor_sync(0xffffffffu, rd, o);
-  if ((threadIdx.x & 31) == 0 && threadIdx.y == 0 && rd) atomicAdd((u64*)p.f[1], rd);
+  if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0 && rd) atomicAdd((u64*)p.f[1], rd);
 }
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 )CUDA";
