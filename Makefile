@@ -24,7 +24,7 @@ all: $(LIB)/libgvx_cuda.so $(LIB)/libgraphvx.so tests/cpp/bin/test_graphvx
 
 build/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(wildcard $(PKG)/csrc/cuda/*.cuh) include/gvxb.h
 	@mkdir -p build/cuda
-	$(NVCC) $(NVCCFLAGS) -dc -c $< -o $@ 2> build/cuda/$*.ptxas.log || (cat build/cuda/$*.ptxas.log; false)
+	$(NVCC) $(NVCCFLAGS) -c $< -o $@ 2> build/cuda/$*.ptxas.log || (cat build/cuda/$*.ptxas.log; false)
 
 $(LIB)/libgvx_cuda.so: $(CUDA_OBJ)
 	@mkdir -p $(LIB)

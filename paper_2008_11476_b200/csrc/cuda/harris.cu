@@ -1,35 +1,45 @@
-// K2 — fused Harris corner graph (U8 -> U8 mask), one pass.
+// K2 — fused Harris corner graph (U8 -> U8 mask), one pass, sm_100a.
 //
 // Graph (SURVEY.md §8a "Harris graph definition"): Sobel3x3 -> Multiply
 // (gx*gx, gy*gy, gx*gy -> S32) -> Box3x3 (S32) -> user point
 // HarrisResponse F32((Sxx*Syy - Sxy^2) - k*(Sxx+Syy)^2) -> user point
 // ThresholdF32 sat_U8(resp > T ? 255 : 0).
-// Exactness:
-//   Sobel |v| <= 1020, products <= 1020^2 (no S32 saturation),
-//   Box3x3 post sat_S32(llround(s * (1/9.0))) == round_half_away(s / 9)
-//   for |s| <= 9*1020^2 (the double product error < 3e-10 is far below the
-//   1/18 distance of s/9 to any half-integer; ref:src/registry.cpp:703-720),
-//   response in int64 + IEEE double exactly as the reference evaluates the
-//   expression (int64 products, double multiply/subtract, float rounding;
-//   ref:src/expr.cpp:351-371), threshold compares double(float(resp)) > T.
-//   => bit-exact mask (and response when stored).
-//   Clamp of the intermediates: products at out-of-image positions take the
-//   value of the clamped position (the Box window clamps into the
-//   materialised product image, ref:src/execute.cpp:242-245).
 //
-// Layout: CTA = 128 threads, tile 512 x 32 outputs; each thread owns 4
-// columns and streams rows with 3-row register rings for the separable Sobel
-// terms and the horizontal box sums.
+// Exactness argument (the kernel output is bit-identical to run_naive):
+//  * Sobel |g| <= 1020, products <= 1020^2, box sums s <= 9*1020^2 < 2^24:
+//    every value up to the box sums is an integer held EXACTLY in fp32, so
+//    the Sobel / product / box stages run as packed FP32 (FFMA2/FADD2/FMUL2).
+//  * The reference rounds each box sum, q = sat_S32(llround(s * (1/9.0)))
+//    = round_half_away(s / 9) (ref:src/registry.cpp:703-720), then evaluates
+//    the response in int64 + IEEE double (ref:src/expr.cpp:351-371).  With
+//    |q - s/9| <= 1/2 and |s_xy| <= (s_xx + s_yy)/2 (Cauchy-Schwarz on the
+//    box sums), |81*resp(q) - (s_xx*s_yy - s_xy^2 - k*(s_xx+s_yy)^2)| <=
+//    (9 + 18|k|)*tr + 40.5 + 81|k|; adding the fp32 evaluation error
+//    (<= 2^-20 * (|p1| + |p2| + |k| tt)) and the float rounding of the final
+//    response gives a bound E per pixel.  If |est - 81 T| > E the decision is
+//    certain; otherwise (and for every pixel when the F32 response image is
+//    observable) the kernel evaluates the reference's exact int64/double
+//    expression for that pixel.
+//  * Clamp borders of the intermediates: products at out-of-image positions
+//    take the clamped position's value (ref:src/execute.cpp:242-245).
+//
+// Layout: CTA = 4 warps; a warp covers 30 owner lanes x 4 columns (lanes 0
+// and 31 are halo lanes whose products reach their neighbours through warp
+// shuffles), 64 rows per CTA streamed with 3-row register rings.  Columns
+// are kept as even/odd float2 pairs ((c, c+2), (c+1, c+3)) so every
+// separable stencil step is a packed, register-aligned FP32 op.
 #include "tile.cuh"
+
+#include <cmath>
 
 namespace gvxd {
 
 constexpr int kHarThreads = 128;
-constexpr int kHarTW = 4 * kHarThreads;
-constexpr int kHarTH = 32;
-constexpr int kHarSW = kHarTW + 64; // columns [x0 - 32, x0 + 544)
-constexpr int kHarSH = kHarTH + 4;  // rows [y0 - 2, y0 + 34)
-constexpr int kHarBox = 192;
+constexpr int kHarWarpCols = 120;                         // 30 owner lanes x 4
+constexpr int kHarTW = kHarWarpCols * (kHarThreads / 32); // 480 output columns per CTA
+constexpr int kHarTH = 64;
+constexpr int kHarSW = kHarTW + 32; // smem columns [x0 - 16, x0 + 496): box x start 16-byte aligned
+constexpr int kHarSH = kHarTH + 4;  // smem rows    [y0 - 2, y0 + 66)
 
 struct HarrisParams {
     int width;
@@ -40,19 +50,49 @@ struct HarrisParams {
     int64_t resp_pitch, resp_fstride;
     double k;
     double threshold;
+    float kabs;  // |k|
+    float kneg;  // -k
+    float t81;   // 81 T
+    float c_tt;  // bound slope in tt = tr^2
+    float c_tr;  // bound slope in tr
+    float c0;    // bound constant
 };
 
-__device__ __forceinline__ void fetch8h(const uint8_t* row, int off, int (&a)[8]) {
-    const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
-    a[0] = byte_of(wl, 2);
-    a[1] = byte_of(wl, 3);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) a[2 + k] = byte_of(wc, k);
-    a[6] = byte_of(wr, 0);
-    a[7] = byte_of(wr, 1);
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+/// 2^23 + byte k of w (the float bit pattern 0x4B0000bb).
+__device__ __forceinline__ float magic_byte(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | static_cast<unsigned>(k)));
 }
 
-__device__ __forceinline__ int box_round(int s) { return round_div_away(s, 9); }
+/// 4 columns of one quantity as (even, odd) float2 pairs: (c, c+2), (c+1, c+3).
+struct Q4 {
+    float2 e, o;
+};
+__device__ __forceinline__ Q4 qadd(Q4 a, Q4 b) { return Q4{add2(a.e, b.e), add2(a.o, b.o)}; }
+__device__ __forceinline__ Q4 qsub(Q4 a, Q4 b) { return Q4{sub2(a.e, b.e), sub2(a.o, b.o)}; }
+__device__ __forceinline__ Q4 qmul(Q4 a, Q4 b) { return Q4{mul2(a.e, b.e), mul2(a.o, b.o)}; }
+
+struct Prod3 {
+    Q4 xx, yy, xy; // horizontal box sums of one product row
+};
+__device__ __forceinline__ Prod3 padd(const Prod3& a, const Prod3& b) {
+    return Prod3{qadd(a.xx, b.xx), qadd(a.yy, b.yy), qadd(a.xy, b.xy)};
+}
+
+/// The reference's exact expression for one pixel from the exact box sums.
+__device__ __forceinline__ float exact_response(float sxx, float syy, float sxy, double k) {
+    const int qxx = round_div_away(__float2int_rn(sxx), 9);
+    const int qyy = round_div_away(__float2int_rn(syy), 9);
+    const int qxy = round_div_away(__float2int_rn(sxy), 9);
+    const long long det = static_cast<long long>(qxx) * qyy - static_cast<long long>(qxy) * qxy;
+    const long long tr = static_cast<long long>(qxx) + qyy;
+    return __double2float_rn(__dsub_rn(__ll2double_rn(det), __dmul_rn(k, __ll2double_rn(tr * tr))));
+}
 
 template <bool kResp>
 __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_constant__ CUtensorMap map,
@@ -65,128 +105,193 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
     const int y1 = min(y0 + kHarTH, p.band.row1);
     const int frame = blockIdx.z;
     const int H = p.band.global_h;
+    const int W = p.width;
 
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         fence_barrier_init();
     }
     __syncthreads();
-    stage_tile_u8<kHarSW, kHarSH>(tile, &map, &bar, x0 - 32, y0 - 2, frame, p.width, p.band);
+    stage_tile_u8<kHarSW, kHarSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band);
 
-    const int c = x0 + 4 * static_cast<int>(threadIdx.x);
-    if (c >= p.width) return;
-    const int off = 4 * static_cast<int>(threadIdx.x) + 32;
-    const int klo = c == 0 ? 0 : -1;              // product column c-1 clamps to c
-    const int khi = min(4, p.width - 1 - c);      // last in-image product slot offset
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = x0 + kHarWarpCols * warp + 4 * (lane - 1); // first column of this lane
+    const int off = c - (x0 - 16);                           // its smem column
+    const bool owner = lane >= 1 && lane <= 30 && c < W;
+    const bool left_edge = c == 0;      // column c-1 clamps to column 0
+    const bool right_edge = c + 4 >= W; // column c+4 (and maybe own columns) clamp to W-1
+    const int last = W - 1 - c;         // index of column W-1 inside this lane (if 0..3)
 
-    // separable Sobel terms per source row, columns c-1 .. c+4
-    int dA[6], dB[6], dC[6]; // D(k) = in(k+1) - in(k-1)
-    int sA[6], sB[6], sC[6]; // S(k) = in(k-1) + 2 in(k) + in(k+1)
-    // horizontal box sums of the products per product row, columns c .. c+3
-    int xA[4], xB[4], xC[4];
-    int yA[4], yB[4], yC[4];
-    int zA[4], zB[4], zC[4];
+    uint8_t* mrow = p.mask + frame * p.mask_fstride + static_cast<int64_t>(y0 - p.band.dst_row0) * p.mask_pitch + c;
+    char* rrow = reinterpret_cast<char*>(p.resp) + frame * p.resp_fstride +
+                 static_cast<int64_t>(y0 - p.band.dst_row0) * p.resp_pitch;
+    const float2 two = f2(2.f, 2.f), magic = f2(-8388608.f, -8388608.f);
 
-    uint8_t* mrow_base = p.mask + frame * p.mask_fstride;
-    char* rrow_base = reinterpret_cast<char*>(p.resp) + frame * p.resp_fstride;
-
-    auto emit = [&](int gy, const int (&xu)[4], const int (&xm)[4], const int (&xd)[4], const int (&yu)[4],
-                    const int (&ym)[4], const int (&yd)[4], const int (&zu)[4], const int (&zm)[4],
-                    const int (&zd)[4]) {
+    /// Separable Sobel terms of smem row j: D = in(x+1) - in(x-1),
+    /// S = in(x-1) + 2 in(x) + in(x+1) for columns c .. c+3.
+    auto sobel_terms = [&](int j, Q4& D, Q4& S) {
+        const uint8_t* row = tile + j * kHarSW;
+        const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
+        // column pairs P1=(c-1, c+1) P2=(c, c+2) P3=(c+1, c+3) P4=(c+2, c+4)
+        const float2 P1 = add2(f2(magic_byte(wl, 3), magic_byte(wc, 1)), magic);
+        const float2 P2 = add2(f2(magic_byte(wc, 0), magic_byte(wc, 2)), magic);
+        const float2 P3 = add2(f2(magic_byte(wc, 1), magic_byte(wc, 3)), magic);
+        const float2 P4 = add2(f2(magic_byte(wc, 2), magic_byte(wr, 0)), magic);
+        D = Q4{sub2(P3, P1), sub2(P4, P2)};
+        S = Q4{fma2(two, P2, add2(P1, P3)), fma2(two, P3, add2(P2, P4))};
+    };
+    /// Own columns beyond W-1 take column W-1's value (right border clamp).
+    auto clamp_right = [&](Q4& q) {
+        float v[4] = {q.e.x, q.o.x, q.e.y, q.o.y};
+#pragma unroll
+        for (int i = 1; i < 4; ++i)
+            if (i > last) v[i] = v[i - 1];
+        q = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
+    };
+    /// Horizontal 3-sums; neighbour columns c-1 / c+4 come from adjacent lanes.
+    auto hsum = [&](Q4 q) {
+        float pm1 = __shfl_up_sync(0xffffffffu, q.o.y, 1);  // left lane's c+3 = my c-1
+        float p4 = __shfl_down_sync(0xffffffffu, q.e.x, 1); // right lane's c  = my c+4
+        pm1 = left_edge ? q.e.x : pm1;
+        p4 = right_edge ? q.o.y : p4;
+        const float2 t = add2(q.e, q.o);
+        return Q4{add2(t, f2(pm1, q.o.x)), add2(t, f2(q.e.y, p4))};
+    };
+    /// Products of one Sobel row and their horizontal box sums.
+    auto products = [&](Q4 gx, Q4 gy) {
+        Q4 xx = qmul(gx, gx), yy = qmul(gy, gy), xy = qmul(gx, gy);
+        if (right_edge && last < 3) {
+            clamp_right(xx);
+            clamp_right(yy);
+            clamp_right(xy);
+        }
+        return Prod3{hsum(xx), hsum(yy), hsum(xy)};
+    };
+    /// Threshold decision (and optional exact response) for one output row.
+    auto emit = [&](int orow, const Prod3& V) {
+        const float sxx[4] = {V.xx.e.x, V.xx.o.x, V.xx.e.y, V.xx.o.y};
+        const float syy[4] = {V.yy.e.x, V.yy.o.x, V.yy.e.y, V.yy.o.y};
+        const float sxy[4] = {V.xy.e.x, V.xy.o.x, V.xy.e.y, V.xy.o.y};
         uint32_t packed = 0;
         float rv[4];
+        if constexpr (kResp) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int sxx = box_round(xu[i] + xm[i] + xd[i]);
-            const int syy = box_round(yu[i] + ym[i] + yd[i]);
-            const int sxy = box_round(zu[i] + zm[i] + zd[i]);
-            const long long det = static_cast<long long>(sxx) * syy - static_cast<long long>(sxy) * sxy;
-            const long long tr = static_cast<long long>(sxx) + syy;
-            const double r = __dsub_rn(__ll2double_rn(det), __dmul_rn(p.k, __ll2double_rn(tr * tr)));
-            const float rf = __double2float_rn(r);
-            rv[i] = rf;
-            const uint32_t m = static_cast<double>(rf) > p.threshold ? 255u : 0u;
-            packed |= m << (8 * i);
+            for (int i = 0; i < 4; ++i) {
+                rv[i] = exact_response(sxx[i], syy[i], sxy[i], p.k);
+                packed |= (static_cast<double>(rv[i]) > p.threshold ? 255u : 0u) << (8 * i);
+            }
+        } else {
+            // certified fp32 estimate of 81 (resp - T); p1 + p2 <= tt / 2
+            const float2 kn = f2(p.kneg, p.kneg), nt = f2(-p.t81, -p.t81);
+            const float2 ctt = f2(p.c_tt, p.c_tt), ctr = f2(p.c_tr, p.c_tr), c0 = f2(p.c0, p.c0);
+            const Q4 tr = qadd(V.xx, V.yy), tt = qmul(tr, tr);
+            const Q4 det = qsub(qmul(V.xx, V.yy), qmul(V.xy, V.xy));
+            const float2 dE = add2(fma2(kn, tt.e, det.e), nt), dO = add2(fma2(kn, tt.o, det.o), nt);
+            const float2 eE = fma2(ctt, tt.e, fma2(ctr, tr.e, c0)), eO = fma2(ctt, tt.o, fma2(ctr, tr.o, c0));
+            const float d[4] = {dE.x, dO.x, dE.y, dO.y};
+            const float e[4] = {eE.x, eO.x, eE.y, eO.y};
+            bool unsure = false;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                unsure |= !(fabsf(d[i]) > e[i]);
+                packed |= (d[i] > 0.f ? 255u : 0u) << (8 * i);
+            }
+            // rare, warp-uniform: the reference's exact expression where the
+            // estimate cannot decide
+            if (__any_sync(0xffffffffu, unsure)) {
+                packed = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    bool on;
+                    if (fabsf(d[i]) > e[i]) on = d[i] > 0.f;
+                    else on = static_cast<double>(exact_response(sxx[i], syy[i], sxy[i], p.k)) > p.threshold;
+                    packed |= (on ? 255u : 0u) << (8 * i);
+                }
+            }
+            (void)rv;
         }
-        const int row = gy - p.band.dst_row0;
-        uint8_t* mp = mrow_base + static_cast<int64_t>(row) * p.mask_pitch + c;
-        if (c + 3 < p.width) {
+        if (!owner) return;
+        uint8_t* mp = mrow + static_cast<int64_t>(orow) * p.mask_pitch;
+        if (c + 3 < W) {
             *reinterpret_cast<uint32_t*>(mp) = packed;
         } else {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                if (c + i < p.width) mp[i] = static_cast<uint8_t>(packed >> (8 * i));
+                if (c + i < W) mp[i] = static_cast<uint8_t>(packed >> (8 * i));
         }
-        if (kResp) {
-            float* rp = reinterpret_cast<float*>(rrow_base + static_cast<int64_t>(row) * p.resp_pitch) + c;
-            if (c + 3 < p.width) {
+        if constexpr (kResp) {
+            float* rp = reinterpret_cast<float*>(rrow + static_cast<int64_t>(orow) * p.resp_pitch) + c;
+            if (c + 3 < W) {
                 *reinterpret_cast<float4*>(rp) = make_float4(rv[0], rv[1], rv[2], rv[3]);
             } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (c + i < p.width) rp[i] = rv[i];
+                    if (c + i < W) rp[i] = rv[i];
             }
         }
     };
 
-    // smem row j <-> global y0-2+j.  Step j: Sobel terms of row j; Sobel row
-    // j-1 (products, horizontal box sums) at j >= 2; output row j-2 at j >= 4.
-    const int steps = (y1 - y0) + 4;
-    auto step = [&](int j, int (&da)[6], int (&db)[6], int (&dc)[6], int (&sa)[6], int (&sb)[6], int (&sc)[6],
-                    int (&xa)[4], int (&xb)[4], int (&xc)[4], int (&ya)[4], int (&yb)[4], int (&yc)[4],
-                    int (&za)[4], int (&zb)[4], int (&zc)[4]) {
-        int s[8];
-        fetch8h(tile + j * kHarSW, off, s);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            dc[k] = s[k + 2] - s[k];
-            sc[k] = s[k] + 2 * s[k + 1] + s[k + 2];
-        }
-        if (j < 2) return;
-        int px[6], py[6], pxy[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            const int gx = da[k] + 2 * db[k] + dc[k];
-            const int gy = sc[k] - sa[k];
-            px[k] = gx * gx;
-            py[k] = gy * gy;
-            pxy[k] = gx * gy;
-        }
-        if (klo == 0) {
-            px[0] = px[1];
-            py[0] = py[1];
-            pxy[0] = pxy[1];
-        }
-        int ex = px[1], ey = py[1], exy = pxy[1]; // last in-image column (static indices)
-#pragma unroll
-        for (int k = 2; k < 6; ++k)
-            if (k - 1 <= khi) {
-                ex = px[k];
-                ey = py[k];
-                exy = pxy[k];
-            }
-#pragma unroll
-        for (int k = 1; k < 6; ++k)
-            if (k - 1 > khi) {
-                px[k] = ex;
-                py[k] = ey;
-                pxy[k] = exy;
-            }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            xc[i] = px[i] + px[i + 1] + px[i + 2];
-            yc[i] = py[i] + py[i + 1] + py[i + 2];
-            zc[i] = pxy[i] + pxy[i + 1] + pxy[i + 2];
-        }
-        if (j < 4) return;
-        const int gy = y0 - 4 + j;
-        const bool t = gy == 0, b = gy == H - 1; // product rows clamp into the image
-        emit(gy, t ? xb : xa, xb, b ? xb : xc, t ? yb : ya, yb, b ? yb : yc, t ? zb : za, zb, b ? zb : zc);
+    // Running sums instead of 3-row rings:
+    //   gx(r-1) = Q(r-1) + Q(r) with Q(r) = D(r-1) + D(r)
+    //   gy(r-1) = T(r-1) + T(r) with T(r) = S(r) - S(r-1)
+    //   box(m-1) = P(m-1) + H(m) with P(m) = H(m-1) + H(m)
+    // smem row j <-> global y0-2+j; Sobel row j-1 -> product row j-1 ->
+    // output row j-2 (global y0-4+j) once j >= 4.
+    // State of the running sums, in two alternating copies (A, B) so the
+    // 2x-unrolled loop renames instead of moving registers.
+    struct State {
+        Q4 Dp, Qp, Sp, Tp; // D(r-1), Q(r-1), S(r-1), T(r-1)
+        Prod3 P, Hp;        // P(m-1), H(m-1)
     };
-    for (int j = 0; j < steps; j += 3) {
-        step(j, dA, dB, dC, sA, sB, sC, xA, xB, xC, yA, yB, yC, zA, zB, zC);
-        if (j + 1 < steps) step(j + 1, dB, dC, dA, sB, sC, sA, xB, xC, xA, yB, yC, yA, zB, zC, zA);
-        if (j + 2 < steps) step(j + 2, dC, dA, dB, sC, sA, sB, xC, xA, xB, yC, yA, yB, zC, zA, zB);
+    State A, B;
+    {
+        Q4 D0, S0, D1, S1;
+        sobel_terms(0, D0, S0);
+        sobel_terms(1, D1, S1);
+        A.Qp = qadd(D0, D1);
+        A.Tp = qsub(S1, S0);
+        A.Dp = D1;
+        A.Sp = S1;
+    }
+    /// Sobel row j-1 from source row j; writes the successor state into `o`.
+    auto sobel_step = [&](int j, const State& i, State& o) {
+        Q4 D, S;
+        sobel_terms(j, D, S);
+        o.Qp = qadd(i.Dp, D);
+        o.Tp = qsub(S, i.Sp);
+        o.Dp = D;
+        o.Sp = S;
+        return products(qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+    };
+    // product rows global y0-1 and y0 (row -1 clamps to row 0 at the top)
+    {
+        const Prod3 H1 = sobel_step(2, A, B);
+        const Prod3 H2 = sobel_step(3, B, A);
+        A.P = padd(y0 == 0 ? H2 : H1, H2);
+        A.Hp = H2;
+    }
+    auto full_step = [&](int j, const State& i, State& o) {
+        const Prod3 Hn = sobel_step(j, i, o);
+        emit(j - 4, padd(i.P, Hn));
+        o.P = padd(i.Hp, Hn);
+        o.Hp = Hn;
+    };
+    auto last_step = [&](int j, const State& i, State& o) {
+        // product row H clamps to row H-1 at the bottom border
+        const Prod3 Hn = sobel_step(j, i, o);
+        emit(j - 4, padd(i.P, (y1 == H) ? i.Hp : Hn));
+    };
+    const int steps = (y1 - y0) + 4;
+    int j = 4;
+    for (; j + 2 < steps; j += 2) {
+        full_step(j, A, B);
+        full_step(j + 1, B, A);
+    }
+    if (j + 1 < steps) {
+        full_step(j, A, B);
+        last_step(j + 1, B, A);
+    } else {
+        last_step(j, A, B);
     }
 }
 
@@ -214,6 +319,19 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     p.resp_fstride = a->response.frames > 1 ? a->response.frame_stride : a->response.pitch * a->response.height;
     p.k = a->k;
     p.threshold = a->threshold;
+    const double ak = a->k < 0 ? -a->k : a->k;
+    const double at = a->threshold < 0 ? -a->threshold : a->threshold;
+    p.kabs = static_cast<float>(ak);
+    p.kneg = static_cast<float>(-a->k);
+    p.t81 = static_cast<float>(81.0 * a->threshold);
+    // rounding perturbation (9 + 18|k|) tr + 40.5 + 81|k| plus the float
+    // representation errors of k and 81 T and the final float rounding of
+    // the response (|81 T| 2^-22); slack factors keep every term conservative
+    // (fl(tr) may be off by 1 above 2^24: +2|k| tr for the tt perturbation)
+    p.c_tr = static_cast<float>((9.0 + 20.0 * ak) * 1.01 + 1.0);
+    // fp32 evaluation error <= 2^-20 (p1 + p2 + |k| tt) <= 2^-20 (1/2 + |k|) tt
+    p.c_tt = static_cast<float>(std::ldexp(0.5 + ak, -20) * 1.01);
+    p.c0 = static_cast<float>((40.5 + 81.0 * ak) * 1.1 + 81.0 * at * 5e-7 + 64.0);
     const int frames = s.frames > 0 ? s.frames : 1;
     dim3 grid((s.width + kHarTW - 1) / kHarTW, (rows + kHarTH - 1) / kHarTH, frames);
     void* args[] = {&map, &p};

@@ -18,8 +18,10 @@ struct Band {
 
 /// smem tile: image columns [x_org, x_org + SW), global rows [y_org, y_org + SH),
 /// one TMA box (the map views the plane as u32, see make_u8_tensor_map).
-/// SW must be a multiple of 16 and <= 1024; x_org a multiple of 4; the
-/// tile base 128-byte aligned.
+/// SW must be a multiple of 16 and <= 1024; the tile base 128-byte aligned;
+/// x_org MUST be a multiple of 16: a tiled TMA box whose inner start
+/// coordinate is not 16-byte aligned faults with "illegal instruction" on
+/// B200 (measured).
 template <int SW, int SH>
 __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* map, uint64_t* bar, int x_org,
                                               int y_org, int frame, int width, const Band& band) {
@@ -37,26 +39,33 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* 
     if (!(left | right | top | bottom)) return; // block-uniform
 
     // 1) replicate edge columns in rows that lie inside the image
+    //    (warp per row, lane per column: no integer division on this path)
+    const int nwarps = static_cast<int>(blockDim.x) >> 5, wid = static_cast<int>(threadIdx.x) >> 5;
+    const int ln = static_cast<int>(threadIdx.x) & 31;
     if (left | right) {
         const int first = clampi(-x_org, 0, SW - 1);           // smem col of image col 0
         const int last = clampi(width - 1 - x_org, 0, SW - 1); // smem col of image col W-1
-        for (int i = threadIdx.x; i < SH * SW; i += blockDim.x) {
-            const int r = i / SW, j = i - r * SW;
+        for (int r = wid; r < SH; r += nwarps) {
             const int gy = y_org + r;
             if (gy < 0 || gy >= band.global_h) continue;
-            if (j < first) tile[r * SW + j] = tile[r * SW + first];
-            else if (j > last) tile[r * SW + j] = tile[r * SW + last];
+            uint8_t* row = tile + r * SW;
+            const uint8_t vf = row[first], vl = row[last];
+            for (int j = ln; j < SW; j += 32) {
+                if (j < first) row[j] = vf;
+                else if (j > last) row[j] = vl;
+            }
         }
         __syncthreads();
     }
     // 2) replicate edge rows
     if (top | bottom) {
-        for (int i = threadIdx.x; i < SH * SW; i += blockDim.x) {
-            const int r = i / SW, j = i - r * SW;
+        for (int r = wid; r < SH; r += nwarps) {
             const int gy = y_org + r;
             if (gy >= 0 && gy < band.global_h) continue;
             const int src = clampi(gy, 0, band.global_h - 1) - y_org;
-            tile[r * SW + j] = tile[src * SW + j];
+            const uint32_t* from = reinterpret_cast<const uint32_t*>(tile + src * SW);
+            uint32_t* to = reinterpret_cast<uint32_t*>(tile + r * SW);
+            for (int j = ln; j < SW / 4; j += 32) to[j] = from[j];
         }
         __syncthreads();
     }
