@@ -1,31 +1,36 @@
 // K1 — fused Gaussian3x3 -> Sobel3x3 -> Magnitude (U8 -> S16), one pass.
 //
 // Reference semantics reproduced bit-exactly:
-//   gaussian3x3  sat_U8(llround(sum(mask*win) * (1/16)))  == (s + 8) >> 4
-//                (ref:src/registry.cpp:722-746; s in [0, 4080] -> exact)
-//   sobel_x/y    sat_S16(sum(mask*win)), |v| <= 1020
-//                (ref:src/registry.cpp:748-784)
-//   magnitude    sat_S16(llround(sqrt((double)(gx*gx + gy*gy))))
-//                (ref:src/registry.cpp:555-575) via gvxd::round_sqrt_exact
+//   gaussian3x3  sat_U8(llround(s * (1/16))) == floor((s + 8) / 16), s <= 4080
+//                (ref:src/registry.cpp:722-746)
+//   sobel_x/y    sat_S16(sum(mask * win)), |v| <= 1020 (ref:src/registry.cpp:748-784)
+//   magnitude    sat_S16(llround(sqrt((double)(gx^2 + gy^2))))
+//                (ref:src/registry.cpp:555-575): fp32 estimate + exact
+//                integer correction, n = gx^2 + gy^2 < 2^22
 //   Clamp of the *intermediate*: the Gaussian at an out-of-image position is
 //   the Gaussian of the clamped position (run_naive materialises it and the
 //   Sobel window clamps into it, ref:src/execute.cpp:242-245).
+// Every intermediate is an integer < 2^24, so the pipeline runs on packed
+// FP32 (FFMA2/FADD2/FMUL2) with exact arithmetic; see packed.cuh.
 //
-// Layout: CTA = 128 threads, output tile 512 x 32; each thread owns 4
-// adjacent columns and streams down the rows keeping the horizontal sums,
-// the Gaussian rows and the Sobel windows in registers (a 3-row ring), so
-// every input byte is read from HBM once (plus a 4-row halo) and every output
-// written once: 1 B in + 2 B out per output (3 B/px algorithmic traffic).
-#include "tile.cuh"
+// Layout: CTA = 4 warps, 30 owner lanes x 4 columns per warp (lanes 0 / 31
+// are halo lanes whose Gaussian columns reach their neighbours by warp
+// shuffles), 64 output rows per CTA streamed with running sums:
+//   Gaussian  v(r-1) = R(r-1) + R(r),  R(r) = Hg(r-1) + Hg(r)
+//   Sobel     gx(r-1) = Q(r-1) + Q(r), Q(r) = D(r-1) + D(r)
+//             gy(r-1) = T(r-1) + T(r), T(r) = S(r) - S(r-1)
+// so every input byte is read from HBM once (+ a 4-row halo) and every
+// output written once: 1 B in + 2 B out per output pixel.
+#include "packed.cuh"
 
 namespace gvxd {
 
 constexpr int kEdgeThreads = 128;
-constexpr int kEdgeTW = 4 * kEdgeThreads; // 512 output columns per CTA
-constexpr int kEdgeTH = 32;               // output rows per CTA
-constexpr int kEdgeSW = kEdgeTW + 64;     // smem columns [x0 - 32, x0 + 544)
-constexpr int kEdgeSH = kEdgeTH + 4;      // smem rows    [y0 - 2, y0 + 34)
-constexpr int kEdgeBox = 192;
+constexpr int kEdgeWarpCols = 120;
+constexpr int kEdgeTW = kEdgeWarpCols * (kEdgeThreads / 32); // 480
+constexpr int kEdgeTH = 64;
+constexpr int kEdgeSW = kEdgeTW + 32; // smem columns [x0 - 16, x0 + 496)
+constexpr int kEdgeSH = kEdgeTH + 4;  // smem rows    [y0 - 2, y0 + 66)
 
 struct OutPlane {
     int16_t* data;
@@ -39,32 +44,45 @@ struct EdgeParams {
     OutPlane gx, gy, mag;
 };
 
-__device__ __forceinline__ void store4(const OutPlane& o, int frame, int row, int c, int width, int v0, int v1,
-                                       int v2, int v3) {
+/// Integer-valued floats |v| < 2^22 to int16 pairs packed in a u32.
+__device__ __forceinline__ uint32_t pack_s16(float lo, float hi) {
+    const float m = 12582912.f; // 1.5 * 2^23: low mantissa bits = two's complement value
+    return __byte_perm(__float_as_uint(lo + m), __float_as_uint(hi + m), 0x5410);
+}
+
+__device__ __forceinline__ void store4(const OutPlane& o, int frame, int row, int c, int width, Q4 v) {
     char* base = reinterpret_cast<char*>(o.data) + frame * o.frame_stride + static_cast<int64_t>(row) * o.pitch;
     int16_t* p = reinterpret_cast<int16_t*>(base) + c;
+    // columns c, c+1, c+2, c+3 = e.x, o.x, e.y, o.y
     if (c + 3 < width) {
-        uint2 w;
-        w.x = (static_cast<uint32_t>(v0) & 0xFFFFu) | (static_cast<uint32_t>(v1) << 16);
-        w.y = (static_cast<uint32_t>(v2) & 0xFFFFu) | (static_cast<uint32_t>(v3) << 16);
-        *reinterpret_cast<uint2*>(p) = w;
+        *reinterpret_cast<uint2*>(p) = make_uint2(pack_s16(v.e.x, v.o.x), pack_s16(v.e.y, v.o.y));
     } else {
-        const int v[4] = {v0, v1, v2, v3};
+        const float vv[4] = {v.e.x, v.o.x, v.e.y, v.o.y};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (c + i < width) p[i] = static_cast<int16_t>(v[i]);
+            if (c + i < width) p[i] = static_cast<int16_t>(__float2int_rn(vv[i]));
     }
 }
 
-/// 8 source bytes for columns c-2 .. c+5 from three aligned words.
-__device__ __forceinline__ void fetch8(const uint8_t* row, int off, int (&a)[8]) {
-    const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
-    a[0] = byte_of(wl, 2);
-    a[1] = byte_of(wl, 3);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) a[2 + k] = byte_of(wc, k);
-    a[6] = byte_of(wr, 0);
-    a[7] = byte_of(wr, 1);
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+/// round(sqrt(n)) half away from zero for integer-valued 0 <= n < 2^22:
+/// k0 = floor(s + 0.49) in {k*-1, k*} for the approximate s, then
+/// k* = k0 + (n > k0^2 + k0) (k* is the largest k with k^2 - k < n).
+__device__ __forceinline__ Q4 round_sqrt4(Q4 n) {
+    const float2 M = f2(12582912.f, 12582912.f), nM = f2(-12582912.f, -12582912.f), d = f2(-0.01f, -0.01f);
+    const Q4 s{f2(sqrt_approx(n.e.x), sqrt_approx(n.e.y)), f2(sqrt_approx(n.o.x), sqrt_approx(n.o.y))};
+    Q4 k{add2(add2(add2(s.e, d), M), nM), add2(add2(add2(s.o, d), M), nM)};
+    const Q4 kk{fma2(k.e, k.e, k.e), fma2(k.o, k.o, k.o)};
+    k.e.x += n.e.x > kk.e.x ? 1.f : 0.f;
+    k.e.y += n.e.y > kk.e.y ? 1.f : 0.f;
+    k.o.x += n.o.x > kk.o.x ? 1.f : 0.f;
+    k.o.y += n.o.y > kk.o.y ? 1.f : 0.f;
+    return k;
 }
 
 template <bool kGauss, bool kGx, bool kGy, bool kMag>
@@ -77,91 +95,144 @@ __global__ void __launch_bounds__(kEdgeThreads) edge_kernel(const __grid_constan
     const int y1 = min(y0 + kEdgeTH, p.band.row1);
     const int frame = blockIdx.z;
     const int H = p.band.global_h;
+    const int W = p.width;
 
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         fence_barrier_init();
     }
     __syncthreads();
-    stage_tile_u8<kEdgeSW, kEdgeSH>(tile, &map, &bar, x0 - 32, y0 - 2, frame, p.width, p.band);
+    stage_tile_u8<kEdgeSW, kEdgeSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band);
 
-    const int c = x0 + 4 * static_cast<int>(threadIdx.x);
-    if (c >= p.width) return;
-    const int off = 4 * static_cast<int>(threadIdx.x) + 32; // smem column of c
-    // horizontal clamp of the Gaussian intermediate: slot k (column c+k,
-    // k = -1..4) reads the column clamped into the image
-    const int klo = c == 0 ? 0 : -1;
-    const int khi = min(4, p.width - 1 - c);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = x0 + kEdgeWarpCols * warp + 4 * (lane - 1);
+    const int off = c - (x0 - 16);
+    const bool owner = lane >= 1 && lane <= 30 && c < W;
+    const bool left_edge = c == 0;
+    const bool right_edge = c + 4 >= W;
+    const int last = W - 1 - c;
+    const int orow0 = y0 - p.band.dst_row0;
 
-    int hA[6], hB[6], hC[6]; // horizontal Gaussian sums, 3-row ring
-    int gA[6], gB[6], gC[6]; // Gaussian (or source) rows, columns c-1 .. c+4
-
-    auto emit = [&](int gy, const int (&u)[6], const int (&m)[6], const int (&d)[6]) {
-        // u = row gy-1, m = row gy, d = row gy+1 (after vertical clamping)
-        int vx[4], vy[4], vm[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            vx[i] = (u[i + 2] - u[i]) + 2 * (m[i + 2] - m[i]) + (d[i + 2] - d[i]);
-            vy[i] = (d[i] + 2 * d[i + 1] + d[i + 2]) - (u[i] + 2 * u[i + 1] + u[i + 2]);
-            if (kMag) vm[i] = round_sqrt_exact(vx[i] * vx[i] + vy[i] * vy[i]);
-        }
-        const int row = gy - p.band.dst_row0;
-        if (kGx) store4(p.gx, frame, row, c, p.width, vx[0], vx[1], vx[2], vx[3]);
-        if (kGy) store4(p.gy, frame, row, c, p.width, vy[0], vy[1], vy[2], vy[3]);
-        if (kMag) store4(p.mag, frame, row, c, p.width, vm[0], vm[1], vm[2], vm[3]);
+    auto emit = [&](int r, Q4 gx, Q4 gy) {
+        if (!owner) return;
+        if (kGx) store4(p.gx, frame, orow0 + r, c, W, gx);
+        if (kGy) store4(p.gy, frame, orow0 + r, c, W, gy);
+        if (kMag)
+            store4(p.mag, frame, orow0 + r, c, W,
+                   round_sqrt4(Q4{fma2(gx.e, gx.e, mul2(gy.e, gy.e)), fma2(gx.o, gx.o, mul2(gy.o, gy.o))}));
     };
 
+    struct State {
+        Q4 Dp, Qp, Sp, Tp; // Sobel running sums over the (Gaussian) rows
+        Q4 Hp, Rp;         // Gaussian running sums over source rows
+    };
+    State A, B;
+
     if constexpr (kGauss) {
-        // smem row j <-> global row y0-2+j; g(j-1) ready at step j >= 2;
-        // output row y0-4+j ready at step j >= 4.
-        const int steps = (y1 - y0) + 4;
-        auto step = [&](int j, int (&a)[6], int (&b)[6], int (&cc)[6], int (&ga)[6], int (&gb)[6],
-                        int (&gc)[6]) {
-            int s[8];
-            fetch8(tile + j * kEdgeSW, off, s);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) cc[k] = s[k] + 2 * s[k + 1] + s[k + 2];
-            if (klo == 0) cc[0] = cc[1];
-            int edge = cc[1]; // value of the last in-image column (static indices only)
-#pragma unroll
-            for (int k = 2; k < 6; ++k)
-                if (k - 1 <= khi) edge = cc[k];
-#pragma unroll
-            for (int k = 1; k < 6; ++k)
-                if (k - 1 > khi) cc[k] = edge;
-            if (j < 2) return;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) gc[k] = (a[k] + 2 * b[k] + cc[k] + 8) >> 4;
-            if (j < 4) return;
-            const int gy = y0 - 4 + j;
-            // vertical clamp of the intermediate: g(-1) := g(0), g(H) := g(H-1)
-            emit(gy, gy == 0 ? gb : ga, gb, gy == H - 1 ? gb : gc);
+        const float2 sc = f2(0.0625f, 0.0625f), M = f2(12582912.f, 12582912.f);
+        const float2 nM = f2(-12582912.f, -12582912.f);
+        /// Gaussian row (exact) from the biased sum v' = v + 8 (the +8 rides
+        /// in the source conversion, see load_cols6_biased):
+        /// floor(v' / 16) = fma_rd(v', 1/16, 1.5 * 2^23) - 1.5 * 2^23.
+        auto gauss_round = [&](Q4 v) {
+            return Q4{add2(__ffma2_rd(v.e, sc, M), nM), add2(__ffma2_rd(v.o, sc, M), nM)};
         };
-        for (int j = 0; j < steps; j += 3) {
-            step(j, hA, hB, hC, gA, gB, gC);
-            if (j + 1 < steps) step(j + 1, hB, hC, hA, gB, gC, gA);
-            if (j + 2 < steps) step(j + 2, hC, hA, hB, gC, gA, gB);
+        /// Sobel row terms of a Gaussian row held in registers (neighbour
+        /// columns through shuffles, clamped at the image border).
+        auto gauss_sobel_terms = [&](Q4 g, Q4& D, Q4& S) {
+            if (right_edge && last < 3) {
+                float v[4] = {g.e.x, g.o.x, g.e.y, g.o.y};
+#pragma unroll
+                for (int i = 1; i < 4; ++i)
+                    if (i > last) v[i] = v[i - 1];
+                g = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
+            }
+            float gl = __shfl_up_sync(0xffffffffu, g.o.y, 1);
+            float gr = __shfl_down_sync(0xffffffffu, g.e.x, 1);
+            gl = left_edge ? g.e.x : gl;
+            gr = right_edge ? g.o.y : gr;
+            diff_smooth(neighbourhood(g, gl, gr), D, S);
+        };
+        /// Source row j: Gaussian horizontal sums; returns the Gaussian row
+        /// centred one row up (smem row j-1).
+        auto src_step = [&](int j, const State& i, State& o) {
+            Q4 Dn, Hg;
+            diff_smooth(load_cols6_biased(tile + j * kEdgeSW, off), Dn, Hg); // Hg + 2 (Dn unused)
+            o.Rp = qadd(i.Hp, Hg);
+            o.Hp = Hg;
+            return gauss_round(qadd(i.Rp, o.Rp));
+        };
+        {
+            Q4 Dn, S0, S1;
+            diff_smooth(load_cols6_biased(tile, off), Dn, S0);
+            diff_smooth(load_cols6_biased(tile + kEdgeSW, off), Dn, S1);
+            A.Hp = S1;
+            A.Rp = qadd(S0, S1);
+        }
+        Q4 D1, G1, D2, G2;
+        gauss_sobel_terms(src_step(2, A, B), D1, G1); // Gaussian row y0-1
+        gauss_sobel_terms(src_step(3, B, A), D2, G2); // Gaussian row y0
+        if (y0 == 0) {                                // Gaussian row -1 clamps to row 0
+            D1 = D2;
+            G1 = G2;
+        }
+        A.Qp = qadd(D1, D2);
+        A.Tp = qsub(G2, G1);
+        A.Dp = D2;
+        A.Sp = G2;
+        auto full_step = [&](int j, const State& i, State& o, bool bottom) {
+            Q4 D, S;
+            gauss_sobel_terms(src_step(j, i, o), D, S);
+            if (bottom) { // Gaussian row H clamps to row H-1
+                D = i.Dp;
+                S = i.Sp;
+            }
+            o.Qp = qadd(i.Dp, D);
+            o.Tp = qsub(S, i.Sp);
+            o.Dp = D;
+            o.Sp = S;
+            emit(j - 4, qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+        };
+        const int steps = (y1 - y0) + 4;
+        int j = 4;
+        for (; j + 2 < steps; j += 2) {
+            full_step(j, A, B, false);
+            full_step(j + 1, B, A, false);
+        }
+        const bool bot = y1 == H;
+        if (j + 1 < steps) {
+            full_step(j, A, B, false);
+            full_step(j + 1, B, A, bot);
+        } else {
+            full_step(j, A, B, bot);
         }
     } else {
-        // Sobel straight on the source: g := input row (Clamp already in smem).
-        // smem row j <-> global row y0-2+j; output row y0-3+j at step j >= 3.
-        const int steps = (y1 - y0) + 3;
-        auto step = [&](int j, int (&ga)[6], int (&gb)[6], int (&gc)[6]) {
-            int s[8];
-            fetch8(tile + j * kEdgeSW, off, s);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) gc[k] = s[k + 1];
-            if (j < 3) return;
-            emit(y0 - 3 + j, ga, gb, gc);
-        };
-        (void)hA;
-        (void)hB;
-        (void)hC;
-        for (int j = 1; j < steps; j += 3) {
-            step(j, gA, gB, gC);
-            if (j + 1 < steps) step(j + 1, gB, gC, gA);
-            if (j + 2 < steps) step(j + 2, gC, gA, gB);
+        // Sobel straight on the source (Clamp is already in shared memory)
+        {
+            Q4 D0, S0, D1, S1;
+            diff_smooth(load_cols6(tile + 1 * kEdgeSW, off), D0, S0); // global y0-1
+            diff_smooth(load_cols6(tile + 2 * kEdgeSW, off), D1, S1); // global y0
+            A.Qp = qadd(D0, D1);
+            A.Tp = qsub(S1, S0);
+            A.Dp = D1;
+            A.Sp = S1;
         }
+        auto step = [&](int j, const State& i, State& o) {
+            Q4 D, S;
+            diff_smooth(load_cols6(tile + j * kEdgeSW, off), D, S);
+            o.Qp = qadd(i.Dp, D);
+            o.Tp = qsub(S, i.Sp);
+            o.Dp = D;
+            o.Sp = S;
+            emit(j - 3, qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+        };
+        const int steps = (y1 - y0) + 3;
+        int j = 3;
+        for (; j + 1 < steps; j += 2) {
+            step(j, A, B);
+            step(j + 1, B, A);
+        }
+        if (j < steps) step(j, A, B);
     }
 }
 
@@ -178,9 +249,6 @@ OutPlane plane(const gvxb_image& img) {
     o.frame_stride = img.frames > 1 ? img.frame_stride : img.pitch * img.height;
     return o;
 }
-
-template <bool G>
-using EdgeFn = void (*)(const CUtensorMap, EdgeParams);
 
 template <bool G>
 void* pick_edge(bool ox, bool oy, bool om) {

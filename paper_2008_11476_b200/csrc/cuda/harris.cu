@@ -28,7 +28,7 @@
 // shuffles), 64 rows per CTA streamed with 3-row register rings.  Columns
 // are kept as even/odd float2 pairs ((c, c+2), (c+1, c+3)) so every
 // separable stencil step is a packed, register-aligned FP32 op.
-#include "tile.cuh"
+#include "packed.cuh"
 
 #include <cmath>
 
@@ -57,25 +57,6 @@ struct HarrisParams {
     float c_tr;  // bound slope in tr
     float c0;    // bound constant
 };
-
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-
-/// 2^23 + byte k of w (the float bit pattern 0x4B0000bb).
-__device__ __forceinline__ float magic_byte(uint32_t w, int k) {
-    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | static_cast<unsigned>(k)));
-}
-
-/// 4 columns of one quantity as (even, odd) float2 pairs: (c, c+2), (c+1, c+3).
-struct Q4 {
-    float2 e, o;
-};
-__device__ __forceinline__ Q4 qadd(Q4 a, Q4 b) { return Q4{add2(a.e, b.e), add2(a.o, b.o)}; }
-__device__ __forceinline__ Q4 qsub(Q4 a, Q4 b) { return Q4{sub2(a.e, b.e), sub2(a.o, b.o)}; }
-__device__ __forceinline__ Q4 qmul(Q4 a, Q4 b) { return Q4{mul2(a.e, b.e), mul2(a.o, b.o)}; }
 
 struct Prod3 {
     Q4 xx, yy, xy; // horizontal box sums of one product row
