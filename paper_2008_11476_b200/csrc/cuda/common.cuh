@@ -124,3 +124,27 @@ struct TileGeom {
 };
 
 } // namespace gvxb_impl
+
+namespace gvxb_impl {
+
+/// Rows per tile for a tiled stencil launch: tiles = strips * ceil(rows / th)
+/// run in waves of `slots` resident CTAs and each tile also pays `halo`
+/// extra rows, so pick th <= th_max minimising waves * (th + halo).
+inline int balanced_tile_rows(long long strips, int rows, long long slots, int th_max, int halo, int th_min = 8) {
+    if (slots < 1) slots = 1;
+    int best = th_max;
+    long long best_cost = -1;
+    for (int th = th_max; th >= th_min; --th) {
+        const long long tiles = strips * ((rows + th - 1) / th);
+        const long long waves = (tiles + slots - 1) / slots;
+        const long long cost = waves * (th + halo);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = th;
+        }
+        if (th >= rows) continue;
+    }
+    return best;
+}
+
+} // namespace gvxb_impl

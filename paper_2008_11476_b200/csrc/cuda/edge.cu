@@ -40,6 +40,7 @@ struct OutPlane {
 
 struct EdgeParams {
     int width;
+    int th; // output rows per tile (<= kEdgeTH), chosen to fill whole waves
     Band band;
     OutPlane gx, gy, mag;
 };
@@ -91,8 +92,8 @@ __global__ void __launch_bounds__(kEdgeThreads) edge_kernel(const __grid_constan
     __shared__ uint64_t bar;
 
     const int x0 = blockIdx.x * kEdgeTW;
-    const int y0 = p.band.row0 + blockIdx.y * kEdgeTH;
-    const int y1 = min(y0 + kEdgeTH, p.band.row1);
+    const int y0 = p.band.row0 + blockIdx.y * p.th;
+    const int y1 = min(y0 + p.th, p.band.row1);
     const int frame = blockIdx.z;
     const int H = p.band.global_h;
     const int W = p.width;
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(kEdgeThreads) edge_kernel(const __grid_constan
         fence_barrier_init();
     }
     __syncthreads();
-    stage_tile_u8<kEdgeSW, kEdgeSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band);
+    stage_tile_u8<kEdgeSW, kEdgeSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band, p.th + 4);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = x0 + kEdgeWarpCols * warp + 4 * (lane - 1);
@@ -276,16 +277,20 @@ extern "C" int gvxb_edge(gvxb_ctx ctx, const gvxb_edge_args* a) {
     if (!fn) return GVXB_OK; // nothing requested
     const int rows = a->band.row1 - a->band.row0;
     if (rows <= 0 || s.width <= 0) return GVXB_OK;
-    CUtensorMap map;
-    if (int rc = make_u8_tensor_map(&map, s, kEdgeSW, kEdgeSH)) return rc;
+    const int frames = s.frames > 0 ? s.frames : 1;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEdgeThreads, 0);
+    const long long strips = static_cast<long long>(frames) * ((s.width + kEdgeTW - 1) / kEdgeTW);
     EdgeParams p;
+    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm) * ctx->sm_count, kEdgeTH, 4);
+    CUtensorMap map;
+    if (int rc = make_u8_tensor_map(&map, s, kEdgeSW, p.th + 4)) return rc;
     p.width = s.width;
     p.band = Band{a->band.row0, a->band.row1, a->band.global_h, a->band.src_row0, a->band.dst_row0};
     p.gx = plane(a->gx);
     p.gy = plane(a->gy);
     p.mag = plane(a->mag);
-    const int frames = s.frames > 0 ? s.frames : 1;
-    dim3 grid((s.width + kEdgeTW - 1) / kEdgeTW, (rows + kEdgeTH - 1) / kEdgeTH, frames);
+    dim3 grid((s.width + kEdgeTW - 1) / kEdgeTW, (rows + p.th - 1) / p.th, frames);
     void* args[] = {&map, &p};
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kEdgeThreads), args, 0, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "edge kernel launch");

@@ -43,6 +43,7 @@ constexpr int kHarSH = kHarTH + 4;  // smem rows    [y0 - 2, y0 + 66)
 
 struct HarrisParams {
     int width;
+    int th; // output rows per tile (<= kHarTH), chosen to fill whole waves
     Band band;
     uint8_t* mask;
     int64_t mask_pitch, mask_fstride;
@@ -82,8 +83,8 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
     __shared__ uint64_t bar;
 
     const int x0 = blockIdx.x * kHarTW;
-    const int y0 = p.band.row0 + blockIdx.y * kHarTH;
-    const int y1 = min(y0 + kHarTH, p.band.row1);
+    const int y0 = p.band.row0 + blockIdx.y * p.th;
+    const int y1 = min(y0 + p.th, p.band.row1);
     const int frame = blockIdx.z;
     const int H = p.band.global_h;
     const int W = p.width;
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
         fence_barrier_init();
     }
     __syncthreads();
-    stage_tile_u8<kHarSW, kHarSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band);
+    stage_tile_u8<kHarSW, kHarSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band, p.th + 4);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int c = x0 + kHarWarpCols * warp + 4 * (lane - 1); // first column of this lane
@@ -287,9 +288,16 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     if (!a->mask.data) return fail(GVXB_ERR_INVALID, "harris: mask output required");
     const int rows = a->band.row1 - a->band.row0;
     if (rows <= 0 || s.width <= 0) return GVXB_OK;
-    CUtensorMap map;
-    if (int rc = make_u8_tensor_map(&map, s, kHarSW, kHarSH)) return rc;
     HarrisParams p;
+    const int frames = s.frames > 0 ? s.frames : 1;
+    void* fn = a->response.data ? reinterpret_cast<void*>(&harris_kernel<true>)
+                                : reinterpret_cast<void*>(&harris_kernel<false>);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kHarThreads, 0);
+    const long long strips = static_cast<long long>(frames) * ((s.width + kHarTW - 1) / kHarTW);
+    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm) * ctx->sm_count, kHarTH, 4);
+    CUtensorMap map;
+    if (int rc = make_u8_tensor_map(&map, s, kHarSW, p.th + 4)) return rc;
     p.width = s.width;
     p.band = Band{a->band.row0, a->band.row1, a->band.global_h, a->band.src_row0, a->band.dst_row0};
     p.mask = static_cast<uint8_t*>(a->mask.data);
@@ -313,10 +321,8 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     // fp32 evaluation error <= 2^-20 (p1 + p2 + |k| tt) <= 2^-20 (1/2 + |k|) tt
     p.c_tt = static_cast<float>(std::ldexp(0.5 + ak, -20) * 1.01);
     p.c0 = static_cast<float>((40.5 + 81.0 * ak) * 1.1 + 81.0 * at * 5e-7 + 64.0);
-    const int frames = s.frames > 0 ? s.frames : 1;
-    dim3 grid((s.width + kHarTW - 1) / kHarTW, (rows + kHarTH - 1) / kHarTH, frames);
+    dim3 grid((s.width + kHarTW - 1) / kHarTW, (rows + p.th - 1) / p.th, frames);
     void* args[] = {&map, &p};
-    void* fn = p.resp ? reinterpret_cast<void*>(&harris_kernel<true>) : reinterpret_cast<void*>(&harris_kernel<false>);
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kHarThreads), args, 0, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "harris kernel launch");
     return check_launch(ctx, "harris kernel");

@@ -22,12 +22,14 @@ struct Band {
 /// x_org MUST be a multiple of 16: a tiled TMA box whose inner start
 /// coordinate is not 16-byte aligned faults with "illegal instruction" on
 /// B200 (measured).
+/// `sh` (<= SH) rows are loaded: the tensor map's box height (a tile of
+/// sh - halo output rows, chosen per launch to fill whole waves).
 template <int SW, int SH>
 __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* map, uint64_t* bar, int x_org,
-                                              int y_org, int frame, int width, const Band& band) {
+                                              int y_org, int frame, int width, const Band& band, int sh = SH) {
     static_assert(SW % 16 == 0 && SW <= 1024 && SH <= 256, "bad tile geometry");
     if (threadIdx.x == 0) {
-        mbar_expect_tx(bar, SW * SH);
+        mbar_expect_tx(bar, SW * sh);
         tma_load_3d(tile, map, bar, x_org / 4, y_org - band.src_row0, frame);
     }
     mbar_wait(bar, 0);
@@ -35,7 +37,7 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* 
     const bool left = x_org < 0;
     const bool right = x_org + SW > width;
     const bool top = y_org < 0;
-    const bool bottom = y_org + SH > band.global_h;
+    const bool bottom = y_org + sh > band.global_h;
     if (!(left | right | top | bottom)) return; // block-uniform
 
     // 1) replicate edge columns in rows that lie inside the image
@@ -45,7 +47,7 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* 
     if (left | right) {
         const int first = clampi(-x_org, 0, SW - 1);           // smem col of image col 0
         const int last = clampi(width - 1 - x_org, 0, SW - 1); // smem col of image col W-1
-        for (int r = wid; r < SH; r += nwarps) {
+        for (int r = wid; r < sh; r += nwarps) {
             const int gy = y_org + r;
             if (gy < 0 || gy >= band.global_h) continue;
             uint8_t* row = tile + r * SW;
@@ -59,7 +61,7 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* 
     }
     // 2) replicate edge rows
     if (top | bottom) {
-        for (int r = wid; r < SH; r += nwarps) {
+        for (int r = wid; r < sh; r += nwarps) {
             const int gy = y_org + r;
             if (gy >= 0 && gy < band.global_h) continue;
             const int src = clampi(gy, 0, band.global_h - 1) - y_org;
