@@ -125,6 +125,7 @@ int gvxb_event_create(void** ev);
 int gvxb_event_destroy(void* ev);
 int gvxb_event_record(gvxb_ctx ctx, void* ev);
 int gvxb_event_elapsed_ms(void* start, void* stop, float* ms);
+int gvxb_event_sync(void* ev); /* host waits for the event */
 
 /* ---- device status word / event counters ----------------------------------- */
 int gvxb_status_reset(gvxb_ctx ctx);

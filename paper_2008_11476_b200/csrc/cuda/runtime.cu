@@ -218,6 +218,11 @@ int gvxb_event_elapsed_ms(void* a, void* b, float* ms) {
     return r == cudaSuccess ? GVXB_OK : cuda_fail(r, "cudaEventElapsedTime");
 }
 
+int gvxb_event_sync(void* ev) {
+    cudaError_t r = cudaEventSynchronize(static_cast<cudaEvent_t>(ev));
+    return r == cudaSuccess ? GVXB_OK : cuda_fail(r, "cudaEventSynchronize");
+}
+
 int gvxb_status_reset(gvxb_ctx ctx) {
     cudaError_t e = cudaMemsetAsync(ctx->status, 0, sizeof(unsigned) + 2 * sizeof(unsigned long long),
                                     ctx->stream);

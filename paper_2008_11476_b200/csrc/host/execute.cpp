@@ -557,8 +557,73 @@ std::shared_ptr<Program> build_plan(const OptimizedPlan& plan, const std::map<Ob
 
 // ============================================================== sessions
 
+/// Pinned double-buffered staging for host<->device image copies: the CPU
+/// copy of chunk i+1 into pinned memory overlaps the DMA of chunk i, instead
+/// of the driver's synchronous pageable path.
+struct Staging {
+    static constexpr std::size_t kChunk = std::size_t(2) << 20;
+    gvxb_ctx ctx = nullptr;
+    void* buf[2] = {nullptr, nullptr};
+    void* ev[2] = {nullptr, nullptr};
+    bool pending[2] = {false, false};
+
+    explicit Staging(gvxb_ctx c) : ctx(c) {
+        for (int i = 0; i < 2; ++i) {
+            dev::check(gvxb_host_alloc(kChunk, &buf[i]), "pinned staging allocation");
+            dev::check(gvxb_event_create(&ev[i]), "staging event");
+        }
+    }
+    ~Staging() {
+        for (int i = 0; i < 2; ++i) {
+            if (ev[i]) gvxb_event_sync(ev[i]), gvxb_event_destroy(ev[i]);
+            if (buf[i]) gvxb_host_free(buf[i]);
+        }
+    }
+    void wait(int k) {
+        if (pending[k]) dev::check(gvxb_event_sync(ev[k]), "staging wait");
+        pending[k] = false;
+    }
+    void mark(int k) {
+        dev::check(gvxb_event_record(ctx, ev[k]), "staging event");
+        pending[k] = true;
+    }
+
+    void upload(char* dst, std::size_t pitch, const std::uint8_t* src, std::size_t row, std::size_t rows) {
+        const std::size_t per = std::max<std::size_t>(1, kChunk / row);
+        int k = 0;
+        for (std::size_t r0 = 0; r0 < rows; r0 += per, k ^= 1) {
+            const std::size_t n = std::min(per, rows - r0);
+            wait(k);
+            std::memcpy(buf[k], src + r0 * row, n * row);
+            dev::check(gvxb_upload_2d(ctx, dst + r0 * pitch, pitch, buf[k], row, row, n), "image upload");
+            mark(k);
+        }
+    }
+
+    void download(std::uint8_t* dst, const char* src, std::size_t pitch, std::size_t row, std::size_t rows) {
+        const std::size_t per = std::max<std::size_t>(1, kChunk / row);
+        const std::size_t chunks = (rows + per - 1) / per;
+        auto issue = [&](std::size_t c) {
+            const int k = static_cast<int>(c & 1);
+            wait(k);
+            const std::size_t r0 = c * per, n = std::min(per, rows - r0);
+            dev::check(gvxb_download_2d(ctx, buf[k], row, src + r0 * pitch, pitch, row, n), "image download");
+            mark(k);
+        };
+        for (std::size_t c = 0; c < std::min<std::size_t>(2, chunks); ++c) issue(c);
+        for (std::size_t c = 0; c < chunks; ++c) {
+            const int k = static_cast<int>(c & 1);
+            wait(k);
+            const std::size_t r0 = c * per, n = std::min(per, rows - r0);
+            std::memcpy(dst + r0 * row, buf[k], n * row);
+            if (c + 2 < chunks) issue(c + 2);
+        }
+    }
+};
+
 struct DeviceSession::Impl {
     std::shared_ptr<dev::Program> prog;
+    std::unique_ptr<Staging> staging; ///< host runs only (run_naive / run_plan)
     const VerifiedGraph* exec_graph = nullptr; ///< graph whose outputs are reported
     VerifiedGraph exec_copy;
     int frames = 1;
@@ -757,6 +822,11 @@ struct DeviceSession::Impl {
         if (oi.desc.kind == ObjKind::Image) {
             const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
             if (b.bytes.size() < row * oi.desc.height) throw Error(ErrorCode::ShapeMismatch, "image payload too small", id);
+            if (staging && row * oi.desc.height > Staging::kChunk / 4) {
+                staging->upload(base, static_cast<std::size_t>(s.pitch), b.bytes.data(), row,
+                                static_cast<std::size_t>(oi.desc.height));
+                return;
+            }
             dev::check(gvxb_upload_2d(ctx, base, static_cast<std::size_t>(s.pitch), b.bytes.data(), row, row,
                                       static_cast<std::size_t>(oi.desc.height)),
                        "image upload");
@@ -803,6 +873,11 @@ struct DeviceSession::Impl {
             b = Buffer::image(b.desc);
             b.id = id;
             const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
+            if (staging && row * oi.desc.height > Staging::kChunk / 4) {
+                staging->download(b.bytes.data(), base, static_cast<std::size_t>(s.pitch), row,
+                                  static_cast<std::size_t>(oi.desc.height));
+                return b;
+            }
             dev::check(gvxb_download_2d(ctx, b.bytes.data(), row, base, static_cast<std::size_t>(s.pitch), row,
                                         static_cast<std::size_t>(oi.desc.height)),
                        "image download");
@@ -970,6 +1045,7 @@ std::shared_ptr<HostSession> host_session(const std::shared_ptr<dev::Program>& p
         slot.second->impl.prog = prog;
         slot.second->impl.frames = 1;
         slot.second->impl.ctx = dev::context();
+        slot.second->impl.staging = std::make_unique<Staging>(slot.second->impl.ctx);
     }
     return slot.second;
 }
