@@ -64,8 +64,37 @@ def port():
         lib.gvxo_unsharp.argtypes = [V, ctypes.c_int, ctypes.c_int, V]
         lib.gvxo_conv_stats.argtypes = [V, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        I = ctypes.c_int
+        lib.gvxo_stencil_u8.argtypes = [V, I, I, I, V, ctypes.c_longlong, I, V]
+        lib.gvxo_conv_stats_ex.argtypes = [V, I, I, I, V, ctypes.c_longlong, I, I, I, I, I, ctypes.c_longlong,
+                                           ctypes.c_longlong, V, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_double), V]
         _port = lib
     return _port
+
+
+def port_stencil(img: np.ndarray, mask, div: int, mode: int) -> np.ndarray:
+    """gvxo_stencil_u8: KxK local node sat_U8(s * (1/div)) [-> unsharp chain]."""
+    img = np.ascontiguousarray(img, np.uint8)
+    m = np.ascontiguousarray(mask, np.int32)
+    out = np.empty_like(img)
+    port().gvxo_stencil_u8(img.ctypes.data, img.shape[1], img.shape[0], m.shape[0], m.ctypes.data, div, mode,
+                           out.ctypes.data)
+    return out
+
+
+def port_conv_stats(img: np.ndarray, mask, scale: int, conv_lo: int = -32768, conv_hi: int = 32767,
+                    shift: int = 0, wrap: bool = False, bins: int = 256, offset: int = 0, rng: int = 256):
+    """gvxo_conv_stats_ex: (converted U8, hist, mean, stddev)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    m = np.ascontiguousarray(mask, np.int32)
+    conv = np.empty_like(img)
+    hist = np.zeros(bins, np.int64)
+    mean, sd = ctypes.c_double(), ctypes.c_double()
+    port().gvxo_conv_stats_ex(img.ctypes.data, img.shape[1], img.shape[0], m.shape[0], m.ctypes.data, scale,
+                              conv_lo, conv_hi, shift, int(wrap), bins, offset, rng, hist.ctypes.data,
+                              ctypes.byref(mean), ctypes.byref(sd), conv.ctypes.data)
+    return conv, hist, mean.value, sd.value
 
 
 HARRIS_K = 0.04

@@ -192,3 +192,61 @@ void gvxo_conv_stats(const uint8_t* in, int w, int h, long long* hist, double* m
     *stddev = (double)(float)sqrt(var);
     free(src);
 }
+
+/* Generalised forms of the cfg3 / cfg4 chains for the C-ABI kernels
+ * (gvxb_stencil_point / gvxb_conv_stats) over any KxK integer mask and
+ * divisor d: the local node post body sat_T(s * (1.0 / d)) (a user local
+ * node, or Convolve with scale d, src/registry.cpp:837-878), then
+ *   mode 0: the U8 result;  mode 1: Subtract -> Add -> ConvertDepth.
+ */
+void gvxo_stencil_u8(const uint8_t* in, int w, int h, int k, const int* mask, long long d, int mode,
+                     uint8_t* out) {
+    size_t n = (size_t)w * h;
+    int32_t* src = widen_u8(in, w, h);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            size_t i = (size_t)y * w + x;
+            int64_t b = sat_real((double)wink(src, w, h, x, y, mask, k) * (1.0 / (double)d), 0, 255);
+            if (mode == 0) {
+                out[i] = (uint8_t)b;
+            } else {
+                int64_t diff = clampi64((int64_t)src[i] - b, -32768, 32767);
+                int64_t sum = clampi64((int64_t)src[i] + diff, -32768, 32767);
+                out[i] = (uint8_t)clampi64(sum, 0, 255);
+            }
+        }
+    (void)n;
+    free(src);
+}
+
+/* Convolve(mask, scale) -> conv format [lo, hi] -> ConvertDepth(U8, shift,
+ * policy: Shr then Saturate / Wrap, src/registry.cpp:642-670) -> Histogram
+ * (bins, offset, range; bin = ((v - offset) * bins) / range truncating,
+ * out-of-range skipped, src/execute.cpp:698-727) + MeanStdDev.  `conv`
+ * (optional) receives the U8 image. */
+void gvxo_conv_stats_ex(const uint8_t* in, int w, int h, int k, const int* mask, long long scale, int conv_lo,
+                        int conv_hi, int shift, int wrap, int bins, long long offset, long long range,
+                        long long* hist, double* mean, double* stddev, uint8_t* conv) {
+    size_t n = (size_t)w * h;
+    int32_t* src = widen_u8(in, w, h);
+    int64_t sum = 0, sumsq = 0;
+    for (int b = 0; b < bins; ++b) hist[b] = 0;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            int64_t c = sat_real((double)wink(src, w, h, x, y, mask, k) * (1.0 / (double)scale), conv_lo, conv_hi);
+            if (shift > 0) c >>= shift;
+            int64_t u = wrap ? (c & 0xFF) : clampi64(c, 0, 255);
+            if (conv) conv[(size_t)y * w + x] = (uint8_t)u;
+            int64_t t = (u - offset) * bins;
+            int64_t bin = t / range;
+            if (bin >= 0 && bin < bins) hist[bin] += 1;
+            sum += u;
+            sumsq += u * u;
+        }
+    double m = (double)(float)(((double)sum * 1.0) / (double)(int64_t)n);
+    double var = ((double)sumsq * 1.0) / (double)(int64_t)n - m * m;
+    if (var < 0.0) var = 0.0;
+    *mean = m;
+    *stddev = (double)(float)sqrt(var);
+    free(src);
+}

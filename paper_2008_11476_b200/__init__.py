@@ -350,6 +350,93 @@ def edge_band(device: "Device", src_ptr: int, src_pitch: int, width: int, src_ro
     _check_cuda(c.gvxb_edge(device.h, ctypes.byref(a)))
 
 
+class GvxbStencilArgs(ctypes.Structure):
+    """include/gvxb.h gvxb_stencil_args."""
+    _fields_ = [("src", GvxbImage), ("dst", GvxbImage), ("ksize", ctypes.c_int32),
+                ("mask", ctypes.c_int32 * 49), ("div_num", ctypes.c_int64), ("div_den", ctypes.c_int64),
+                ("mode", ctypes.c_int32), ("band", GvxbBand)]
+
+
+class GvxbConvStatsArgs(ctypes.Structure):
+    """include/gvxb.h gvxb_conv_stats_args."""
+    _fields_ = [("src", GvxbImage), ("converted", GvxbImage), ("ksize", ctypes.c_int32),
+                ("mask", ctypes.c_int32 * 49), ("scale", ctypes.c_int64), ("conv_format", ctypes.c_int32),
+                ("shift", ctypes.c_int32), ("wrap", ctypes.c_int32), ("bins", ctypes.c_int32),
+                ("offset", ctypes.c_int64), ("range", ctypes.c_int64), ("hist", ctypes.c_void_p),
+                ("sum", ctypes.c_void_p), ("sumsq", ctypes.c_void_p), ("mean", ctypes.c_void_p),
+                ("stddev", ctypes.c_void_p)]
+
+
+def _mask49(mask):
+    m = (ctypes.c_int32 * 49)()
+    for i, v in enumerate(np.asarray(mask, np.int64).ravel()):
+        m[i] = int(v)
+    return m
+
+
+def stencil_point(device: "Device", img: np.ndarray, mask, div: int, mode: int) -> np.ndarray:
+    """Host wrapper over gvxb_stencil_point (KxK U8 stencil, mode 0 plain,
+    mode 1 unsharp chain) on one U8 frame; returns the U8 result."""
+    c, _ = _load()
+    c.gvxb_stencil_point.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbStencilArgs)]
+    h, w = img.shape
+    pitch = (w + 127) // 128 * 128
+    src, dst = device.alloc(pitch * h), device.alloc(pitch * h)
+    try:
+        device.upload(src, pitch, np.ascontiguousarray(img, np.uint8))
+        a = GvxbStencilArgs()
+        a.src = GvxbImage(src, pitch, w, h, 0, 1, 0)
+        a.dst = GvxbImage(dst, pitch, w, h, 0, 1, 0)
+        a.ksize = int(np.asarray(mask).shape[0])
+        a.mask = _mask49(mask)
+        a.div_num, a.div_den, a.mode = 1, int(div), int(mode)
+        a.band = GvxbBand(0, h, h, 0, 0)
+        _check_cuda(c.gvxb_stencil_point(device.h, ctypes.byref(a)))
+        out = np.empty((h, w), np.uint8)
+        device.download(out, dst, pitch)
+        device.sync()
+        return out
+    finally:
+        device.sync()
+        device.free(src), device.free(dst)
+
+
+def conv_stats(device: "Device", img: np.ndarray, mask, scale: int, conv_format: int = 2, shift: int = 0,
+               wrap: bool = False, bins: int = 256, offset: int = 0, rng: int = 256):
+    """Host wrapper over gvxb_conv_stats on one U8 frame: returns
+    (converted U8 image, histogram int64[bins], mean, stddev)."""
+    c, _ = _load()
+    c.gvxb_conv_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbConvStatsArgs)]
+    h, w = img.shape
+    pitch = (w + 127) // 128 * 128
+    src, conv = device.alloc(pitch * h), device.alloc(pitch * h)
+    aux = device.alloc(16 * bins + 64 + 32)
+    try:
+        device.upload(src, pitch, np.ascontiguousarray(img, np.uint8))
+        a = GvxbConvStatsArgs()
+        a.src = GvxbImage(src, pitch, w, h, 0, 1, 0)
+        a.converted = GvxbImage(conv, pitch, w, h, 0, 1, 0)
+        a.ksize = int(np.asarray(mask).shape[0])
+        a.mask = _mask49(mask)
+        a.scale, a.conv_format, a.shift, a.wrap = int(scale), int(conv_format), int(shift), int(wrap)
+        a.bins, a.offset, a.range = int(bins), int(offset), int(rng)
+        a.hist, a.sum, a.sumsq = aux, aux + 16 * bins, aux + 16 * bins + 8
+        a.mean, a.stddev = aux + 16 * bins + 16, aux + 16 * bins + 32
+        _check_cuda(c.gvxb_conv_stats(device.h, ctypes.byref(a)))
+        out = np.empty((h, w), np.uint8)
+        device.download(out, conv, pitch)
+        raw = np.empty(2 * bins + 6, np.int64)
+        device.download(raw.reshape(1, -1).view(np.uint8), aux, raw.nbytes)
+        device.sync()
+        hist = raw[1:2 * bins:2].copy()
+        mean = float(raw[2 * bins + 3:2 * bins + 4].view(np.float64)[0])
+        sd = float(raw[2 * bins + 5:2 * bins + 6].view(np.float64)[0])
+        return out, hist, mean, sd
+    finally:
+        device.sync()
+        device.free(src), device.free(conv), device.free(aux)
+
+
 def band_rows(height: int, world: int, rank: int):
     c, _ = _load()
     r0, r1 = ctypes.c_int32(), ctypes.c_int32()
@@ -358,4 +445,5 @@ def band_rows(height: int, world: int, rank: int):
 
 
 __all__ = ["GraphvxError", "ConfigGraph", "Session", "Device", "build", "device_count", "random_u8",
+           "stencil_point", "conv_stats",
            "band_rows", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]

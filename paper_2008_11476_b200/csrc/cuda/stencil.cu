@@ -13,7 +13,10 @@
 //   ref:src/execute.cpp:698-727); sums are exact int64;
 //   MeanStdDev finalize in IEEE double without contraction, in the
 //   reference's operation order (ref:src/registry.cpp:957-1010).
-#include "tile.cuh"
+#include "packed.cuh"
+
+#include <algorithm>
+#include <type_traits>
 
 namespace gvxd {
 
@@ -239,6 +242,18 @@ __global__ void __launch_bounds__(kStThreads) conv_stats_kernel(const __grid_con
     }
 }
 
+/// One launch clearing the histogram slots and both per-frame sums.
+__global__ void zero_scratch_kernel(unsigned long long* hist, long long nh, unsigned long long* sum,
+                                    unsigned long long* sumsq, int frames) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nh + 2LL * frames;
+         i += stride) {
+        if (i < nh) hist[i] = 0;
+        else if (i < nh + frames) sum[i - nh] = 0;
+        else sumsq[i - nh - frames] = 0;
+    }
+}
+
 /// MeanStdDev finalize, one thread per frame:
 ///   mean = F32((sum * 1.0) / n);  sd = F32(sqrt(max((sumsq * 1.0) / n - m*m, 0.0)))
 /// with m the F32-rounded mean (the reduce_stddev node reads the mean scalar).
@@ -262,11 +277,380 @@ __global__ void meanstd_finalize_kernel(const unsigned long long* sum, const uns
     }
 }
 
+
+// ======================================================= separable fast path
+//
+// Masks that factor as m = u v^T with non-negative integers (the binomial
+// blurs of cfg3 / cfg4 do) and a power-of-two divisor run a packed-FP32
+// pipeline: every lane owns 4 columns as (even, odd) float2 pairs, the
+// horizontal K-tap pass reads its 4 + 2R source bytes from the TMA tile,
+// the vertical pass streams rows through K push-accumulators (each new
+// horizontal row adds u[i] * h into the K outputs it touches), and the
+// rounding division is one FFMA2 in round-down mode:
+//   q = floor((s + d/2) / d) = round_half_away(s / d)   (s >= 0, d = 2^k)
+// landing as the float 1.5*2^23 + q whose low byte is q.  All sums are
+// integers < 2^24 (checked on the host), so every step is exact.
+
+constexpr int kSepThreads = 96;
+constexpr int kSepTW = 4 * kSepThreads; // 384 columns: 4K / 8K / 1080p split evenly
+constexpr int kSepSW = kSepTW + 32;     // tile origin x0 - 16 (16-byte aligned TMA start)
+constexpr int kSepTHMax = 64;
+constexpr int kSepHistTH = 32;          // u8 counters (4 px * rows <= 255); small tile for occupancy
+constexpr int kSepHistBytes = 256 * 32 * 4;
+
+struct SepParams {
+    int width;
+    Band band;
+    int th;
+    float u[7], v[7];
+    float bias;     // d / 2 (0 for d == 1)
+    float inv_d;    // 1 / (d << shift), exact power of two
+    int clamp255;   // q may exceed 255 (saturating U8 output)
+    uint8_t* dst;   // K3 output, or K4's converted image (may be null)
+    int64_t dst_pitch, dst_fstride;
+    // K4
+    gvxb_value* hist;
+    int bins;
+    long long offset, range;
+    int identity;
+    unsigned long long* sum;
+    unsigned long long* sumsq;
+};
+
+/// Columns c+j, j = -R .. R+3, of one tile row as pairs P(j) = (c+j, c+j+2).
+template <int R>
+struct SepRow {
+    float2 p[2 * R + 2];
+};
+
+template <int R>
+__device__ __forceinline__ SepRow<R> sep_load(const uint8_t* row, int off) {
+    const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
+    // column c + j for j = -4 .. 7 lives in byte (j & 3) of word (j >> 2) + 1
+    auto col = [&](int j) -> float {
+        const uint32_t w = j < 0 ? wl : (j < 4 ? wc : wr);
+        return magic_byte(w, j & 3);
+    };
+    const float2 magic = f2(-8388608.f, -8388608.f);
+    SepRow<R> r;
+    // de-magic half of the pairs; the others are recombined halves
+#pragma unroll
+    for (int j = -R; j <= R + 1; ++j) {
+        const int k = j + R;
+        if ((k & 2) == 0) r.p[k] = add2(f2(col(j), col(j + 2)), magic);
+    }
+#pragma unroll
+    for (int j = -R; j <= R + 1; ++j) {
+        const int k = j + R;
+        if ((k & 2) != 0) {
+            // P(j) = (c+j, c+j+2) = (P(j-2).y, P(j+2).x) when both exist
+            if (k - 2 >= 0 && k + 2 <= 2 * R + 1) r.p[k] = f2(r.p[k - 2].y, r.p[k + 2].x);
+            else r.p[k] = add2(f2(col(j), col(j + 2)), magic);
+        }
+    }
+    return r;
+}
+
+template <int K>
+__device__ __forceinline__ Q4 sep_horizontal(const SepRow<K / 2>& r, const float* v) {
+    Q4 h;
+    h.e = mul2(f2(v[0], v[0]), r.p[0]);
+    h.o = mul2(f2(v[0], v[0]), r.p[1]);
+#pragma unroll
+    for (int t = 1; t < K; ++t) {
+        h.e = fma2(f2(v[t], v[t]), r.p[t], h.e);
+        h.o = fma2(f2(v[t], v[t]), r.p[t + 1], h.o);
+    }
+    return h;
+}
+
+/// Division epilogue: 1.5*2^23 + min(q, 255) per column.
+__device__ __forceinline__ Q4 sep_quotient(Q4 acc, float inv_d, int clamp255) {
+    const float2 M = f2(12582912.f, 12582912.f), id = f2(inv_d, inv_d);
+    Q4 q{__ffma2_rd(acc.e, id, M), __ffma2_rd(acc.o, id, M)};
+    if (clamp255) {
+        const float top = 12582912.f + 255.f;
+        q.e = f2(fminf(q.e.x, top), fminf(q.e.y, top));
+        q.o = f2(fminf(q.o.x, top), fminf(q.o.y, top));
+    }
+    return q;
+}
+
+__device__ __forceinline__ Q4 sep_neg_quotient(Q4 acc, float inv_d, int clamp255) {
+    const float2 M = f2(-12582912.f, -12582912.f), id = f2(-inv_d, -inv_d);
+    Q4 q{__ffma2_ru(acc.e, id, M), __ffma2_ru(acc.o, id, M)};
+    if (clamp255) {
+        const float bot = -12582912.f - 255.f;
+        q.e = f2(fmaxf(q.e.x, bot), fmaxf(q.e.y, bot));
+        q.o = f2(fmaxf(q.o.x, bot), fmaxf(q.o.y, bot));
+    }
+    return q;
+}
+
+/// ++ of a u8 shared-memory counter.  Volatile asm keeps the increments of
+/// one thread in program order (two may hit the same counter) while leaving
+/// the tile loads free to be scheduled around them.
+__device__ __forceinline__ void smem_inc_u8(uint32_t addr) {
+    asm volatile(
+        "{\n"
+        ".reg .u16 t;\n"
+        "ld.shared.u8 t, [%0];\n"
+        "add.u16 t, t, 1;\n"
+        "st.shared.u8 [%0], t;\n"
+        "}\n" ::"r"(addr));
+}
+
+/// Low bytes of (e.x, o.x, e.y, o.y) = columns c .. c+3.
+__device__ __forceinline__ uint32_t sep_pack(Q4 q) {
+    const uint32_t a = __byte_perm(__float_as_uint(q.e.x), __float_as_uint(q.o.x), 0x0040u);
+    const uint32_t b = __byte_perm(__float_as_uint(q.e.y), __float_as_uint(q.o.y), 0x0040u);
+    return __byte_perm(a, b, 0x5410u);
+}
+
+__device__ __forceinline__ void store4(uint8_t* dp, uint32_t w, int c, int width) {
+    if (c + 3 < width) {
+        *reinterpret_cast<uint32_t*>(dp) = w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (c + i < width) dp[i] = static_cast<uint8_t>(w >> (8 * i));
+    }
+}
+
+/// kMode 0: U8 stencil output; 1: unsharp chain sat_u8(2x - blur);
+/// 2: Convolve -> ConvertDepth -> per-CTA value histogram (+ optional image).
+template <int K, int kMode, bool kClamp>
+__global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
+    constexpr int R = K / 2;
+    constexpr int SH = (kMode == 2 ? kSepHistTH : kSepTHMax) + 2 * R;
+    __shared__ alignas(128) uint8_t tile[SH * kSepSW];
+    __shared__ uint64_t bar;
+    extern __shared__ uint4 hist_dyn[]; // kMode 2: [bin][lane][warp] u8 counters
+    uint8_t* hist = reinterpret_cast<uint8_t*>(hist_dyn);
+
+    const int tid = static_cast<int>(threadIdx.x);
+    const int x0 = blockIdx.x * kSepTW;
+    const int y0 = p.band.row0 + blockIdx.y * p.th;
+    const int n = min(y0 + p.th, p.band.row1) - y0;
+    const int frame = blockIdx.z;
+    if (kMode == 2) {
+        for (int i = tid; i < kSepHistBytes / 16; i += kSepThreads) hist_dyn[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    stage_tile_u8<kSepSW, SH>(tile, &map, &bar, x0 - 16, y0 - R, frame, p.width, p.band, p.th + 2 * R);
+
+    const int c = x0 + 4 * tid;
+    const int off = 16 + 4 * tid;
+    const int dy0 = kMode == 2 ? y0 : y0 - p.band.dst_row0;
+    uint8_t* drow = p.dst ? p.dst + frame * p.dst_fstride + static_cast<int64_t>(dy0) * p.dst_pitch + c : nullptr;
+    const uint8_t* crow = tile + R * kSepSW + off; // kMode 1: centre pixels of output row o
+    // kMode 2 counter of (value, lane, warp): value * 128 + lane * 4 + warp
+    const uint32_t hbase = smem_u32(hist_dyn) + (((tid & 31) << 2) | (tid >> 5));
+    float u[K], v[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) u[t] = p.u[t], v[t] = p.v[t];
+    const float2 bias = f2(p.bias, p.bias);
+
+    // kEdge: this strip crosses the right image border, so lanes may own
+    // fewer than 4 (or no) columns; interior strips run without any checks
+    auto body = [&](auto edge_tag) {
+        constexpr bool kEdge = decltype(edge_tag)::value;
+        const bool live = !kEdge || c < p.width, full = !kEdge || c + 3 < p.width;
+        const int nv = kEdge ? min(4, p.width - c) : 4;
+        auto store = [&](uint32_t w) {
+            if (full) {
+                *reinterpret_cast<uint32_t*>(drow) = w;
+            } else if (live) {
+                for (int i = 0; i < nv; ++i) drow[i] = static_cast<uint8_t>(w >> (8 * i));
+            }
+        };
+        auto count = [&](float qv, int i) {
+            if (!kEdge || i < nv) smem_inc_u8(hbase + ((__float_as_uint(qv) & 0xFFu) << 7));
+        };
+        auto emit = [&](Q4 acc) {
+            if (kMode == 1) {
+                // -(1.5*2^23 + b) by round-up of the negated product, then
+                // 2(2^23 + x) - (1.5*2^23 + b) = 2^22 + (2x - b), clamped to U8
+                const Q4 q = sep_neg_quotient(acc, p.inv_d, kClamp);
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(crow);
+                const float2 xe = f2(magic_byte(w, 0), magic_byte(w, 2)), xo = f2(magic_byte(w, 1), magic_byte(w, 3));
+                const float2 two = f2(2.f, 2.f), lift = f2(8388608.f, 8388608.f);
+                float2 re = fma2(two, xe, q.e), ro = fma2(two, xo, q.o);
+                const float lo = 4194304.f, hi = 4194304.f + 255.f;
+                re = f2(fminf(fmaxf(re.x, lo), hi), fminf(fmaxf(re.y, lo), hi));
+                ro = f2(fminf(fmaxf(ro.x, lo), hi), fminf(fmaxf(ro.y, lo), hi));
+                store(sep_pack(Q4{add2(re, lift), add2(ro, lift)})); // 1.5*2^23 + y
+                crow += kSepSW;
+                drow += p.dst_pitch;
+            } else if (kMode == 0) {
+                store(sep_pack(sep_quotient(acc, p.inv_d, kClamp)));
+                drow += p.dst_pitch;
+            } else {
+                const Q4 q = sep_quotient(acc, p.inv_d, kClamp);
+                if (drow) {
+                    store(sep_pack(q));
+                    drow += p.dst_pitch;
+                }
+                count(q.e.x, 0);
+                count(q.o.x, 1);
+                count(q.e.y, 2);
+                count(q.o.y, 3);
+            }
+        };
+        // push accumulation: smem row j (global row y0 - R + j) adds u[i] * h(j)
+        // into output o = j - i; output o is complete after row j = o + K - 1.
+        Q4 acc[K];
+        auto row = [&](int j, int slot0) { // slot0 = j mod K
+            const Q4 h = sep_horizontal<K>(sep_load<R>(tile + j * kSepSW, off), v);
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                Q4& a = acc[(slot0 - i + 2 * K) % K];
+                if (i == 0) a = Q4{fma2(f2(u[0], u[0]), h.e, bias), fma2(f2(u[0], u[0]), h.o, bias)};
+                else a = Q4{fma2(f2(u[i], u[i]), h.e, a.e), fma2(f2(u[i], u[i]), h.o, a.o)};
+            }
+        };
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) row(j, j);
+        for (int O = 0; O < n; O += K) {
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+                if (O + t >= n) break;
+                row(O + t + K - 1, (t + K - 1) % K); // O is a multiple of K
+                emit(acc[t]);                        // output o = O + t
+            }
+        }
+    };
+    if (x0 + kSepTW > p.width) body(std::true_type{});
+    else body(std::false_type{});
+
+    if (kMode != 2) return;
+    __syncthreads();
+    // merge: thread t owns values t, t + 96, t + 192 (< 256); the 128 counter
+    // bytes of a value are read as 8 uint4 in a rotated order (bank spread)
+    long long s1 = 0, s2 = 0;
+    for (int val = tid; val < 256; val += kSepThreads) {
+        const uint4* rowp = hist_dyn + val * 8;
+        unsigned cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint4 q = rowp[(k + val) & 7];
+            cnt = __dp4a(q.x, 0x01010101u, cnt);
+            cnt = __dp4a(q.y, 0x01010101u, cnt);
+            cnt = __dp4a(q.z, 0x01010101u, cnt);
+            cnt = __dp4a(q.w, 0x01010101u, cnt);
+        }
+        if (!cnt) continue;
+        s1 += static_cast<long long>(cnt) * val;
+        s2 += static_cast<long long>(cnt) * val * val;
+        if (p.hist) {
+            long long bin = val;
+            if (!p.identity) {
+                const long long t = (static_cast<long long>(val) - p.offset) * p.bins;
+                bin = t / p.range;
+                if (bin < 0 || bin >= p.bins) continue;
+            }
+            atomicAdd(reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + bin].bits),
+                      static_cast<unsigned long long>(cnt));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(&p.sum[frame], static_cast<unsigned long long>(s1));
+        atomicAdd(&p.sumsq[frame], static_cast<unsigned long long>(s2));
+    }
+}
+
 } // namespace gvxd
 
 using namespace gvxd;
 
 namespace {
+
+/// m = u v^T with non-negative integer u, v (v primitive).
+bool factor_mask(const int32_t* m, int K, int* u, int* v) {
+    int i0 = -1, j0 = -1;
+    for (int i = 0; i < K * K; ++i) {
+        if (m[i] < 0) return false;
+        if (m[i] && i0 < 0) i0 = i / K, j0 = i % K;
+    }
+    if (i0 < 0) return false;
+    long long g = 0;
+    for (int j = 0; j < K; ++j) {
+        long long a = m[i0 * K + j], b = g;
+        while (b) { long long t = a % b; a = b; b = t; }
+        g = a;
+    }
+    for (int j = 0; j < K; ++j) v[j] = static_cast<int>(m[i0 * K + j] / g);
+    for (int i = 0; i < K; ++i) {
+        if (m[i * K + j0] % v[j0]) return false;
+        u[i] = m[i * K + j0] / v[j0];
+        for (int j = 0; j < K; ++j)
+            if (static_cast<long long>(u[i]) * v[j] != m[i * K + j]) return false;
+    }
+    return true;
+}
+
+bool is_pow2(long long d) { return d >= 1 && (d & (d - 1)) == 0; }
+
+/// Fills the separable parameters when the fast path is exact for this
+/// mask / divisor; returns the largest quotient floor((255 sum + d/2) / d).
+bool sep_setup(const int32_t* mask, int K, long long d, int shift, SepParams& p, long long& qmax) {
+    int u[7], v[7];
+    if (!is_pow2(d) || shift < 0 || shift > 16 || !factor_mask(mask, K, u, v)) return false;
+    long long su = 0, sv = 0;
+    for (int t = 0; t < K; ++t) su += u[t], sv += v[t];
+    const long long smax = 255 * su * sv + d / 2;
+    if (255 * sv >= (1 << 24) || smax >= (1 << 24)) return false;
+    for (int t = 0; t < 7; ++t) p.u[t] = t < K ? static_cast<float>(u[t]) : 0.f, p.v[t] = t < K ? static_cast<float>(v[t]) : 0.f;
+    p.bias = static_cast<float>(d / 2);
+    p.inv_d = 1.0f / static_cast<float>(d << shift);
+    qmax = smax / d;
+    return true;
+}
+
+template <int K, int M>
+void* sep_fn(bool clamp) {
+    return clamp ? reinterpret_cast<void*>(&sep_kernel<K, M, true>) : reinterpret_cast<void*>(&sep_kernel<K, M, false>);
+}
+
+template <int M>
+void* sep_fn_k(int k, bool clamp) {
+    switch (k) {
+    case 3: return sep_fn<3, M>(clamp);
+    case 5: return sep_fn<5, M>(clamp);
+    case 7: return sep_fn<7, M>(clamp);
+    default: return nullptr;
+    }
+}
+
+int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K, int rows, int th_max, size_t dyn) {
+    using namespace gvxb_impl;
+    if (dyn > 0) { // static tile + dynamic histogram exceed the 48 KB default
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+        if (e != cudaSuccess) return cuda_fail(e, "separable stencil smem attribute");
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSepThreads, dyn);
+    const int frames = s.frames > 0 ? s.frames : 1;
+    const long long strips = static_cast<long long>((s.width + kSepTW - 1) / kSepTW) * frames;
+    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, th_max,
+                              K - 1);
+    CUtensorMap map;
+    if (int rc = make_u8_tensor_map(&map, s, kSepSW, p.th + K - 1)) return rc;
+    dim3 grid((s.width + kSepTW - 1) / kSepTW, (rows + p.th - 1) / p.th, frames);
+    void* args[] = {&map, &p};
+    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kSepThreads), args, dyn, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "separable stencil launch");
+    return check_launch(ctx, "separable stencil kernel");
+}
 
 template <int K>
 void* stencil_fn(int mode) {
@@ -292,6 +676,20 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
     if (a->div_num != 1 || a->div_den < 1) return fail(GVXB_ERR_INVALID, "stencil: divisor must be 1/d");
     const int rows = a->band.row1 - a->band.row0;
     if (rows <= 0 || s.width <= 0) return GVXB_OK;
+    if (a->mode == 0 || a->mode == 1) {
+        SepParams sp{};
+        long long qmax = 0;
+        if (sep_setup(a->mask, a->ksize, a->div_den, 0, sp, qmax)) {
+            sp.width = s.width;
+            sp.band = Band{a->band.row0, a->band.row1, a->band.global_h, a->band.src_row0, a->band.dst_row0};
+            sp.clamp255 = qmax > 255;
+            sp.dst = static_cast<uint8_t*>(a->dst.data);
+            sp.dst_pitch = a->dst.pitch;
+            sp.dst_fstride = a->dst.frames > 1 ? a->dst.frame_stride : a->dst.pitch * a->dst.height;
+            void* fn = a->mode == 0 ? sep_fn_k<0>(a->ksize, sp.clamp255) : sep_fn_k<1>(a->ksize, sp.clamp255);
+            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0);
+        }
+    }
     StencilParams p;
     p.width = s.width;
     p.band = Band{a->band.row0, a->band.row1, a->band.global_h, a->band.src_row0, a->band.dst_row0};
@@ -318,6 +716,16 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kStThreads), args, 0, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "stencil kernel launch");
     return check_launch(ctx, "stencil kernel");
+}
+
+static int meanstd(gvxb_ctx ctx, const gvxb_conv_stats_args* a, const ConvStatsParams& p, int frames, const gvxb_image& s) {
+    if (a->mean || a->stddev) {
+        const long long n = static_cast<long long>(s.width) * s.height;
+        meanstd_finalize_kernel<<<(frames + 63) / 64, 64, 0, ctx->stream>>>(p.sum, p.sumsq, n, frames, a->mean,
+                                                                              a->stddev);
+        return gvxb_impl::check_launch(ctx, "meanstd finalize");
+    }
+    return GVXB_OK;
 }
 
 extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
@@ -348,12 +756,40 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
     p.sumsq = reinterpret_cast<unsigned long long*>(a->sumsq);
     if (a->range == 0 && !p.identity_bins) return fail(GVXB_ERR_DIV_BY_ZERO, "histogram range is zero");
 
-    cudaError_t e = cudaMemsetAsync(a->sum, 0, sizeof(int64_t) * frames, ctx->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a->sumsq, 0, sizeof(int64_t) * frames, ctx->stream);
-    if (e == cudaSuccess && a->hist)
-        e = cudaMemsetAsync(a->hist, 0, sizeof(gvxb_value) * frames * static_cast<size_t>(p.bins), ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "conv_stats memset");
+    {
+        const long long nh = a->hist ? static_cast<long long>(frames) * p.bins * 2 : 0;
+        const long long total = nh + 2LL * frames;
+        const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 1024));
+        zero_scratch_kernel<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<unsigned long long*>(a->hist), nh,
+                                                             p.sum, p.sumsq, frames);
+        if (int rc = check_launch(ctx, "conv_stats scratch clear")) return rc;
+    }
+    cudaError_t e = cudaSuccess;
 
+    {
+        SepParams sp{};
+        long long qmax = 0;
+        int lo = 0, hi = 0;
+        range_of(a->conv_format, lo, hi);
+        if (sep_setup(a->mask, a->ksize, a->scale, a->shift, sp, qmax) && qmax <= hi && sep_fn_k<2>(a->ksize, false)) {
+            sp.width = s.width;
+            sp.band = Band{0, s.height, s.height, 0, 0};
+            sp.clamp255 = !a->wrap && (qmax >> a->shift) > 255;
+            sp.dst = static_cast<uint8_t*>(a->converted.data);
+            sp.dst_pitch = a->converted.pitch;
+            sp.dst_fstride = p.conv_fstride;
+            sp.hist = a->hist;
+            sp.bins = p.bins;
+            sp.offset = a->offset;
+            sp.range = a->range;
+            sp.identity = p.identity_bins;
+            sp.sum = p.sum;
+            sp.sumsq = p.sumsq;
+            if (int rc = sep_launch(ctx, sep_fn_k<2>(a->ksize, sp.clamp255), s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes))
+                return rc;
+            return meanstd(ctx, a, p, frames, s);
+        }
+    }
     void* fn = nullptr;
     int sh = 0;
     switch (a->ksize) {
@@ -374,11 +810,5 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
     e = cudaLaunchKernel(fn, grid, dim3(kStThreads), args, dyn, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "conv_stats kernel launch");
     if (int rc = check_launch(ctx, "conv_stats kernel")) return rc;
-    if (a->mean || a->stddev) {
-        const long long n = static_cast<long long>(s.width) * s.height;
-        meanstd_finalize_kernel<<<(frames + 63) / 64, 64, 0, ctx->stream>>>(
-            p.sum, p.sumsq, n, frames, a->mean, a->stddev);
-        if (int rc = check_launch(ctx, "meanstd finalize")) return rc;
-    }
-    return GVXB_OK;
+    return meanstd(ctx, a, p, frames, s);
 }

@@ -440,7 +440,7 @@ int Program::launches_per_run() const {
     int n = 0;
     for (const Unit& u : units) {
         if (u.kind == Unit::Kind::Jit) n += static_cast<int>(u.prog.kernels.size());
-        else if (u.kind == Unit::Kind::ConvStats) n += (u.out[2] != kInvalidId || u.out[3] != kInvalidId) ? 2 : 1;
+        else if (u.kind == Unit::Kind::ConvStats) n += (u.out[2] != kInvalidId || u.out[3] != kInvalidId) ? 3 : 2;
         else n += 1;
     }
     return n;

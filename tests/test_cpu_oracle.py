@@ -49,3 +49,21 @@ def test_known_answers_from_reference_tests(oracle_mod):
     assert (oracle_mod.port_run(3, c) == 17).all()       # unsharp of a constant is the constant
     hist, mean, sd = oracle_mod.port_run(4, c)
     assert hist[17] == c.size and mean == 17.0 and sd == 0.0
+
+
+def test_generalised_oracle_agrees_with_pinned_configs(oracle_mod):
+    """gvxo_stencil_u8 / gvxo_conv_stats_ex (used for the C-ABI mask sweep)
+    reduce to the reference-pinned cfg3 / cfg4 restatements on their masks."""
+    rng = np.random.default_rng(5)
+    b5 = np.outer([1, 4, 6, 4, 1], [1, 4, 6, 4, 1])
+    for w, h in [(1, 1), (7, 5), (64, 48), (130, 3)]:
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        assert np.array_equal(oracle_mod.port_stencil(img, b5, 256, 1), oracle_mod.port_run(3, img))
+        conv, hist, mean, sd = oracle_mod.port_conv_stats(img, b5, 256)
+        whist, wmean, wsd = oracle_mod.port_run(4, img)
+        assert np.array_equal(hist, whist) and mean == wmean and sd == wsd
+        # mode 0 output is the blur itself: a constant image stays constant
+    c = np.full((9, 11), 200, np.uint8)
+    assert (oracle_mod.port_stencil(c, b5, 256, 0) == 200).all()
+    assert (oracle_mod.port_stencil(c, np.ones((3, 3)), 8, 0) == 225).all()   # 1800/8 = 225
+    assert (oracle_mod.port_stencil(c, np.ones((3, 3)), 4, 0) == 255).all()   # saturates
