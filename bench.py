@@ -40,9 +40,9 @@ CONFIG_NAME = {
 }
 # algorithmic HBM bytes per output pixel of the fused program
 ALGO_BYTES = {1: 3, 2: 2, 3: 2, 4: 1, 5: 3}
-KERNEL_NAME = {1: "edge_kernel", 2: "harris_kernel", 3: "stencil_point_kernel", 4: "conv_stats_kernel",
+KERNEL_NAME = {1: "edge_kernel", 2: "harris_kernel", 3: "sep_kernel<5,1> (separable stencil, unsharp epilogue)", 4: "sep_kernel<5,2> (separable conv + value histogram)",
                5: "edge_kernel"}
-DEFAULT_FRAMES = {1: 16, 2: 8, 3: 2, 4: 16, 5: 1}
+DEFAULT_FRAMES = {1: 16, 2: 8, 3: 2, 4: 64, 5: 1}
 CPU_SAMPLE = {1: (1920, 1080), 2: (3840, 544), 3: (7680, 272), 4: (3840, 544), 5: (16384, 128)}
 
 
@@ -467,11 +467,23 @@ def main():
     roof = None
     if res["kernel_ms"]:
         achieved = ALGO_BYTES[cfg] * res["px_step"] / (res["kernel_ms"] / 1e3) / 1e9
-        traffic = ncu_traffic(cfg)
+        prof = ncu_traffic(cfg) or {}
+        traffic = None
+        if prof.get("dram_bytes_per_launch") and prof.get("px_per_launch"):
+            # per launch of this run (the capture used the same command; scale if frames differ)
+            traffic = round(prof["dram_bytes_per_launch"] * res["px_step"] / prof["px_per_launch"])
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
                 "kernel": KERNEL_NAME[cfg], "algorithmic_bytes_per_px": ALGO_BYTES[cfg],
                 "px_per_launch": res["px_step"], "kernel_ms": round(res["kernel_ms"], 4)}
+        if prof.get("warp_inst_per_px"):
+            # the kernels are issue-bound: lane instructions/s against 148 SMs x 4 schedulers x 32 lanes x clock
+            mhz = (res.get("clocks") or {}).get("sm_mhz") or 1965.0
+            lane_rate = prof["warp_inst_per_px"] * 32 * res["px_step"] / (res["kernel_ms"] / 1e3)
+            issue_peak = 148 * 4 * 32 * mhz * 1e6
+            roof["issue"] = {"warp_inst_per_px": prof["warp_inst_per_px"], "lane_inst_per_s": round(lane_rate),
+                             "peak": round(issue_peak), "frac": round(lane_rate / issue_peak, 4),
+                             "source": prof.get("source")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:

@@ -305,7 +305,7 @@ struct SepParams {
     float u[7], v[7];
     float bias;     // d / 2 (0 for d == 1)
     float inv_d;    // 1 / (d << shift), exact power of two
-    int clamp255;   // q may exceed 255 (saturating U8 output)
+    int clamp255;   // q may exceed 255: 1 saturate to 255, 2 wrap (low byte)
     uint8_t* dst;   // K3 output, or K4's converted image (may be null)
     int64_t dst_pitch, dst_fstride;
     // K4
@@ -418,11 +418,12 @@ __device__ __forceinline__ void store4(uint8_t* dp, uint32_t w, int c, int width
 }
 
 /// kMode 0: U8 stencil output; 1: unsharp chain sat_u8(2x - blur);
-/// 2: Convolve -> ConvertDepth -> per-CTA value histogram (+ optional image).
+/// 2: Convolve -> ConvertDepth -> per-CTA value histogram; 3: as 2 and also
+/// store the converted image.
 template <int K, int kMode, bool kClamp>
 __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
     constexpr int R = K / 2;
-    constexpr int SH = (kMode == 2 ? kSepHistTH : kSepTHMax) + 2 * R;
+    constexpr int SH = (kMode >= 2 ? kSepHistTH : kSepTHMax) + 2 * R;
     __shared__ alignas(128) uint8_t tile[SH * kSepSW];
     __shared__ uint64_t bar;
     extern __shared__ uint4 hist_dyn[]; // kMode 2: [bin][lane][warp] u8 counters
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
     const int y0 = p.band.row0 + blockIdx.y * p.th;
     const int n = min(y0 + p.th, p.band.row1) - y0;
     const int frame = blockIdx.z;
-    if (kMode == 2) {
+    if (kMode >= 2) {
         for (int i = tid; i < kSepHistBytes / 16; i += kSepThreads) hist_dyn[i] = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) {
@@ -445,11 +446,12 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
 
     const int c = x0 + 4 * tid;
     const int off = 16 + 4 * tid;
-    const int dy0 = kMode == 2 ? y0 : y0 - p.band.dst_row0;
+    const int dy0 = kMode >= 2 ? y0 : y0 - p.band.dst_row0;
     uint8_t* drow = p.dst ? p.dst + frame * p.dst_fstride + static_cast<int64_t>(dy0) * p.dst_pitch + c : nullptr;
     const uint8_t* crow = tile + R * kSepSW + off; // kMode 1: centre pixels of output row o
     // kMode 2 counter of (value, lane, warp): value * 128 + lane * 4 + warp
     const uint32_t hbase = smem_u32(hist_dyn) + (((tid & 31) << 2) | (tid >> 5));
+    const uint32_t hcnt = hbase - (0x4B400000u << 7);
     float u[K], v[K];
 #pragma unroll
     for (int t = 0; t < K; ++t) u[t] = p.u[t], v[t] = p.v[t];
@@ -468,8 +470,12 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
                 for (int i = 0; i < nv; ++i) drow[i] = static_cast<uint8_t>(w >> (8 * i));
             }
         };
+        // qv = 1.5*2^23 + value has bits 0x4B400000 + value, so one
+        // multiply-add gives the counter address hbase + value * 128
         auto count = [&](float qv, int i) {
-            if (!kEdge || i < nv) smem_inc_u8(hbase + ((__float_as_uint(qv) & 0xFFu) << 7));
+            if (kEdge && i >= nv) return;
+            if (kClamp && p.clamp255 == 2) smem_inc_u8(hbase + ((__float_as_uint(qv) & 0xFFu) << 7)); // Wrap
+            else smem_inc_u8(hcnt + (__float_as_uint(qv) << 7));
         };
         auto emit = [&](Q4 acc) {
             if (kMode == 1) {
@@ -490,8 +496,8 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
                 store(sep_pack(sep_quotient(acc, p.inv_d, kClamp)));
                 drow += p.dst_pitch;
             } else {
-                const Q4 q = sep_quotient(acc, p.inv_d, kClamp);
-                if (drow) {
+                const Q4 q = sep_quotient(acc, p.inv_d, kClamp && p.clamp255 == 1);
+                if (kMode == 3) {
                     store(sep_pack(q));
                     drow += p.dst_pitch;
                 }
@@ -527,7 +533,7 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
     if (x0 + kSepTW > p.width) body(std::true_type{});
     else body(std::false_type{});
 
-    if (kMode != 2) return;
+    if (kMode < 2) return;
     __syncthreads();
     // merge: thread t owns values t, t + 96, t + 192 (< 256); the 128 counter
     // bytes of a value are read as 8 uint4 in a rotated order (bank spread)
@@ -774,7 +780,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
         if (sep_setup(a->mask, a->ksize, a->scale, a->shift, sp, qmax) && qmax <= hi && sep_fn_k<2>(a->ksize, false)) {
             sp.width = s.width;
             sp.band = Band{0, s.height, s.height, 0, 0};
-            sp.clamp255 = !a->wrap && (qmax >> a->shift) > 255;
+            sp.clamp255 = (qmax >> a->shift) > 255 ? (a->wrap ? 2 : 1) : 0;
             sp.dst = static_cast<uint8_t*>(a->converted.data);
             sp.dst_pitch = a->converted.pitch;
             sp.dst_fstride = p.conv_fstride;
@@ -785,7 +791,8 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
             sp.identity = p.identity_bins;
             sp.sum = p.sum;
             sp.sumsq = p.sumsq;
-            if (int rc = sep_launch(ctx, sep_fn_k<2>(a->ksize, sp.clamp255), s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes))
+            void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255) : sep_fn_k<2>(a->ksize, sp.clamp255);
+            if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes))
                 return rc;
             return meanstd(ctx, a, p, frames, s);
         }

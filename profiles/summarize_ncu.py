@@ -37,6 +37,40 @@ def read(rep):
     return d
 
 
+SCALE = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}
+
+
+def update_traffic(tag, res):
+    """profiles/ncu_traffic.json: per config, DRAM bytes and warp instructions
+    per launch of the dominant kernel (bench.py reports them as
+    roofline.traffic / roofline.issue).  Captures are named prof_cfgN and
+    come from profiles/run_ncu.sh, i.e. bench.py's default frames per step."""
+    import os
+    sys.path.insert(0, os.getcwd())
+    from bench import DEFAULT_FRAMES
+    size = {1: (1920, 1080), 2: (3840, 2160), 3: (7680, 4320), 4: (3840, 2160)}
+    path = "profiles/ncu_traffic.json"
+    try:
+        table = json.load(open(path))
+    except Exception:
+        table = {}
+    for name, d in res.items():
+        if not name.startswith("prof_cfg"):
+            continue
+        cfg = int(name[len("prof_cfg"):])
+        w, h = size[cfg]
+        px = w * h * DEFAULT_FRAMES[cfg]
+        b = sum(d[m] * SCALE.get(d.get(m + ".unit", "byte"), 1.0)
+                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        table[str(cfg)] = {"kernel": d["kernel"], "dram_bytes_per_launch": round(b), "px_per_launch": px,
+                           "dram_bytes_per_px": round(b / px, 4),
+                           "warp_inst_per_px": round(d["smsp__inst_executed.sum"] / px, 4),
+                           "duration_us_under_ncu": d["gpu__time_duration.sum"],
+                           "source": f"profiles/ncu_{tag}.json"}
+    with open(path, "w") as f:
+        json.dump(table, f, indent=1, sort_keys=True)
+
+
 def main():
     tag, reps = sys.argv[1], sys.argv[2:]
     res = {}
@@ -45,6 +79,7 @@ def main():
         res[r.split("/")[-1].replace(".ncu-rep", "")] = d
     with open(f"profiles/ncu_{tag}.json", "w") as f:
         json.dump(res, f, indent=1)
+    update_traffic(tag, res)
     print(json.dumps(res, indent=1)[:3000])
 
 
