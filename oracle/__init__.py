@@ -73,6 +73,16 @@ def port():
     return _port
 
 
+def port_harris(img: np.ndarray, k: float, threshold: float):
+    """gvxo_harris with explicit k / T: (U8 mask, F32 response)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    mask = np.empty_like(img)
+    resp = np.empty(img.shape, np.float32)
+    port().gvxo_harris(img.ctypes.data, img.shape[1], img.shape[0], k, threshold, mask.ctypes.data,
+                       resp.ctypes.data)
+    return mask, resp
+
+
 def port_stencil(img: np.ndarray, mask, div: int, mode: int) -> np.ndarray:
     """gvxo_stencil_u8: KxK local node sat_U8(s * (1/div)) [-> unsharp chain]."""
     img = np.ascontiguousarray(img, np.uint8)

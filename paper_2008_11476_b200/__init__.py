@@ -374,6 +374,44 @@ def _mask49(mask):
     return m
 
 
+class GvxbHarrisArgs(ctypes.Structure):
+    """include/gvxb.h gvxb_harris_args."""
+    _fields_ = [("src", GvxbImage), ("mask", GvxbImage), ("response", GvxbImage), ("k", ctypes.c_double),
+                ("threshold", ctypes.c_double), ("band", GvxbBand)]
+
+
+def harris(device: "Device", img: np.ndarray, k: float, threshold: float, response: bool = False):
+    """Host wrapper over gvxb_harris on one U8 frame: returns the U8 mask
+    (and the F32 response image when `response`)."""
+    c, _ = _load()
+    c.gvxb_harris.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbHarrisArgs)]
+    h, w = img.shape
+    pitch = (w + 127) // 128 * 128
+    src, dst = device.alloc(pitch * h), device.alloc(pitch * h)
+    rsp = device.alloc(4 * pitch * h) if response else 0
+    try:
+        device.upload(src, pitch, np.ascontiguousarray(img, np.uint8))
+        a = GvxbHarrisArgs()
+        a.src = GvxbImage(src, pitch, w, h, 0, 1, 0)
+        a.mask = GvxbImage(dst, pitch, w, h, 0, 1, 0)
+        a.response = GvxbImage(rsp or None, 4 * pitch, w, h, 4, 1, 0)
+        a.k, a.threshold = float(k), float(threshold)
+        a.band = GvxbBand(0, h, h, 0, 0)
+        _check_cuda(c.gvxb_harris(device.h, ctypes.byref(a)))
+        out = np.empty((h, w), np.uint8)
+        device.download(out, dst, pitch)
+        if not response:
+            return out
+        r = np.empty((h, w), np.float32)
+        device.download(r, rsp, 4 * pitch)
+        return out, r
+    finally:
+        device.sync()
+        device.free(src), device.free(dst)
+        if rsp:
+            device.free(rsp)
+
+
 def stencil_point(device: "Device", img: np.ndarray, mask, div: int, mode: int) -> np.ndarray:
     """Host wrapper over gvxb_stencil_point (KxK U8 stencil, mode 0 plain,
     mode 1 unsharp chain) on one U8 frame; returns the U8 result."""
@@ -445,5 +483,5 @@ def band_rows(height: int, world: int, rank: int):
 
 
 __all__ = ["GraphvxError", "ConfigGraph", "Session", "Device", "build", "device_count", "random_u8",
-           "stencil_point", "conv_stats",
+           "stencil_point", "conv_stats", "harris",
            "band_rows", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]

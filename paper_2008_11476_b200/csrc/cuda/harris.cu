@@ -165,11 +165,14 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
         } else {
             // certified fp32 estimate of 81 (resp - T); p1 + p2 <= tt / 2
             const float2 kn = f2(p.kneg, p.kneg), nt = f2(-p.t81, -p.t81);
-            const float2 ctt = f2(p.c_tt, p.c_tt), ctr = f2(p.c_tr, p.c_tr), c0 = f2(p.c0, p.c0);
+            const float2 ctt = f2(p.c_tt, p.c_tt), c0 = f2(p.c0, p.c0);
             const Q4 tr = qadd(V.xx, V.yy), tt = qmul(tr, tr);
-            const Q4 det = qsub(qmul(V.xx, V.yy), qmul(V.xy, V.xy));
+            // det = xx yy - xy^2 with one rounding less (FMA), error within the bound
+            const float2 nxyE = mul2(V.xy.e, f2(-1.f, -1.f)), nxyO = mul2(V.xy.o, f2(-1.f, -1.f));
+            const Q4 det{fma2(nxyE, V.xy.e, mul2(V.xx.e, V.yy.e)), fma2(nxyO, V.xy.o, mul2(V.xx.o, V.yy.o))};
             const float2 dE = add2(fma2(kn, tt.e, det.e), nt), dO = add2(fma2(kn, tt.o, det.o), nt);
-            const float2 eE = fma2(ctt, tt.e, fma2(ctr, tr.e, c0)), eO = fma2(ctt, tt.o, fma2(ctr, tr.o, c0));
+            // bound linear in tt: the tr term folded in by tr <= (tt / a + a) / 2 (host picks a)
+            const float2 eE = fma2(ctt, tt.e, c0), eO = fma2(ctt, tt.o, c0);
             const float d[4] = {dE.x, dO.x, dE.y, dO.y};
             const float e[4] = {eE.x, eO.x, eE.y, eO.y};
             bool unsure = false;
@@ -317,10 +320,19 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     // representation errors of k and 81 T and the final float rounding of
     // the response (|81 T| 2^-22); slack factors keep every term conservative
     // (fl(tr) may be off by 1 above 2^24: +2|k| tr for the tt perturbation)
-    p.c_tr = static_cast<float>((9.0 + 20.0 * ak) * 1.01 + 1.0);
+    const double c_tr = (9.0 + 20.0 * ak) * 1.01 + 1.0;
     // fp32 evaluation error <= 2^-20 (p1 + p2 + |k| tt) <= 2^-20 (1/2 + |k|) tt
-    p.c_tt = static_cast<float>(std::ldexp(0.5 + ak, -20) * 1.01);
-    p.c0 = static_cast<float>((40.5 + 81.0 * ak) * 1.1 + 81.0 * at * 5e-7 + 64.0);
+    const double c_tt = std::ldexp(0.5 + ak, -20) * 1.01;
+    const double c_0 = (40.5 + 81.0 * ak) * 1.1 + 81.0 * at * 5e-7 + 64.0;
+    // c_tr tr <= c_tr (tt / a + a) / 2 for any a > 0; the bound is tightest at
+    // tr = a, so take a = the smallest tr that can reach the threshold
+    // (det <= tt / 4, hence tt >= 81 T / (1/4 - k) on the decision boundary)
+    double a_tr = 1.0;
+    if (a->threshold > 0 && a->k < 0.24) a_tr = std::sqrt(81.0 * a->threshold / (0.25 - a->k));
+    if (!(a_tr >= 1.0) || !std::isfinite(a_tr)) a_tr = 1.0;
+    p.c_tr = static_cast<float>(c_tr);
+    p.c_tt = static_cast<float>((c_tt + c_tr / (2.0 * a_tr)) * 1.001);
+    p.c0 = static_cast<float>((c_0 + c_tr * a_tr / 2.0) * 1.001 + 1.0);
     dim3 grid((s.width + kHarTW - 1) / kHarTW, (rows + p.th - 1) / p.th, frames);
     void* args[] = {&map, &p};
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kHarThreads), args, 0, ctx->stream);
