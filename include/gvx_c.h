@@ -69,6 +69,24 @@ void* gvxc_default_stream(void);
 /* Reference-identical synthetic input (random_buffer, U8). */
 int gvxc_random_u8(int width, int height, unsigned long long seed, uint8_t* out);
 
+/* ---- graph description files (graph_io.hpp, ref:src/graph_io.cpp) -------- */
+typedef struct gvxc_json_s* gvxc_json;
+/* save_graph_json(load_graph_json(text)); *len = bytes needed (incl. NUL). */
+int gvxc_json_roundtrip(const char* text, char* out, size_t cap, size_t* len);
+/* load -> verify -> expand -> verify -> optimize. */
+int gvxc_json_load(const char* text, gvxc_json* out);
+int gvxc_json_destroy(gvxc_json g);
+/* Runs with random_buffer(desc, seed + id) for every non-virtual source
+ * image; writes the declared outputs serialised as [u32 kind][u32 n][bytes]
+ * (configs/json_runner.hpp); *len = bytes needed; counters as in
+ * gvxc_graph_run_host. */
+int gvxc_json_run(gvxc_json g, int naive, unsigned long long seed, uint8_t* out, size_t cap, size_t* len,
+                  long long counters[4]);
+/* PassStats of the plan (same layout as gvxc_graph_pass_stats). */
+int gvxc_json_pass_stats(gvxc_json g, long long st[8]);
+/* Device program summary (naive = 1: per-node program, else the plan's). */
+int gvxc_json_describe(gvxc_json g, int naive, char* buf, size_t cap);
+
 #ifdef __cplusplus
 }
 #endif

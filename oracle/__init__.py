@@ -48,8 +48,42 @@ def ref():
         lib.oref_run_config.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p] * 2 + [
             ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         lib.oref_config_counters.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)]
+        lib.oref_have_graph_io.restype = ctypes.c_int
+        if lib.oref_have_graph_io():
+            SZ = ctypes.c_size_t
+            lib.oref_json_roundtrip.argtypes = [ctypes.c_char_p, ctypes.c_char_p, SZ, ctypes.POINTER(SZ)]
+            lib.oref_json_run.argtypes = [ctypes.c_char_p, ctypes.c_ulonglong, ctypes.c_void_p, SZ,
+                                          ctypes.POINTER(SZ), ctypes.POINTER(ctypes.c_longlong)]
         _ref = lib
     return _ref
+
+
+def have_ref_graph_io() -> bool:
+    return have_ref() and bool(ref().oref_have_graph_io())
+
+
+def ref_json_roundtrip(text: str) -> str:
+    """The reference's save_graph_json(load_graph_json(text))."""
+    lib = ref()
+    need = ctypes.c_size_t()
+    if lib.oref_json_roundtrip(text.encode(), None, 0, ctypes.byref(need)):
+        raise RuntimeError(lib.oref_last_error().decode())
+    buf = ctypes.create_string_buffer(need.value)
+    lib.oref_json_roundtrip(text.encode(), buf, need.value, ctypes.byref(need))
+    return buf.value.decode()
+
+
+def ref_json_run(text: str, seed: int):
+    """The reference pipeline over a graph file (run_naive); returns the raw
+    serialised outputs and the event counters."""
+    lib = ref()
+    need = ctypes.c_size_t()
+    counters = (ctypes.c_longlong * 4)()
+    if lib.oref_json_run(text.encode(), seed, None, 0, ctypes.byref(need), counters):
+        raise RuntimeError(lib.oref_last_error().decode())
+    buf = (ctypes.c_uint8 * max(1, need.value))()
+    lib.oref_json_run(text.encode(), seed, buf, need.value, ctypes.byref(need), counters)
+    return bytes(buf)[:need.value], list(counters)
 
 
 def port():

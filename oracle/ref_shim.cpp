@@ -16,6 +16,10 @@
 #include "graphvx/verify.hpp"
 
 #include "../paper_2008_11476_b200/csrc/configs/config_graphs.hpp"
+#ifdef OREF_GRAPH_IO
+#define GVX_JSON_RUNNER_NS gvxref_json_runner
+#include "../paper_2008_11476_b200/csrc/configs/json_runner.hpp"
+#endif
 
 #include <chrono>
 #include <cstring>
@@ -114,5 +118,49 @@ int oref_config_counters(int cfg, int w, int h, const unsigned char* in, long lo
         return 1;
     }
 }
+
+#ifdef OREF_GRAPH_IO
+/// save_graph_json(load_graph_json(text)) of the reference.
+int oref_json_roundtrip(const char* text, char* out, size_t cap, size_t* len) {
+    try {
+        const std::string t = gvx::save_graph_json(gvx::load_graph_json(text));
+        *len = t.size() + 1;
+        if (out && cap > 0) {
+            const size_t n = t.size() < cap - 1 ? t.size() : cap - 1;
+            std::memcpy(out, t.data(), n);
+            out[n] = 0;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+/// The reference pipeline over a graph file (configs/json_runner.hpp),
+/// run_naive with random_buffer(seed + id) inputs.
+int oref_json_run(const char* text, unsigned long long seed, unsigned char* out, size_t cap, size_t* len,
+                  long long* counters) {
+    try {
+        auto L = gvxref_json_runner::load(text);
+        const std::vector<std::uint8_t> r = gvxref_json_runner::run(*L, true, seed);
+        *len = r.size();
+        if (out) std::memcpy(out, r.data(), r.size() < cap ? r.size() : cap);
+        if (counters) {
+            counters[0] = L->counters.kernel_launches;
+            counters[1] = L->counters.pixels_read;
+            counters[2] = L->counters.pixels_written;
+            counters[3] = L->counters.transfers_executed;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+int oref_have_graph_io(void) { return 1; }
+#else
+int oref_have_graph_io(void) { return 0; }
+#endif
 
 } // extern "C"

@@ -113,6 +113,13 @@ def _declare(c, g):
     g.gvxc_random_u8.argtypes = [I, I, ctypes.c_ulonglong, U8P]
     g.gvxc_launch_count.restype = ctypes.c_longlong
     g.gvxc_default_stream.restype = P
+    SZ = ctypes.c_size_t
+    g.gvxc_json_roundtrip.argtypes = [ctypes.c_char_p, ctypes.c_char_p, SZ, ctypes.POINTER(SZ)]
+    g.gvxc_json_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(P)]
+    g.gvxc_json_destroy.argtypes = [P]
+    g.gvxc_json_run.argtypes = [P, I, ctypes.c_ulonglong, U8P, SZ, ctypes.POINTER(SZ), ctypes.POINTER(L)]
+    g.gvxc_json_pass_stats.argtypes = [P, ctypes.POINTER(L)]
+    g.gvxc_json_describe.argtypes = [P, I, ctypes.c_char_p, ctypes.c_size_t]
 
 
 def _check_graph(rc: int):
@@ -148,6 +155,64 @@ def random_u8(width: int, height: int, seed: int) -> np.ndarray:
     out = np.empty((height, width), np.uint8)
     _check_graph(g.gvxc_random_u8(width, height, seed, out.ctypes.data))
     return out
+
+
+def parse_outputs(blob: bytes):
+    """Declared outputs serialised by configs/json_runner.hpp:
+    [u32 kind][u32 n][payload]...; returns [(kind, bytes)]."""
+    out, i = [], 0
+    while i < len(blob):
+        kind = int.from_bytes(blob[i:i + 4], "little")
+        n = int.from_bytes(blob[i + 4:i + 8], "little")
+        out.append((kind, bytes(blob[i + 8:i + 8 + n])))
+        i += 8 + n
+    return out
+
+
+def json_roundtrip(text: str) -> str:
+    """save_graph_json(load_graph_json(text)) (graph_io.hpp)."""
+    _, g = _load()
+    need = ctypes.c_size_t()
+    _check_graph(g.gvxc_json_roundtrip(text.encode(), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check_graph(g.gvxc_json_roundtrip(text.encode(), buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
+
+
+class GraphFile:
+    """A graph-description file loaded through graph_io + verify/expand/
+    optimize; run() executes run_plan / run_naive on random_buffer inputs."""
+
+    def __init__(self, text: str):
+        _, self._g = _load()
+        self._h = ctypes.c_void_p()
+        _check_graph(self._g.gvxc_json_load(text.encode(), ctypes.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._g.gvxc_json_destroy(self._h)
+            self._h = None
+
+    def run(self, naive: bool = False, seed: int = 1):
+        need = ctypes.c_size_t()
+        counters = (ctypes.c_longlong * 4)()
+        _check_graph(self._g.gvxc_json_run(self._h, int(naive), seed, None, 0, ctypes.byref(need), counters))
+        buf = (ctypes.c_uint8 * max(1, need.value))()
+        _check_graph(self._g.gvxc_json_run(self._h, int(naive), seed, buf, need.value, ctypes.byref(need), counters))
+        names = ["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"]
+        return parse_outputs(bytes(buf)[:need.value]), dict(zip(names, list(counters)))
+
+    def describe(self, naive: bool = False) -> str:
+        buf = ctypes.create_string_buffer(8192)
+        _check_graph(self._g.gvxc_json_describe(self._h, int(naive), buf, 8192))
+        return buf.value.decode()
+
+    def pass_stats(self) -> dict:
+        st = (ctypes.c_longlong * 8)()
+        _check_graph(self._g.gvxc_json_pass_stats(self._h, st))
+        keys = ["nodes_before", "nodes_alive", "nodes_removed", "transfers_naive", "transfers_optimized",
+                "fused_groups", "launches_before", "launches_after"]
+        return dict(zip(keys, list(st)))
 
 
 class ConfigGraph:
@@ -483,5 +548,5 @@ def band_rows(height: int, world: int, rank: int):
 
 
 __all__ = ["GraphvxError", "ConfigGraph", "Session", "Device", "build", "device_count", "random_u8",
-           "stencil_point", "conv_stats", "harris",
+           "stencil_point", "conv_stats", "harris", "GraphFile", "json_roundtrip", "parse_outputs",
            "band_rows", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]

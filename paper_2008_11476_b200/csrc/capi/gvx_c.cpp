@@ -2,10 +2,12 @@
 #include "gvx_c.h"
 
 #include "../configs/config_graphs.hpp"
+#include "../configs/json_runner.hpp"
 #include "graphvx/device.hpp"
 #include "graphvx/optimize.hpp"
 #include "program.hpp"
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -225,6 +227,74 @@ int gvxc_random_u8(int w, int h, unsigned long long seed, uint8_t* out) {
         gvx::Buffer b = gvx::random_buffer(d, seed);
         std::memcpy(out, b.bytes.data(), b.bytes.size());
     });
+}
+
+} // extern "C"
+
+// ------------------------------------------------------------ graph files
+
+struct gvxc_json_s {
+    std::unique_ptr<gvx_json_runner::Loaded> L;
+};
+
+extern "C" {
+
+int gvxc_json_roundtrip(const char* text, char* out, size_t cap, size_t* len) {
+    return guarded([&] {
+        const std::string t = gvx::save_graph_json(gvx::load_graph_json(text));
+        if (len) *len = t.size() + 1;
+        if (out && cap > 0) {
+            const size_t n = std::min(cap - 1, t.size());
+            std::memcpy(out, t.data(), n);
+            out[n] = 0;
+        }
+    });
+}
+
+int gvxc_json_load(const char* text, gvxc_json* out) {
+    return guarded([&] {
+        auto g = std::make_unique<gvxc_json_s>();
+        g->L = gvx_json_runner::load(text);
+        *out = g.release();
+    });
+}
+
+int gvxc_json_destroy(gvxc_json g) {
+    delete g;
+    return 0;
+}
+
+int gvxc_json_run(gvxc_json g, int naive, unsigned long long seed, uint8_t* out, size_t cap, size_t* len,
+                  long long counters[4]) {
+    return guarded([&] {
+        const std::vector<std::uint8_t> r = gvx_json_runner::run(*g->L, naive != 0, seed);
+        if (len) *len = r.size();
+        if (out) std::memcpy(out, r.data(), std::min(cap, r.size()));
+        if (counters) {
+            counters[0] = g->L->counters.kernel_launches;
+            counters[1] = g->L->counters.pixels_read;
+            counters[2] = g->L->counters.pixels_written;
+            counters[3] = g->L->counters.transfers_executed;
+        }
+    });
+}
+
+int gvxc_json_describe(gvxc_json g, int naive, char* buf, size_t cap) {
+    return guarded([&] {
+        std::string d = naive ? gvx::DeviceSession(g->L->impl).describe() : gvx::DeviceSession(*g->L->plan).describe();
+        if (cap) {
+            std::strncpy(buf, d.c_str(), cap - 1);
+            buf[cap - 1] = '\0';
+        }
+    });
+}
+
+int gvxc_json_pass_stats(gvxc_json g, long long st[8]) {
+    const gvx::PassStats& p = g->L->plan->stats;
+    const long long v[8] = {p.nodes_before, p.nodes_alive, p.nodes_removed, p.transfers_naive,
+                            p.transfers_optimized, p.fused_groups, p.launches_before, p.launches_after};
+    std::memcpy(st, v, sizeof(v));
+    return 0;
 }
 
 } // extern "C"

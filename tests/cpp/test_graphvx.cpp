@@ -10,9 +10,12 @@
 
 #include "../../paper_2008_11476_b200/csrc/configs/config_graphs.hpp"
 #include "graphvx/device.hpp"
+#include "graphvx/image_io.hpp"
 #include "graphvx/optimize.hpp"
 
+#include <cstdio>
 #include <cstdlib>
+#include <fstream>
 #include <random>
 
 using namespace gvx;
@@ -197,6 +200,44 @@ TEST_CASE("execution without a device fails loudly (no host fallback)") {
     } catch (const Error& e) {
         CHECK(e.code() == ErrorCode::UnsupportedKind);
     }
+}
+
+TEST_CASE("image files: PGM / PPM / raw round trips and header errors (ref:src/image_io.cpp)") {
+    const std::string dir = std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp";
+    for (ImageFormat f : {ImageFormat::U8, ImageFormat::RGB, ImageFormat::S16, ImageFormat::F32, ImageFormat::UYVY}) {
+        Buffer b = random_buffer(img_desc(37, 11, f), 5);
+        const std::string path = dir + "/gvx_img_test" + default_extension(f);
+        write_image_file(path, b);
+        Buffer r = read_image_file(path);
+        CHECK(r.desc.width == 37);
+        CHECK(r.desc.height == 11);
+        CHECK(r.desc.format == f);
+        CHECK(r.bytes == b.bytes);
+        std::remove(path.c_str());
+    }
+    CHECK(default_extension(ImageFormat::U8) == ".pgm");
+    CHECK(default_extension(ImageFormat::RGB) == ".ppm");
+    CHECK(default_extension(ImageFormat::S32) == ".raw");
+    const std::string bad = dir + "/gvx_img_bad.pgm";
+    {
+        std::ofstream o(bad, std::ios::binary);
+        o << "P5\n# comment\n4 2\n65535\n";
+    }
+    CHECK_THROWS_AS(read_image_file(bad), Error);
+    {
+        std::ofstream o(bad, std::ios::binary);
+        o << "P5\n# comment\n4 2\n255\nab"; // truncated payload
+    }
+    CHECK_THROWS_AS(read_image_file(bad), Error);
+    {
+        std::ofstream o(bad, std::ios::binary);
+        o << "P5 4 2 255\nabcdefgh"; // single-line header
+    }
+    Buffer ok = read_image_file(bad);
+    CHECK(ok.desc.width == 4);
+    CHECK(ok.bytes[7] == 'h');
+    std::remove(bad.c_str());
+    CHECK_THROWS_AS(read_image_file(dir + "/gvx_no_such_file.pgm"), Error);
 }
 
 // ----------------------------------------------------------------- GPU
