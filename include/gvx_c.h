@@ -69,6 +69,12 @@ void* gvxc_default_stream(void);
 /* Reference-identical synthetic input (random_buffer, U8). */
 int gvxc_random_u8(int width, int height, unsigned long long seed, uint8_t* out);
 
+/* Zero-copy host runs: the graph's own page-locked input buffer (fill it and
+ * pass it as `in` to gvxc_graph_run_host, or pass NULL), and the first image
+ * output of the latest host run (valid until the next run). */
+int gvxc_graph_input_ptr(gvxc_graph g, uint8_t** ptr, size_t* bytes);
+int gvxc_graph_output_ptr(gvxc_graph g, const void** ptr, size_t* bytes);
+
 /* ---- graph description files (graph_io.hpp, ref:src/graph_io.cpp) -------- */
 typedef struct gvxc_json_s* gvxc_json;
 /* save_graph_json(load_graph_json(text)); *len = bytes needed (incl. NUL). */

@@ -113,6 +113,11 @@ int gvxb_alloc(gvxb_ctx ctx, size_t bytes, void** dptr);
 int gvxb_free(gvxb_ctx ctx, void* dptr);
 int gvxb_host_alloc(size_t bytes, void** hptr); /* pinned */
 int gvxb_host_free(void* hptr);
+/* Page-lock existing host memory (cudaHostRegister) so copies DMA from/to it
+ * directly; gvxb_host_is_pinned reports whether [ptr, ptr+bytes) is. */
+int gvxb_host_register(void* hptr, size_t bytes);
+int gvxb_host_unregister(void* hptr);
+int gvxb_host_is_pinned(const void* hptr, int* pinned);
 int gvxb_memset(gvxb_ctx ctx, void* dptr, int value, size_t bytes);
 int gvxb_upload_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
                    size_t row_bytes, size_t rows);
@@ -129,6 +134,8 @@ int gvxb_event_sync(void* ev); /* host waits for the event */
 
 /* ---- device status word / event counters ----------------------------------- */
 int gvxb_status_reset(gvxb_ctx ctx);
+/* Status word and read counter in one device->host read (one sync). */
+int gvxb_status_counter_read(gvxb_ctx ctx, uint32_t* status, long long* counter);
 /* Synchronises; returns the OR of GVXB_STATUS_* raised since the reset. */
 int gvxb_status_read(gvxb_ctx ctx, uint32_t* status);
 /* Device addresses of the status word and of the read counter (the

@@ -111,6 +111,8 @@ def _declare(c, g):
     g.gvxc_session_upload_input.argtypes = [P, I, U8P]
     g.gvxc_session_download.argtypes = [P, I, I, P, ctypes.POINTER(L), ctypes.POINTER(D)]
     g.gvxc_random_u8.argtypes = [I, I, ctypes.c_ulonglong, U8P]
+    g.gvxc_graph_input_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
+    g.gvxc_graph_output_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_launch_count.restype = ctypes.c_longlong
     g.gvxc_default_stream.restype = P
     SZ = ctypes.c_size_t
@@ -272,6 +274,25 @@ class ConfigGraph:
         if self.cfg == 4:
             return (np.array(list(hist), np.int64), stats[0], stats[1]), cnt
         return out, cnt
+
+    def run_host_inplace(self, image: np.ndarray, naive: bool = False):
+        """run_plan / run_naive with host buffers, leaving the result in the
+        graph's own (page-locked) output buffer instead of copying it out:
+        returns (read-only view of the output plane or cfg4 stats, counters).
+        The view is valid until the next host run."""
+        img = np.ascontiguousarray(image, dtype=np.uint8)
+        hist = (ctypes.c_longlong * 256)()
+        stats = (ctypes.c_double * 2)()
+        counters = (ctypes.c_longlong * 4)()
+        _check_graph(_graph.gvxc_graph_run_host(self._h, int(naive), img.ctypes.data, None, hist, stats, counters))
+        cnt = dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(counters)))
+        if self.cfg == 4:
+            return (np.array(list(hist), np.int64), stats[0], stats[1]), cnt
+        ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check_graph(_graph.gvxc_graph_output_ptr(self._h, ctypes.byref(ptr), ctypes.byref(n)))
+        dt = np.dtype(CONFIG_OUTPUT[self.cfg])
+        view = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), shape=(n.value,))
+        return view.view(dt).reshape(self.height, self.width), cnt
 
 
 class Session:

@@ -5,11 +5,13 @@
 #include "../configs/json_runner.hpp"
 #include "graphvx/device.hpp"
 #include "graphvx/optimize.hpp"
+#include "hostcopy.hpp"
 #include "program.hpp"
 
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <set>
 #include <string>
 
 namespace {
@@ -41,7 +43,20 @@ struct gvxc_graph_s {
     gvx_configs::ConfigGraph cg;
     gvx::VerifiedGraph impl;
     gvx::OptimizedPlan plan;
-    gvx::Buffer input; ///< reused between host runs (no per-call allocation)
+    gvx::Buffer input; ///< reused between host runs, page-locked once
+    /// page-locked output vectors handed back to the engine before each run
+    /// (detail::run_*_pooled): outputs DMA straight into them
+    std::map<gvx::ObjectId, std::vector<std::uint8_t>> pool;
+    gvx::ExecutionReport last; ///< outputs of the latest host run (output_ptr)
+    std::set<const void*> registered;
+
+    void pin(const std::vector<std::uint8_t>& v) {
+        if (v.size() < (1u << 20) || registered.count(v.data())) return;
+        if (gvxb_host_register(const_cast<std::uint8_t*>(v.data()), v.size()) == GVXB_OK) registered.insert(v.data());
+    }
+    ~gvxc_graph_s() {
+        for (const void* p : registered) gvxb_host_unregister(const_cast<void*>(p));
+    }
 };
 
 struct gvxc_session_s {
@@ -105,7 +120,19 @@ void copy_outputs(gvxc_graph g, const std::map<gvx::ObjectId, gvx::Buffer>& outs
         return;
     }
     const gvx::Buffer& b = outs.at(g->cg.outputs[0]);
-    if (out) std::memcpy(out, b.bytes.data(), b.bytes.size());
+    if (out) gvx::dev::parallel_copy(out, b.bytes.data(), b.bytes.size());
+}
+
+void ensure_input(gvxc_graph g) {
+    if (!g->input.bytes.empty()) return;
+    gvx::ResolvedDesc d;
+    d.kind = gvx::ObjKind::Image;
+    d.width = g->width;
+    d.height = g->height;
+    d.format = gvx::ImageFormat::U8;
+    g->input = gvx::Buffer::image(d);
+    g->input.id = g->cg.input;
+    g->pin(g->input.bytes);
 }
 
 gvx::Buffer input_buffer(gvxc_graph g, const uint8_t* in) {
@@ -125,11 +152,27 @@ int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, l
                         long long counters[4]) {
     return guarded([&] {
         gvx::InputMap inputs;
-        if (g->input.bytes.empty()) g->input = input_buffer(g, in);
-        else std::memcpy(g->input.bytes.data(), in, g->input.bytes.size());
+        ensure_input(g);
+        // in == the buffer from gvxc_graph_input_ptr: the caller filled it in place
+        if (in && in != g->input.bytes.data())
+            gvx::dev::parallel_copy(g->input.bytes.data(), in, g->input.bytes.size(), /*streaming=*/true);
+        // recycle the previous run's (page-locked) output vectors
+        for (auto& [id, b] : g->last.outputs)
+            if (b.desc.kind == gvx::ObjKind::Image && !b.bytes.empty()) {
+                g->pin(b.bytes);
+                g->pool[id] = std::move(b.bytes);
+            }
+        g->last = gvx::ExecutionReport{};
         gvx::Buffer& slot = inputs[g->cg.input];
         slot = std::move(g->input);
-        gvx::ExecutionReport r = naive ? gvx::run_naive(g->impl, inputs) : gvx::run_plan(g->plan, inputs);
+        gvx::ExecutionReport r;
+        try {
+            r = naive ? gvx::detail::run_naive_pooled(g->impl, inputs, &g->pool)
+                      : gvx::detail::run_plan_pooled(g->plan, inputs, &g->pool);
+        } catch (...) {
+            g->input = std::move(slot);
+            throw;
+        }
         g->input = std::move(slot);
         copy_outputs(g, r.outputs, out, hist, stats);
         if (counters) {
@@ -138,6 +181,25 @@ int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, l
             counters[2] = r.counters.pixels_written;
             counters[3] = r.counters.transfers_executed;
         }
+        g->last = std::move(r);
+    });
+}
+
+int gvxc_graph_input_ptr(gvxc_graph g, uint8_t** ptr, size_t* bytes) {
+    return guarded([&] {
+        ensure_input(g);
+        *ptr = g->input.bytes.data();
+        if (bytes) *bytes = g->input.bytes.size();
+    });
+}
+
+int gvxc_graph_output_ptr(gvxc_graph g, const void** ptr, size_t* bytes) {
+    return guarded([&] {
+        auto it = g->last.outputs.find(g->cg.outputs.at(0));
+        if (it == g->last.outputs.end() || it->second.desc.kind != gvx::ObjKind::Image)
+            throw gvx::Error(gvx::ErrorCode::UnknownObject, "no image output from a previous host run");
+        *ptr = it->second.bytes.data();
+        if (bytes) *bytes = it->second.bytes.size();
     });
 }
 

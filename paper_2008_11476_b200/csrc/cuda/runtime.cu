@@ -168,6 +168,28 @@ int gvxb_host_free(void* p) {
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaFreeHost");
 }
 
+int gvxb_host_register(void* p, size_t bytes) {
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaHostRegister");
+}
+
+int gvxb_host_unregister(void* p) {
+    cudaError_t e = cudaHostUnregister(p);
+    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaHostUnregister");
+}
+
+int gvxb_host_is_pinned(const void* p, int* pinned) {
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError(); // unregistered pageable memory on older drivers
+        *pinned = 0;
+        return GVXB_OK;
+    }
+    *pinned = a.type == cudaMemoryTypeHost ? 1 : 0;
+    return GVXB_OK;
+}
+
 int gvxb_memset(gvxb_ctx ctx, void* p, int v, size_t bytes) {
     cudaError_t e = cudaMemsetAsync(p, v, bytes, ctx->stream);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemsetAsync");
@@ -176,16 +198,21 @@ int gvxb_memset(gvxb_ctx ctx, void* p, int v, size_t bytes) {
 int gvxb_upload_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
                    size_t row_bytes, size_t rows) {
     if (!rows || !row_bytes) return GVXB_OK;
-    cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyHostToDevice,
-                                      ctx->stream);
+    // dense on both sides: one linear copy (the DMA engines stream it faster)
+    cudaError_t e = dpitch == row_bytes && spitch == row_bytes
+                        ? cudaMemcpyAsync(dst, src, row_bytes * rows, cudaMemcpyHostToDevice, ctx->stream)
+                        : cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyHostToDevice,
+                                            ctx->stream);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemcpy2DAsync(H2D)");
 }
 
 int gvxb_download_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
                      size_t row_bytes, size_t rows) {
     if (!rows || !row_bytes) return GVXB_OK;
-    cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyDeviceToHost,
-                                      ctx->stream);
+    cudaError_t e = dpitch == row_bytes && spitch == row_bytes
+                        ? cudaMemcpyAsync(dst, src, row_bytes * rows, cudaMemcpyDeviceToHost, ctx->stream)
+                        : cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyDeviceToHost,
+                                            ctx->stream);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemcpy2DAsync(D2H)");
 }
 
@@ -245,6 +272,17 @@ int gvxb_status_ptr(gvxb_ctx ctx, uint32_t** p) {
 
 int gvxb_counter_ptr(gvxb_ctx ctx, unsigned long long** p) {
     *p = ctx->counter;
+    return GVXB_OK;
+}
+
+int gvxb_status_counter_read(gvxb_ctx ctx, uint32_t* status, long long* counter) {
+    // status word at +0, counter at +8 of the same allocation
+    unsigned long long v[2] = {0, 0};
+    cudaError_t e = cudaMemcpyAsync(v, ctx->status, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "status read");
+    *status = static_cast<uint32_t>(v[0] & 0xFFFFFFFFu);
+    *counter = static_cast<long long>(v[1]);
     return GVXB_OK;
 }
 

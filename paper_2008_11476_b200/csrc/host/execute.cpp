@@ -9,9 +9,12 @@
 //   transfers_executed                        :880-897
 // Everything per pixel runs on the device through include/gvxb.h.
 #include "graphvx/device.hpp"
+#include "hostcopy.hpp"
 #include "program.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -594,7 +597,7 @@ struct Staging {
         for (std::size_t r0 = 0; r0 < rows; r0 += per, k ^= 1) {
             const std::size_t n = std::min(per, rows - r0);
             wait(k);
-            std::memcpy(buf[k], src + r0 * row, n * row);
+            dev::parallel_copy(buf[k], src + r0 * row, n * row, /*streaming=*/true);
             dev::check(gvxb_upload_2d(ctx, dst + r0 * pitch, pitch, buf[k], row, row, n), "image upload");
             mark(k);
         }
@@ -615,7 +618,7 @@ struct Staging {
             const int k = static_cast<int>(c & 1);
             wait(k);
             const std::size_t r0 = c * per, n = std::min(per, rows - r0);
-            std::memcpy(dst + r0 * row, buf[k], n * row);
+            dev::parallel_copy(dst + r0 * row, buf[k], n * row);
             if (c + 2 < chunks) issue(c + 2);
         }
     }
@@ -624,6 +627,8 @@ struct Staging {
 struct DeviceSession::Impl {
     std::shared_ptr<dev::Program> prog;
     std::unique_ptr<Staging> staging; ///< host runs only (run_naive / run_plan)
+    /// optional pinned destinations for image outputs (C facade recycling)
+    std::map<ObjectId, std::vector<std::uint8_t>>* out_pool = nullptr;
     const VerifiedGraph* exec_graph = nullptr; ///< graph whose outputs are reported
     VerifiedGraph exec_copy;
     int frames = 1;
@@ -822,7 +827,14 @@ struct DeviceSession::Impl {
         if (oi.desc.kind == ObjKind::Image) {
             const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
             if (b.bytes.size() < row * oi.desc.height) throw Error(ErrorCode::ShapeMismatch, "image payload too small", id);
-            if (staging && row * oi.desc.height > Staging::kChunk / 4) {
+            int pinned = 0;
+            if (staging && row * oi.desc.height > Staging::kChunk / 4) gvxb_host_is_pinned(b.bytes.data(), &pinned);
+            static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
+            if (trace) std::fprintf(stderr, "[gvx host] upload object %llu (%p, %zu B): %s\n",
+                                    static_cast<unsigned long long>(id), static_cast<const void*>(b.bytes.data()),
+                                    row * static_cast<std::size_t>(oi.desc.height),
+                                    pinned ? "page-locked, direct DMA" : "pageable, staged");
+            if (staging && !pinned && row * oi.desc.height > Staging::kChunk / 4) {
                 staging->upload(base, static_cast<std::size_t>(s.pitch), b.bytes.data(), row,
                                 static_cast<std::size_t>(oi.desc.height));
                 return;
@@ -870,9 +882,25 @@ struct DeviceSession::Impl {
         b.id = id;
         b.desc = exec_graph->resolved().count(id) ? exec_graph->desc(id) : oi.desc;
         if (oi.desc.kind == ObjKind::Image) {
+            const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
+            if (out_pool) { // a recycled page-locked vector: DMA straight into it
+                auto it = out_pool->find(id);
+                if (it != out_pool->end() && it->second.size() == row * static_cast<std::size_t>(oi.desc.height)) {
+                    const ResolvedDesc d = b.desc;
+                    b = Buffer{};
+                    b.id = id;
+                    b.desc = d;
+                    b.bytes = std::move(it->second);
+                    out_pool->erase(it);
+                    dev::check(gvxb_download_2d(ctx, b.bytes.data(), row, base, static_cast<std::size_t>(s.pitch), row,
+                                                static_cast<std::size_t>(oi.desc.height)),
+                               "image download");
+                    dev::check(gvxb_sync(ctx), "download sync");
+                    return b;
+                }
+            }
             b = Buffer::image(b.desc);
             b.id = id;
-            const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
             if (staging && row * oi.desc.height > Staging::kChunk / 4) {
                 staging->download(b.bytes.data(), base, static_cast<std::size_t>(s.pitch), row,
                                   static_cast<std::size_t>(oi.desc.height));
@@ -1050,7 +1078,8 @@ std::shared_ptr<HostSession> host_session(const std::shared_ptr<dev::Program>& p
     return slot.second;
 }
 
-ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const VerifiedGraph& vg, const InputMap& inputs) {
+ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const VerifiedGraph& vg, const InputMap& inputs,
+                        std::map<ObjectId, std::vector<std::uint8_t>>* out_pool = nullptr) {
     std::map<ObjectId, Buffer> defaults;
     auto bound = bind_inputs(vg, inputs, defaults);
 
@@ -1058,19 +1087,30 @@ ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const Verifie
     std::lock_guard<std::mutex> lock(hs->mu);
     DeviceSession::Impl& s = hs->impl;
     s.exec_graph = &vg;
+    s.out_pool = out_pool;
+    struct PoolReset {
+        DeviceSession::Impl& s;
+        ~PoolReset() { s.out_pool = nullptr; }
+    } pool_reset{s};
+    static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
     gvxb_ctx_set_stream(s.ctx, nullptr);
     if (s.scratch.size() != prog->units.size()) s.prepare();
     for (const auto& [id, b] : bound)
         if (prog->objects.count(id)) s.upload(id, *b, 0);
+    if (trace) gvxb_sync(s.ctx); // attribute the H2D DMA to the upload phase
+    const auto t1 = clock::now();
     dev::check(gvxb_status_reset(s.ctx), "status reset");
     const std::int64_t launches0 = gvxb_launch_count(s.ctx);
     s.run_all();
+    const auto t1b = clock::now();
     std::uint32_t status = 0;
-    dev::check(gvxb_status_read(s.ctx, &status), "device status");
+    long long dyn_reads = 0;
+    dev::check(gvxb_status_counter_read(s.ctx, &status, &dyn_reads), "device status");
     if (status & GVXB_STATUS_DIV_BY_ZERO) throw Error(ErrorCode::DivByZero, "division by zero");
     if (status & GVXB_STATUS_INDEX_RANGE) throw Error(ErrorCode::ShapeMismatch, "array index out of range");
-    long long dyn_reads = 0;
-    dev::check(gvxb_counter_read(s.ctx, &dyn_reads), "counter read");
+    const auto t2 = clock::now();
 
     ExecutionReport report;
     report.counters.kernel_launches = gvxb_launch_count(s.ctx) - launches0;
@@ -1087,25 +1127,45 @@ ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const Verifie
         if (!prog->objects.count(id)) continue;
         report.outputs[id] = s.download(id, 0);
     }
+    if (trace) {
+        const auto t3 = clock::now();
+        auto us = [](clock::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+        std::fprintf(stderr, "[gvx host] upload %.1f us, launch (host) %.1f us, device+status %.1f us, download %.1f us\n",
+                     us(t1 - t0), us(t1b - t1), us(t2 - t1b), us(t3 - t2));
+    }
     return report;
 }
 
 } // namespace
 
-ExecutionReport run_naive(const VerifiedGraph& g, const InputMap& inputs) {
+namespace detail {
+
+ExecutionReport run_naive_pooled(const VerifiedGraph& g, const InputMap& inputs,
+                                 std::map<ObjectId, std::vector<std::uint8_t>>* out_pool) {
     if (!g.stamped()) throw Error(ErrorCode::UnstampedGraph, "execution needs a verified graph");
     auto prog = naive_program(g, &inputs);
-    ExecutionReport r = execute(prog, g, inputs);
+    ExecutionReport r = execute(prog, g, inputs, out_pool);
     r.counters.transfers_executed = static_cast<std::int64_t>(g.graph().nodes().size()) * 2;
     return r;
 }
 
-ExecutionReport run_plan(const OptimizedPlan& plan, const InputMap& inputs) {
+ExecutionReport run_plan_pooled(const OptimizedPlan& plan, const InputMap& inputs,
+                                std::map<ObjectId, std::vector<std::uint8_t>>* out_pool) {
     if (!plan.fused.stamped()) throw Error(ErrorCode::UnstampedGraph, "plan execution needs a verified fused graph");
     auto prog = plan_program(plan, &inputs);
-    ExecutionReport r = execute(prog, plan.fused, inputs);
+    ExecutionReport r = execute(prog, plan.fused, inputs, out_pool);
     r.counters.transfers_executed = plan.transfers.optimized_count();
     return r;
+}
+
+} // namespace detail
+
+ExecutionReport run_naive(const VerifiedGraph& g, const InputMap& inputs) {
+    return detail::run_naive_pooled(g, inputs, nullptr);
+}
+
+ExecutionReport run_plan(const OptimizedPlan& plan, const InputMap& inputs) {
+    return detail::run_plan_pooled(plan, inputs, nullptr);
 }
 
 // ------------------------------------------------------------ DeviceSession

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "graphvx/execute.hpp"
+#include "graphvx/optimize.hpp"
 #include "gvxb.h"
 #include "jit.hpp"
 
@@ -115,3 +116,16 @@ std::vector<Unit> match_fused_groups(const GraphView& view);
 bool static_counts(const OperatorNode& n, const VerifiedGraph& vg, std::int64_t& reads, std::int64_t& writes);
 
 } // namespace gvx::dev
+
+namespace gvx::detail {
+
+/// run_naive / run_plan whose image outputs are downloaded into vectors
+/// taken from `out_pool` (keyed by object id, matching size) when present:
+/// the C facade keeps page-locked vectors there and hands each report's
+/// vectors back before the next run, so outputs DMA straight into them.
+ExecutionReport run_naive_pooled(const VerifiedGraph& g, const InputMap& inputs,
+                                 std::map<ObjectId, std::vector<std::uint8_t>>* out_pool);
+ExecutionReport run_plan_pooled(const OptimizedPlan& plan, const InputMap& inputs,
+                                std::map<ObjectId, std::vector<std::uint8_t>>* out_pool);
+
+} // namespace gvx::detail

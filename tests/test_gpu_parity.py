@@ -105,3 +105,23 @@ def test_row_bands_reproduce_full_image(world, gvx, oracle_mod):
     assert np.array_equal(a, oracle_mod.port_run(1, img))
     for p in (src, full, banded):
         dev.free(p)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_host_runs_recycle_pinned_buffers(cfg, gvx, oracle_mod):
+    """Repeated host runs through the C facade: the input is copied into the
+    graph's page-locked Buffer and outputs DMA into recycled page-locked
+    vectors; every run must still return its own frame's result."""
+    w, h = 1031, 517
+    g = gvx.ConfigGraph(cfg, w, h)
+    frames = [gvx.random_u8(w, h, 40 + i) for i in range(3)]
+    for rnd in range(2):
+        for f in frames:
+            got, _ = g.run_host_inplace(f)
+            want = oracle_mod.port_run(cfg, f)
+            if cfg == 4:
+                assert np.array_equal(got[0], want[0]) and got[1] == want[1] and got[2] == want[2]
+            else:
+                assert np.array_equal(np.array(got), want), (cfg, rnd)
+            plain, _ = g.run_host(f)
+            assert _same(cfg, plain, want)
