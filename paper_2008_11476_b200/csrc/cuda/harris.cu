@@ -31,6 +31,7 @@
 #include "packed.cuh"
 
 #include <cmath>
+#include <type_traits>
 
 namespace gvxd {
 
@@ -109,175 +110,184 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
                  static_cast<int64_t>(y0 - p.band.dst_row0) * p.resp_pitch;
     const float2 two = f2(2.f, 2.f), magic = f2(-8388608.f, -8388608.f);
 
-    /// Separable Sobel terms of smem row j: D = in(x+1) - in(x-1),
-    /// S = in(x-1) + 2 in(x) + in(x+1) for columns c .. c+3.
-    auto sobel_terms = [&](int j, Q4& D, Q4& S) {
-        const uint8_t* row = tile + j * kHarSW;
-        const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
-        // column pairs P1=(c-1, c+1) P2=(c, c+2) P3=(c+1, c+3) P4=(c+2, c+4)
-        const float2 P1 = add2(f2(magic_byte(wl, 3), magic_byte(wc, 1)), magic);
-        const float2 P2 = add2(f2(magic_byte(wc, 0), magic_byte(wc, 2)), magic);
-        const float2 P3 = add2(f2(magic_byte(wc, 1), magic_byte(wc, 3)), magic);
-        const float2 P4 = add2(f2(magic_byte(wc, 2), magic_byte(wr, 0)), magic);
-        D = Q4{sub2(P3, P1), sub2(P4, P2)};
-        S = Q4{fma2(two, P2, add2(P1, P3)), fma2(two, P3, add2(P2, P4))};
-    };
-    /// Own columns beyond W-1 take column W-1's value (right border clamp).
-    auto clamp_right = [&](Q4& q) {
-        float v[4] = {q.e.x, q.o.x, q.e.y, q.o.y};
+    // kEdge: the warp touches the left / right image border (clamped
+    // neighbour columns); interior warps run without those selects
+    auto body = [&](auto edge_tag) {
+        constexpr bool kEdge = decltype(edge_tag)::value;
+        /// Separable Sobel terms of smem row j: D = in(x+1) - in(x-1),
+        /// S = in(x-1) + 2 in(x) + in(x+1) for columns c .. c+3.
+        auto sobel_terms = [&](int j, Q4& D, Q4& S) {
+            const uint8_t* row = tile + j * kHarSW;
+            const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
+            // column pairs P1=(c-1, c+1) P2=(c, c+2) P3=(c+1, c+3) P4=(c+2, c+4)
+            const float2 P1 = add2(f2(magic_byte(wl, 3), magic_byte(wc, 1)), magic);
+            const float2 P2 = add2(f2(magic_byte(wc, 0), magic_byte(wc, 2)), magic);
+            const float2 P3 = add2(f2(magic_byte(wc, 1), magic_byte(wc, 3)), magic);
+            const float2 P4 = add2(f2(magic_byte(wc, 2), magic_byte(wr, 0)), magic);
+            D = Q4{sub2(P3, P1), sub2(P4, P2)};
+            S = Q4{fma2(two, P2, add2(P1, P3)), fma2(two, P3, add2(P2, P4))};
+        };
+        /// Own columns beyond W-1 take column W-1's value (right border clamp).
+        auto clamp_right = [&](Q4& q) {
+            float v[4] = {q.e.x, q.o.x, q.e.y, q.o.y};
 #pragma unroll
-        for (int i = 1; i < 4; ++i)
-            if (i > last) v[i] = v[i - 1];
-        q = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
-    };
-    /// Horizontal 3-sums; neighbour columns c-1 / c+4 come from adjacent lanes.
-    auto hsum = [&](Q4 q) {
-        float pm1 = __shfl_up_sync(0xffffffffu, q.o.y, 1);  // left lane's c+3 = my c-1
-        float p4 = __shfl_down_sync(0xffffffffu, q.e.x, 1); // right lane's c  = my c+4
-        pm1 = left_edge ? q.e.x : pm1;
-        p4 = right_edge ? q.o.y : p4;
-        const float2 t = add2(q.e, q.o);
-        return Q4{add2(t, f2(pm1, q.o.x)), add2(t, f2(q.e.y, p4))};
-    };
-    /// Products of one Sobel row and their horizontal box sums.
-    auto products = [&](Q4 gx, Q4 gy) {
-        Q4 xx = qmul(gx, gx), yy = qmul(gy, gy), xy = qmul(gx, gy);
-        if (right_edge && last < 3) {
-            clamp_right(xx);
-            clamp_right(yy);
-            clamp_right(xy);
-        }
-        return Prod3{hsum(xx), hsum(yy), hsum(xy)};
-    };
-    /// Threshold decision (and optional exact response) for one output row.
-    auto emit = [&](int orow, const Prod3& V) {
-        const float sxx[4] = {V.xx.e.x, V.xx.o.x, V.xx.e.y, V.xx.o.y};
-        const float syy[4] = {V.yy.e.x, V.yy.o.x, V.yy.e.y, V.yy.o.y};
-        const float sxy[4] = {V.xy.e.x, V.xy.o.x, V.xy.e.y, V.xy.o.y};
-        uint32_t packed = 0;
-        float rv[4];
-        if constexpr (kResp) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                rv[i] = exact_response(sxx[i], syy[i], sxy[i], p.k);
-                packed |= (static_cast<double>(rv[i]) > p.threshold ? 255u : 0u) << (8 * i);
+            for (int i = 1; i < 4; ++i)
+                if (i > last) v[i] = v[i - 1];
+            q = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
+        };
+        /// Horizontal 3-sums; neighbour columns c-1 / c+4 come from adjacent lanes.
+        auto hsum = [&](Q4 q) {
+            float pm1 = __shfl_up_sync(0xffffffffu, q.o.y, 1);  // left lane's c+3 = my c-1
+            float p4 = __shfl_down_sync(0xffffffffu, q.e.x, 1); // right lane's c  = my c+4
+            if (kEdge) {
+                pm1 = left_edge ? q.e.x : pm1;
+                p4 = right_edge ? q.o.y : p4;
             }
-        } else {
-            // certified fp32 estimate of 81 (resp - T); p1 + p2 <= tt / 2
-            const float2 kn = f2(p.kneg, p.kneg), nt = f2(-p.t81, -p.t81);
-            const float2 ctt = f2(p.c_tt, p.c_tt), c0 = f2(p.c0, p.c0);
-            const Q4 tr = qadd(V.xx, V.yy), tt = qmul(tr, tr);
-            // det = xx yy - xy^2 with one rounding less (FMA), error within the bound
-            const float2 nxyE = mul2(V.xy.e, f2(-1.f, -1.f)), nxyO = mul2(V.xy.o, f2(-1.f, -1.f));
-            const Q4 det{fma2(nxyE, V.xy.e, mul2(V.xx.e, V.yy.e)), fma2(nxyO, V.xy.o, mul2(V.xx.o, V.yy.o))};
-            const float2 dE = add2(fma2(kn, tt.e, det.e), nt), dO = add2(fma2(kn, tt.o, det.o), nt);
-            // bound linear in tt: the tr term folded in by tr <= (tt / a + a) / 2 (host picks a)
-            const float2 eE = fma2(ctt, tt.e, c0), eO = fma2(ctt, tt.o, c0);
-            const float d[4] = {dE.x, dO.x, dE.y, dO.y};
-            const float e[4] = {eE.x, eO.x, eE.y, eO.y};
-            bool unsure = false;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                unsure |= !(fabsf(d[i]) > e[i]);
-                packed |= (d[i] > 0.f ? 255u : 0u) << (8 * i);
+            const float2 t = add2(q.e, q.o);
+            return Q4{add2(t, f2(pm1, q.o.x)), add2(t, f2(q.e.y, p4))};
+        };
+        /// Products of one Sobel row and their horizontal box sums.
+        auto products = [&](Q4 gx, Q4 gy) {
+            Q4 xx = qmul(gx, gx), yy = qmul(gy, gy), xy = qmul(gx, gy);
+            if (kEdge && right_edge && last < 3) {
+                clamp_right(xx);
+                clamp_right(yy);
+                clamp_right(xy);
             }
-            // rare, warp-uniform: the reference's exact expression where the
-            // estimate cannot decide
-            if (__any_sync(0xffffffffu, unsure)) {
-                packed = 0;
+            return Prod3{hsum(xx), hsum(yy), hsum(xy)};
+        };
+        /// Threshold decision (and optional exact response) for one output row.
+        auto emit = [&](int orow, const Prod3& V) {
+            const float sxx[4] = {V.xx.e.x, V.xx.o.x, V.xx.e.y, V.xx.o.y};
+            const float syy[4] = {V.yy.e.x, V.yy.o.x, V.yy.e.y, V.yy.o.y};
+            const float sxy[4] = {V.xy.e.x, V.xy.o.x, V.xy.e.y, V.xy.o.y};
+            uint32_t packed = 0;
+            float rv[4];
+            if constexpr (kResp) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    bool on;
-                    if (fabsf(d[i]) > e[i]) on = d[i] > 0.f;
-                    else on = static_cast<double>(exact_response(sxx[i], syy[i], sxy[i], p.k)) > p.threshold;
-                    packed |= (on ? 255u : 0u) << (8 * i);
+                    rv[i] = exact_response(sxx[i], syy[i], sxy[i], p.k);
+                    packed |= (static_cast<double>(rv[i]) > p.threshold ? 255u : 0u) << (8 * i);
                 }
-            }
-            (void)rv;
-        }
-        if (!owner) return;
-        uint8_t* mp = mrow + static_cast<int64_t>(orow) * p.mask_pitch;
-        if (c + 3 < W) {
-            *reinterpret_cast<uint32_t*>(mp) = packed;
-        } else {
+            } else {
+                // certified fp32 estimate of 81 (resp - T); p1 + p2 <= tt / 2
+                const float2 kn = f2(p.kneg, p.kneg), nt = f2(-p.t81, -p.t81);
+                const float2 ctt = f2(p.c_tt, p.c_tt), c0 = f2(p.c0, p.c0);
+                const Q4 tr = qadd(V.xx, V.yy), tt = qmul(tr, tr);
+                // det = xx yy - xy^2 with one rounding less (FMA), error within the bound
+                const float2 qE = mul2(V.xy.e, V.xy.e), qO = mul2(V.xy.o, V.xy.o);
+                const Q4 det{fma2(V.xx.e, V.yy.e, f2(-qE.x, -qE.y)), fma2(V.xx.o, V.yy.o, f2(-qO.x, -qO.y))};
+                const float2 dE = add2(fma2(kn, tt.e, det.e), nt), dO = add2(fma2(kn, tt.o, det.o), nt);
+                // bound linear in tt: the tr term folded in by tr <= (tt / a + a) / 2 (host picks a)
+                const float2 eE = fma2(ctt, tt.e, c0), eO = fma2(ctt, tt.o, c0);
+                const float d[4] = {dE.x, dO.x, dE.y, dO.y};
+                const float e[4] = {eE.x, eO.x, eE.y, eO.y};
+                bool unsure = false;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (c + i < W) mp[i] = static_cast<uint8_t>(packed >> (8 * i));
-        }
-        if constexpr (kResp) {
-            float* rp = reinterpret_cast<float*>(rrow + static_cast<int64_t>(orow) * p.resp_pitch) + c;
-            if (c + 3 < W) {
-                *reinterpret_cast<float4*>(rp) = make_float4(rv[0], rv[1], rv[2], rv[3]);
+                for (int i = 0; i < 4; ++i) {
+                    unsure |= !(fabsf(d[i]) > e[i]);
+                    packed |= (d[i] > 0.f ? 255u : 0u) << (8 * i);
+                }
+                // rare, warp-uniform: the reference's exact expression where the
+                // estimate cannot decide
+                if (__any_sync(0xffffffffu, unsure)) {
+                    packed = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        bool on;
+                        if (fabsf(d[i]) > e[i]) on = d[i] > 0.f;
+                        else on = static_cast<double>(exact_response(sxx[i], syy[i], sxy[i], p.k)) > p.threshold;
+                        packed |= (on ? 255u : 0u) << (8 * i);
+                    }
+                }
+                (void)rv;
+            }
+            if (!owner) return;
+            uint8_t* mp = mrow + static_cast<int64_t>(orow) * p.mask_pitch;
+            if (!kEdge || c + 3 < W) {
+                *reinterpret_cast<uint32_t*>(mp) = packed;
             } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (c + i < W) rp[i] = rv[i];
+                    if (c + i < W) mp[i] = static_cast<uint8_t>(packed >> (8 * i));
             }
+            if constexpr (kResp) {
+                float* rp = reinterpret_cast<float*>(rrow + static_cast<int64_t>(orow) * p.resp_pitch) + c;
+                if (!kEdge || c + 3 < W) {
+                    *reinterpret_cast<float4*>(rp) = make_float4(rv[0], rv[1], rv[2], rv[3]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (c + i < W) rp[i] = rv[i];
+                }
+            }
+        };
+
+        // Running sums instead of 3-row rings:
+        //   gx(r-1) = Q(r-1) + Q(r) with Q(r) = D(r-1) + D(r)
+        //   gy(r-1) = T(r-1) + T(r) with T(r) = S(r) - S(r-1)
+        //   box(m-1) = P(m-1) + H(m) with P(m) = H(m-1) + H(m)
+        // smem row j <-> global y0-2+j; Sobel row j-1 -> product row j-1 ->
+        // output row j-2 (global y0-4+j) once j >= 4.
+        // State of the running sums, in two alternating copies (A, B) so the
+        // 2x-unrolled loop renames instead of moving registers.
+        struct State {
+            Q4 Dp, Qp, Sp, Tp; // D(r-1), Q(r-1), S(r-1), T(r-1)
+            Prod3 P, Hp;        // P(m-1), H(m-1)
+        };
+        State A, B;
+        {
+            Q4 D0, S0, D1, S1;
+            sobel_terms(0, D0, S0);
+            sobel_terms(1, D1, S1);
+            A.Qp = qadd(D0, D1);
+            A.Tp = qsub(S1, S0);
+            A.Dp = D1;
+            A.Sp = S1;
+        }
+        /// Sobel row j-1 from source row j; writes the successor state into `o`.
+        auto sobel_step = [&](int j, const State& i, State& o) {
+            Q4 D, S;
+            sobel_terms(j, D, S);
+            o.Qp = qadd(i.Dp, D);
+            o.Tp = qsub(S, i.Sp);
+            o.Dp = D;
+            o.Sp = S;
+            return products(qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+        };
+        // product rows global y0-1 and y0 (row -1 clamps to row 0 at the top)
+        {
+            const Prod3 H1 = sobel_step(2, A, B);
+            const Prod3 H2 = sobel_step(3, B, A);
+            A.P = padd(y0 == 0 ? H2 : H1, H2);
+            A.Hp = H2;
+        }
+        auto full_step = [&](int j, const State& i, State& o) {
+            const Prod3 Hn = sobel_step(j, i, o);
+            emit(j - 4, padd(i.P, Hn));
+            o.P = padd(i.Hp, Hn);
+            o.Hp = Hn;
+        };
+        auto last_step = [&](int j, const State& i, State& o) {
+            // product row H clamps to row H-1 at the bottom border
+            const Prod3 Hn = sobel_step(j, i, o);
+            emit(j - 4, padd(i.P, (y1 == H) ? i.Hp : Hn));
+        };
+        const int steps = (y1 - y0) + 4;
+        int j = 4;
+        for (; j + 2 < steps; j += 2) {
+            full_step(j, A, B);
+            full_step(j + 1, B, A);
+        }
+        if (j + 1 < steps) {
+            full_step(j, A, B);
+            last_step(j + 1, B, A);
+        } else {
+            last_step(j, A, B);
         }
     };
-
-    // Running sums instead of 3-row rings:
-    //   gx(r-1) = Q(r-1) + Q(r) with Q(r) = D(r-1) + D(r)
-    //   gy(r-1) = T(r-1) + T(r) with T(r) = S(r) - S(r-1)
-    //   box(m-1) = P(m-1) + H(m) with P(m) = H(m-1) + H(m)
-    // smem row j <-> global y0-2+j; Sobel row j-1 -> product row j-1 ->
-    // output row j-2 (global y0-4+j) once j >= 4.
-    // State of the running sums, in two alternating copies (A, B) so the
-    // 2x-unrolled loop renames instead of moving registers.
-    struct State {
-        Q4 Dp, Qp, Sp, Tp; // D(r-1), Q(r-1), S(r-1), T(r-1)
-        Prod3 P, Hp;        // P(m-1), H(m-1)
-    };
-    State A, B;
-    {
-        Q4 D0, S0, D1, S1;
-        sobel_terms(0, D0, S0);
-        sobel_terms(1, D1, S1);
-        A.Qp = qadd(D0, D1);
-        A.Tp = qsub(S1, S0);
-        A.Dp = D1;
-        A.Sp = S1;
-    }
-    /// Sobel row j-1 from source row j; writes the successor state into `o`.
-    auto sobel_step = [&](int j, const State& i, State& o) {
-        Q4 D, S;
-        sobel_terms(j, D, S);
-        o.Qp = qadd(i.Dp, D);
-        o.Tp = qsub(S, i.Sp);
-        o.Dp = D;
-        o.Sp = S;
-        return products(qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
-    };
-    // product rows global y0-1 and y0 (row -1 clamps to row 0 at the top)
-    {
-        const Prod3 H1 = sobel_step(2, A, B);
-        const Prod3 H2 = sobel_step(3, B, A);
-        A.P = padd(y0 == 0 ? H2 : H1, H2);
-        A.Hp = H2;
-    }
-    auto full_step = [&](int j, const State& i, State& o) {
-        const Prod3 Hn = sobel_step(j, i, o);
-        emit(j - 4, padd(i.P, Hn));
-        o.P = padd(i.Hp, Hn);
-        o.Hp = Hn;
-    };
-    auto last_step = [&](int j, const State& i, State& o) {
-        // product row H clamps to row H-1 at the bottom border
-        const Prod3 Hn = sobel_step(j, i, o);
-        emit(j - 4, padd(i.P, (y1 == H) ? i.Hp : Hn));
-    };
-    const int steps = (y1 - y0) + 4;
-    int j = 4;
-    for (; j + 2 < steps; j += 2) {
-        full_step(j, A, B);
-        full_step(j + 1, B, A);
-    }
-    if (j + 1 < steps) {
-        full_step(j, A, B);
-        last_step(j + 1, B, A);
-    } else {
-        last_step(j, A, B);
-    }
+    if (__any_sync(0xffffffffu, left_edge || right_edge)) body(std::true_type{});
+    else body(std::false_type{});
 }
 
 } // namespace gvxd
