@@ -23,6 +23,8 @@
 // output written once: 1 B in + 2 B out per output pixel.
 #include "packed.cuh"
 
+#include <type_traits>
+
 namespace gvxd {
 
 constexpr int kEdgeThreads = 128;
@@ -62,6 +64,18 @@ __device__ __forceinline__ void store4(const OutPlane& o, int frame, int row, in
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             if (c + i < width) p[i] = static_cast<int16_t>(__float2int_rn(vv[i]));
+    }
+}
+
+/// Four S16 columns at p (columns c .. c+3); `full` = all inside the image.
+__device__ __forceinline__ void store4p(int16_t* p, bool full, int nvalid, Q4 v) {
+    if (full) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(pack_s16(v.e.x, v.o.x), pack_s16(v.e.y, v.o.y));
+    } else {
+        const float vv[4] = {v.e.x, v.o.x, v.e.y, v.o.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (i < nvalid) p[i] = static_cast<int16_t>(__float2int_rn(vv[i]));
     }
 }
 
@@ -114,127 +128,151 @@ __global__ void __launch_bounds__(kEdgeThreads) edge_kernel(const __grid_constan
     const int last = W - 1 - c;
     const int orow0 = y0 - p.band.dst_row0;
 
-    auto emit = [&](int r, Q4 gx, Q4 gy) {
-        if (!owner) return;
-        if (kGx) store4(p.gx, frame, orow0 + r, c, W, gx);
-        if (kGy) store4(p.gy, frame, orow0 + r, c, W, gy);
-        if (kMag)
-            store4(p.mag, frame, orow0 + r, c, W,
-                   round_sqrt4(Q4{fma2(gx.e, gx.e, mul2(gy.e, gy.e)), fma2(gx.o, gx.o, mul2(gy.o, gy.o))}));
-    };
-
-    struct State {
-        Q4 Dp, Qp, Sp, Tp; // Sobel running sums over the (Gaussian) rows
-        Q4 Hp, Rp;         // Gaussian running sums over source rows
-    };
-    State A, B;
-
-    if constexpr (kGauss) {
-        const float2 sc = f2(0.0625f, 0.0625f), M = f2(12582912.f, 12582912.f);
-        const float2 nM = f2(-12582912.f, -12582912.f);
-        /// Gaussian row (exact) from the biased sum v' = v + 8 (the +8 rides
-        /// in the source conversion, see load_cols6_biased):
-        /// floor(v' / 16) = fma_rd(v', 1/16, 1.5 * 2^23) - 1.5 * 2^23.
-        auto gauss_round = [&](Q4 v) {
-            return Q4{add2(__ffma2_rd(v.e, sc, M), nM), add2(__ffma2_rd(v.o, sc, M), nM)};
+    // kEdge: the warp touches the left / right image border (clamped
+    // neighbour columns, partial stores); interior warps skip that code
+    auto body = [&](auto edge_tag) {
+        constexpr bool kEdge = decltype(edge_tag)::value;
+        // output row pointers advance one row per emit (rows are emitted in order)
+        auto row_ptr = [&](const OutPlane& o) {
+            return reinterpret_cast<int16_t*>(reinterpret_cast<char*>(o.data) + frame * o.frame_stride +
+                                              static_cast<int64_t>(orow0) * o.pitch) + c;
         };
-        /// Sobel row terms of a Gaussian row held in registers (neighbour
-        /// columns through shuffles, clamped at the image border).
-        auto gauss_sobel_terms = [&](Q4 g, Q4& D, Q4& S) {
-            if (right_edge && last < 3) {
-                float v[4] = {g.e.x, g.o.x, g.e.y, g.o.y};
+        int16_t* pgx = kGx ? row_ptr(p.gx) : nullptr;
+        int16_t* pgy = kGy ? row_ptr(p.gy) : nullptr;
+        int16_t* pmag = kMag ? row_ptr(p.mag) : nullptr;
+        const bool full = c + 3 < W;
+        const int nvalid = W - c;
+        auto emit = [&](Q4 gx, Q4 gy) {
+            if (owner) {
+                const bool f = !kEdge || full;
+                if (kGx) store4p(pgx, f, nvalid, gx);
+                if (kGy) store4p(pgy, f, nvalid, gy);
+                if (kMag)
+                    store4p(pmag, f, nvalid,
+                            round_sqrt4(Q4{fma2(gx.e, gx.e, mul2(gy.e, gy.e)), fma2(gx.o, gx.o, mul2(gy.o, gy.o))}));
+            }
+            if (kGx) pgx = reinterpret_cast<int16_t*>(reinterpret_cast<char*>(pgx) + p.gx.pitch);
+            if (kGy) pgy = reinterpret_cast<int16_t*>(reinterpret_cast<char*>(pgy) + p.gy.pitch);
+            if (kMag) pmag = reinterpret_cast<int16_t*>(reinterpret_cast<char*>(pmag) + p.mag.pitch);
+        };
+
+        struct State {
+            Q4 Dp, Qp, Sp, Tp; // Sobel running sums over the (Gaussian) rows
+            Q4 Hp, Rp;         // Gaussian running sums over source rows
+        };
+        State A, B;
+
+        if constexpr (kGauss) {
+            const float2 sc = f2(0.0625f, 0.0625f), M = f2(12582912.f, 12582912.f);
+            const float2 nM = f2(-12582912.f, -12582912.f);
+            /// Gaussian row (exact) from the biased sum v' = v + 8 (the +8 rides
+            /// in the source conversion, see load_cols6_biased):
+            /// floor(v' / 16) = fma_rd(v', 1/16, 1.5 * 2^23) - 1.5 * 2^23.
+            auto gauss_round = [&](Q4 v) {
+                return Q4{add2(__ffma2_rd(v.e, sc, M), nM), add2(__ffma2_rd(v.o, sc, M), nM)};
+            };
+            /// Sobel row terms of a Gaussian row held in registers (neighbour
+            /// columns through shuffles, clamped at the image border).
+            auto gauss_sobel_terms = [&](Q4 g, Q4& D, Q4& S) {
+                if (kEdge && right_edge && last < 3) {
+                    float v[4] = {g.e.x, g.o.x, g.e.y, g.o.y};
 #pragma unroll
-                for (int i = 1; i < 4; ++i)
-                    if (i > last) v[i] = v[i - 1];
-                g = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
+                    for (int i = 1; i < 4; ++i)
+                        if (i > last) v[i] = v[i - 1];
+                    g = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
+                }
+                float gl = __shfl_up_sync(0xffffffffu, g.o.y, 1);
+                float gr = __shfl_down_sync(0xffffffffu, g.e.x, 1);
+                if (kEdge) {
+                    gl = left_edge ? g.e.x : gl;
+                    gr = right_edge ? g.o.y : gr;
+                }
+                diff_smooth(neighbourhood(g, gl, gr), D, S);
+            };
+            /// Source row j: Gaussian horizontal sums; returns the Gaussian row
+            /// centred one row up (smem row j-1).
+            auto src_step = [&](int j, const State& i, State& o) {
+                Q4 Dn, Hg;
+                diff_smooth(load_cols6_biased(tile + j * kEdgeSW, off), Dn, Hg); // Hg + 2 (Dn unused)
+                o.Rp = qadd(i.Hp, Hg);
+                o.Hp = Hg;
+                return gauss_round(qadd(i.Rp, o.Rp));
+            };
+            {
+                Q4 Dn, S0, S1;
+                diff_smooth(load_cols6_biased(tile, off), Dn, S0);
+                diff_smooth(load_cols6_biased(tile + kEdgeSW, off), Dn, S1);
+                A.Hp = S1;
+                A.Rp = qadd(S0, S1);
             }
-            float gl = __shfl_up_sync(0xffffffffu, g.o.y, 1);
-            float gr = __shfl_down_sync(0xffffffffu, g.e.x, 1);
-            gl = left_edge ? g.e.x : gl;
-            gr = right_edge ? g.o.y : gr;
-            diff_smooth(neighbourhood(g, gl, gr), D, S);
-        };
-        /// Source row j: Gaussian horizontal sums; returns the Gaussian row
-        /// centred one row up (smem row j-1).
-        auto src_step = [&](int j, const State& i, State& o) {
-            Q4 Dn, Hg;
-            diff_smooth(load_cols6_biased(tile + j * kEdgeSW, off), Dn, Hg); // Hg + 2 (Dn unused)
-            o.Rp = qadd(i.Hp, Hg);
-            o.Hp = Hg;
-            return gauss_round(qadd(i.Rp, o.Rp));
-        };
-        {
-            Q4 Dn, S0, S1;
-            diff_smooth(load_cols6_biased(tile, off), Dn, S0);
-            diff_smooth(load_cols6_biased(tile + kEdgeSW, off), Dn, S1);
-            A.Hp = S1;
-            A.Rp = qadd(S0, S1);
-        }
-        Q4 D1, G1, D2, G2;
-        gauss_sobel_terms(src_step(2, A, B), D1, G1); // Gaussian row y0-1
-        gauss_sobel_terms(src_step(3, B, A), D2, G2); // Gaussian row y0
-        if (y0 == 0) {                                // Gaussian row -1 clamps to row 0
-            D1 = D2;
-            G1 = G2;
-        }
-        A.Qp = qadd(D1, D2);
-        A.Tp = qsub(G2, G1);
-        A.Dp = D2;
-        A.Sp = G2;
-        auto full_step = [&](int j, const State& i, State& o, bool bottom) {
-            Q4 D, S;
-            gauss_sobel_terms(src_step(j, i, o), D, S);
-            if (bottom) { // Gaussian row H clamps to row H-1
-                D = i.Dp;
-                S = i.Sp;
+            Q4 D1, G1, D2, G2;
+            gauss_sobel_terms(src_step(2, A, B), D1, G1); // Gaussian row y0-1
+            gauss_sobel_terms(src_step(3, B, A), D2, G2); // Gaussian row y0
+            if (y0 == 0) {                                // Gaussian row -1 clamps to row 0
+                D1 = D2;
+                G1 = G2;
             }
-            o.Qp = qadd(i.Dp, D);
-            o.Tp = qsub(S, i.Sp);
-            o.Dp = D;
-            o.Sp = S;
-            emit(j - 4, qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
-        };
-        const int steps = (y1 - y0) + 4;
-        int j = 4;
-        for (; j + 2 < steps; j += 2) {
-            full_step(j, A, B, false);
-            full_step(j + 1, B, A, false);
-        }
-        const bool bot = y1 == H;
-        if (j + 1 < steps) {
-            full_step(j, A, B, false);
-            full_step(j + 1, B, A, bot);
+            A.Qp = qadd(D1, D2);
+            A.Tp = qsub(G2, G1);
+            A.Dp = D2;
+            A.Sp = G2;
+            auto full_step = [&](int j, const State& i, State& o, bool bottom) {
+                Q4 D, S;
+                gauss_sobel_terms(src_step(j, i, o), D, S);
+                if (bottom) { // Gaussian row H clamps to row H-1
+                    D = i.Dp;
+                    S = i.Sp;
+                }
+                o.Qp = qadd(i.Dp, D);
+                o.Tp = qsub(S, i.Sp);
+                o.Dp = D;
+                o.Sp = S;
+                emit(qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+            };
+            const int steps = (y1 - y0) + 4;
+            int j = 4;
+            for (; j + 2 < steps; j += 2) {
+                full_step(j, A, B, false);
+                full_step(j + 1, B, A, false);
+            }
+            const bool bot = y1 == H;
+            if (j + 1 < steps) {
+                full_step(j, A, B, false);
+                full_step(j + 1, B, A, bot);
+            } else {
+                full_step(j, A, B, bot);
+            }
         } else {
-            full_step(j, A, B, bot);
+            // Sobel straight on the source (Clamp is already in shared memory)
+            {
+                Q4 D0, S0, D1, S1;
+                diff_smooth(load_cols6(tile + 1 * kEdgeSW, off), D0, S0); // global y0-1
+                diff_smooth(load_cols6(tile + 2 * kEdgeSW, off), D1, S1); // global y0
+                A.Qp = qadd(D0, D1);
+                A.Tp = qsub(S1, S0);
+                A.Dp = D1;
+                A.Sp = S1;
+            }
+            auto step = [&](int j, const State& i, State& o) {
+                Q4 D, S;
+                diff_smooth(load_cols6(tile + j * kEdgeSW, off), D, S);
+                o.Qp = qadd(i.Dp, D);
+                o.Tp = qsub(S, i.Sp);
+                o.Dp = D;
+                o.Sp = S;
+                emit(qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+            };
+            const int steps = (y1 - y0) + 3;
+            int j = 3;
+            for (; j + 1 < steps; j += 2) {
+                step(j, A, B);
+                step(j + 1, B, A);
+            }
+            if (j < steps) step(j, A, B);
         }
-    } else {
-        // Sobel straight on the source (Clamp is already in shared memory)
-        {
-            Q4 D0, S0, D1, S1;
-            diff_smooth(load_cols6(tile + 1 * kEdgeSW, off), D0, S0); // global y0-1
-            diff_smooth(load_cols6(tile + 2 * kEdgeSW, off), D1, S1); // global y0
-            A.Qp = qadd(D0, D1);
-            A.Tp = qsub(S1, S0);
-            A.Dp = D1;
-            A.Sp = S1;
-        }
-        auto step = [&](int j, const State& i, State& o) {
-            Q4 D, S;
-            diff_smooth(load_cols6(tile + j * kEdgeSW, off), D, S);
-            o.Qp = qadd(i.Dp, D);
-            o.Tp = qsub(S, i.Sp);
-            o.Dp = D;
-            o.Sp = S;
-            emit(j - 3, qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
-        };
-        const int steps = (y1 - y0) + 3;
-        int j = 3;
-        for (; j + 1 < steps; j += 2) {
-            step(j, A, B);
-            step(j + 1, B, A);
-        }
-        if (j < steps) step(j, A, B);
-    }
+    };
+    if (__any_sync(0xffffffffu, left_edge || right_edge)) body(std::true_type{});
+    else body(std::false_type{});
 }
 
 } // namespace gvxd
