@@ -42,7 +42,10 @@ CONFIG_NAME = {
 ALGO_BYTES = {1: 3, 2: 2, 3: 2, 4: 1, 5: 3}
 KERNEL_NAME = {1: "edge_kernel", 2: "harris_kernel", 3: "sep_kernel<5,1> (separable stencil, unsharp epilogue)", 4: "sep_kernel<5,2> (separable conv + value histogram)",
                5: "edge_kernel"}
-DEFAULT_FRAMES = {1: 16, 2: 8, 3: 2, 4: 64, 5: 1}
+# frames per launch: each step is one fused launch over a batch of frames; the
+# two rotating batches (inputs + outputs) span >= 4x the 126 MB L2 (SURVEY.md
+# §8d), which also amortises the ~20 us fixed cost of a launch (ramp + tail)
+DEFAULT_FRAMES = {1: 64, 2: 32, 3: 8, 4: 64, 5: 1}
 CPU_SAMPLE = {1: (1920, 1080), 2: (3840, 544), 3: (7680, 272), 4: (3840, 544), 5: (16384, 128)}
 
 
@@ -497,7 +500,7 @@ def main():
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (reference random_buffer frame + derived frames)",
             "config": {"workload": CONFIG_NAME[cfg], "width": res["w"], "height": res["h"],
-                       "frames_per_step": res["frames"], "l2": "inputs rotate over 2 batches larger than L2"
+                       "frames_per_step": res["frames"], "l2": "inputs/outputs rotate over 2 batches spanning >= 4x L2"
                        if cfg != 5 else "16384^2 input > L2",
                        "parallelism": f"{'row bands' if cfg == 5 else 'frame replicas'} x{world}"},
             "e2e": res["e2e"], "roofline": roof, "cpu_baseline": cpu, "clocks": res["clocks"],
