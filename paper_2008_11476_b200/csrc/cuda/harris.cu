@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
     uint8_t* mrow = p.mask + frame * p.mask_fstride + static_cast<int64_t>(y0 - p.band.dst_row0) * p.mask_pitch + c;
     char* rrow = reinterpret_cast<char*>(p.resp) + frame * p.resp_fstride +
                  static_cast<int64_t>(y0 - p.band.dst_row0) * p.resp_pitch;
-    const float2 two = f2(2.f, 2.f), magic = f2(-8388608.f, -8388608.f);
+    const float2 two = f2(2.f, 2.f);
 
     // kEdge: the warp touches the left / right image border (clamped
     // neighbour columns); interior warps run without those selects
@@ -116,16 +116,28 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
         constexpr bool kEdge = decltype(edge_tag)::value;
         /// Separable Sobel terms of smem row j: D = in(x+1) - in(x-1),
         /// S = in(x-1) + 2 in(x) + in(x+1) for columns c .. c+3.
-        auto sobel_terms = [&](int j, Q4& D, Q4& S) {
+        /// Source row j as magic floats 2^23 + x in column pairs
+        /// P1=(c-1, c+1) P2=(c, c+2) P3=(c+1, c+3) P4=(c+2, c+4): byte
+        /// permutes only.  Every use below is a difference of two such
+        /// floats, where the 2^23 cancels exactly, so no conversion op.
+        auto raw_pairs = [&](int j) {
             const uint8_t* row = tile + j * kHarSW;
             const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
-            // column pairs P1=(c-1, c+1) P2=(c, c+2) P3=(c+1, c+3) P4=(c+2, c+4)
-            const float2 P1 = add2(f2(magic_byte(wl, 3), magic_byte(wc, 1)), magic);
-            const float2 P2 = add2(f2(magic_byte(wc, 0), magic_byte(wc, 2)), magic);
-            const float2 P3 = add2(f2(magic_byte(wc, 1), magic_byte(wc, 3)), magic);
-            const float2 P4 = add2(f2(magic_byte(wc, 2), magic_byte(wr, 0)), magic);
-            D = Q4{sub2(P3, P1), sub2(P4, P2)};
-            S = Q4{fma2(two, P2, add2(P1, P3)), fma2(two, P3, add2(P2, P4))};
+            Cols6 q;
+            q.p1 = f2(magic_byte(wl, 3), magic_byte(wc, 1));
+            q.p2 = f2(magic_byte(wc, 0), magic_byte(wc, 2));
+            q.p3 = f2(magic_byte(wc, 1), magic_byte(wc, 3));
+            q.p4 = f2(magic_byte(wc, 2), magic_byte(wr, 0));
+            return q;
+        };
+        /// Sobel-x row term D = in(x+1) - in(x-1) of source row j.
+        auto sobel_d = [&](const Cols6& q) { return Q4{sub2(q.p3, q.p1), sub2(q.p4, q.p2)}; };
+        /// Sobel-y of the row between source rows j and j-2: vertical
+        /// difference first, then the 1-2-1 smoothing across columns.
+        auto sobel_y = [&](const Cols6& q, const Cols6& m) {
+            const float2 v1 = sub2(q.p1, m.p1), v2 = sub2(q.p2, m.p2), v3 = sub2(q.p3, m.p3),
+                         v4 = sub2(q.p4, m.p4);
+            return Q4{fma2(two, v2, add2(v1, v3)), fma2(two, v3, add2(v2, v4))};
         };
         /// Own columns beyond W-1 take column W-1's value (right border clamp).
         auto clamp_right = [&](Q4& q) {
@@ -171,13 +183,15 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
                 }
             } else {
                 // certified fp32 estimate of 81 (resp - T); p1 + p2 <= tt / 2
-                const float2 kn = f2(p.kneg, p.kneg), nt = f2(-p.t81, -p.t81);
+                const float2 kn = f2(p.kneg, p.kneg);
                 const float2 ctt = f2(p.c_tt, p.c_tt), c0 = f2(p.c0, p.c0);
                 const Q4 tr = qadd(V.xx, V.yy), tt = qmul(tr, tr);
                 // det = xx yy - xy^2 with one rounding less (FMA), error within the bound
-                const float2 qE = mul2(V.xy.e, V.xy.e), qO = mul2(V.xy.o, V.xy.o);
+                // with 81 T folded into the xy^2 term: d = xx yy - (xy^2 + 81 T) - k tt
+                const float2 t81 = f2(p.t81, p.t81);
+                const float2 qE = fma2(V.xy.e, V.xy.e, t81), qO = fma2(V.xy.o, V.xy.o, t81);
                 const Q4 det{fma2(V.xx.e, V.yy.e, f2(-qE.x, -qE.y)), fma2(V.xx.o, V.yy.o, f2(-qO.x, -qO.y))};
-                const float2 dE = add2(fma2(kn, tt.e, det.e), nt), dO = add2(fma2(kn, tt.o, det.o), nt);
+                const float2 dE = fma2(kn, tt.e, det.e), dO = fma2(kn, tt.o, det.o);
                 // bound linear in tt: the tr term folded in by tr <= (tt / a + a) / 2 (host picks a)
                 const float2 eE = fma2(ctt, tt.e, c0), eO = fma2(ctt, tt.o, c0);
                 const float d[4] = {dE.x, dO.x, dE.y, dO.y};
@@ -232,28 +246,27 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
         // State of the running sums, in two alternating copies (A, B) so the
         // 2x-unrolled loop renames instead of moving registers.
         struct State {
-            Q4 Dp, Qp, Sp, Tp; // D(r-1), Q(r-1), S(r-1), T(r-1)
-            Prod3 P, Hp;        // P(m-1), H(m-1)
+            Q4 Dp, Qp;   // D(r-1), Q(r-1)
+            Cols6 Raw;   // raw pairs of the source row this copy last consumed
+            Prod3 P, Hp; // P(m-1), H(m-1)
         };
         State A, B;
         {
-            Q4 D0, S0, D1, S1;
-            sobel_terms(0, D0, S0);
-            sobel_terms(1, D1, S1);
+            B.Raw = raw_pairs(0); // the copies alternate, so each holds row j-2 when step j reads it
+            A.Raw = raw_pairs(1);
+            const Q4 D0 = sobel_d(B.Raw), D1 = sobel_d(A.Raw);
             A.Qp = qadd(D0, D1);
-            A.Tp = qsub(S1, S0);
             A.Dp = D1;
-            A.Sp = S1;
         }
-        /// Sobel row j-1 from source row j; writes the successor state into `o`.
+        /// Sobel row j-1 from source rows j-2 .. j; writes the successor state into `o`.
         auto sobel_step = [&](int j, const State& i, State& o) {
-            Q4 D, S;
-            sobel_terms(j, D, S);
+            const Cols6 q = raw_pairs(j);
+            const Q4 D = sobel_d(q);
+            const Q4 gy = sobel_y(q, o.Raw); // o.Raw = source row j-2
+            o.Raw = q;
             o.Qp = qadd(i.Dp, D);
-            o.Tp = qsub(S, i.Sp);
             o.Dp = D;
-            o.Sp = S;
-            return products(qadd(i.Qp, o.Qp), qadd(i.Tp, o.Tp));
+            return products(qadd(i.Qp, o.Qp), gy);
         };
         // product rows global y0-1 and y0 (row -1 clamps to row 0 at the top)
         {
