@@ -9,6 +9,9 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -154,8 +157,15 @@ int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, l
         gvx::InputMap inputs;
         ensure_input(g);
         // in == the buffer from gvxc_graph_input_ptr: the caller filled it in place
-        if (in && in != g->input.bytes.data())
-            gvx::dev::parallel_copy(g->input.bytes.data(), in, g->input.bytes.size(), /*streaming=*/true);
+        // the caller's frame goes into the page-locked input Buffer during the
+        // upload, chunk by chunk (copy of chunk k+1 overlaps the DMA of chunk k)
+        gvx::detail::HostFill fill;
+        if (in && in != g->input.bytes.data()) {
+            fill.id = g->cg.input;
+            fill.src = in;
+            if (!g->registered.count(g->input.bytes.data())) // not page-locked: copy up front
+                gvx::dev::parallel_copy(g->input.bytes.data(), in, g->input.bytes.size()), fill.src = nullptr;
+        }
         // recycle the previous run's (page-locked) output vectors
         for (auto& [id, b] : g->last.outputs)
             if (b.desc.kind == gvx::ObjKind::Image && !b.bytes.empty()) {
@@ -167,8 +177,8 @@ int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, l
         slot = std::move(g->input);
         gvx::ExecutionReport r;
         try {
-            r = naive ? gvx::detail::run_naive_pooled(g->impl, inputs, &g->pool)
-                      : gvx::detail::run_plan_pooled(g->plan, inputs, &g->pool);
+            r = naive ? gvx::detail::run_naive_pooled(g->impl, inputs, &g->pool, &fill)
+                      : gvx::detail::run_plan_pooled(g->plan, inputs, &g->pool, &fill);
         } catch (...) {
             g->input = std::move(slot);
             throw;

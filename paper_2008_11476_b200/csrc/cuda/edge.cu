@@ -53,20 +53,6 @@ __device__ __forceinline__ uint32_t pack_s16(float lo, float hi) {
     return __byte_perm(__float_as_uint(lo + m), __float_as_uint(hi + m), 0x5410);
 }
 
-__device__ __forceinline__ void store4(const OutPlane& o, int frame, int row, int c, int width, Q4 v) {
-    char* base = reinterpret_cast<char*>(o.data) + frame * o.frame_stride + static_cast<int64_t>(row) * o.pitch;
-    int16_t* p = reinterpret_cast<int16_t*>(base) + c;
-    // columns c, c+1, c+2, c+3 = e.x, o.x, e.y, o.y
-    if (c + 3 < width) {
-        *reinterpret_cast<uint2*>(p) = make_uint2(pack_s16(v.e.x, v.o.x), pack_s16(v.e.y, v.o.y));
-    } else {
-        const float vv[4] = {v.e.x, v.o.x, v.e.y, v.o.y};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (c + i < width) p[i] = static_cast<int16_t>(__float2int_rn(vv[i]));
-    }
-}
-
 /// Four S16 columns at p (columns c .. c+3); `full` = all inside the image.
 __device__ __forceinline__ void store4p(int16_t* p, bool full, int nvalid, Q4 v) {
     if (full) {

@@ -63,31 +63,6 @@ __device__ __forceinline__ Cols6 load_cols6_biased(const uint8_t* row, int off) 
     return c;
 }
 
-/// Input Clamp for lanes whose 6 columns straddle the image border: columns
-/// outside [0, W) take the value of the nearest in-image column (TMA filled
-/// them with zeros).  Divergent slow path, border lanes only.
-__device__ __forceinline__ void clamp_cols6(Cols6& q, int c, int W) {
-    // v[i] = column c - 1 + i
-    float v[6] = {q.p1.x, q.p2.x, q.p1.y, q.p2.y, q.p3.y, q.p4.y};
-    const int lo = 1 - c;     // index of column 0
-    const int hi = W - c;     // index of column W-1
-    float vlo = v[0], vhi = v[5];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-        if (i == lo) vlo = v[i];
-        if (i == hi) vhi = v[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-        if (i < lo) v[i] = vlo;
-        if (i > hi) v[i] = vhi;
-    }
-    q.p1 = f2(v[0], v[2]);
-    q.p2 = f2(v[1], v[3]);
-    q.p3 = f2(v[2], v[4]);
-    q.p4 = f2(v[3], v[5]);
-}
-
 /// Separable 3-tap terms of 4 columns from their 6-column neighbourhood:
 /// D = x[k+1] - x[k-1] (Sobel-x row term), S = x[k-1] + 2 x[k] + x[k+1].
 __device__ __forceinline__ void diff_smooth(const Cols6& c, Q4& D, Q4& S) {

@@ -629,6 +629,8 @@ struct DeviceSession::Impl {
     std::unique_ptr<Staging> staging; ///< host runs only (run_naive / run_plan)
     /// optional pinned destinations for image outputs (C facade recycling)
     std::map<ObjectId, std::vector<std::uint8_t>>* out_pool = nullptr;
+    /// optional: fill this input Buffer from `src` during its upload (C facade)
+    const detail::HostFill* fill = nullptr;
     const VerifiedGraph* exec_graph = nullptr; ///< graph whose outputs are reported
     VerifiedGraph exec_copy;
     int frames = 1;
@@ -830,10 +832,27 @@ struct DeviceSession::Impl {
             int pinned = 0;
             if (staging && row * oi.desc.height > Staging::kChunk / 4) gvxb_host_is_pinned(b.bytes.data(), &pinned);
             static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
-            if (trace) std::fprintf(stderr, "[gvx host] upload object %llu (%p, %zu B): %s\n",
+            if (trace) std::fprintf(stderr, "[gvx host] upload object %llu (%p, %zu B): %s%s\n",
                                     static_cast<unsigned long long>(id), static_cast<const void*>(b.bytes.data()),
                                     row * static_cast<std::size_t>(oi.desc.height),
-                                    pinned ? "page-locked, direct DMA" : "pageable, staged");
+                                    pinned ? "page-locked, direct DMA" : "pageable, staged",
+                                    fill && fill->id == id ? ", filled chunk-wise" : "");
+            if (fill && fill->id == id && fill->src) {
+                // the facade's input Buffer is filled from the caller's frame here
+                auto* dst = const_cast<std::uint8_t*>(b.bytes.data());
+                const std::size_t total = row * static_cast<std::size_t>(oi.desc.height);
+                if (pinned && s.pitch == static_cast<std::int64_t>(row)) {
+                    // chunk by chunk, each chunk's DMA overlapping the next copy
+                    constexpr std::size_t kFill = std::size_t(2) << 20;
+                    for (std::size_t o = 0; o < total; o += kFill) {
+                        const std::size_t n = std::min(kFill, total - o);
+                        dev::parallel_copy(dst + o, fill->src + o, n, /*streaming=*/true);
+                        dev::check(gvxb_upload_2d(ctx, base + o, n, dst + o, n, n, 1), "image upload");
+                    }
+                    return;
+                }
+                dev::parallel_copy(dst, fill->src, total, /*streaming=*/true);
+            }
             if (staging && !pinned && row * oi.desc.height > Staging::kChunk / 4) {
                 staging->upload(base, static_cast<std::size_t>(s.pitch), b.bytes.data(), row,
                                 static_cast<std::size_t>(oi.desc.height));
@@ -1079,7 +1098,8 @@ std::shared_ptr<HostSession> host_session(const std::shared_ptr<dev::Program>& p
 }
 
 ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const VerifiedGraph& vg, const InputMap& inputs,
-                        std::map<ObjectId, std::vector<std::uint8_t>>* out_pool = nullptr) {
+                        std::map<ObjectId, std::vector<std::uint8_t>>* out_pool = nullptr,
+                        const detail::HostFill* fill = nullptr) {
     std::map<ObjectId, Buffer> defaults;
     auto bound = bind_inputs(vg, inputs, defaults);
 
@@ -1088,9 +1108,13 @@ ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const Verifie
     DeviceSession::Impl& s = hs->impl;
     s.exec_graph = &vg;
     s.out_pool = out_pool;
+    s.fill = fill;
     struct PoolReset {
         DeviceSession::Impl& s;
-        ~PoolReset() { s.out_pool = nullptr; }
+        ~PoolReset() {
+            s.out_pool = nullptr;
+            s.fill = nullptr;
+        }
     } pool_reset{s};
     static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
     using clock = std::chrono::steady_clock;
@@ -1141,19 +1165,19 @@ ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const Verifie
 namespace detail {
 
 ExecutionReport run_naive_pooled(const VerifiedGraph& g, const InputMap& inputs,
-                                 std::map<ObjectId, std::vector<std::uint8_t>>* out_pool) {
+                                 std::map<ObjectId, std::vector<std::uint8_t>>* out_pool, const HostFill* fill) {
     if (!g.stamped()) throw Error(ErrorCode::UnstampedGraph, "execution needs a verified graph");
     auto prog = naive_program(g, &inputs);
-    ExecutionReport r = execute(prog, g, inputs, out_pool);
+    ExecutionReport r = execute(prog, g, inputs, out_pool, fill);
     r.counters.transfers_executed = static_cast<std::int64_t>(g.graph().nodes().size()) * 2;
     return r;
 }
 
 ExecutionReport run_plan_pooled(const OptimizedPlan& plan, const InputMap& inputs,
-                                std::map<ObjectId, std::vector<std::uint8_t>>* out_pool) {
+                                std::map<ObjectId, std::vector<std::uint8_t>>* out_pool, const HostFill* fill) {
     if (!plan.fused.stamped()) throw Error(ErrorCode::UnstampedGraph, "plan execution needs a verified fused graph");
     auto prog = plan_program(plan, &inputs);
-    ExecutionReport r = execute(prog, plan.fused, inputs, out_pool);
+    ExecutionReport r = execute(prog, plan.fused, inputs, out_pool, fill);
     r.counters.transfers_executed = plan.transfers.optimized_count();
     return r;
 }
@@ -1161,11 +1185,11 @@ ExecutionReport run_plan_pooled(const OptimizedPlan& plan, const InputMap& input
 } // namespace detail
 
 ExecutionReport run_naive(const VerifiedGraph& g, const InputMap& inputs) {
-    return detail::run_naive_pooled(g, inputs, nullptr);
+    return detail::run_naive_pooled(g, inputs, nullptr, nullptr);
 }
 
 ExecutionReport run_plan(const OptimizedPlan& plan, const InputMap& inputs) {
-    return detail::run_plan_pooled(plan, inputs, nullptr);
+    return detail::run_plan_pooled(plan, inputs, nullptr, nullptr);
 }
 
 // ------------------------------------------------------------ DeviceSession

@@ -119,13 +119,20 @@ bool static_counts(const OperatorNode& n, const VerifiedGraph& vg, std::int64_t&
 
 namespace gvx::detail {
 
+/// Facade-only: the input Buffer `id` is page-locked and still to be filled
+/// from `src` (its size); the upload copies and DMAs it chunk by chunk.
+struct HostFill {
+    ObjectId id = kInvalidId;
+    const std::uint8_t* src = nullptr;
+};
+
 /// run_naive / run_plan whose image outputs are downloaded into vectors
 /// taken from `out_pool` (keyed by object id, matching size) when present:
 /// the C facade keeps page-locked vectors there and hands each report's
 /// vectors back before the next run, so outputs DMA straight into them.
 ExecutionReport run_naive_pooled(const VerifiedGraph& g, const InputMap& inputs,
-                                 std::map<ObjectId, std::vector<std::uint8_t>>* out_pool);
+                                 std::map<ObjectId, std::vector<std::uint8_t>>* out_pool, const HostFill* fill);
 ExecutionReport run_plan_pooled(const OptimizedPlan& plan, const InputMap& inputs,
-                                std::map<ObjectId, std::vector<std::uint8_t>>* out_pool);
+                                std::map<ObjectId, std::vector<std::uint8_t>>* out_pool, const HostFill* fill);
 
 } // namespace gvx::detail
