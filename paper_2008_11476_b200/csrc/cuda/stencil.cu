@@ -294,8 +294,8 @@ __global__ void meanstd_finalize_kernel(const unsigned long long* sum, const uns
 constexpr int kSepThreads = 96;
 constexpr int kSepTW = 4 * kSepThreads; // 384 columns: 4K / 8K / 1080p split evenly
 constexpr int kSepSW = kSepTW + 32;     // tile origin x0 - 16 (16-byte aligned TMA start)
-constexpr int kSepTHMax = 64;
-constexpr int kSepHistTH = 32;          // u8 counters (4 px * rows <= 255); small tile for occupancy
+constexpr int kSepTHMax = 48;  // measured best of 32 / 48 / 64 (cfg3)
+constexpr int kSepHistTH = 24;          // u8 counters: 4 px * rows <= 255; measured best (16..63)
 constexpr int kSepHistBytes = 256 * 32 * 4;
 
 struct SepParams {
