@@ -629,9 +629,9 @@ bool static_counts(const OperatorNode& n, const VerifiedGraph& vg, std::int64_t&
             const bool rgb = bodies.size() == 3 && vg.desc(io.outs[o]).format == ImageFormat::RGB;
             for (std::size_t c = 0; c < (rgb ? 3u : 1u); ++c) tally(*bodies[c], image_slot, t, false);
         }
+        writes = px * slots; // writes are static even when reads depend on data
         if (t.conditional) return false;
         reads = px * t.image_reads;
-        writes = px * slots;
         return true;
     }
     case AbstractionKind::Local: {

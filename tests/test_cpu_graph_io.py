@@ -112,3 +112,24 @@ def test_numbers_keep_their_json_types(gvx):
     assert type(attrs["i"]) is int and type(attrs["f"]) is float
     assert attrs["e"] == 1e-7 and attrs["big"] == 1.5e300 and attrs["neg"] == -0.25 and attrs["s"] == 'a"b\\n'
     assert '"f": 3.0' in gvx.json_roundtrip(text) and '"e": 1e-07' in gvx.json_roundtrip(text)
+
+
+def test_kernel_golden_covers_every_case():
+    """tests/golden/kernels.json (reference run_naive of every built-in
+    kernel as a one-node graph file) matches tests/kernel_graphs.py."""
+    import sys
+    sys.path.insert(0, str(REPO / "tests"))
+    import kernel_graphs
+    gold = json.loads((REPO / "tests" / "golden" / "kernels.json").read_text())
+    cases = {c for c, _ in kernel_graphs.all_cases()}
+    assert cases == set(gold["cases"]) | set(gold["reference_errors"])
+    # the only reference failures are its ScaleImage / EqualizeHist defects
+    assert {c.split("_")[0] for c in gold["reference_errors"]} == {"ScaleImage", "EqualizeHist"}
+
+
+def test_loaded_kernel_cases_verify(gvx):
+    import sys
+    sys.path.insert(0, str(REPO / "tests"))
+    import kernel_graphs
+    for case, text in kernel_graphs.all_cases():
+        gvx.GraphFile(text)  # load + verify + expand + optimize (no device needed)
