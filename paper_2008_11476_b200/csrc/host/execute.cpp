@@ -245,6 +245,14 @@ gvxb_module compile(const jit::NodeProgram& prog) {
         auto it = module_cache().find(key);
         if (it != module_cache().end()) return it->second;
     }
+    if (const char* dir = std::getenv("GVX_DUMP_JIT")) { // debugging aid: keep the generated CUDA
+        const std::string path = std::string(dir) + "/" + prog.kernels.at(0).name + "_" +
+                                 std::to_string(std::hash<std::string>{}(key) % 1000000007ull) + ".cu";
+        if (FILE* f = std::fopen(path.c_str(), "w")) {
+            std::fwrite(src.data(), 1, src.size(), f);
+            std::fclose(f);
+        }
+    }
     std::vector<const char*> names;
     for (const auto& k : prog.kernels) names.push_back(k.name.c_str());
     gvxb_module m = nullptr;
@@ -305,7 +313,9 @@ Unit jit_unit(const OperatorNode& n, const VerifiedGraph& vg,
             if (id != kInvalidId) u.writes.push_back(id);
         }
     }
-    u.prog = jit::lower_node(*u.k, u.in_slots, u.out_slots, matrix_for(u, vg.context(), matrices));
+    std::int64_t r = 0, w = 0;
+    const bool stat = static_counts(n, vg, r, w);
+    u.prog = jit::lower_node(*u.k, u.in_slots, u.out_slots, matrix_for(u, vg.context(), matrices), !stat);
     const ResolvedDesc* d = nullptr;
     if (u.prog.dims_from >= 0 && u.prog.dims_from < static_cast<int>(u.in_slots.size()))
         d = &u.in_slots[static_cast<std::size_t>(u.prog.dims_from)].desc;
@@ -315,12 +325,9 @@ Unit jit_unit(const OperatorNode& n, const VerifiedGraph& vg,
         u.width = d->width;
         u.height = d->height;
     }
-    std::int64_t r = 0, w = 0;
-    const bool stat = static_counts(n, vg, r, w);
     u.static_writes = w;
     u.device_counts_reads = u.prog.counts_reads;
     u.static_reads = u.prog.counts_reads ? 0 : r;
-    (void)stat;
     return u;
 }
 
@@ -814,6 +821,13 @@ struct DeviceSession::Impl {
                 grid[0] = static_cast<unsigned>((u.width + ks.block_x - 1) / ks.block_x);
                 grid[1] = static_cast<unsigned>((u.height + ks.block_y - 1) / ks.block_y);
                 break;
+            case jit::KernelSpec::Grid::Strided: {
+                grid[0] = static_cast<unsigned>((u.width + ks.block_x - 1) / ks.block_x);
+                const long long rows = (u.height + ks.block_y - 1) / ks.block_y;
+                const long long want = std::max<long long>(1, 1184 / (static_cast<long long>(grid[0]) * frames));
+                grid[1] = static_cast<unsigned>(std::max<long long>(1, std::min(rows, want)));
+                break;
+            }
             case jit::KernelSpec::Grid::Single: block[1] = 1; break;
             case jit::KernelSpec::Grid::Rows: grid[0] = static_cast<unsigned>((u.height + 127) / 128); break;
             case jit::KernelSpec::Grid::Cols: grid[0] = static_cast<unsigned>((u.width + 127) / 128); break;

@@ -331,6 +331,16 @@ const char* kPixelHead = R"CUDA(
   const bool live = px < W && py < H;
 )CUDA";
 
+const char* kStridedHead = R"CUDA(
+  const int W = (int)p.f[2], H = (int)p.f[3];
+  const int px = blockIdx.x * blockDim.x + threadIdx.x;
+  const int fr = blockIdx.z;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  u64 rd = 0;
+)CUDA";
+const char* kStridedLoop =
+    "  for (int py = blockIdx.y * blockDim.y + threadIdx.y; py < H; py += gridDim.y * blockDim.y) if (px < W) {\n";
+
 // ----------------------------------------------------------------- point
 
 NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
@@ -502,26 +512,34 @@ NodeProgram lower_reduce(const AbstractionKernel& k, const std::vector<SlotInfo>
                                 "] + (u64)fr * p.f[" + std::to_string(prog.fields() - 1) + "]))";
 
     std::ostringstream src;
+    // parallel forms: rows strided over a few blocks per frame, per-thread
+    // partials, then warp + block aggregation and ONE global atomic per block
+    const char* block_sum =
+        "  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);\n"
+        "  __shared__ i64 red[32];\n  if ((tid & 31) == 0) red[tid >> 5] = part;\n  __syncthreads();\n"
+        "  if (tid < 32) { part = tid < (int)((blockDim.x * blockDim.y + 31) >> 5) ? red[tid] : 0;\n"
+        "    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o); }\n";
+    const char* block_min =
+        "  for (int o = 16; o > 0; o >>= 1) { u64 q = __shfl_xor_sync(0xffffffffu, key, o); key = q < key ? q : key; }\n"
+        "  __shared__ u64 red[32];\n  if ((tid & 31) == 0) red[tid >> 5] = key;\n  __syncthreads();\n"
+        "  if (tid < 32) { key = tid < (int)((blockDim.x * blockDim.y + 31) >> 5) ? red[tid] : ~0ull;\n"
+        "    for (int o = 16; o > 0; o >>= 1) { u64 q = __shfl_xor_sync(0xffffffffu, key, o); key = q < key ? q : key; } }\n";
     if (par_sum) {
         em.mode = Emitter::Mode::Combine;
         std::string t = em.emit(*term);
-        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {" << kPixelHead
-            << "  i64 part = 0;\n  if (live) { V pix = " << ldpix << "(p, fr, px, py, rd); V acc = vi(0); (void)acc; part = vl("
-            << t << "); }\n"
-            << "  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);\n"
-            << "  if ((threadIdx.x & 31) == 0 && part) atomicAdd((u64*)(" << scratch << " + 1), (u64)part);\n"
+        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {" << kStridedHead << "  i64 part = 0;\n"
+            << kStridedLoop << "    V pix = " << ldpix << "(p, fr, px, py, rd); V acc = vi(0); (void)acc;\n"
+            << "    part = (i64)((u64)part + (u64)vl(" << t << "));\n  }\n"
+            << block_sum << "  if (tid == 0 && part) atomicAdd((u64*)(" << scratch << " + 1), (u64)part);\n"
             << "  flush_reads(p, rd);\n}\n";
     } else if (par_min || par_max) {
         // key: (biased value, linear index) packed so that atomicMin picks the
         // extreme value and, among equals, the first row-major position
-        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {" << kPixelHead
-            << "  u64 key = ~0ull;\n  if (live) { V pix = " << ldpix
-            << "(p, fr, px, py, rd); u64 b = (u64)(pix.i + 2147483648ll);\n"
+        src << "extern \"C\" __global__ void gvx_reduce_part(const P p) {" << kStridedHead << "  u64 key = ~0ull;\n"
+            << kStridedLoop << "    V pix = " << ldpix << "(p, fr, px, py, rd); u64 b = (u64)(pix.i + 2147483648ll);\n"
             << (par_min ? "    u64 kv = b;\n" : "    u64 kv = 0xFFFFFFFFull - b;\n")
-            << "    key = (kv << 32) | (u64)(py * (u64)W + px); }\n"
-            << "  for (int o = 16; o > 0; o >>= 1) { u64 q = __shfl_xor_sync(0xffffffffu, key, o); key = q < key ? q : "
-               "key; }\n"
-            << "  if ((threadIdx.x & 31) == 0 && key != ~0ull) atomicMin((u64*)(" << scratch << " + 2), key);\n"
+            << "    u64 k = (kv << 32) | (u64)(py * (u64)W + px); key = k < key ? k : key;\n  }\n"
+            << block_min << "  if (tid == 0 && key != ~0ull) atomicMin((u64*)(" << scratch << " + 2), key);\n"
             << "  flush_reads(p, rd);\n}\n";
     } else {
         // exact row-major fold on one thread (general user combine bodies)
@@ -581,7 +599,7 @@ NodeProgram lower_reduce(const AbstractionKernel& k, const std::vector<SlotInfo>
     k0.name = "gvx_reduce_init";
     k0.grid = KernelSpec::Grid::Single;
     k1.name = "gvx_reduce_part";
-    k1.grid = (par_sum || par_min || par_max) ? KernelSpec::Grid::Pixels : KernelSpec::Grid::Single;
+    k1.grid = (par_sum || par_min || par_max) ? KernelSpec::Grid::Strided : KernelSpec::Grid::Single;
     k2.name = "gvx_reduce_final";
     k2.grid = KernelSpec::Grid::Single;
     const std::string all = assemble(em, init.str() + src.str() + fin.str(), prog.fields());
@@ -606,14 +624,25 @@ NodeProgram lower_histogram(const AbstractionKernel& k, const std::vector<SlotIn
     src << "extern \"C\" __global__ void gvx_hist_clear(const P p) {\n  const int fr = blockIdx.z;\n"
         << "  i64* o = " << em.out_slot_ptr(0) << ";\n  for (int b = threadIdx.x; b < " << hk.bins
         << "; b += blockDim.x) { o[2 * b] = 0; o[2 * b + 1] = 0; }\n}\n"
-        << "extern \"C\" __global__ void gvx_hist(const P p) {" << kPixelHead
-        << "  if (live) { i64 b = vl(" << bin << "); if (b >= 0 && b < " << hk.bins << ") atomicAdd((u64*)(" << em.out_slot_ptr(0)
-        << " + 2 * b + 1), 1ull); }\n  flush_reads(p, rd);\n}\n";
+        << "extern \"C\" __global__ void gvx_hist(const P p) {";
+    const bool smem = hk.bins <= 8192; // per-block u32 counts in shared memory
+    if (smem) {
+        src << kStridedHead << "  __shared__ unsigned sh[" << hk.bins << "];\n"
+            << "  for (int i = tid; i < " << hk.bins << "; i += blockDim.x * blockDim.y) sh[i] = 0;\n  __syncthreads();\n"
+            << kStridedLoop << "    i64 b = vl(" << bin << "); if (b >= 0 && b < " << hk.bins << ") atomicAdd(&sh[b], 1u);\n  }\n"
+            << "  __syncthreads();\n  i64* o = " << em.out_slot_ptr(0) << ";\n"
+            << "  for (int i = tid; i < " << hk.bins << "; i += blockDim.x * blockDim.y) if (sh[i]) atomicAdd((u64*)(o + 2 * i + 1), (u64)sh[i]);\n";
+    } else {
+        src << kPixelHead << "  if (live) { i64 b = vl(" << bin << "); if (b >= 0 && b < " << hk.bins
+            << ") atomicAdd((u64*)(" << em.out_slot_ptr(0) << " + 2 * b + 1), 1ull); }\n";
+    }
+    src << "  flush_reads(p, rd);\n}\n";
     KernelSpec k0, k1;
     k0.name = "gvx_hist_clear";
     k0.grid = KernelSpec::Grid::Single;
     k0.block_x = 256;
     k1.name = "gvx_hist";
+    if (smem) k1.grid = KernelSpec::Grid::Strided;
     k0.source = assemble(em, src.str(), prog.fields());
     prog.kernels = {k0, k1};
     return prog;
@@ -753,7 +782,8 @@ NodeProgram lower_table(const std::vector<SlotInfo>& ins, const std::vector<Slot
 } // namespace
 
 NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
-                       const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values) {
+                       const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values,
+                       bool count_reads) {
     NodeProgram p;
     switch (k.kind) {
     case AbstractionKind::Point: p = lower_point(k, ins, outs); break;
@@ -763,6 +793,15 @@ NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& 
     case AbstractionKind::Scan: p = lower_scan(ins, outs); break;
     case AbstractionKind::Scale: p = lower_scale(k, ins, outs); break;
     case AbstractionKind::Table: p = lower_table(ins, outs); break;
+    }
+    if (!count_reads && p.counts_reads) {
+        // the host knows the reads statically: drop the per-warp atomic flush
+        // of the device read counter (a single-address atomic per warp would
+        // otherwise serialise the whole kernel at L2), `rd` then folds away
+        const std::string flush = "  flush_reads(p, rd);\n";
+        for (KernelSpec& ks : p.kernels)
+            for (std::size_t at; (at = ks.source.find(flush)) != std::string::npos;) ks.source.erase(at, flush.size());
+        p.counts_reads = false;
     }
     // every kernel of a node shares one source (one NVRTC module)
     for (std::size_t i = 1; i < p.kernels.size(); ++i)

@@ -33,7 +33,9 @@ struct SlotInfo {
 struct KernelSpec {
     std::string name;
     std::string source;
-    enum class Grid : std::uint8_t { Pixels, OutPixels, Single, Rows, Cols } grid = Grid::Pixels;
+    /// Strided: 32-column strips x a few row groups per frame; the kernel
+    /// loops over rows and aggregates per block (histograms, reductions).
+    enum class Grid : std::uint8_t { Pixels, OutPixels, Single, Rows, Cols, Strided } grid = Grid::Pixels;
     int block_x = 32, block_y = 8;
 };
 
@@ -56,7 +58,10 @@ struct NodeProgram {
 /// Lowers one abstraction node.  `ins` / `outs` describe the bound objects
 /// per INPUT / OUTPUT parameter (None when unbound).  Mask values of a
 /// matrix-driven local are taken from `matrix_values` (baked as constants).
+/// `count_reads` = false when the host can count the node's reads
+/// statically: the kernels then keep no device read counter.
 NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
-                       const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values);
+                       const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values,
+                       bool count_reads = true);
 
 } // namespace gvx::jit
