@@ -22,6 +22,39 @@ def band_slab(height: int, world: int, rank: int, halo: int, band_rows=None):
     return r0, r1, max(0, r0 - halo), min(height, r1 + halo)
 
 
+def band_pieces(r0: int, r1: int, rank: int, world: int, halo: int):
+    """Split band [r0, r1) for overlap: (interior, edges).  `interior` rows
+    read only owned source rows, so they are computed while the halo rows
+    are in flight; each `edges` range reads halo rows and runs after the
+    exchange.  The ranges partition [r0, r1); a band thinner than 2 halos
+    is all edge."""
+    lo = r0 + halo if rank > 0 else r0
+    hi = r1 - halo if rank < world - 1 else r1
+    if lo >= hi:
+        return None, [(r0, r1)] if r1 > r0 else []
+    edges = []
+    if lo > r0:
+        edges.append((r0, lo))
+    if hi < r1:
+        edges.append((hi, r1))
+    return (lo, hi), edges
+
+
+def halo_exchange_start(dist, slab, r0: int, r1: int, s0: int, s1: int, rank: int, world: int, halo: int):
+    """Post the halo sends / receives of halo_exchange and return the
+    requests without waiting (wait() on each before reading the halo)."""
+    if world <= 1:
+        return []
+    ops = []
+    if rank > 0 and r0 > s0:
+        ops.append(dist.P2POp(dist.isend, slab[r0 - s0:r0 - s0 + halo], rank - 1))
+        ops.append(dist.P2POp(dist.irecv, slab[0:r0 - s0], rank - 1))
+    if rank < world - 1 and s1 > r1:
+        ops.append(dist.P2POp(dist.isend, slab[r1 - s0 - halo:r1 - s0], rank + 1))
+        ops.append(dist.P2POp(dist.irecv, slab[r1 - s0:s1 - s0], rank + 1))
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
 def halo_exchange(dist, slab, r0: int, r1: int, s0: int, s1: int, rank: int, world: int, halo: int) -> None:
     """Fill the halo rows of `slab` (global rows s0..s1) from the neighbours.
 
