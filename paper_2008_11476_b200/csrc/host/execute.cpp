@@ -818,7 +818,7 @@ struct DeviceSession::Impl {
             switch (ks.grid) {
             case jit::KernelSpec::Grid::Pixels:
             case jit::KernelSpec::Grid::OutPixels:
-                grid[0] = static_cast<unsigned>((u.width + ks.block_x - 1) / ks.block_x);
+                grid[0] = static_cast<unsigned>((u.width + ks.block_x * ks.cols - 1) / (ks.block_x * ks.cols));
                 grid[1] = static_cast<unsigned>((u.height + ks.block_y - 1) / ks.block_y);
                 break;
             case jit::KernelSpec::Grid::Strided: {

@@ -341,6 +341,19 @@ const char* kStridedHead = R"CUDA(
 const char* kStridedLoop =
     "  for (int py = blockIdx.y * blockDim.y + threadIdx.y; py < H; py += gridDim.y * blockDim.y) if (px < W) {\n";
 
+/// Four horizontally adjacent pixels per thread (point / local kernels):
+/// address arithmetic, clamps and window loads are shared across them.
+constexpr int kCols = 4;
+const char* kPixelHead4 = R"CUDA(
+  const int W = (int)p.f[2], H = (int)p.f[3];
+  const int px4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int py = blockIdx.y * blockDim.y + threadIdx.y;
+  const int fr = blockIdx.z;
+  u64 rd = 0;
+  const bool live = px4 < W && py < H;
+)CUDA";
+const char* kEachPixel = "#pragma unroll\n    for (int i = 0; i < 4; ++i) { const int px = px4 + i; if (px >= W) break;\n";
+
 // ----------------------------------------------------------------- point
 
 NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
@@ -368,15 +381,109 @@ NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>&
     }
     KernelSpec ks;
     ks.name = "gvx_point";
+    ks.cols = kCols;
     std::ostringstream src;
-    src << "extern \"C\" __global__ void gvx_point(const P p) {" << kPixelHead << "  if (live) {\n"
-        << b.str() << "  }\n  flush_reads(p, rd);\n}\n";
+    src << "extern \"C\" __global__ void gvx_point(const P p) {" << kPixelHead4 << "  if (live) {\n    " << kEachPixel
+        << b.str() << "    }\n  }\n  flush_reads(p, rd);\n}\n";
     ks.source = assemble(em, src.str(), prog.fields());
     prog.kernels.push_back(std::move(ks));
     return prog;
 }
 
 // ----------------------------------------------------------------- local
+
+/// Range of an integer image format, or false for non-integer formats.
+bool int_format_range(ImageFormat f, std::int64_t& lo, std::int64_t& hi) {
+    switch (f) {
+    case ImageFormat::U8: lo = 0, hi = 255; return true;
+    case ImageFormat::U16: lo = 0, hi = 65535; return true;
+    case ImageFormat::S16: lo = -32768, hi = 32767; return true;
+    case ImageFormat::S32: lo = -2147483648LL, hi = 2147483647LL; return true;
+    default: return false;
+    }
+}
+
+/// The common shapes of a local tap loop, in exact 32-bit integer
+/// arithmetic: Sum of (integer mask coefficient x window pixel) when the
+/// worst-case sum fits int32 (then int32 and the reference's int64 agree),
+/// or Min / Max of the window pixel.  Clamp borders only.  Emits the body
+/// that defines `V cmb` (the combined value) or returns "" when the node
+/// does not have such a shape.
+std::string int_tap_loop(const LocalKernel& lk, const std::vector<SlotInfo>& ins, const std::vector<Value>& mask,
+                         const Emitter& em) {
+    if (lk.boundary != BoundaryMode::Clamp || lk.median3x3 || !lk.tap_body) return "";
+    const Expr& t = *lk.tap_body;
+    const Expr* win = nullptr;
+    bool masked = false;
+    if (t.op == ExprOp::WindowPixel) {
+        win = &t;
+    } else if (t.op == ExprOp::Mul && lk.combine == CombineMode::Sum) {
+        if (t.a->op == ExprOp::MaskCoef && t.b->op == ExprOp::WindowPixel) win = t.b.get(), masked = true;
+        if (t.b->op == ExprOp::MaskCoef && t.a->op == ExprOp::WindowPixel) win = t.a.get(), masked = true;
+        const Expr* mc = masked ? (t.a->op == ExprOp::MaskCoef ? t.a.get() : t.b.get()) : nullptr;
+        if (mc && (mc->dx != 0 || mc->dy != 0)) return "";
+    }
+    if (!win || win->channel != Channel::C0 || win->dx != 0 || win->dy != 0) return "";
+    const int slot = win->input;
+    if (slot < 0 || slot >= static_cast<int>(ins.size()) || ins[static_cast<std::size_t>(slot)].kind != SlotKind::Image)
+        return "";
+    std::int64_t lo = 0, hi = 0;
+    if (!int_format_range(ins[static_cast<std::size_t>(slot)].desc.format, lo, hi)) return "";
+    const int ww = lk.window_w, wh = lk.window_h, hw = ww / 2, hh = wh / 2;
+    std::vector<std::int64_t> m(static_cast<std::size_t>(ww * wh), 1);
+    if (masked) {
+        if (mask.size() != m.size()) return "";
+        for (std::size_t i = 0; i < m.size(); ++i) {
+            if (mask[i].real) return "";
+            m[i] = mask[i].i;
+            if (m[i] > 2147483647LL || m[i] < -2147483647LL) return "";
+        }
+    }
+    if (lk.combine == CombineMode::Sum) { // every partial sum must fit int32
+        std::int64_t bound = 0;
+        for (std::int64_t c : m) {
+            bound += std::llabs(c) * std::max(std::llabs(lo), std::llabs(hi));
+            if (bound > 2147483647LL) return "";
+        }
+    }
+    const char* ctype = "";
+    switch (ins[static_cast<std::size_t>(slot)].desc.format) {
+    case ImageFormat::U8: ctype = "const unsigned char*"; break;
+    case ImageFormat::U16: ctype = "const unsigned short*"; break;
+    case ImageFormat::S16: ctype = "const short*"; break;
+    default: ctype = "const int*"; break;
+    }
+    std::ostringstream b;
+    // the 4 pixels' windows share 4 + 2 hw clamped columns per window row:
+    // every source pixel is loaded once per thread
+    const int nc = 4 + 2 * hw;
+    for (int k = 0; k < nc; ++k) b << "    const int c" << k << " = clampi(px4 + (" << k - hw << "), 0, W - 1);\n";
+    b << "    int acc[4];\n";
+    bool first = true;
+    const bool sum = lk.combine == CombineMode::Sum;
+    for (int dy = -hh; dy <= hh; ++dy) {
+        bool used = !sum;
+        for (int dx = -hw; dx <= hw && !used; ++dx) used = m[static_cast<std::size_t>((dy + hh) * ww + dx + hw)] != 0;
+        if (!used) continue; // an all-zero mask row adds nothing (its reads are still counted)
+        b << "    {\n      " << ctype << " r = (" << ctype << ")(" << em.in_base(slot) << " + (u64)clampi(py + (" << dy
+          << "), 0, H - 1) * p.f[" << field_in(slot) + 1 << "]);\n      int v[" << nc << "];\n";
+        for (int k = 0; k < nc; ++k) b << "      v[" << k << "] = (int)r[c" << k << "];\n";
+        b << "#pragma unroll\n      for (int i = 0; i < 4; ++i) {\n";
+        for (int dx = -hw; dx <= hw; ++dx) {
+            const std::int64_t coef = m[static_cast<std::size_t>((dy + hh) * ww + dx + hw)];
+            if (sum && coef == 0) continue;
+            std::string term = "v[i + " + std::to_string(dx + hw) + "]";
+            if (sum && coef != 1) term = "(" + std::to_string(coef) + " * " + term + ")";
+            if (first) b << "        acc[i] = " << term << ";\n";
+            else if (sum) b << "        acc[i] += " << term << ";\n";
+            else b << "        acc[i] = " << (lk.combine == CombineMode::Min ? "min" : "max") << "(acc[i], " << term << ");\n";
+            first = false;
+        }
+        b << "      }\n    }\n";
+    }
+    if (first) return ""; // all-zero mask: leave it to the general path
+    return b.str();
+}
 
 NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
                         const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values) {
@@ -391,14 +498,19 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     const int hw = lk.window_w / 2, hh = lk.window_h / 2;
     const ScalarType out_t = scalar_of(outs.at(0).desc.format);
 
-    std::ostringstream b;
+    std::ostringstream pre, b; // pre: once per thread; b: per pixel (inside the 4-pixel loop)
     if (lk.boundary == BoundaryMode::Undefined) {
         b << "    if (px < " << hw << " || py < " << hh << " || px >= W - " << hw << " || py >= H - " << hh << ") {\n"
           << "      " << em.store(0, "v_cast(vi(0), " + std::to_string(type_code(out_t)) + ", 0)", 0, "px", "py")
-          << "      goto done;\n    }\n";
+          << "      continue;\n    }\n";
     }
     em.mode = Emitter::Mode::Tap;
-    if (lk.median3x3) {
+    const std::string fast = int_tap_loop(lk, ins, *em.mask, em);
+    if (!fast.empty()) {
+        pre << fast;
+        b << "    V cmb = vi((i64)acc[i]);\n";
+        prog.counts_reads = false; // the host counts these reads (static window)
+    } else if (lk.median3x3) {
         b << "    V t[9];\n";
         int idx = 0;
         for (int dy = -hh; dy <= hh; ++dy)
@@ -438,10 +550,10 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     }
     KernelSpec ks;
     ks.name = "gvx_local";
+    ks.cols = kCols;
     std::ostringstream src;
-    src << "extern \"C\" __global__ void gvx_local(const P p) {" << kPixelHead << "  if (live) {\n"
-        << b.str() << "  }\n" << (lk.boundary == BoundaryMode::Undefined ? "done:\n" : "")
-        << "  flush_reads(p, rd);\n}\n";
+    src << "extern \"C\" __global__ void gvx_local(const P p) {" << kPixelHead4 << "  if (live) {\n" << pre.str()
+        << "    " << kEachPixel << b.str() << "    }\n  }\n  flush_reads(p, rd);\n}\n";
     ks.source = assemble(em, src.str(), prog.fields());
     prog.kernels.push_back(std::move(ks));
     return prog;

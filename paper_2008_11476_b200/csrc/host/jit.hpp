@@ -37,6 +37,7 @@ struct KernelSpec {
     /// loops over rows and aggregates per block (histograms, reductions).
     enum class Grid : std::uint8_t { Pixels, OutPixels, Single, Rows, Cols, Strided } grid = Grid::Pixels;
     int block_x = 32, block_y = 8;
+    int cols = 1; ///< pixels per thread along x (Pixels grids)
 };
 
 /// A node lowered to one or more generated kernels.
