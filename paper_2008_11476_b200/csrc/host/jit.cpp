@@ -186,10 +186,19 @@ struct Emitter {
         return s.str();
     }
 
+    /// Image slots whose four pixels were loaded into `in<slot>[4]` by a
+    /// vector load (point kernels); reads at (px, py) use the registers.
+    std::vector<bool> preloaded;
+
     /// Pointwise read of kernel slot `slot` at (x, y) expressions.
     std::string pointwise(int slot, Channel ch, const std::string& x, const std::string& y) {
         if (slot < 0 || slot >= n_in) throw Error(ErrorCode::TypeMismatch, "input index out of range");
         const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
+        if (s.kind == SlotKind::Image && ch == Channel::C0 && x == "px" && y == "py" &&
+            static_cast<std::size_t>(slot) < preloaded.size() && preloaded[static_cast<std::size_t>(slot)]) {
+            const std::string r = "in" + std::to_string(slot) + "[i]";
+            return s.desc.format == ImageFormat::F32 ? "vf((double)" + r + ")" : "vi((i64)" + r + ")";
+        }
         switch (s.kind) {
         case SlotKind::Scalar: return scalar_load(slot);
         case SlotKind::Image: return image_loader(slot, ch) + "(p, fr, " + x + ", " + y + ", rd)";
@@ -356,8 +365,20 @@ const char* kEachPixel = "#pragma unroll\n    for (int i = 0; i < 4; ++i) { cons
 
 // ----------------------------------------------------------------- point
 
+/// Element type and 4-wide vector type of a single-channel image format.
+bool vec_types(ImageFormat f, std::string& t, std::string& vt, int& bytes) {
+    switch (f) {
+    case ImageFormat::U8: t = "unsigned char", vt = "uchar4", bytes = 1; return true;
+    case ImageFormat::U16: t = "unsigned short", vt = "ushort4", bytes = 2; return true;
+    case ImageFormat::S16: t = "short", vt = "short4", bytes = 2; return true;
+    case ImageFormat::S32: t = "int", vt = "int4", bytes = 4; return true;
+    case ImageFormat::F32: t = "float", vt = "float4", bytes = 4; return true;
+    default: return false;
+    }
+}
+
 NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
-                        const std::vector<SlotInfo>& outs) {
+                        const std::vector<SlotInfo>& outs, bool vector_io) {
     NodeProgram prog;
     prog.n_inputs = static_cast<int>(ins.size());
     prog.n_outputs = static_cast<int>(outs.size());
@@ -368,13 +389,42 @@ NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>&
         }
     Emitter em(ins, outs);
     em.mode = Emitter::Mode::Point;
-    std::ostringstream b;
+    std::ostringstream pre, b, post;
+    // vector loads of the four pixels of every single-channel image input
+    // (when the host counts the reads; a device read counter needs the
+    // per-read loaders), with a scalar fallback at the right edge or for
+    // rows that are not vector-aligned
+    em.preloaded.assign(ins.size(), false);
+    for (std::size_t s = 0; vector_io && s < ins.size(); ++s) {
+        std::string t, vt;
+        int bytes = 0;
+        if (ins[s].kind != SlotKind::Image || !vec_types(ins[s].desc.format, t, vt, bytes)) continue;
+        em.preloaded[s] = true;
+        pre << "    " << t << " in" << s << "[4];\n    { const " << t << "* r = (const " << t << "*)(" << em.in_base(static_cast<int>(s))
+            << " + (u64)py * p.f[" << field_in(static_cast<int>(s)) + 1 << "]) + px4;\n"
+            << "      if (px4 + 3 < W && ((u64)r & " << 4 * bytes - 1 << ") == 0) { const " << vt << " v = *(const " << vt
+            << "*)r; in" << s << "[0] = v.x; in" << s << "[1] = v.y; in" << s << "[2] = v.z; in" << s << "[3] = v.w; }\n"
+            << "      else { for (int i = 0; i < 4; ++i) in" << s << "[i] = px4 + i < W ? r[i] : (" << t << ")0; } }\n";
+    }
     const PointKernel& pk = k.point();
     for (std::size_t o = 0; o < pk.outputs.size() && o < outs.size(); ++o) {
         if (outs[o].kind != SlotKind::Image) continue;
         const auto& bodies = pk.outputs[o].channel_bodies;
+        std::string t, vt;
+        int bytes = 0;
         if (bodies.size() == 3 && outs[o].desc.format == ImageFormat::RGB) {
             for (int c = 0; c < 3; ++c) b << "  " << em.store(static_cast<int>(o), em.emit(*bodies[static_cast<std::size_t>(c)]), c, "px", "py");
+        } else if (vector_io && vec_types(outs[o].desc.format, t, vt, bytes)) {
+            // the four results gather in registers and leave as one vector store
+            const int f = field_in(static_cast<int>(ins.size() + o));
+            pre << "    " << t << " out" << o << "[4];\n";
+            const std::string cvt = outs[o].desc.format == ImageFormat::F32 ? "(float)vd(sv)" : "(" + t + ")sv.i";
+            b << "      { V sv = " << em.emit(*bodies[0]) << "; out" << o << "[i] = " << cvt << "; }\n";
+            post << "    { " << t << "* r = (" << t << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
+                 << "] + (u64)py * p.f[" << f + 1 << "]) + px4;\n"
+                 << "      if (px4 + 3 < W && ((u64)r & " << 4 * bytes - 1 << ") == 0) *(" << vt << "*)r = make_" << vt
+                 << "(out" << o << "[0], out" << o << "[1], out" << o << "[2], out" << o << "[3]);\n"
+                 << "      else { for (int i = 0; i < 4 && px4 + i < W; ++i) r[i] = out" << o << "[i]; } }\n";
         } else {
             b << "  " << em.store(static_cast<int>(o), em.emit(*bodies[0]), 0, "px", "py");
         }
@@ -383,8 +433,8 @@ NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>&
     ks.name = "gvx_point";
     ks.cols = kCols;
     std::ostringstream src;
-    src << "extern \"C\" __global__ void gvx_point(const P p) {" << kPixelHead4 << "  if (live) {\n    " << kEachPixel
-        << b.str() << "    }\n  }\n  flush_reads(p, rd);\n}\n";
+    src << "extern \"C\" __global__ void gvx_point(const P p) {" << kPixelHead4 << "  if (live) {\n" << pre.str()
+        << "    " << kEachPixel << b.str() << "    }\n" << post.str() << "  }\n  flush_reads(p, rd);\n}\n";
     ks.source = assemble(em, src.str(), prog.fields());
     prog.kernels.push_back(std::move(ks));
     return prog;
@@ -898,7 +948,7 @@ NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& 
                        bool count_reads) {
     NodeProgram p;
     switch (k.kind) {
-    case AbstractionKind::Point: p = lower_point(k, ins, outs); break;
+    case AbstractionKind::Point: p = lower_point(k, ins, outs, /*vector_io=*/!count_reads); break;
     case AbstractionKind::Local: p = lower_local(k, ins, outs, matrix_values); break;
     case AbstractionKind::Reduce: p = lower_reduce(k, ins, outs); break;
     case AbstractionKind::Histogram: p = lower_histogram(k, ins, outs); break;
