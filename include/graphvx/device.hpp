@@ -59,6 +59,38 @@ private:
     std::unique_ptr<Impl> impl_;
 };
 
+/// Pipelined host execution (additive): run_plan / run_naive semantics on
+/// a stream of frames held in host Buffers, with up to `depth` frames in
+/// flight.  Each slot owns device storage, a stream and page-locked
+/// staging, so the upload of frame k+1, the kernels of frame k and the
+/// download of frame k-1 overlap (two copy engines + the SMs).  Reports
+/// come back in submission order and equal run_plan's / run_naive's.
+class HostPipeline {
+public:
+    explicit HostPipeline(const OptimizedPlan& plan, int depth = 3);
+    explicit HostPipeline(const VerifiedGraph& g, int depth = 3);
+    ~HostPipeline();
+    HostPipeline(const HostPipeline&) = delete;
+    HostPipeline& operator=(const HostPipeline&) = delete;
+    /// Copies the frame's inputs and enqueues it; when all slots are busy,
+    /// first completes the oldest frame (its report waits for next()).
+    void submit(const InputMap& inputs);
+    /// FFI form: one image input from raw host memory (other inputs take
+    /// the graph's bound values).
+    void submit(ObjectId image_input, const void* data, std::size_t bytes);
+    /// Report of the oldest submitted frame not yet returned (blocks).
+    ExecutionReport next();
+    /// As next(), but image output `image_output` is copied straight to
+    /// `dst` (`bytes`, packed rows) and left out of the report.
+    ExecutionReport next_into(ObjectId image_output, void* dst, std::size_t bytes);
+    /// Frames submitted and not yet returned by next().
+    int pending() const;
+    struct Impl;
+
+private:
+    std::unique_ptr<Impl> impl_;
+};
+
 /// Number of CUDA devices visible (0 on a host without GPUs).
 int device_count();
 

@@ -75,6 +75,17 @@ int gvxc_random_u8(int width, int height, unsigned long long seed, uint8_t* out)
 int gvxc_graph_input_ptr(gvxc_graph g, uint8_t** ptr, size_t* bytes);
 int gvxc_graph_output_ptr(gvxc_graph g, const void** ptr, size_t* bytes);
 
+/* Pipelined host runs (gvx::HostPipeline): up to `depth` frames in flight,
+ * upload / kernels / download of consecutive frames overlapped.  submit
+ * copies the frame; next returns the oldest frame's result in submission
+ * order (same outputs / counters as gvxc_graph_run_host). */
+typedef struct gvxc_pipeline_s* gvxc_pipeline;
+int gvxc_pipeline_create(gvxc_graph g, int naive, int depth, gvxc_pipeline* out);
+int gvxc_pipeline_destroy(gvxc_pipeline p);
+int gvxc_pipeline_submit(gvxc_pipeline p, const uint8_t* in);
+int gvxc_pipeline_pending(gvxc_pipeline p);
+int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stats, long long counters[4]);
+
 /* ---- graph description files (graph_io.hpp, ref:src/graph_io.cpp) -------- */
 typedef struct gvxc_json_s* gvxc_json;
 /* save_graph_json(load_graph_json(text)); *len = bytes needed (incl. NUL). */

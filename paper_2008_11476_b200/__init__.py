@@ -111,6 +111,11 @@ def _declare(c, g):
     g.gvxc_session_upload_input.argtypes = [P, I, U8P]
     g.gvxc_session_download.argtypes = [P, I, I, P, ctypes.POINTER(L), ctypes.POINTER(D)]
     g.gvxc_random_u8.argtypes = [I, I, ctypes.c_ulonglong, U8P]
+    g.gvxc_pipeline_create.argtypes = [P, I, I, ctypes.POINTER(P)]
+    g.gvxc_pipeline_destroy.argtypes = [P]
+    g.gvxc_pipeline_submit.argtypes = [P, U8P]
+    g.gvxc_pipeline_pending.argtypes = [P]
+    g.gvxc_pipeline_next.argtypes = [P, P, ctypes.POINTER(L), ctypes.POINTER(D), ctypes.POINTER(L)]
     g.gvxc_graph_input_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_graph_output_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_launch_count.restype = ctypes.c_longlong
@@ -293,6 +298,43 @@ class ConfigGraph:
         dt = np.dtype(CONFIG_OUTPUT[self.cfg])
         view = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), shape=(n.value,))
         return view.view(dt).reshape(self.height, self.width), cnt
+
+
+class Pipeline:
+    """gvx::HostPipeline over a ConfigGraph: submit host frames, get results
+    back in order, with up to `depth` frames in flight."""
+
+    def __init__(self, graph: "ConfigGraph", depth: int = 3, naive: bool = False):
+        self.graph = graph
+        self._h = ctypes.c_void_p()
+        _check_graph(_graph.gvxc_pipeline_create(graph._h, int(naive), depth, ctypes.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _graph.gvxc_pipeline_destroy(self._h)
+            self._h = None
+
+    def submit(self, image: np.ndarray):
+        img = np.ascontiguousarray(image, dtype=np.uint8)
+        assert img.shape == (self.graph.height, self.graph.width)
+        _check_graph(_graph.gvxc_pipeline_submit(self._h, img.ctypes.data))
+
+    def pending(self) -> int:
+        return _graph.gvxc_pipeline_pending(self._h)
+
+    def next(self, out: np.ndarray = None):
+        """Oldest frame's result: (output plane, counters), or
+        ((hist, mean, stddev), counters) for config 4."""
+        if out is None:
+            out = self.graph.output_array()
+        hist = (ctypes.c_longlong * 256)()
+        stats = (ctypes.c_double * 2)()
+        counters = (ctypes.c_longlong * 4)()
+        _check_graph(_graph.gvxc_pipeline_next(self._h, None if out is None else out.ctypes.data, hist, stats, counters))
+        cnt = dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(counters)))
+        if self.graph.cfg == 4:
+            return (np.array(list(hist), np.int64), stats[0], stats[1]), cnt
+        return out, cnt
 
 
 class Session:
@@ -569,5 +611,5 @@ def band_rows(height: int, world: int, rank: int):
 
 
 __all__ = ["GraphvxError", "ConfigGraph", "Session", "Device", "build", "device_count", "random_u8",
-           "stencil_point", "conv_stats", "harris", "GraphFile", "json_roundtrip", "parse_outputs",
+           "stencil_point", "conv_stats", "harris", "GraphFile", "json_roundtrip", "parse_outputs", "Pipeline",
            "band_rows", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]

@@ -303,6 +303,61 @@ int gvxc_random_u8(int w, int h, unsigned long long seed, uint8_t* out) {
 
 } // extern "C"
 
+// ------------------------------------------------------------ pipelines
+
+struct gvxc_pipeline_s {
+    gvxc_graph g = nullptr;
+    std::unique_ptr<gvx::HostPipeline> p;
+};
+
+extern "C" {
+
+int gvxc_pipeline_create(gvxc_graph g, int naive, int depth, gvxc_pipeline* out) {
+    return guarded([&] {
+        auto pl = std::make_unique<gvxc_pipeline_s>();
+        pl->g = g;
+        pl->p = naive ? std::make_unique<gvx::HostPipeline>(g->impl, depth)
+                      : std::make_unique<gvx::HostPipeline>(g->plan, depth);
+        *out = pl.release();
+    });
+}
+
+int gvxc_pipeline_destroy(gvxc_pipeline p) {
+    delete p;
+    return 0;
+}
+
+int gvxc_pipeline_submit(gvxc_pipeline p, const uint8_t* in) {
+    return guarded([&] {
+        p->p->submit(p->g->cg.input, in, static_cast<std::size_t>(p->g->width) * static_cast<std::size_t>(p->g->height));
+    });
+}
+
+int gvxc_pipeline_pending(gvxc_pipeline p) { return p->p->pending(); }
+
+int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stats, long long counters[4]) {
+    return guarded([&] {
+        gvxc_graph g = p->g;
+        gvx::ExecutionReport r;
+        if (g->cfg != 4 && out) {
+            const gvx::ObjectId id = g->cg.outputs.at(0);
+            const std::size_t bpp = g->cfg == 1 || g->cfg == 5 ? 2 : 1;
+            r = p->p->next_into(id, out, bpp * static_cast<std::size_t>(g->width) * static_cast<std::size_t>(g->height));
+        } else {
+            r = p->p->next();
+            copy_outputs(g, r.outputs, out, hist, stats);
+        }
+        if (counters) {
+            counters[0] = r.counters.kernel_launches;
+            counters[1] = r.counters.pixels_read;
+            counters[2] = r.counters.pixels_written;
+            counters[3] = r.counters.transfers_executed;
+        }
+    });
+}
+
+} // extern "C"
+
 // ------------------------------------------------------------ graph files
 
 struct gvxc_json_s {

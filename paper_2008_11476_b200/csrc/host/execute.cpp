@@ -13,6 +13,7 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <deque>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -1290,6 +1291,245 @@ Buffer DeviceSession::download(ObjectId id, int frame) {
 int DeviceSession::frames() const { return impl_->frames; }
 int DeviceSession::launches_per_run() const { return impl_->prog->launches_per_run(); }
 std::string DeviceSession::describe() const { return impl_->prog->describe(); }
+
+// ------------------------------------------------------------ HostPipeline
+
+struct HostPipeline::Impl {
+    struct Slot {
+        DeviceSession::Impl s; // device storage + lowered program; s.ctx = own context
+        void* done = nullptr;  // event after the slot's last download
+        void* pin_status = nullptr;
+        std::map<ObjectId, void*> pin;         // page-locked staging per image object
+        std::map<ObjectId, std::size_t> bytes; // its size
+        std::vector<ObjectId> image_outs, other_outs;
+        std::int64_t launches0 = 0;
+        bool busy = false;
+        ~Slot() {
+            if (!s.ctx) return;
+            gvxb_sync(s.ctx);
+            if (done) gvxb_event_destroy(done);
+            if (pin_status) gvxb_host_free(pin_status);
+            for (auto& kv : pin) gvxb_host_free(kv.second);
+            for (auto& kv : s.store)
+                if (kv.second.owned) gvxb_free(s.ctx, kv.second.ptr);
+            for (void* x : s.scratch)
+                if (x) gvxb_free(s.ctx, x);
+            s.store.clear();
+            s.scratch.clear();
+            gvxb_ctx_destroy(s.ctx);
+            s.ctx = nullptr;
+        }
+    };
+    std::shared_ptr<dev::Program> prog;
+    VerifiedGraph exec;
+    std::int64_t transfers = 0;
+    std::vector<std::unique_ptr<Slot>> slots;
+    std::deque<int> inflight; // slot indices in submission order
+    std::deque<ExecutionReport> ready;
+    int next_slot = 0;
+
+    void init(int depth) {
+        dev::context(); // device check + the shared NVRTC modules
+        int device = 0;
+        if (const char* e = std::getenv("GVX_DEVICE")) device = std::atoi(e);
+        for (int i = 0; i < std::max(1, depth); ++i) {
+            auto sl = std::make_unique<Slot>();
+            sl->s.prog = prog;
+            sl->s.exec_graph = &exec;
+            sl->s.frames = 1;
+            dev::check(gvxb_ctx_create(device, &sl->s.ctx), "pipeline context");
+            dev::check(gvxb_event_create(&sl->done), "pipeline event");
+            dev::check(gvxb_host_alloc(32, &sl->pin_status), "pipeline status staging");
+            sl->s.prepare();
+            const AppGraph& g = exec.graph();
+            const Context& ctx = exec.context();
+            for (ObjectId id : g.data()) {
+                const DataObject* o = ctx.find(id);
+                if (!o || o->is_virtual || g.producer(id) == kInvalidId || !prog->objects.count(id)) continue;
+                (prog->objects.at(id).desc.kind == ObjKind::Image ? sl->image_outs : sl->other_outs).push_back(id);
+            }
+            slots.push_back(std::move(sl));
+        }
+    }
+
+    void* staging(Slot& sl, ObjectId id, std::size_t n) {
+        auto it = sl.pin.find(id);
+        if (it != sl.pin.end() && sl.bytes[id] >= n) return it->second;
+        if (it != sl.pin.end()) gvxb_host_free(it->second);
+        void* p = nullptr;
+        dev::check(gvxb_host_alloc(n, &p), "pipeline staging");
+        sl.pin[id] = p;
+        sl.bytes[id] = n;
+        return p;
+    }
+
+    void complete_oldest(ObjectId direct = kInvalidId, void* dst = nullptr, std::size_t dst_bytes = 0) {
+        const int k = inflight.front();
+        inflight.pop_front();
+        Slot& sl = *slots[static_cast<std::size_t>(k)];
+        dev::check(gvxb_event_sync(sl.done), "pipeline wait");
+        sl.busy = false;
+        std::uint64_t st[2];
+        std::memcpy(st, sl.pin_status, sizeof st);
+        if (st[0] & GVXB_STATUS_DIV_BY_ZERO) throw Error(ErrorCode::DivByZero, "division by zero");
+        if (st[0] & GVXB_STATUS_INDEX_RANGE) throw Error(ErrorCode::ShapeMismatch, "array index out of range");
+        ExecutionReport r;
+        r.counters.kernel_launches = gvxb_launch_count(sl.s.ctx) - sl.launches0;
+        r.counters.pixels_read = static_cast<std::int64_t>(st[1]);
+        for (const dev::Unit& u : prog->units) {
+            r.counters.pixels_read += u.static_reads;
+            r.counters.pixels_written += u.static_writes;
+        }
+        r.counters.transfers_executed = transfers;
+        for (ObjectId id : sl.image_outs) {
+            const dev::ObjInfo& oi = prog->objects.at(id);
+            if (id == direct) {
+                const std::size_t n = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format) *
+                                      static_cast<std::size_t>(oi.desc.height);
+                if (dst_bytes < n) throw Error(ErrorCode::ShapeMismatch, "output buffer too small", id);
+                dev::parallel_copy(dst, sl.pin.at(id), n);
+                continue;
+            }
+            Buffer b = Buffer::image(exec.resolved().count(id) ? exec.desc(id) : oi.desc);
+            b.id = id;
+            dev::parallel_copy(b.bytes.data(), sl.pin.at(id), b.bytes.size());
+            r.outputs[id] = std::move(b);
+        }
+        for (ObjectId id : sl.other_outs) r.outputs[id] = sl.s.download(id, 0); // small: values / counts
+        ready.push_back(std::move(r));
+    }
+
+    void upload_image(Slot& sl, ObjectId id, const void* data, std::size_t bytes) {
+        const dev::ObjInfo& oi = prog->objects.at(id);
+        const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
+        const std::size_t n = row * static_cast<std::size_t>(oi.desc.height);
+        if (bytes < n) throw Error(ErrorCode::ShapeMismatch, "image payload too small", id);
+        void* pin = staging(sl, id, n);
+        dev::parallel_copy(pin, data, n, /*streaming=*/true);
+        DeviceSession::Impl::Store& st = sl.s.ensure(id);
+        dev::check(gvxb_upload_2d(sl.s.ctx, st.ptr, static_cast<std::size_t>(st.pitch), pin, row, row,
+                                  static_cast<std::size_t>(oi.desc.height)),
+                   "pipeline upload");
+    }
+
+    /// The slot the next frame uses (round robin = submission order): when
+    /// every slot is in flight, the oldest completes first.
+    Slot& take_slot() {
+        if (static_cast<int>(inflight.size()) >= static_cast<int>(slots.size())) complete_oldest();
+        return *slots[static_cast<std::size_t>(next_slot)];
+    }
+
+    void submit_raw(ObjectId id, const void* data, std::size_t bytes) {
+        InputMap none;
+        std::map<ObjectId, Buffer> defaults;
+        // the graph's other inputs (bound scalars / matrices) as run_plan binds them
+        InputMap probe;
+        Buffer placeholder;
+        placeholder.id = id;
+        placeholder.desc = exec.desc(id);
+        probe[id] = placeholder;
+        auto bound = bind_inputs(exec, probe, defaults);
+        Slot& sl = take_slot();
+        for (const auto& [oid, b] : bound) {
+            if (oid == id || !prog->objects.count(oid)) continue;
+            if (prog->objects.at(oid).desc.kind == ObjKind::Image)
+                throw Error(ErrorCode::MissingInput, "the raw-pointer submit takes a graph with one image input", oid);
+            sl.s.upload(oid, *b, 0);
+        }
+        if (prog->objects.count(id)) upload_image(sl, id, data, bytes);
+        launch_slot(sl);
+    }
+
+    void submit(const InputMap& inputs) {
+        std::map<ObjectId, Buffer> defaults;
+        auto bound = bind_inputs(exec, inputs, defaults);
+        Slot& sl = take_slot();
+        for (const auto& [id, b] : bound) {
+            if (!prog->objects.count(id)) continue;
+            if (prog->objects.at(id).desc.kind != ObjKind::Image) sl.s.upload(id, *b, 0);
+            else upload_image(sl, id, b->bytes.data(), b->bytes.size());
+        }
+        launch_slot(sl);
+    }
+
+    void launch_slot(Slot& sl) {
+        gvxb_ctx sctx = sl.s.ctx;
+        dev::check(gvxb_status_reset(sctx), "status reset");
+        sl.launches0 = gvxb_launch_count(sctx);
+        sl.s.run_all();
+        for (ObjectId id : sl.image_outs) {
+            const dev::ObjInfo& oi = prog->objects.at(id);
+            const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
+            void* pin = staging(sl, id, row * static_cast<std::size_t>(oi.desc.height));
+            DeviceSession::Impl::Store& st = sl.s.ensure(id);
+            dev::check(gvxb_download_2d(sctx, pin, row, st.ptr, static_cast<std::size_t>(st.pitch), row,
+                                        static_cast<std::size_t>(oi.desc.height)),
+                       "pipeline download");
+        }
+        std::uint32_t* status = nullptr;
+        dev::check(gvxb_status_ptr(sctx, &status), "status pointer");
+        dev::check(gvxb_download_2d(sctx, sl.pin_status, 16, status, 16, 16, 1), "status download");
+        dev::check(gvxb_event_record(sctx, sl.done), "pipeline event");
+        sl.busy = true;
+        inflight.push_back(next_slot); // only once everything is enqueued
+        next_slot = (next_slot + 1) % static_cast<int>(slots.size());
+    }
+};
+
+HostPipeline::HostPipeline(const OptimizedPlan& plan, int depth) : impl_(std::make_unique<Impl>()) {
+    if (!plan.fused.stamped()) throw Error(ErrorCode::UnstampedGraph, "plan execution needs a verified fused graph");
+    impl_->prog = plan_program(plan, nullptr);
+    impl_->exec = plan.fused;
+    impl_->transfers = plan.transfers.optimized_count();
+    impl_->init(depth);
+}
+
+HostPipeline::HostPipeline(const VerifiedGraph& g, int depth) : impl_(std::make_unique<Impl>()) {
+    if (!g.stamped()) throw Error(ErrorCode::UnstampedGraph, "execution needs a verified graph");
+    impl_->prog = naive_program(g, nullptr);
+    impl_->exec = g;
+    impl_->transfers = static_cast<std::int64_t>(g.graph().nodes().size()) * 2;
+    impl_->init(depth);
+}
+
+HostPipeline::~HostPipeline() = default;
+
+void HostPipeline::submit(const InputMap& inputs) { impl_->submit(inputs); }
+
+void HostPipeline::submit(ObjectId image_input, const void* data, std::size_t bytes) {
+    impl_->submit_raw(image_input, data, bytes);
+}
+
+ExecutionReport HostPipeline::next_into(ObjectId image_output, void* dst, std::size_t bytes) {
+    if (!impl_->ready.empty()) { // already completed into a Buffer (submit ran ahead)
+        ExecutionReport r = std::move(impl_->ready.front());
+        impl_->ready.pop_front();
+        auto it = r.outputs.find(image_output);
+        if (it != r.outputs.end()) {
+            if (bytes < it->second.bytes.size()) throw Error(ErrorCode::ShapeMismatch, "output buffer too small");
+            dev::parallel_copy(dst, it->second.bytes.data(), it->second.bytes.size());
+            r.outputs.erase(it);
+        }
+        return r;
+    }
+    if (impl_->inflight.empty()) throw Error(ErrorCode::MissingInput, "no frame submitted");
+    impl_->complete_oldest(image_output, dst, bytes);
+    ExecutionReport r = std::move(impl_->ready.front());
+    impl_->ready.pop_front();
+    return r;
+}
+
+ExecutionReport HostPipeline::next() {
+    if (impl_->ready.empty()) {
+        if (impl_->inflight.empty()) throw Error(ErrorCode::MissingInput, "no frame submitted");
+        impl_->complete_oldest();
+    }
+    ExecutionReport r = std::move(impl_->ready.front());
+    impl_->ready.pop_front();
+    return r;
+}
+
+int HostPipeline::pending() const { return static_cast<int>(impl_->inflight.size() + impl_->ready.size()); }
 
 int device_count() {
     int n = 0;

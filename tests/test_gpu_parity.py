@@ -125,3 +125,28 @@ def test_host_runs_recycle_pinned_buffers(cfg, gvx, oracle_mod):
                 assert np.array_equal(np.array(got), want), (cfg, rnd)
             plain, _ = g.run_host(f)
             assert _same(cfg, plain, want)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+@pytest.mark.parametrize("naive", [False, True])
+def test_host_pipeline_matches_run_host(cfg, naive, gvx, oracle_mod):
+    """gvx::HostPipeline: frames in flight, results in submission order and
+    identical (outputs and event counters) to one-at-a-time run_plan /
+    run_naive."""
+    w, h = 643, 211
+    g = gvx.ConfigGraph(cfg, w, h)
+    frames = [gvx.random_u8(w, h, 70 + i) for i in range(7)]
+    want = [g.run_host(f, naive=naive) for f in frames]
+    for depth in (1, 3):
+        pl = gvx.Pipeline(g, depth=depth, naive=naive)
+        got = []
+        for f in frames:
+            if pl.pending() >= depth:
+                got.append(pl.next())
+            pl.submit(f)
+        while pl.pending():
+            got.append(pl.next())
+        assert len(got) == len(frames)
+        for (gr, gc), (wr, wc), f in zip(got, want, frames):
+            assert _same(cfg, gr, wr) and _same(cfg, gr, oracle_mod.port_run(cfg, f))
+            assert gc == wc
