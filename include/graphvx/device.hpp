@@ -83,6 +83,10 @@ public:
     /// As next(), but image output `image_output` is copied straight to
     /// `dst` (`bytes`, packed rows) and left out of the report.
     ExecutionReport next_into(ObjectId image_output, void* dst, std::size_t bytes);
+    /// As next(), but image output `image_output` stays in the pipeline's
+    /// page-locked staging: `*view` points at its packed rows, valid until
+    /// the next submit().
+    ExecutionReport next_view(ObjectId image_output, const void** view);
     /// Frames submitted and not yet returned by next().
     int pending() const;
     struct Impl;

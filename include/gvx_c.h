@@ -85,6 +85,9 @@ int gvxc_pipeline_destroy(gvxc_pipeline p);
 int gvxc_pipeline_submit(gvxc_pipeline p, const uint8_t* in);
 int gvxc_pipeline_pending(gvxc_pipeline p);
 int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stats, long long counters[4]);
+/* As gvxc_pipeline_next for image-output graphs, without the copy: *view
+ * points at the result in page-locked staging until the next submit. */
+int gvxc_pipeline_next_view(gvxc_pipeline p, const void** view, size_t* bytes, long long counters[4]);
 
 /* ---- graph description files (graph_io.hpp, ref:src/graph_io.cpp) -------- */
 typedef struct gvxc_json_s* gvxc_json;

@@ -116,6 +116,7 @@ def _declare(c, g):
     g.gvxc_pipeline_submit.argtypes = [P, U8P]
     g.gvxc_pipeline_pending.argtypes = [P]
     g.gvxc_pipeline_next.argtypes = [P, P, ctypes.POINTER(L), ctypes.POINTER(D), ctypes.POINTER(L)]
+    g.gvxc_pipeline_next_view.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(L)]
     g.gvxc_graph_input_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_graph_output_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_launch_count.restype = ctypes.c_longlong
@@ -321,6 +322,21 @@ class Pipeline:
 
     def pending(self) -> int:
         return _graph.gvxc_pipeline_pending(self._h)
+
+    def next_view(self):
+        """Oldest frame's output plane as a read-only view of the pipeline's
+        page-locked staging (valid until the next submit), and counters."""
+        ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+        counters = (ctypes.c_longlong * 4)()
+        _check_graph(_graph.gvxc_pipeline_next_view(self._h, ctypes.byref(ptr), ctypes.byref(n), counters))
+        views = self.__dict__.setdefault("_views", {})  # one numpy view per staging buffer
+        key = (ptr.value, n.value)
+        if key not in views:
+            dt = np.dtype(CONFIG_OUTPUT[self.graph.cfg])
+            raw = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), shape=(n.value,))
+            views[key] = raw.view(dt).reshape(self.graph.height, self.graph.width)
+        cnt = dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(counters)))
+        return views[key], cnt
 
     def next(self, out: np.ndarray = None):
         """Oldest frame's result: (output plane, counters), or

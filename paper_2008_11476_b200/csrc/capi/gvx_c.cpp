@@ -335,6 +335,23 @@ int gvxc_pipeline_submit(gvxc_pipeline p, const uint8_t* in) {
 
 int gvxc_pipeline_pending(gvxc_pipeline p) { return p->p->pending(); }
 
+int gvxc_pipeline_next_view(gvxc_pipeline p, const void** view, size_t* bytes, long long counters[4]) {
+    return guarded([&] {
+        gvxc_graph g = p->g;
+        if (g->cfg == 4) throw gvx::Error(gvx::ErrorCode::UnknownObject, "config 4 has no image output");
+        gvx::ExecutionReport r = p->p->next_view(g->cg.outputs.at(0), view);
+        if (bytes)
+            *bytes = (g->cfg == 1 || g->cfg == 5 ? 2u : 1u) * static_cast<std::size_t>(g->width) *
+                     static_cast<std::size_t>(g->height);
+        if (counters) {
+            counters[0] = r.counters.kernel_launches;
+            counters[1] = r.counters.pixels_read;
+            counters[2] = r.counters.pixels_written;
+            counters[3] = r.counters.transfers_executed;
+        }
+    });
+}
+
 int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stats, long long counters[4]) {
     return guarded([&] {
         gvxc_graph g = p->g;

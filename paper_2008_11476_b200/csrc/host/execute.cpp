@@ -1327,6 +1327,8 @@ struct HostPipeline::Impl {
     std::deque<int> inflight; // slot indices in submission order
     std::deque<ExecutionReport> ready;
     int next_slot = 0;
+    const void* last_view = nullptr;
+    std::vector<std::uint8_t> view_hold;
 
     void init(int depth) {
         dev::context(); // device check + the shared NVRTC modules
@@ -1384,6 +1386,10 @@ struct HostPipeline::Impl {
         for (ObjectId id : sl.image_outs) {
             const dev::ObjInfo& oi = prog->objects.at(id);
             if (id == direct) {
+                if (!dst) { // view: the caller reads the staging in place
+                    last_view = sl.pin.at(id);
+                    continue;
+                }
                 const std::size_t n = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format) *
                                       static_cast<std::size_t>(oi.desc.height);
                 if (dst_bytes < n) throw Error(ErrorCode::ShapeMismatch, "output buffer too small", id);
@@ -1419,7 +1425,13 @@ struct HostPipeline::Impl {
         return *slots[static_cast<std::size_t>(next_slot)];
     }
 
+    static double us_since(std::chrono::steady_clock::time_point t) {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t).count();
+    }
+
     void submit_raw(ObjectId id, const void* data, std::size_t bytes) {
+        static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         InputMap none;
         std::map<ObjectId, Buffer> defaults;
         // the graph's other inputs (bound scalars / matrices) as run_plan binds them
@@ -1430,6 +1442,7 @@ struct HostPipeline::Impl {
         probe[id] = placeholder;
         auto bound = bind_inputs(exec, probe, defaults);
         Slot& sl = take_slot();
+        const double t_take = trace ? us_since(t0) : 0;
         for (const auto& [oid, b] : bound) {
             if (oid == id || !prog->objects.count(oid)) continue;
             if (prog->objects.at(oid).desc.kind == ObjKind::Image)
@@ -1437,7 +1450,11 @@ struct HostPipeline::Impl {
             sl.s.upload(oid, *b, 0);
         }
         if (prog->objects.count(id)) upload_image(sl, id, data, bytes);
+        const double t_up = trace ? us_since(t0) : 0;
         launch_slot(sl);
+        if (trace)
+            std::fprintf(stderr, "[gvx pipeline] submit: take %.1f us, copy+upload %.1f us, launch %.1f us\n", t_take,
+                         t_up - t_take, us_since(t0) - t_up);
     }
 
     void submit(const InputMap& inputs) {
@@ -1526,6 +1543,27 @@ ExecutionReport HostPipeline::next() {
     }
     ExecutionReport r = std::move(impl_->ready.front());
     impl_->ready.pop_front();
+    return r;
+}
+
+ExecutionReport HostPipeline::next_view(ObjectId image_output, const void** view) {
+    if (!impl_->ready.empty()) { // completed early into a Buffer: serve that copy
+        ExecutionReport r = std::move(impl_->ready.front());
+        impl_->ready.pop_front();
+        auto it = r.outputs.find(image_output);
+        if (it == r.outputs.end()) throw Error(ErrorCode::UnknownObject, "no such image output", image_output);
+        impl_->view_hold = std::move(it->second.bytes);
+        r.outputs.erase(it);
+        *view = impl_->view_hold.data();
+        return r;
+    }
+    if (impl_->inflight.empty()) throw Error(ErrorCode::MissingInput, "no frame submitted");
+    impl_->last_view = nullptr;
+    impl_->complete_oldest(image_output, nullptr, 0);
+    ExecutionReport r = std::move(impl_->ready.front());
+    impl_->ready.pop_front();
+    if (!impl_->last_view) throw Error(ErrorCode::UnknownObject, "no such image output", image_output);
+    *view = impl_->last_view;
     return r;
 }
 

@@ -150,3 +150,22 @@ def test_host_pipeline_matches_run_host(cfg, naive, gvx, oracle_mod):
         for (gr, gc), (wr, wc), f in zip(got, want, frames):
             assert _same(cfg, gr, wr) and _same(cfg, gr, oracle_mod.port_run(cfg, f))
             assert gc == wc
+
+
+def test_host_pipeline_views(gvx, oracle_mod):
+    """next_view: results read in place from the pipeline's staging."""
+    w, h = 517, 333
+    g = gvx.ConfigGraph(2, w, h)
+    frames = [gvx.random_u8(w, h, 90 + i) for i in range(6)]
+    pl = gvx.Pipeline(g, depth=3)
+    got = []
+    for f in frames:
+        if pl.pending() >= 3:
+            v, _ = pl.next_view()
+            got.append(np.array(v))  # consumed before the next submit
+        pl.submit(f)
+    while pl.pending():
+        v, _ = pl.next_view()
+        got.append(np.array(v))
+    for r, f in zip(got, frames):
+        assert np.array_equal(r, oracle_mod.port_run(2, f))
