@@ -291,6 +291,24 @@ TEST_CASE("gpu: runtime division by zero surfaces as DivByZero") {
     } catch (const Error& e) {
         CHECK(e.code() == ErrorCode::DivByZero);
     }
+    // the pipelined host path reports it for the offending frame only
+    HostPipeline pipe(impl, 2);
+    InputMap ok = in;
+    ok[b] = random_buffer(img_desc(8, 8, ImageFormat::U8), 2);
+    for (std::size_t i = 0; i < ok[b].bytes.size(); ++i) ok[b].bytes[i] |= 1; // no zero divisor
+    pipe.submit(ok);
+    pipe.submit(in);
+    ExecutionReport first = pipe.next();
+    CHECK(first.outputs.at(o).bytes == run_naive(impl, ok).outputs.at(o).bytes);
+    bool raised = false;
+    try {
+        pipe.next();
+    } catch (const Error& e) {
+        raised = e.code() == ErrorCode::DivByZero;
+    }
+    CHECK(raised);
+    pipe.submit(ok); // the pipeline stays usable
+    CHECK(pipe.next().outputs.at(o).bytes == first.outputs.at(o).bytes);
 }
 
 namespace {
