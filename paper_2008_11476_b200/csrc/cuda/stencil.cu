@@ -477,6 +477,8 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
             if (kClamp && p.clamp255 == 2) smem_inc_u8(hbase + ((__float_as_uint(qv) & 0xFFu) << 7)); // Wrap
             else smem_inc_u8(hcnt + (__float_as_uint(qv) << 7));
         };
+        Q4 pend{};
+        bool have_pend = false;
         auto emit = [&](Q4 acc) {
             if (kMode == 1) {
                 // -(1.5*2^23 + b) by round-up of the negated product, then
@@ -501,10 +503,16 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
                     store(sep_pack(q));
                     drow += p.dst_pitch;
                 }
-                count(q.e.x, 0);
-                count(q.o.x, 1);
-                count(q.e.y, 2);
-                count(q.o.y, 3);
+                // count the PREVIOUS row now: its increment chain overlaps
+                // this row's arithmetic instead of ending it
+                if (have_pend) {
+                    count(pend.e.x, 0);
+                    count(pend.o.x, 1);
+                    count(pend.e.y, 2);
+                    count(pend.o.y, 3);
+                }
+                pend = q;
+                have_pend = true;
             }
         };
         // push accumulation: smem row j (global row y0 - R + j) adds u[i] * h(j)
@@ -528,6 +536,12 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
                 row(O + t + K - 1, (t + K - 1) % K); // O is a multiple of K
                 emit(acc[t]);                        // output o = O + t
             }
+        }
+        if (kMode >= 2 && have_pend) {
+            count(pend.e.x, 0);
+            count(pend.o.x, 1);
+            count(pend.e.y, 2);
+            count(pend.o.y, 3);
         }
     };
     if (x0 + kSepTW > p.width) body(std::true_type{});
