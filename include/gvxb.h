@@ -107,6 +107,8 @@ int gvxb_ctx_sm_count(gvxb_ctx ctx);
 int gvxb_sync(gvxb_ctx ctx);
 /* Number of device kernels this context launched so far. */
 int64_t gvxb_launch_count(gvxb_ctx ctx);
+/* Kernels launched by every context of the process. */
+int64_t gvxb_total_launch_count(void);
 
 /* ---- memory and copies ---------------------------------------------------- */
 int gvxb_alloc(gvxb_ctx ctx, size_t bytes, void** dptr);

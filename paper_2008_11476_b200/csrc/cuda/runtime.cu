@@ -6,6 +6,8 @@
 // driver (the CPU test suite checks the exported symbols there).
 #include "common.cuh"
 
+#include <atomic>
+
 #include <cuda.h>
 #include <nvrtc.h>
 
@@ -29,10 +31,13 @@ int cuda_fail(cudaError_t e, const char* what) {
     return fail(GVXB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+std::atomic<long long> g_total_launches{0}; // every context's launches
+
 int check_launch(gvxb_ctx ctx, const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, what);
     ++ctx->launches;
+    ++g_total_launches;
     return GVXB_OK;
 }
 
@@ -140,6 +145,7 @@ void* gvxb_ctx_stream(gvxb_ctx ctx) { return ctx->stream; }
 int gvxb_ctx_device(gvxb_ctx ctx) { return ctx->device; }
 int gvxb_ctx_sm_count(gvxb_ctx ctx) { return ctx->sm_count; }
 int64_t gvxb_launch_count(gvxb_ctx ctx) { return ctx->launches; }
+int64_t gvxb_total_launch_count(void) { return g_total_launches.load(); }
 
 int gvxb_sync(gvxb_ctx ctx) {
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
@@ -364,6 +370,7 @@ int gvxb_jit_launch(gvxb_ctx ctx, gvxb_module m, int k, const unsigned grid[3], 
                                         static_cast<CUstream>(ctx->stream), args, nullptr);
     if (r != CUDA_SUCCESS) return fail(GVXB_ERR_CUDA, "cuLaunchKernel failed (" + std::to_string(r) + ")");
     ++ctx->launches;
+    ++g_total_launches;
     return GVXB_OK;
 }
 

@@ -223,7 +223,19 @@ gvxb_ctx context() {
     return ctx;
 }
 
-long long launch_count() { return gvxb_launch_count(context()); }
+long long launch_count() {
+    context();
+    return gvxb_total_launch_count();
+}
+
+/// A context of its own (stream, status word, read counter) on the library's
+/// device: sessions executing concurrently never share error flags or
+/// counters (the reference allows concurrent run_* calls).
+gvxb_ctx own_context() {
+    gvxb_ctx c = nullptr;
+    check(gvxb_ctx_create(gvxb_ctx_device(context()), &c), "gvxb_ctx_create");
+    return c;
+}
 
 namespace {
 
@@ -655,6 +667,8 @@ struct DeviceSession::Impl {
     std::map<ObjectId, Store> store;
     std::vector<void*> scratch; ///< per unit (JIT reduce scratch, conv sums)
 
+    bool owns_ctx = false; ///< ctx created for this storage (destroyed with it)
+
     ~Impl() {
         if (!ctx) return;
         gvxb_sync(ctx);
@@ -662,6 +676,7 @@ struct DeviceSession::Impl {
             if (kv.second.owned) gvxb_free(ctx, kv.second.ptr);
         for (void* s : scratch)
             if (s) gvxb_free(ctx, s);
+        if (owns_ctx) gvxb_ctx_destroy(ctx);
     }
 
     static std::int64_t row_pitch(const ResolvedDesc& d) {
@@ -1106,7 +1121,8 @@ std::shared_ptr<HostSession> host_session(const std::shared_ptr<dev::Program>& p
         slot.second = std::make_shared<HostSession>();
         slot.second->impl.prog = prog;
         slot.second->impl.frames = 1;
-        slot.second->impl.ctx = dev::context();
+        slot.second->impl.ctx = dev::own_context();
+        slot.second->impl.owns_ctx = true;
         slot.second->impl.staging = std::make_unique<Staging>(slot.second->impl.ctx);
     }
     return slot.second;
@@ -1215,7 +1231,8 @@ DeviceSession::DeviceSession(const OptimizedPlan& plan, int frames) : impl_(std:
     impl_->exec_copy = plan.fused;
     impl_->exec_graph = &impl_->exec_copy;
     impl_->frames = std::max(1, frames);
-    impl_->ctx = dev::context();
+    impl_->ctx = dev::own_context();
+    impl_->owns_ctx = true;
 }
 
 DeviceSession::DeviceSession(const VerifiedGraph& g, int frames) : impl_(std::make_unique<Impl>()) {
@@ -1224,7 +1241,8 @@ DeviceSession::DeviceSession(const VerifiedGraph& g, int frames) : impl_(std::ma
     impl_->exec_copy = g;
     impl_->exec_graph = &impl_->exec_copy;
     impl_->frames = std::max(1, frames);
-    impl_->ctx = dev::context();
+    impl_->ctx = dev::own_context();
+    impl_->owns_ctx = true;
 }
 
 DeviceSession::~DeviceSession() = default;
@@ -1304,20 +1322,12 @@ struct HostPipeline::Impl {
         std::vector<ObjectId> image_outs, other_outs;
         std::int64_t launches0 = 0;
         bool busy = false;
-        ~Slot() {
+        ~Slot() { // device storage and the context go with `s`
             if (!s.ctx) return;
             gvxb_sync(s.ctx);
             if (done) gvxb_event_destroy(done);
             if (pin_status) gvxb_host_free(pin_status);
             for (auto& kv : pin) gvxb_host_free(kv.second);
-            for (auto& kv : s.store)
-                if (kv.second.owned) gvxb_free(s.ctx, kv.second.ptr);
-            for (void* x : s.scratch)
-                if (x) gvxb_free(s.ctx, x);
-            s.store.clear();
-            s.scratch.clear();
-            gvxb_ctx_destroy(s.ctx);
-            s.ctx = nullptr;
         }
     };
     std::shared_ptr<dev::Program> prog;
@@ -1340,6 +1350,7 @@ struct HostPipeline::Impl {
             sl->s.exec_graph = &exec;
             sl->s.frames = 1;
             dev::check(gvxb_ctx_create(device, &sl->s.ctx), "pipeline context");
+            sl->s.owns_ctx = true;
             dev::check(gvxb_event_create(&sl->done), "pipeline event");
             dev::check(gvxb_host_alloc(32, &sl->pin_status), "pipeline status staging");
             sl->s.prepare();

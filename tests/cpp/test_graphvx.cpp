@@ -13,8 +13,10 @@
 #include "graphvx/image_io.hpp"
 #include "graphvx/optimize.hpp"
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <thread>
 #include <fstream>
 #include <random>
 
@@ -309,6 +311,40 @@ TEST_CASE("gpu: runtime division by zero surfaces as DivByZero") {
     CHECK(raised);
     pipe.submit(ok); // the pipeline stays usable
     CHECK(pipe.next().outputs.at(o).bytes == first.outputs.at(o).bytes);
+
+    // concurrent executions keep their own error flags and counters: a
+    // thread hitting DivByZero never leaks it into another graph's run
+    Context ctx2;
+    gvx_configs::ConfigGraph cg = gvx_configs::build_config(ctx2, 2, 97, 61, true);
+    VerifiedGraph impl2 = impl_of(ctx2, *cg.graph);
+    OptimizedPlan plan2 = optimize(impl2, ctx2);
+    InputMap in2;
+    in2[cg.input] = random_buffer(img_desc(97, 61, ImageFormat::U8), 3);
+    const ExecutionReport want = run_plan(plan2, in2);
+    std::atomic<int> bad{0}, div_errors{0};
+    std::thread t1([&] {
+        for (int i = 0; i < 40; ++i) {
+            try {
+                run_naive(impl, in);
+            } catch (const Error& e) {
+                if (e.code() == ErrorCode::DivByZero) ++div_errors;
+            }
+        }
+    });
+    std::thread t2([&] {
+        for (int i = 0; i < 40; ++i) {
+            try {
+                const ExecutionReport r = run_plan(plan2, in2);
+                if (!same_outputs(r, want) || r.counters.pixels_read != want.counters.pixels_read) ++bad;
+            } catch (const Error&) {
+                ++bad;
+            }
+        }
+    });
+    t1.join();
+    t2.join();
+    CHECK(bad.load() == 0);
+    CHECK(div_errors.load() == 40);
 }
 
 namespace {
