@@ -133,3 +133,33 @@ def test_loaded_kernel_cases_verify(gvx):
     import kernel_graphs
     for case, text in kernel_graphs.all_cases():
         gvx.GraphFile(text)  # load + verify + expand + optimize (no device needed)
+
+
+def test_attribute_fuzz_roundtrip(gvx, oracle_mod):
+    """Random attribute strings (escapes, control characters, unicode) and
+    numbers (integers, subnormal / huge doubles) survive load -> save ->
+    load, and match the reference serializer when it is available."""
+    import random
+    rng = random.Random(1234)
+    alphabet = ['a', 'Z', '"', '\\\\', '/', '\\n', '\\t', '\\x01', '\\x1f', 'é', '€', '😀', ' ', '{', '}']
+    for trial in range(60):
+        attrs = {}
+        for k in range(rng.randint(1, 6)):
+            key = "k" + "".join(rng.choice("abcxyz_") for _ in range(rng.randint(1, 6)))
+            kind = rng.randint(0, 3)
+            if kind == 0:
+                attrs[key] = "".join(rng.choice(alphabet) for _ in range(rng.randint(0, 12)))
+            elif kind == 1:
+                attrs[key] = rng.randint(-2 ** 62, 2 ** 62)
+            elif kind == 2:
+                attrs[key] = rng.choice([0.0, -0.0, 5e-324, 1.7976931348623157e308, 1e-7, 123456.789, -2.5e22])
+            else:
+                attrs[key] = rng.uniform(-1e6, 1e6) * 10 ** rng.randint(-30, 30)
+        doc = {"name": "fuzz", "images": [], "nodes": [{"kernel": "Copy", "params": [], "attrs": attrs}]}
+        text = json.dumps(doc)
+        ours = gvx.json_roundtrip(text)
+        back = json.loads(ours)["nodes"][0]["attrs"]
+        assert strict_eq(back, attrs), (trial, attrs, back)
+        assert gvx.json_roundtrip(ours) == ours
+        if oracle_mod.have_ref_graph_io():
+            assert ours == oracle_mod.ref_json_roundtrip(text), trial
