@@ -23,28 +23,33 @@
 //  * Clamp borders of the intermediates: products at out-of-image positions
 //    take the clamped position's value (ref:src/execute.cpp:242-245).
 //
-// Layout: CTA = 4 warps; a warp covers 30 owner lanes x 4 columns (lanes 0
-// and 31 are halo lanes whose products reach their neighbours through warp
-// shuffles), 64 rows per CTA streamed with 3-row register rings.  Columns
-// are kept as even/odd float2 pairs ((c, c+2), (c+1, c+3)) so every
-// separable stencil step is a packed, register-aligned FP32 op.
+// Layout (v4): one warp per CTA owns a strip of 248 output columns and a
+// band of rows.  Lane L holds 8 columns c = x - 4 + 8L .. c + 7 as four
+// float2 pairs (A_i, B_i) = (column c+i, column c+4+i): every stencil step
+// is then a plain packed op on register pairs with no lane-internal
+// shuffling of halves, and only the strip's outer half-lanes (lane 0's A
+// half, lane 31's B half) are halo.  Source rows stream through a 16-row
+// shared-memory ring filled by 8-row TMA chunks, so a band pays its 4 halo
+// rows once however tall it is.
 #include "packed.cuh"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 namespace gvxd {
 
-constexpr int kHarThreads = 128;
-constexpr int kHarWarpCols = 120;                         // 30 owner lanes x 4
-constexpr int kHarTW = kHarWarpCols * (kHarThreads / 32); // 480 output columns per CTA
-constexpr int kHarTH = 64;
-constexpr int kHarSW = kHarTW + 32; // smem columns [x0 - 16, x0 + 496): box x start 16-byte aligned
-constexpr int kHarSH = kHarTH + 4;  // smem rows    [y0 - 2, y0 + 66)
+constexpr int kHarThreads = 32;  // one warp per CTA
+constexpr int kHarCols = 248;    // output columns per strip (32 lanes x 8 - 8 halo)
+constexpr int kHarSW = 288;      // ring row bytes: image columns [x_org, x_org + 288)
+constexpr int kHarChunk = 8;     // rows per TMA chunk
+constexpr int kHarRing = 2 * kHarChunk;
+constexpr int kHarTHMax = 1024;
 
 struct HarrisParams {
     int width;
-    int th; // output rows per tile (<= kHarTH), chosen to fill whole waves
+    int th; // output rows per band (<= kHarTHMax), chosen to fill whole waves
     Band band;
     uint8_t* mask;
     int64_t mask_pitch, mask_fstride;
@@ -52,20 +57,33 @@ struct HarrisParams {
     int64_t resp_pitch, resp_fstride;
     double k;
     double threshold;
-    float kabs;  // |k|
-    float kneg;  // -k
+    float kpos;  // k
     float t81;   // 81 T
     float c_tt;  // bound slope in tt = tr^2
-    float c_tr;  // bound slope in tr
     float c0;    // bound constant
 };
 
-struct Prod3 {
-    Q4 xx, yy, xy; // horizontal box sums of one product row
+/// Four column pairs (A_i, B_i) = (c+i, c+4+i).
+struct Q8 {
+    float2 v[4];
 };
-__device__ __forceinline__ Prod3 padd(const Prod3& a, const Prod3& b) {
-    return Prod3{qadd(a.xx, b.xx), qadd(a.yy, b.yy), qadd(a.xy, b.xy)};
+/// Source pairs for i = -1 .. 4 at v[i + 1].
+struct Raw8 {
+    float2 v[6];
+};
+struct Prod3 {
+    Q8 xx, yy, xy;
+};
+__device__ __forceinline__ Q8 q8add(const Q8& a, const Q8& b) {
+    return Q8{{add2(a.v[0], b.v[0]), add2(a.v[1], b.v[1]), add2(a.v[2], b.v[2]), add2(a.v[3], b.v[3])}};
 }
+__device__ __forceinline__ Q8 q8mul(const Q8& a, const Q8& b) {
+    return Q8{{mul2(a.v[0], b.v[0]), mul2(a.v[1], b.v[1]), mul2(a.v[2], b.v[2]), mul2(a.v[3], b.v[3])}};
+}
+__device__ __forceinline__ Prod3 padd(const Prod3& a, const Prod3& b) {
+    return Prod3{q8add(a.xx, b.xx), q8add(a.yy, b.yy), q8add(a.xy, b.xy)};
+}
+__device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
 
 /// The reference's exact expression for one pixel from the exact box sums.
 __device__ __forceinline__ float exact_response(float sxx, float syy, float sxy, double k) {
@@ -77,196 +95,308 @@ __device__ __forceinline__ float exact_response(float sxx, float syy, float sxy,
     return __double2float_rn(__dsub_rn(__ll2double_rn(det), __dmul_rn(k, __ll2double_rn(tr * tr))));
 }
 
-template <bool kResp>
-__global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_constant__ CUtensorMap map,
-                                                             HarrisParams p) {
-    __shared__ alignas(128) uint8_t tile[kHarSH * kHarSW];
-    __shared__ uint64_t bar;
+/// Bytes 0, 1 = 0xFF where a / b is negative (sign bit set), else 0x00:
+/// prmt's sign-replicate selector mode (the __byte_perm intrinsic masks it).
+__device__ __forceinline__ uint32_t sign_bytes(float a, float b) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, 0xFBFB;" : "=r"(r) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
+    return r;
+}
 
-    const int x0 = blockIdx.x * kHarTW;
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <bool kResp>
+__global__ void __launch_bounds__(kHarThreads, 12) harris_kernel(const __grid_constant__ CUtensorMap map,
+                                                                 HarrisParams p) {
+    __shared__ alignas(128) uint8_t ring[kHarRing * kHarSW];
+    __shared__ uint64_t bar[2];
+
+    const int lane = threadIdx.x;
+    // first output column of the strip (a multiple of 8: keeps the lanes'
+    // 64-bit ring loads aligned); the last strip is pulled left to end at
+    // roundup8(W) so that it has no idle lanes (overlapping columns are
+    // computed twice, with identical results)
+    const int x = max(0, min(static_cast<int>(blockIdx.x) * kHarCols, ((p.width + 7) & ~7) - kHarCols));
+    const int x_org = ((x - 5) >> 4) << 4;    // ring column 0 (16-byte aligned TMA origin)
     const int y0 = p.band.row0 + blockIdx.y * p.th;
     const int y1 = min(y0 + p.th, p.band.row1);
     const int frame = blockIdx.z;
     const int H = p.band.global_h;
     const int W = p.width;
+    const int steps = (y1 - y0) + 4; // virtual rows j <-> global row y0 - 2 + j
+    const int nchunks = (steps + kHarChunk - 1) / kHarChunk;
 
-    if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         fence_barrier_init();
     }
-    __syncthreads();
-    stage_tile_u8<kHarSW, kHarSH>(tile, &map, &bar, x0 - 16, y0 - 2, frame, W, p.band, p.th + 4);
+    __syncwarp();
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c = x0 + kHarWarpCols * warp + 4 * (lane - 1); // first column of this lane
-    const int off = c - (x0 - 16);                           // its smem column
-    const bool owner = lane >= 1 && lane <= 30 && c < W;
-    const bool left_edge = c == 0;      // column c-1 clamps to column 0
-    const bool right_edge = c + 4 >= W; // column c+4 (and maybe own columns) clamp to W-1
-    const int last = W - 1 - c;         // index of column W-1 inside this lane (if 0..3)
+    auto issue = [&](int k) { // lane 0: chunk k -> ring half k & 1
+        uint64_t* b = &bar[k & 1];
+        mbar_expect_tx(b, kHarChunk * kHarSW);
+        tma_load_3d(ring + (k & 1) * kHarChunk * kHarSW, &map, b, x_org / 4,
+                    y0 - 2 + kHarChunk * k - p.band.src_row0, frame);
+    };
+    // Clamp borders of the source: columns outside [0, W) replicate the edge
+    // column, rows outside [0, H) the edge row (ref:src/execute.cpp:242-245).
+    const bool col_patch = x_org < 0 || x_org + kHarSW > W;
+    bool dirty = false; // the ring half about to be refilled holds generic-proxy writes
+    auto patch = [&](int k) {
+        uint8_t* base = ring + (k & 1) * kHarChunk * kHarSW;
+        const int g0 = y0 - 2 + kHarChunk * k;
+        const bool rows = g0 < 0 || g0 + kHarChunk > H;
+        if (col_patch) {
+            // smem columns [0, first) take column first (image column 0),
+            // (lastc, kHarSW) take column lastc (image column W-1)
+            const int first = clampi(-x_org, 0, kHarSW - 1), lastc = clampi(W - 1 - x_org, 0, kHarSW - 1);
+            for (int r = 0; r < kHarChunk; ++r) {
+                uint8_t* row = base + r * kHarSW;
+                if (lane < first) row[lane] = row[first];
+                for (int j = lastc + 1 + lane; j < kHarSW; j += 32) row[j] = row[lastc];
+            }
+            __syncwarp();
+        }
+        if (rows) {
+            for (int r = 0; r < kHarChunk; ++r) {
+                const int gy = g0 + r;
+                if ((gy >= 0 && gy < H) || kHarChunk * k + r >= steps) continue;
+                const int v = clampi(gy, 0, H - 1) - (y0 - 2); // virtual row of the clamped source row
+                const uint32_t* from = reinterpret_cast<const uint32_t*>(ring + (v % kHarRing) * kHarSW);
+                uint32_t* to = reinterpret_cast<uint32_t*>(base + r * kHarSW);
+                for (int j = lane; j < kHarSW / 4; j += 32) to[j] = from[j];
+            }
+            __syncwarp();
+        }
+        return col_patch || rows;
+    };
+    /// Waits for chunk k, patches its borders, then starts chunk k + 1 into
+    /// the other half (whose rows the warp has finished reading).
+    auto next_chunk = [&](int k) {
+        mbar_wait(&bar[k & 1], (k >> 1) & 1);
+        const bool patched = patch(k);
+        if (lane == 0 && k + 1 < nchunks) {
+            if (dirty) fence_proxy_async_smem();
+            issue(k + 1);
+        }
+        dirty = patched;
+    };
+
+    const int c = x - 4 + 8 * lane; // first column of this lane
+    const int off = c - x_org;      // its ring column (4 <= off, off % 8 == 4)
+    const int last = W - 1 - c;     // index of column W-1 among c .. c+7 (when 0..7)
+    const bool store_a = lane > 0 && c < W;
+    const bool store_b = lane < 31 && c + 4 < W;
 
     uint8_t* mrow = p.mask + frame * p.mask_fstride + static_cast<int64_t>(y0 - p.band.dst_row0) * p.mask_pitch + c;
     char* rrow = reinterpret_cast<char*>(p.resp) + frame * p.resp_fstride +
                  static_cast<int64_t>(y0 - p.band.dst_row0) * p.resp_pitch;
     const float2 two = f2(2.f, 2.f);
 
-    // kEdge: the warp touches the left / right image border (clamped
-    // neighbour columns); interior warps run without those selects
+    if (lane == 0) issue(0);
+    next_chunk(0);
+
+    // kEdge: the strip touches the left / right image border (clamped
+    // product columns); interior strips run without those selects
     auto body = [&](auto edge_tag) {
         constexpr bool kEdge = decltype(edge_tag)::value;
-        /// Separable Sobel terms of smem row j: D = in(x+1) - in(x-1),
-        /// S = in(x-1) + 2 in(x) + in(x+1) for columns c .. c+3.
-        /// Source row j as magic floats 2^23 + x in column pairs
-        /// P1=(c-1, c+1) P2=(c, c+2) P3=(c+1, c+3) P4=(c+2, c+4): byte
-        /// permutes only.  Every use below is a difference of two such
-        /// floats, where the 2^23 cancels exactly, so no conversion op.
+        /// Source row j as magic floats 2^23 + x (byte permutes only): pairs
+        /// for i = -1 .. 4.  Every use is a difference of two of them, where
+        /// the 2^23 cancels exactly.
         auto raw_pairs = [&](int j) {
-            const uint8_t* row = tile + j * kHarSW;
-            const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
-            Cols6 q;
-            q.p1 = f2(magic_byte(wl, 3), magic_byte(wc, 1));
-            q.p2 = f2(magic_byte(wc, 0), magic_byte(wc, 2));
-            q.p3 = f2(magic_byte(wc, 1), magic_byte(wc, 3));
-            q.p4 = f2(magic_byte(wc, 2), magic_byte(wr, 0));
-            return q;
+            const uint8_t* row = ring + (j % kHarRing) * kHarSW + off;
+            const uint2 lo = lds64(row - 4), hi = lds64(row + 4); // columns c-4 .. c+3, c+4 .. c+11
+            Raw8 r;
+            r.v[0] = f2(magic_byte(lo.x, 3), magic_byte(lo.y, 3));
+            r.v[1] = f2(magic_byte(lo.y, 0), magic_byte(hi.x, 0));
+            r.v[2] = f2(magic_byte(lo.y, 1), magic_byte(hi.x, 1));
+            r.v[3] = f2(magic_byte(lo.y, 2), magic_byte(hi.x, 2));
+            r.v[4] = f2(magic_byte(lo.y, 3), magic_byte(hi.x, 3));
+            r.v[5] = f2(magic_byte(hi.x, 0), magic_byte(hi.y, 0));
+            return r;
         };
-        /// Sobel-x row term D = in(x+1) - in(x-1) of source row j.
-        auto sobel_d = [&](const Cols6& q) { return Q4{sub2(q.p3, q.p1), sub2(q.p4, q.p2)}; };
+        /// Sobel-x row term D = in(x+1) - in(x-1).
+        auto sobel_d = [&](const Raw8& q) {
+            return Q8{{sub2(q.v[2], q.v[0]), sub2(q.v[3], q.v[1]), sub2(q.v[4], q.v[2]), sub2(q.v[5], q.v[3])}};
+        };
         /// Sobel-y of the row between source rows j and j-2: vertical
         /// difference first, then the 1-2-1 smoothing across columns.
-        auto sobel_y = [&](const Cols6& q, const Cols6& m) {
-            const float2 v1 = sub2(q.p1, m.p1), v2 = sub2(q.p2, m.p2), v3 = sub2(q.p3, m.p3),
-                         v4 = sub2(q.p4, m.p4);
-            return Q4{fma2(two, v2, add2(v1, v3)), fma2(two, v3, add2(v2, v4))};
-        };
-        /// Own columns beyond W-1 take column W-1's value (right border clamp).
-        auto clamp_right = [&](Q4& q) {
-            float v[4] = {q.e.x, q.o.x, q.e.y, q.o.y};
+        auto sobel_y = [&](const Raw8& q, const Raw8& m) {
+            float2 d[6];
 #pragma unroll
-            for (int i = 1; i < 4; ++i)
-                if (i > last) v[i] = v[i - 1];
-            q = Q4{f2(v[0], v[2]), f2(v[1], v[3])};
+            for (int i = 0; i < 6; ++i) d[i] = sub2(q.v[i], m.v[i]);
+            Q8 g;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) g.v[i] = fma2(two, d[i + 1], add2(d[i], d[i + 2]));
+            return g;
         };
-        /// Horizontal 3-sums; neighbour columns c-1 / c+4 come from adjacent lanes.
-        auto hsum = [&](Q4 q) {
-            float pm1 = __shfl_up_sync(0xffffffffu, q.o.y, 1);  // left lane's c+3 = my c-1
-            float p4 = __shfl_down_sync(0xffffffffu, q.e.x, 1); // right lane's c  = my c+4
-            if (kEdge) {
-                pm1 = left_edge ? q.e.x : pm1;
-                p4 = right_edge ? q.o.y : p4;
+        /// Columns beyond W-1 take column W-1's value; at the left border the
+        /// product at column -1 (lane 0's A3) takes column 0's (B0).
+        auto clamp_cols = [&](Q8& q) {
+            if (!kEdge) return;
+            if (last < 7) { // divergent: only the lane holding column W-1 (and idle lanes)
+                float v[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v[i] = q.v[i].x;
+                    v[i + 4] = q.v[i].y;
+                }
+#pragma unroll
+                for (int i = 1; i < 8; ++i)
+                    if (i > last) v[i] = v[i - 1];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) q.v[i] = f2(v[i], v[i + 4]);
             }
-            const float2 t = add2(q.e, q.o);
-            return Q4{add2(t, f2(pm1, q.o.x)), add2(t, f2(q.e.y, p4))};
+            if (x == 0 && lane == 0) q.v[3].x = q.v[0].y;
+        };
+        /// Horizontal 3-sums; columns c-1 / c+8 come from the adjacent lanes.
+        auto hsum = [&](const Q8& q) {
+            const float L = __shfl_up_sync(0xffffffffu, q.v[3].y, 1); // left lane's B3 = my c-1
+            float R = __shfl_down_sync(0xffffffffu, q.v[0].x, 1);     // right lane's A0 = my c+8
+            if (kEdge) R = last <= 7 ? q.v[3].y : R;
+            const float2 sa = add2(q.v[0], q.v[1]), sb = add2(q.v[2], q.v[3]);
+            return Q8{{add2(f2(L, q.v[3].x), sa), add2(sa, q.v[2]), add2(q.v[1], sb), add2(sb, f2(q.v[0].y, R))}};
         };
         /// Products of one Sobel row and their horizontal box sums.
-        auto products = [&](Q4 gx, Q4 gy) {
-            Q4 xx = qmul(gx, gx), yy = qmul(gy, gy), xy = qmul(gx, gy);
-            if (kEdge && right_edge && last < 3) {
-                clamp_right(xx);
-                clamp_right(yy);
-                clamp_right(xy);
-            }
+        auto products = [&](const Q8& gx, const Q8& gy) {
+            Q8 xx = q8mul(gx, gx), yy = q8mul(gy, gy), xy = q8mul(gx, gy);
+            clamp_cols(xx);
+            clamp_cols(yy);
+            clamp_cols(xy);
             return Prod3{hsum(xx), hsum(yy), hsum(xy)};
         };
         /// Threshold decision (and optional exact response) for one output row.
-        auto emit = [&](int orow, const Prod3& V) {
-            const float sxx[4] = {V.xx.e.x, V.xx.o.x, V.xx.e.y, V.xx.o.y};
-            const float syy[4] = {V.yy.e.x, V.yy.o.x, V.yy.e.y, V.yy.o.y};
-            const float sxy[4] = {V.xy.e.x, V.xy.o.x, V.xy.e.y, V.xy.o.y};
-            uint32_t packed = 0;
-            float rv[4];
+        auto emit = [&](const Prod3& V) { // output rows in order, from y0
+            uint32_t ma = 0, mb = 0;
+            float rv[8];
             if constexpr (kResp) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    rv[i] = exact_response(sxx[i], syy[i], sxy[i], p.k);
-                    packed |= (static_cast<double>(rv[i]) > p.threshold ? 255u : 0u) << (8 * i);
+                    rv[i] = exact_response(V.xx.v[i].x, V.yy.v[i].x, V.xy.v[i].x, p.k);
+                    rv[i + 4] = exact_response(V.xx.v[i].y, V.yy.v[i].y, V.xy.v[i].y, p.k);
+                    ma |= (static_cast<double>(rv[i]) > p.threshold ? 255u : 0u) << (8 * i);
+                    mb |= (static_cast<double>(rv[i + 4]) > p.threshold ? 255u : 0u) << (8 * i);
                 }
             } else {
-                // certified fp32 estimate of 81 (resp - T); p1 + p2 <= tt / 2
-                const float2 kn = f2(p.kneg, p.kneg);
+                // certified fp32 estimate of -81 (resp - T):
+                //   nd = k tt - xx yy + (xy^2 + 81 T), bound e = c_tt tt + c0
+                const float2 kk = f2(p.kpos, p.kpos), t81 = f2(p.t81, p.t81);
                 const float2 ctt = f2(p.c_tt, p.c_tt), c0 = f2(p.c0, p.c0);
-                const Q4 tr = qadd(V.xx, V.yy), tt = qmul(tr, tr);
-                // det = xx yy - xy^2 with one rounding less (FMA), error within the bound
-                // with 81 T folded into the xy^2 term: d = xx yy - (xy^2 + 81 T) - k tt
-                const float2 t81 = f2(p.t81, p.t81);
-                const float2 qE = fma2(V.xy.e, V.xy.e, t81), qO = fma2(V.xy.o, V.xy.o, t81);
-                const Q4 det{fma2(V.xx.e, V.yy.e, f2(-qE.x, -qE.y)), fma2(V.xx.o, V.yy.o, f2(-qO.x, -qO.y))};
-                const float2 dE = fma2(kn, tt.e, det.e), dO = fma2(kn, tt.o, det.o);
-                // bound linear in tt: the tr term folded in by tr <= (tt / a + a) / 2 (host picks a)
-                const float2 eE = fma2(ctt, tt.e, c0), eO = fma2(ctt, tt.o, c0);
-                const float d[4] = {dE.x, dO.x, dE.y, dO.y};
-                const float e[4] = {eE.x, eO.x, eE.y, eO.y};
+                float2 nd[4], e[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 tr = add2(V.xx.v[i], V.yy.v[i]);
+                    const float2 tt = mul2(tr, tr);
+                    const float2 w = fma2(V.xy.v[i], V.xy.v[i], t81);
+                    const float2 ndet = fma2(f2(-V.xx.v[i].x, -V.xx.v[i].y), V.yy.v[i], w);
+                    nd[i] = fma2(kk, tt, ndet);
+                    e[i] = fma2(ctt, tt, c0);
+                }
                 bool unsure = false;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    unsure |= !(fabsf(d[i]) > e[i]);
-                    packed |= (d[i] > 0.f ? 255u : 0u) << (8 * i);
+                    unsure |= !(fabsf(nd[i].x) > e[i].x);
+                    unsure |= !(fabsf(nd[i].y) > e[i].y);
                 }
+                // mask byte = sign of nd replicated (nd < 0 <=> resp > T)
+                const uint32_t a01 = sign_bytes(nd[0].x, nd[1].x), a23 = sign_bytes(nd[2].x, nd[3].x);
+                const uint32_t b01 = sign_bytes(nd[0].y, nd[1].y), b23 = sign_bytes(nd[2].y, nd[3].y);
+                ma = __byte_perm(a01, a23, 0x5410);
+                mb = __byte_perm(b01, b23, 0x5410);
                 // rare, warp-uniform: the reference's exact expression where the
                 // estimate cannot decide
                 if (__any_sync(0xffffffffu, unsure)) {
-                    packed = 0;
+                    // one compact loop over this lane's undecided pixels (values
+                    // spilled to a local array: the path is rare and kept small)
+                    unsigned ub = 0;
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        bool on;
-                        if (fabsf(d[i]) > e[i]) on = d[i] > 0.f;
-                        else on = static_cast<double>(exact_response(sxx[i], syy[i], sxy[i], p.k)) > p.threshold;
-                        packed |= (on ? 255u : 0u) << (8 * i);
+                        ub |= (fabsf(nd[i].x) > e[i].x ? 0u : 1u) << i;
+                        ub |= (fabsf(nd[i].y) > e[i].y ? 0u : 1u) << (i + 4);
+                    }
+                    if (ub) {
+                        float buf[24];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            buf[i] = V.xx.v[i].x, buf[i + 4] = V.xx.v[i].y;
+                            buf[8 + i] = V.yy.v[i].x, buf[12 + i] = V.yy.v[i].y;
+                            buf[16 + i] = V.xy.v[i].x, buf[20 + i] = V.xy.v[i].y;
+                        }
+#pragma unroll 1
+                        while (ub) {
+                            const int i = __ffs(ub) - 1;
+                            ub &= ub - 1;
+                            const bool on =
+                                static_cast<double>(exact_response(buf[i], buf[8 + i], buf[16 + i], p.k)) > p.threshold;
+                            const int sh = 8 * (i & 3);
+                            const uint32_t bit = (on ? 255u : 0u) << sh, keep = ~(255u << sh);
+                            if (i < 4) ma = (ma & keep) | bit;
+                            else mb = (mb & keep) | bit;
+                        }
                     }
                 }
                 (void)rv;
             }
-            if (!owner) return;
-            uint8_t* mp = mrow + static_cast<int64_t>(orow) * p.mask_pitch;
-            if (!kEdge || c + 3 < W) {
-                *reinterpret_cast<uint32_t*>(mp) = packed;
-            } else {
+            uint8_t* mp = mrow;
+            mrow += p.mask_pitch;
+            if (!kEdge || c + 7 < W) {
+                if (store_a) *reinterpret_cast<uint32_t*>(mp) = ma;
+                if (store_b) *reinterpret_cast<uint32_t*>(mp + 4) = mb;
+            } else { // the lane holding column W-1 (and lanes past it, which store nothing)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (c + i < W) mp[i] = static_cast<uint8_t>(packed >> (8 * i));
+                for (int i = 0; i < 4; ++i) {
+                    if (store_a && c + i < W) mp[i] = static_cast<uint8_t>(ma >> (8 * i));
+                    if (store_b && c + 4 + i < W) mp[4 + i] = static_cast<uint8_t>(mb >> (8 * i));
+                }
             }
             if constexpr (kResp) {
-                float* rp = reinterpret_cast<float*>(rrow + static_cast<int64_t>(orow) * p.resp_pitch) + c;
-                if (!kEdge || c + 3 < W) {
-                    *reinterpret_cast<float4*>(rp) = make_float4(rv[0], rv[1], rv[2], rv[3]);
+                float* rp = reinterpret_cast<float*>(rrow) + c;
+                rrow += p.resp_pitch;
+                if (!kEdge || c + 7 < W) {
+                    if (store_a) *reinterpret_cast<float4*>(rp) = make_float4(rv[0], rv[1], rv[2], rv[3]);
+                    if (store_b) *reinterpret_cast<float4*>(rp + 4) = make_float4(rv[4], rv[5], rv[6], rv[7]);
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (c + i < W) rp[i] = rv[i];
+                    for (int i = 0; i < 4; ++i) {
+                        if (store_a && c + i < W) rp[i] = rv[i];
+                        if (store_b && c + 4 + i < W) rp[4 + i] = rv[4 + i];
+                    }
                 }
             }
         };
 
-        // Running sums instead of 3-row rings:
+        // Running sums (as v3):
         //   gx(r-1) = Q(r-1) + Q(r) with Q(r) = D(r-1) + D(r)
-        //   gy(r-1) = T(r-1) + T(r) with T(r) = S(r) - S(r-1)
+        //   gy(r-1) = S(r) - S(r-2), taken as vertical differences first
         //   box(m-1) = P(m-1) + H(m) with P(m) = H(m-1) + H(m)
-        // smem row j <-> global y0-2+j; Sobel row j-1 -> product row j-1 ->
-        // output row j-2 (global y0-4+j) once j >= 4.
-        // State of the running sums, in two alternating copies (A, B) so the
+        // virtual row j -> Sobel row j-1 -> product row j-1 -> output row
+        // j-4 once j >= 4.  Two alternating state copies (A, B) so the
         // 2x-unrolled loop renames instead of moving registers.
         struct State {
-            Q4 Dp, Qp;   // D(r-1), Q(r-1)
-            Cols6 Raw;   // raw pairs of the source row this copy last consumed
+            Q8 Dp, Qp;   // D(r-1), Q(r-1)
+            Raw8 Raw;    // source pairs of the row this copy last consumed
             Prod3 P, Hp; // P(m-1), H(m-1)
         };
         State A, B;
         {
             B.Raw = raw_pairs(0); // the copies alternate, so each holds row j-2 when step j reads it
             A.Raw = raw_pairs(1);
-            const Q4 D0 = sobel_d(B.Raw), D1 = sobel_d(A.Raw);
-            A.Qp = qadd(D0, D1);
+            const Q8 D0 = sobel_d(B.Raw), D1 = sobel_d(A.Raw);
+            A.Qp = q8add(D0, D1);
             A.Dp = D1;
         }
         /// Sobel row j-1 from source rows j-2 .. j; writes the successor state into `o`.
         auto sobel_step = [&](int j, const State& i, State& o) {
-            const Cols6 q = raw_pairs(j);
-            const Q4 D = sobel_d(q);
-            const Q4 gy = sobel_y(q, o.Raw); // o.Raw = source row j-2
+            const Raw8 q = raw_pairs(j);
+            const Q8 D = sobel_d(q);
+            const Q8 gy = sobel_y(q, o.Raw); // o.Raw = source row j-2
             o.Raw = q;
-            o.Qp = qadd(i.Dp, D);
+            o.Qp = q8add(i.Dp, D);
             o.Dp = D;
-            return products(qadd(i.Qp, o.Qp), gy);
+            return products(q8add(i.Qp, o.Qp), gy);
         };
         // product rows global y0-1 and y0 (row -1 clamps to row 0 at the top)
         {
@@ -277,21 +407,22 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
         }
         auto full_step = [&](int j, const State& i, State& o) {
             const Prod3 Hn = sobel_step(j, i, o);
-            emit(j - 4, padd(i.P, Hn));
+            emit(padd(i.P, Hn));
             o.P = padd(i.Hp, Hn);
             o.Hp = Hn;
         };
         auto last_step = [&](int j, const State& i, State& o) {
             // product row H clamps to row H-1 at the bottom border
             const Prod3 Hn = sobel_step(j, i, o);
-            emit(j - 4, padd(i.P, (y1 == H) ? i.Hp : Hn));
+            emit(padd(i.P, (y1 == H) ? i.Hp : Hn));
         };
-        const int steps = (y1 - y0) + 4;
         int j = 4;
         for (; j + 2 < steps; j += 2) {
+            if (j % kHarChunk == 0) next_chunk(j / kHarChunk);
             full_step(j, A, B);
             full_step(j + 1, B, A);
         }
+        if (j % kHarChunk == 0) next_chunk(j / kHarChunk);
         if (j + 1 < steps) {
             full_step(j, A, B);
             last_step(j + 1, B, A);
@@ -299,7 +430,9 @@ __global__ void __launch_bounds__(kHarThreads) harris_kernel(const __grid_consta
             last_step(j, A, B);
         }
     };
-    if (__any_sync(0xffffffffu, left_edge || right_edge)) body(std::true_type{});
+    // right border: the product at column x + 248 (right neighbour of the
+    // strip's last output) or any output column lies past W-1
+    if (col_patch || x + kHarCols + 1 > W) body(std::true_type{});
     else body(std::false_type{});
 }
 
@@ -320,10 +453,12 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
                                 : reinterpret_cast<void*>(&harris_kernel<false>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kHarThreads, 0);
-    const long long strips = static_cast<long long>(frames) * ((s.width + kHarTW - 1) / kHarTW);
-    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm) * ctx->sm_count, kHarTH, 4);
+    const long long strips = static_cast<long long>(frames) * ((s.width + kHarCols - 1) / kHarCols);
+    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count,
+                              kHarTHMax, 4);
+    if (const char* e = std::getenv("GVX_HARRIS_TH")) p.th = std::max(8, std::atoi(e)); // tuning experiments
     CUtensorMap map;
-    if (int rc = make_u8_tensor_map(&map, s, kHarSW, p.th + 4)) return rc;
+    if (int rc = make_u8_tensor_map(&map, s, kHarSW, kHarChunk)) return rc;
     p.width = s.width;
     p.band = Band{a->band.row0, a->band.row1, a->band.global_h, a->band.src_row0, a->band.dst_row0};
     p.mask = static_cast<uint8_t*>(a->mask.data);
@@ -336,8 +471,7 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     p.threshold = a->threshold;
     const double ak = a->k < 0 ? -a->k : a->k;
     const double at = a->threshold < 0 ? -a->threshold : a->threshold;
-    p.kabs = static_cast<float>(ak);
-    p.kneg = static_cast<float>(-a->k);
+    p.kpos = static_cast<float>(a->k);
     p.t81 = static_cast<float>(81.0 * a->threshold);
     // rounding perturbation (9 + 18|k|) tr + 40.5 + 81|k| plus the float
     // representation errors of k and 81 T and the final float rounding of
@@ -353,10 +487,9 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     double a_tr = 1.0;
     if (a->threshold > 0 && a->k < 0.24) a_tr = std::sqrt(81.0 * a->threshold / (0.25 - a->k));
     if (!(a_tr >= 1.0) || !std::isfinite(a_tr)) a_tr = 1.0;
-    p.c_tr = static_cast<float>(c_tr);
     p.c_tt = static_cast<float>((c_tt + c_tr / (2.0 * a_tr)) * 1.001);
     p.c0 = static_cast<float>((c_0 + c_tr * a_tr / 2.0) * 1.001 + 1.0);
-    dim3 grid((s.width + kHarTW - 1) / kHarTW, (rows + p.th - 1) / p.th, frames);
+    dim3 grid((s.width + kHarCols - 1) / kHarCols, (rows + p.th - 1) / p.th, frames);
     void* args[] = {&map, &p};
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kHarThreads), args, 0, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "harris kernel launch");
