@@ -78,6 +78,12 @@ public:
     /// FFI form: one image input from raw host memory (other inputs take
     /// the graph's bound values).
     void submit(ObjectId image_input, const void* data, std::size_t bytes);
+    /// As the FFI submit, without the staging copy: `data` must be
+    /// page-locked (gvxb_host_alloc / gvxb_host_register; ErrorCode::BadFormat
+    /// otherwise) and is DMAed to the device directly, so the caller must
+    /// leave it unchanged until this frame's result has been taken by
+    /// next() / next_into() / next_view().
+    void submit_pinned(ObjectId image_input, const void* data, std::size_t bytes);
     /// Report of the oldest submitted frame not yet returned (blocks).
     ExecutionReport next();
     /// As next(), but image output `image_output` is copied straight to

@@ -83,6 +83,12 @@ typedef struct gvxc_pipeline_s* gvxc_pipeline;
 int gvxc_pipeline_create(gvxc_graph g, int naive, int depth, gvxc_pipeline* out);
 int gvxc_pipeline_destroy(gvxc_pipeline p);
 int gvxc_pipeline_submit(gvxc_pipeline p, const uint8_t* in);
+/* As gvxc_pipeline_submit without the staging copy: `in` must be page-locked
+ * (gvxc_host_register) and stay unchanged until the frame's result is taken. */
+int gvxc_pipeline_submit_pinned(gvxc_pipeline p, const uint8_t* in);
+/* Page-lock / release caller memory (cudaHostRegister) for the pinned submit. */
+int gvxc_host_register(void* ptr, size_t bytes);
+int gvxc_host_unregister(void* ptr);
 int gvxc_pipeline_pending(gvxc_pipeline p);
 int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stats, long long counters[4]);
 /* As gvxc_pipeline_next for image-output graphs, without the copy: *view

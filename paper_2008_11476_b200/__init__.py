@@ -114,6 +114,9 @@ def _declare(c, g):
     g.gvxc_pipeline_create.argtypes = [P, I, I, ctypes.POINTER(P)]
     g.gvxc_pipeline_destroy.argtypes = [P]
     g.gvxc_pipeline_submit.argtypes = [P, U8P]
+    g.gvxc_pipeline_submit_pinned.argtypes = [P, U8P]
+    g.gvxc_host_register.argtypes = [P, ctypes.c_size_t]
+    g.gvxc_host_unregister.argtypes = [P]
     g.gvxc_pipeline_pending.argtypes = [P]
     g.gvxc_pipeline_next.argtypes = [P, P, ctypes.POINTER(L), ctypes.POINTER(D), ctypes.POINTER(L)]
     g.gvxc_pipeline_next_view.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(L)]
@@ -315,10 +318,17 @@ class Pipeline:
             _graph.gvxc_pipeline_destroy(self._h)
             self._h = None
 
-    def submit(self, image: np.ndarray):
+    def submit(self, image: np.ndarray, pinned: bool = False):
+        """Copies the frame into the pipeline's page-locked staging, or with
+        `pinned` DMAs it straight from `image` (which must be page-locked,
+        see PinnedHost, and stay unchanged until its result is taken)."""
         img = np.ascontiguousarray(image, dtype=np.uint8)
         assert img.shape == (self.graph.height, self.graph.width)
-        _check_graph(_graph.gvxc_pipeline_submit(self._h, img.ctypes.data))
+        if pinned:
+            assert img.ctypes.data == image.ctypes.data, "a pinned frame must be a contiguous uint8 array"
+            _check_graph(_graph.gvxc_pipeline_submit_pinned(self._h, img.ctypes.data))
+        else:
+            _check_graph(_graph.gvxc_pipeline_submit(self._h, img.ctypes.data))
 
     def pending(self) -> int:
         return _graph.gvxc_pipeline_pending(self._h)
@@ -351,6 +361,39 @@ class Pipeline:
         if self.graph.cfg == 4:
             return (np.array(list(hist), np.int64), stats[0], stats[1]), cnt
         return out, cnt
+
+
+class PinnedHost:
+    """Page-locks (cudaHostRegister) the memory of host arrays for the
+    lifetime of the object, so Pipeline.submit(..., pinned=True) DMAs from
+    them directly; releases them on close()."""
+
+    def __init__(self, arrays):
+        _load()
+        self._ptrs = []
+        try:
+            for a in arrays:
+                assert a.flags["C_CONTIGUOUS"]
+                _check_graph(_graph.gvxc_host_register(a.ctypes.data, a.nbytes))
+                self._ptrs.append(a.ctypes.data)
+        except BaseException:
+            self.close()
+            raise
+
+    def close(self):
+        for p in self._ptrs:
+            _graph.gvxc_host_unregister(p)
+        self._ptrs = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        if getattr(self, "_ptrs", None):
+            self.close()
 
 
 class Session:

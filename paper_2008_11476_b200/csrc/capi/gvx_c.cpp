@@ -333,6 +333,21 @@ int gvxc_pipeline_submit(gvxc_pipeline p, const uint8_t* in) {
     });
 }
 
+int gvxc_pipeline_submit_pinned(gvxc_pipeline p, const uint8_t* in) {
+    return guarded([&] {
+        p->p->submit_pinned(p->g->cg.input, in,
+                            static_cast<std::size_t>(p->g->width) * static_cast<std::size_t>(p->g->height));
+    });
+}
+
+int gvxc_host_register(void* ptr, size_t bytes) {
+    return guarded([&] { gvx::dev::check(gvxb_host_register(ptr, bytes), "host register"); });
+}
+
+int gvxc_host_unregister(void* ptr) {
+    return guarded([&] { gvx::dev::check(gvxb_host_unregister(ptr), "host unregister"); });
+}
+
 int gvxc_pipeline_pending(gvxc_pipeline p) { return p->p->pending(); }
 
 int gvxc_pipeline_next_view(gvxc_pipeline p, const void** view, size_t* bytes, long long counters[4]) {

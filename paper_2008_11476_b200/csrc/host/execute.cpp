@@ -1416,15 +1416,25 @@ struct HostPipeline::Impl {
         ready.push_back(std::move(r));
     }
 
-    void upload_image(Slot& sl, ObjectId id, const void* data, std::size_t bytes) {
+    /// Stages the frame through the slot's page-locked buffer, or (direct)
+    /// DMAs it from the caller's page-locked memory.
+    void upload_image(Slot& sl, ObjectId id, const void* data, std::size_t bytes, bool direct = false) {
         const dev::ObjInfo& oi = prog->objects.at(id);
         const std::size_t row = static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format);
         const std::size_t n = row * static_cast<std::size_t>(oi.desc.height);
         if (bytes < n) throw Error(ErrorCode::ShapeMismatch, "image payload too small", id);
-        void* pin = staging(sl, id, n);
-        dev::parallel_copy(pin, data, n, /*streaming=*/true);
+        const void* from = data;
+        if (direct) {
+            int pinned = 0;
+            dev::check(gvxb_host_is_pinned(data, &pinned), "pinned query");
+            if (!pinned) throw Error(ErrorCode::BadFormat, "submit_pinned: input is not page-locked host memory", id);
+        } else {
+            void* pin = staging(sl, id, n);
+            dev::parallel_copy(pin, data, n, /*streaming=*/true);
+            from = pin;
+        }
         DeviceSession::Impl::Store& st = sl.s.ensure(id);
-        dev::check(gvxb_upload_2d(sl.s.ctx, st.ptr, static_cast<std::size_t>(st.pitch), pin, row, row,
+        dev::check(gvxb_upload_2d(sl.s.ctx, st.ptr, static_cast<std::size_t>(st.pitch), from, row, row,
                                   static_cast<std::size_t>(oi.desc.height)),
                    "pipeline upload");
     }
@@ -1440,7 +1450,7 @@ struct HostPipeline::Impl {
         return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t).count();
     }
 
-    void submit_raw(ObjectId id, const void* data, std::size_t bytes) {
+    void submit_raw(ObjectId id, const void* data, std::size_t bytes, bool direct = false) {
         static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
         const auto t0 = std::chrono::steady_clock::now();
         InputMap none;
@@ -1460,7 +1470,7 @@ struct HostPipeline::Impl {
                 throw Error(ErrorCode::MissingInput, "the raw-pointer submit takes a graph with one image input", oid);
             sl.s.upload(oid, *b, 0);
         }
-        if (prog->objects.count(id)) upload_image(sl, id, data, bytes);
+        if (prog->objects.count(id)) upload_image(sl, id, data, bytes, direct);
         const double t_up = trace ? us_since(t0) : 0;
         launch_slot(sl);
         if (trace)
@@ -1526,6 +1536,10 @@ void HostPipeline::submit(const InputMap& inputs) { impl_->submit(inputs); }
 
 void HostPipeline::submit(ObjectId image_input, const void* data, std::size_t bytes) {
     impl_->submit_raw(image_input, data, bytes);
+}
+
+void HostPipeline::submit_pinned(ObjectId image_input, const void* data, std::size_t bytes) {
+    impl_->submit_raw(image_input, data, bytes, /*direct=*/true);
 }
 
 ExecutionReport HostPipeline::next_into(ObjectId image_output, void* dst, std::size_t bytes) {

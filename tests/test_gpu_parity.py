@@ -169,3 +169,25 @@ def test_host_pipeline_views(gvx, oracle_mod):
         got.append(np.array(v))
     for r, f in zip(got, frames):
         assert np.array_equal(r, oracle_mod.port_run(2, f))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_host_pipeline_pinned_inputs(cfg, gvx, oracle_mod):
+    """submit(pinned=True): frames DMAed straight from registered host memory
+    give the same results as staged submits; unregistered memory is refused."""
+    w, h = 517, 333
+    g = gvx.ConfigGraph(cfg, w, h)
+    stack = np.stack([gvx.random_u8(w, h, 120 + i) for i in range(5)])
+    pl = gvx.Pipeline(g, depth=3)
+    with gvx.PinnedHost([stack]):
+        got = []
+        for f in stack:
+            if pl.pending() >= 3:
+                got.append(pl.next())
+            pl.submit(f, pinned=True)
+        while pl.pending():
+            got.append(pl.next())
+    for (r, _), f in zip(got, stack):
+        assert _same(cfg, r, oracle_mod.port_run(cfg, f))
+    with pytest.raises(gvx.GraphvxError):
+        pl.submit(gvx.random_u8(w, h, 7), pinned=True)
