@@ -202,41 +202,44 @@ def run_frames(args, cfg, rank, world, local_rank):
     host = make_frames(gvx, w, h, F, gvx.CONFIG_SEED[cfg] + 97 * rank)
     # end to end through the public API (host buffers in and out, H2D + D2H
     # inside), measured first, on a quiet device
-    e2e_frames = max(1, args.e2e_frames)
-    # frames stream through gvx::HostPipeline: frame k+1's upload, frame k's
-    # kernels and frame k-1's download overlap; every result is read back
-    depth = 3  # measured best of 2 / 3 / 4 / 6
-    pipe = gvx.Pipeline(graph, depth=depth)
-    out_host = graph.output_array()
-    # the input frames live in page-locked host memory (registered once,
-    # outside the timed region): every frame is still DMAed host->device
-    # inside it, without a staging copy
-    pinned = gvx.PinnedHost([host])
-    for i in range(max(depth + 1, F)):  # warm: staging, contexts, modules, every registered frame's first DMA
-        if pipe.pending() >= depth:
-            pipe.next(out_host)
-        pipe.submit(host[i % F], pinned=True)
-    while pipe.pending():
-        pipe.next(out_host)
-    view = cfg != 4  # image results are read in place from page-locked staging
-    for rep in range(2):  # rep 0: untimed warm-up pass of the same loop
-        barrier()
-        t0 = time.perf_counter()
-        for i in range(e2e_frames):
+    # --e2e-frames 0 (profiling runs only) skips this leg
+    e2e_frames = args.e2e_frames
+    e2e = None
+    if e2e_frames > 0:
+        # frames stream through gvx::HostPipeline: frame k+1's upload, frame k's
+        # kernels and frame k-1's download overlap; every result is read back
+        depth = 3  # measured best of 2 / 3 / 4 / 6
+        pipe = gvx.Pipeline(graph, depth=depth)
+        out_host = graph.output_array()
+        # the input frames live in page-locked host memory (registered once,
+        # outside the timed region): every frame is still DMAed host->device
+        # inside it, without a staging copy
+        pinned = gvx.PinnedHost([host])
+        for i in range(max(depth + 1, F)):  # warm: staging, contexts, modules, every registered frame's first DMA
             if pipe.pending() >= depth:
-                pipe.next_view() if view else pipe.next(out_host)
+                pipe.next(out_host)
             pipe.submit(host[i % F], pinned=True)
         while pipe.pending():
-            pipe.next_view() if view else pipe.next(out_host)
-    e2e_s = allreduce_max(time.perf_counter() - t0)
-    e2e_value = w * h * e2e_frames * world / e2e_s / 1e6
-    out_b = {1: 2, 2: 1, 3: 1, 4: 256 * 8 + 16, 5: 2}[cfg]
-    e2e = {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": w * h,
-           "d2h_bytes_per_step": out_b * (w * h if cfg != 4 else 1), "frames": e2e_frames,
-           "path": "gvx::HostPipeline (run_plan semantics, 3 frames in flight) via gvx_c.h: page-locked host "
-                   "frame in (DMA, no staging copy), host result out, in submission order"}
-    del pipe
-    pinned.close()
+            pipe.next(out_host)
+        view = cfg != 4  # image results are read in place from page-locked staging
+        for rep in range(2):  # rep 0: untimed warm-up pass of the same loop
+            barrier()
+            t0 = time.perf_counter()
+            for i in range(e2e_frames):
+                if pipe.pending() >= depth:
+                    pipe.next_view() if view else pipe.next(out_host)
+                pipe.submit(host[i % F], pinned=True)
+            while pipe.pending():
+                pipe.next_view() if view else pipe.next(out_host)
+        e2e_s = allreduce_max(time.perf_counter() - t0)
+        e2e_value = w * h * e2e_frames * world / e2e_s / 1e6
+        out_b = {1: 2, 2: 1, 3: 1, 4: 256 * 8 + 16, 5: 2}[cfg]
+        e2e = {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": w * h,
+               "d2h_bytes_per_step": out_b * (w * h if cfg != 4 else 1), "frames": e2e_frames,
+               "path": "gvx::HostPipeline (run_plan semantics, 3 frames in flight) via gvx_c.h: page-locked host "
+                       "frame in (DMA, no staging copy), host result out, in submission order"}
+        del pipe
+        pinned.close()
 
     for b in range(2):
         din = dev.alloc(in_bytes)
