@@ -52,10 +52,9 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const CUtensorMap* 
             if (gy < 0 || gy >= band.global_h) continue;
             uint8_t* row = tile + r * SW;
             const uint8_t vf = row[first], vl = row[last];
-            for (int j = ln; j < SW; j += 32) {
-                if (j < first) row[j] = vf;
-                else if (j > last) row[j] = vl;
-            }
+            // only the patched columns: [0, first) and (last, SW)
+            for (int j = ln; j < first; j += 32) row[j] = vf;
+            for (int j = last + 1 + ln; j < SW; j += 32) row[j] = vl;
         }
         __syncthreads();
     }
