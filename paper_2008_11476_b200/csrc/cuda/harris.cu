@@ -108,7 +108,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 template <bool kResp>
-__global__ void __launch_bounds__(kHarThreads, 12) harris_kernel(const __grid_constant__ CUtensorMap map,
+#ifndef GVX_HARRIS_MINB
+#define GVX_HARRIS_MINB 12 // resident one-warp CTAs per SM: 3 per scheduler at <= 168 registers
+#endif
+__global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(const __grid_constant__ CUtensorMap map,
                                                                  HarrisParams p) {
     __shared__ alignas(128) uint8_t ring[kHarRing * kHarSW];
     __shared__ uint64_t bar[2];
