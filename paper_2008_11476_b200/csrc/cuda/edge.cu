@@ -23,6 +23,8 @@
 // output written once: 1 B in + 2 B out per output pixel.
 #include "packed.cuh"
 
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace gvxd {
@@ -307,6 +309,7 @@ extern "C" int gvxb_edge(gvxb_ctx ctx, const gvxb_edge_args* a) {
     const long long strips = static_cast<long long>(frames) * ((s.width + kEdgeTW - 1) / kEdgeTW);
     EdgeParams p;
     p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm) * ctx->sm_count, kEdgeTH, 4);
+    if (const char* e = std::getenv("GVX_EDGE_TH")) p.th = std::max(8, std::min(kEdgeTH, std::atoi(e))); // tuning experiments
     CUtensorMap map;
     if (int rc = make_u8_tensor_map(&map, s, kEdgeSW, p.th + 4)) return rc;
     p.width = s.width;

@@ -16,6 +16,7 @@
 #include "packed.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace gvxd {
@@ -295,7 +296,10 @@ constexpr int kSepThreads = 96;
 constexpr int kSepTW = 4 * kSepThreads; // 384 columns: 4K / 8K / 1080p split evenly
 constexpr int kSepSW = kSepTW + 32;     // tile origin x0 - 16 (16-byte aligned TMA start)
 constexpr int kSepTHMax = 48;  // measured best of 32 / 48 / 64 (cfg3)
-constexpr int kSepHistTH = 24;          // u8 counters: 4 px * rows <= 255; measured best (16..63)
+#ifndef GVX_SEP_HIST_TH
+#define GVX_SEP_HIST_TH 48
+#endif
+constexpr int kSepHistTH = GVX_SEP_HIST_TH; // u8 counters: 4 px * rows <= 255; measured best (24..60): 4 CTAs / SM
 constexpr int kSepHistBytes = 256 * 32 * 4;
 
 struct SepParams {
@@ -663,6 +667,7 @@ int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K,
     const long long strips = static_cast<long long>((s.width + kSepTW - 1) / kSepTW) * frames;
     p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, th_max,
                               K - 1);
+    if (const char* e = std::getenv("GVX_SEP_TH")) p.th = std::max(8, std::min(th_max, std::atoi(e))); // tuning experiments
     CUtensorMap map;
     if (int rc = make_u8_tensor_map(&map, s, kSepSW, p.th + K - 1)) return rc;
     dim3 grid((s.width + kSepTW - 1) / kSepTW, (rows + p.th - 1) / p.th, frames);
