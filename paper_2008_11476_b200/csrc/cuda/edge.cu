@@ -32,7 +32,10 @@ namespace gvxd {
 constexpr int kEdgeThreads = 128;
 constexpr int kEdgeWarpCols = 120;
 constexpr int kEdgeTW = kEdgeWarpCols * (kEdgeThreads / 32); // 480
-constexpr int kEdgeTH = 40; // measured best of 24..64 (occupancy vs halo rows)
+#ifndef GVX_EDGE_TH_MAX
+#define GVX_EDGE_TH_MAX 40
+#endif
+constexpr int kEdgeTH = GVX_EDGE_TH_MAX; // measured best of 24..64 (occupancy vs halo rows)
 constexpr int kEdgeSW = kEdgeTW + 32; // smem columns [x0 - 16, x0 + 496)
 constexpr int kEdgeSH = kEdgeTH + 4;  // smem rows    [y0 - 2, y0 + 66)
 

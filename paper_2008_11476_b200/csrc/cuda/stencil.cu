@@ -295,7 +295,10 @@ __global__ void meanstd_finalize_kernel(const unsigned long long* sum, const uns
 constexpr int kSepThreads = 96;
 constexpr int kSepTW = 4 * kSepThreads; // 384 columns: 4K / 8K / 1080p split evenly
 constexpr int kSepSW = kSepTW + 32;     // tile origin x0 - 16 (16-byte aligned TMA start)
-constexpr int kSepTHMax = 48;  // measured best of 32 / 48 / 64 (cfg3)
+#ifndef GVX_SEP_TH_MAX
+#define GVX_SEP_TH_MAX 48
+#endif
+constexpr int kSepTHMax = GVX_SEP_TH_MAX; // measured best of 32 / 48 / 64 (cfg3)
 #ifndef GVX_SEP_HIST_TH
 #define GVX_SEP_HIST_TH 48
 #endif
