@@ -208,7 +208,7 @@ def run_frames(args, cfg, rank, world, local_rank):
     if e2e_frames > 0:
         # frames stream through gvx::HostPipeline: frame k+1's upload, frame k's
         # kernels and frame k-1's download overlap; every result is read back
-        depth = 3  # measured best of 2 / 3 / 4 / 6
+        depth = int(os.environ.get("GVX_E2E_DEPTH", 3))  # frames in flight; measured best of 2 / 3 / 4 / 6
         pipe = gvx.Pipeline(graph, depth=depth)
         out_host = graph.output_array()
         # the input frames live in page-locked host memory (registered once,
