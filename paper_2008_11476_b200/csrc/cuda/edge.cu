@@ -297,6 +297,10 @@ void* pick_edge(bool ox, bool oy, bool om) {
 
 } // namespace
 
+namespace gvxb_impl {
+int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a); // edge8.cu
+}
+
 extern "C" int gvxb_edge(gvxb_ctx ctx, const gvxb_edge_args* a) {
     using namespace gvxb_impl;
     const gvxb_image& s = a->src;
@@ -306,6 +310,10 @@ extern "C" int gvxb_edge(gvxb_ctx ctx, const gvxb_edge_args* a) {
     if (!fn) return GVXB_OK; // nothing requested
     const int rows = a->band.row1 - a->band.row0;
     if (rows <= 0 || s.width <= 0) return GVXB_OK;
+    // Gaussian graphs run the one-warp / 8-column kernel (edge8.cu);
+    // GVX_EDGE_V2=1 selects this file's 4-warp tiled kernel (A/B tests)
+    static const bool v2 = std::getenv("GVX_EDGE_V2") != nullptr;
+    if (a->with_gauss && !v2) return edge8_launch(ctx, a);
     const int frames = s.frames > 0 ? s.frames : 1;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEdgeThreads, 0);

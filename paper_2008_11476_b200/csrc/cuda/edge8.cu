@@ -1,0 +1,415 @@
+// K1 v3 — fused Gaussian3x3 -> Sobel3x3 -> {gx, gy, Magnitude} (U8 -> S16)
+// in the layout of the Harris kernel: one warp per CTA, 8 columns per lane,
+// source rows streamed through a TMA row ring, long row bands.
+//
+// Reference semantics, exactly as edge.cu:
+//   gaussian3x3  floor((s + 8) / 16), s <= 4080   (ref:src/registry.cpp:722-746)
+//   sobel_x/y    sat_S16(sum(mask * win)), |v| <= 1020 (ref:src/registry.cpp:748-784)
+//   magnitude    sat_S16(llround(sqrt(gx^2 + gy^2))) (ref:src/registry.cpp:555-575)
+//   Clamp of the intermediate: the Gaussian at an out-of-image position is
+//   the Gaussian of the clamped position (ref:src/execute.cpp:242-245).
+//
+// Layout: a strip of 248 output columns per warp; lane L holds columns
+// c = x - 4 + 8L .. c + 7 as four float2 pairs (A_i, B_i) = (c+i, c+4+i), so
+// every 3-tap step is a packed op on register pairs; only lane 0's A half
+// and lane 31's B half are halo.  Per source row j (virtual row j <-> global
+// row y0 - 2 + j):
+//   Hg(j)       horizontal 1-2-1 of the source bytes, each held as the float
+//               1 + (x + 1/2) / 2^15 straight from a byte permute (the
+//               half-biases carry the +8 of the rounding through the sums)
+//   G(j-1)      = fma_rd(Hg(j-2) + 2 Hg(j-1) + Hg(j), 2^11, 1.5*2^23 - 2^15)
+//               = 1.5*2^23 + floor((S + 8) / 16), kept in this magic form
+//               (running sums R = Hg(j-1) + Hg(j))
+//   gx(j-2)     = Q(j-2) + Q(j-1), Q(m) = D(m-1) + D(m), D = G(x+1) - G(x-1)
+//   gy(j-2)     = horizontal 1-2-1 of G(j-1) - G(j-3) (the magic cancels)
+// so output row j - 4 is emitted at step j.  Every quantity is an integer
+// (or, before rounding, a half-integer) below 2^24: exact in fp32.
+#include "packed.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+namespace gvxd {
+
+constexpr int kE8Threads = 32;  // one warp per CTA
+constexpr int kE8Cols = 248;    // output columns per strip
+constexpr int kE8SW = 288;      // ring row bytes: image columns [x_org, x_org + 288)
+constexpr int kE8Chunk = 16;    // rows per TMA chunk
+constexpr int kE8Ring = 2 * kE8Chunk;
+constexpr int kE8THMax = 64;    // band rows (many short bands balance best, as for Harris)
+
+struct E8Plane {
+    int16_t* data;
+    int64_t pitch, frame_stride; // bytes
+};
+
+struct Edge8Params {
+    int width;
+    int th;
+    Band band;
+    E8Plane gx, gy, mag;
+};
+
+struct P8 {
+    float2 v[4]; // (c+i, c+4+i)
+};
+/// Six pairs for i = -1 .. 4 at v[i + 1]: columns (c+i, c+4+i).
+struct P12 {
+    float2 v[6];
+};
+
+__device__ __forceinline__ float e8_sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+/// round(sqrt(n)) half away from zero for integer-valued 0 <= n < 2^22, in
+/// magic form 1.5*2^23 + k (low 16 bits = k): k0 = rn(s - 0.01) is k* or
+/// k* - 1 for the approximate root s, and k* = k0 + (n > k0^2 + k0).
+__device__ __forceinline__ float2 e8_round_sqrt(float2 n) {
+    const float2 M = f2(12582912.f, 12582912.f), nM = f2(-12582912.f, -12582912.f);
+    const float2 d = f2(-0.01f, -0.01f);
+    const float2 s = f2(e8_sqrt_approx(n.x), e8_sqrt_approx(n.y));
+    float2 km = add2(add2(s, d), M); // 1.5*2^23 + k0
+    const float2 k = add2(km, nM);
+    const float2 kk = fma2(k, k, k);
+    km.x += n.x > kk.x ? 1.f : 0.f;
+    km.y += n.y > kk.y ? 1.f : 0.f;
+    return km;
+}
+
+/// 1 + (byte k of w + 1/2) / 2^15: the byte lands in mantissa bits 8..15 and
+/// the constant supplies exponent 0 and the half (bit 7).  Sums of up to 2^8
+/// such values stay exact (all multiples of 2^-16 below 2^8).
+__device__ __forceinline__ float frac_byte(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x3F800080u, 0x7604u | (static_cast<unsigned>(k) << 4)));
+}
+
+/// Integer-valued floats |v| < 2^22 as two int16 in a u32.
+__device__ __forceinline__ uint32_t e8_pack(float lo, float hi) {
+    const float m = 12582912.f;
+    return __byte_perm(__float_as_uint(lo + m), __float_as_uint(hi + m), 0x5410);
+}
+/// Magic-form values (1.5*2^23 + v) as two int16 in a u32.
+__device__ __forceinline__ uint32_t e8_pack_magic(float lo, float hi) {
+    return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x5410);
+}
+
+template <bool kGx, bool kGy, bool kMag>
+#ifndef GVX_EDGE8_MINB
+#define GVX_EDGE8_MINB 1
+#endif
+__global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const __grid_constant__ CUtensorMap map, Edge8Params p) {
+    __shared__ alignas(128) uint8_t ring[kE8Ring * kE8SW];
+    __shared__ uint64_t bar[2];
+
+    const int lane = threadIdx.x;
+    const int x = max(0, min(static_cast<int>(blockIdx.x) * kE8Cols, ((p.width + 7) & ~7) - kE8Cols));
+    const int x_org = ((x - 5) >> 4) << 4; // ring column 0 (16-byte aligned TMA origin)
+    const int y0 = p.band.row0 + blockIdx.y * p.th;
+    const int y1 = min(y0 + p.th, p.band.row1);
+    const int frame = blockIdx.z;
+    const int H = p.band.global_h;
+    const int W = p.width;
+    const int steps = (y1 - y0) + 4;
+    const int nchunks = (steps + kE8Chunk - 1) / kE8Chunk;
+
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+
+    auto issue = [&](int k) {
+        uint64_t* b = &bar[k & 1];
+        mbar_expect_tx(b, kE8Chunk * kE8SW);
+        tma_load_3d(ring + (k & 1) * kE8Chunk * kE8SW, &map, b, x_org / 4, y0 - 2 + kE8Chunk * k - p.band.src_row0,
+                    frame);
+    };
+    const bool col_patch = x_org < 0 || x_org + kE8SW > W;
+    bool dirty = false;
+    auto patch = [&](int k) {
+        uint8_t* base = ring + (k & 1) * kE8Chunk * kE8SW;
+        const int g0 = y0 - 2 + kE8Chunk * k;
+        const bool rows = g0 < 0 || g0 + kE8Chunk > H;
+        if (col_patch) {
+            const int first = clampi(-x_org, 0, kE8SW - 1), lastc = clampi(W - 1 - x_org, 0, kE8SW - 1);
+            for (int r = 0; r < kE8Chunk; ++r) {
+                uint8_t* row = base + r * kE8SW;
+                if (lane < first) row[lane] = row[first];
+                for (int j = lastc + 1 + lane; j < kE8SW; j += 32) row[j] = row[lastc];
+            }
+            __syncwarp();
+        }
+        if (rows) {
+            for (int r = 0; r < kE8Chunk; ++r) {
+                const int gy = g0 + r;
+                if ((gy >= 0 && gy < H) || kE8Chunk * k + r >= steps) continue;
+                const int v = clampi(gy, 0, H - 1) - (y0 - 2);
+                const uint32_t* from = reinterpret_cast<const uint32_t*>(ring + (v % kE8Ring) * kE8SW);
+                uint32_t* to = reinterpret_cast<uint32_t*>(base + r * kE8SW);
+                for (int j = lane; j < kE8SW / 4; j += 32) to[j] = from[j];
+            }
+            __syncwarp();
+        }
+        return col_patch || rows;
+    };
+    auto next_chunk = [&](int k) {
+        mbar_wait(&bar[k & 1], (k >> 1) & 1);
+        const bool patched = patch(k);
+        if (lane == 0 && k + 1 < nchunks) {
+            if (dirty) fence_proxy_async_smem();
+            issue(k + 1);
+        }
+        dirty = patched;
+    };
+
+    const int c = x - 4 + 8 * lane;
+    const int off = c - x_org; // 4 <= off, off % 8 == 4
+    const int last = W - 1 - c;
+    const bool store_a = lane > 0 && c < W;
+    const bool store_b = lane < 31 && c + 4 < W;
+    auto out_row = [&](const E8Plane& o) {
+        return reinterpret_cast<char*>(o.data) + frame * o.frame_stride +
+               static_cast<int64_t>(y0 - p.band.dst_row0) * o.pitch + 2 * static_cast<int64_t>(c);
+    };
+    char* pgx = kGx ? out_row(p.gx) : nullptr;
+    char* pgy = kGy ? out_row(p.gy) : nullptr;
+    char* pmag = kMag ? out_row(p.mag) : nullptr;
+
+    if (lane == 0) issue(0);
+    next_chunk(0);
+
+    auto body = [&](auto edge_tag) {
+        constexpr bool kEdge = decltype(edge_tag)::value;
+        /// Source row j in fractional form 1 + (x + 1/2) / 2^15 (byte permutes
+        /// only): pairs for i = -1 .. 4.
+        auto src_pairs = [&](int j) {
+            const uint8_t* row = ring + (j % kE8Ring) * kE8SW + off;
+            const uint2 lo = *reinterpret_cast<const uint2*>(row - 4), hi = *reinterpret_cast<const uint2*>(row + 4);
+            P12 r;
+            r.v[0] = f2(frac_byte(lo.x, 3), frac_byte(lo.y, 3));
+            r.v[1] = f2(frac_byte(lo.y, 0), frac_byte(hi.x, 0));
+            r.v[2] = f2(frac_byte(lo.y, 1), frac_byte(hi.x, 1));
+            r.v[3] = f2(frac_byte(lo.y, 2), frac_byte(hi.x, 2));
+            r.v[4] = f2(frac_byte(lo.y, 3), frac_byte(hi.x, 3));
+            r.v[5] = f2(frac_byte(hi.x, 0), frac_byte(hi.y, 0));
+            return r;
+        };
+        const float2 two = f2(2.f, 2.f);
+        /// Horizontal 1-2-1: 4 + (s + 2) / 2^15 (the four half-biases).
+        auto smooth = [&](const P12& q) {
+            P8 h;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h.v[i] = fma2(two, q.v[i + 1], add2(q.v[i], q.v[i + 2]));
+            return h;
+        };
+        /// Gaussian columns beyond W-1 take column W-1's value; column -1
+        /// (lane 0's A3 in the first strip) takes column 0's (B0).
+        auto clamp_cols = [&](P8& g) {
+            if (!kEdge) return;
+            if (last < 7) {
+                float v[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v[i] = g.v[i].x;
+                    v[i + 4] = g.v[i].y;
+                }
+#pragma unroll
+                for (int i = 1; i < 8; ++i)
+                    if (i > last) v[i] = v[i - 1];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) g.v[i] = f2(v[i], v[i + 4]);
+            }
+            if (x == 0 && lane == 0) g.v[3].x = g.v[0].y;
+        };
+        /// Gaussian row pairs for i = -1 .. 4 (columns c-1 / c+8 from the
+        /// neighbour lanes; clamped at the image border).
+        auto neighbourhood = [&](const P8& g) {
+            const float L = __shfl_up_sync(0xffffffffu, g.v[3].y, 1);
+            float R = __shfl_down_sync(0xffffffffu, g.v[0].x, 1);
+            if (kEdge) R = last <= 7 ? g.v[3].y : R;
+            return P12{{f2(L, g.v[3].x), g.v[0], g.v[1], g.v[2], g.v[3], f2(g.v[0].y, R)}};
+        };
+        auto emit = [&](const P8& gx, const P8& gy) {
+            const bool full = !kEdge || c + 7 < W;
+            auto put = [&](char* base, uint32_t a01, uint32_t a23, uint32_t b01, uint32_t b23) {
+                if (full) {
+                    if (store_a) *reinterpret_cast<uint2*>(base) = make_uint2(a01, a23);
+                    if (store_b) *reinterpret_cast<uint2*>(base + 8) = make_uint2(b01, b23);
+                } else {
+                    const uint32_t w[4] = {a01, a23, b01, b23};
+                    int16_t* q = reinterpret_cast<int16_t*>(base);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const bool mine = i < 4 ? store_a : store_b;
+                        if (mine && c + i < W) q[i] = static_cast<int16_t>(w[i >> 1] >> (16 * (i & 1)));
+                    }
+                }
+            };
+            if (kGx) {
+                put(pgx, e8_pack(gx.v[0].x, gx.v[1].x), e8_pack(gx.v[2].x, gx.v[3].x), e8_pack(gx.v[0].y, gx.v[1].y),
+                    e8_pack(gx.v[2].y, gx.v[3].y));
+                pgx += p.gx.pitch;
+            }
+            if (kGy) {
+                put(pgy, e8_pack(gy.v[0].x, gy.v[1].x), e8_pack(gy.v[2].x, gy.v[3].x), e8_pack(gy.v[0].y, gy.v[1].y),
+                    e8_pack(gy.v[2].y, gy.v[3].y));
+                pgy += p.gy.pitch;
+            }
+            if (kMag) {
+                float2 m[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) m[i] = e8_round_sqrt(fma2(gx.v[i], gx.v[i], mul2(gy.v[i], gy.v[i])));
+                put(pmag, e8_pack_magic(m[0].x, m[1].x), e8_pack_magic(m[2].x, m[3].x), e8_pack_magic(m[0].y, m[1].y),
+                    e8_pack_magic(m[2].y, m[3].y));
+                pmag += p.mag.pitch;
+            }
+        };
+
+        // State of the running sums; two alternating copies (A, B) so the
+        // 2x-unrolled loop renames instead of moving registers.
+        struct State {
+            P8 Hp, Rp;  // Hg(j-1), Hg(j-2) + Hg(j-1)
+            P8 Dp, Qp;  // D(m), Q(m) of the newest Gaussian row
+            P12 Gn;     // Gaussian neighbourhood of the row this copy last produced
+        };
+        State A, B;
+        // 16 + (S + 8) / 2^15 -> 1.5*2^23 + floor((S + 8) / 16): exact scaling by
+        // 2^11, one rounding (down) of the sum with 1.5*2^23 - 2^15
+        const float2 sc = f2(2048.f, 2048.f), M = f2(12550144.f, 12550144.f);
+        /// Source row j -> Gaussian row j-1 (magic form, clamped columns).
+        auto gauss_step = [&](int j, const State& i, State& o) {
+            const P8 h = smooth(src_pairs(j));
+            P8 g;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                o.Rp.v[t] = add2(i.Hp.v[t], h.v[t]);
+                g.v[t] = __ffma2_rd(add2(i.Rp.v[t], o.Rp.v[t]), sc, M);
+            }
+            o.Hp = h;
+            clamp_cols(g);
+            return neighbourhood(g);
+        };
+        auto diff = [&](const P12& n) {
+            P8 d;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) d.v[t] = sub2(n.v[t + 2], n.v[t]);
+            return d;
+        };
+        /// gy of the row between Gaussian rows n (newer) and m (two older).
+        auto grad_y = [&](const P12& n, const P12& m) {
+            float2 d[6];
+#pragma unroll
+            for (int t = 0; t < 6; ++t) d[t] = sub2(n.v[t], m.v[t]);
+            P8 g;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) g.v[t] = fma2(two, d[t + 1], add2(d[t], d[t + 2]));
+            return g;
+        };
+        // prologue: Hg rows 0, 1; Gaussian rows y0-1 (j = 2) and y0 (j = 3)
+        {
+            const P8 h0 = smooth(src_pairs(0)), h1 = smooth(src_pairs(1));
+#pragma unroll
+            for (int t = 0; t < 4; ++t) A.Rp.v[t] = add2(h0.v[t], h1.v[t]);
+            A.Hp = h1;
+        }
+        P12 G1 = gauss_step(2, A, B); // Gaussian row y0-1
+        P12 G2 = gauss_step(3, B, A); // Gaussian row y0
+        if (y0 == 0) G1 = G2;          // Gaussian row -1 clamps to row 0
+        {
+            const P8 D1 = diff(G1), D2 = diff(G2);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) A.Qp.v[t] = add2(D1.v[t], D2.v[t]);
+            A.Dp = D2;
+            A.Gn = G2; // newest row
+            B.Gn = G1; // the copy read at the next step holds the row two back
+        }
+        /// Step j: Gaussian row j-1 -> Sobel / outputs of row j-4 (global).
+        /// `bottom`: Gaussian row j-1 is row H, which clamps to row H-1.
+        auto full_step = [&](int j, State& i, State& o, bool bottom) {
+            P12 Gn = gauss_step(j, i, o);
+            if (bottom) Gn = i.Gn;
+            const P8 D = diff(Gn);
+            const P8 gy = grad_y(Gn, o.Gn); // o.Gn = Gaussian row j-3
+            P8 Q, gx;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                Q.v[t] = add2(i.Dp.v[t], D.v[t]);
+                gx.v[t] = add2(i.Qp.v[t], Q.v[t]);
+            }
+            o.Qp = Q;
+            o.Dp = D;
+            o.Gn = Gn;
+            emit(gx, gy);
+        };
+        int j = 4;
+        for (; j + 2 < steps; j += 2) {
+            if (j % kE8Chunk == 0) next_chunk(j / kE8Chunk);
+            full_step(j, A, B, false);
+            full_step(j + 1, B, A, false);
+        }
+        if (j % kE8Chunk == 0) next_chunk(j / kE8Chunk);
+        const bool bot = y1 == H;
+        if (j + 1 < steps) {
+            full_step(j, A, B, false);
+            full_step(j + 1, B, A, bot);
+        } else {
+            full_step(j, A, B, bot);
+        }
+    };
+    if (col_patch || x + kE8Cols + 1 > W) body(std::true_type{});
+    else body(std::false_type{});
+}
+
+template <bool X, bool Y>
+void* pick_e8(bool om) {
+    return om ? reinterpret_cast<void*>(&edge8_kernel<X, Y, true>) : reinterpret_cast<void*>(&edge8_kernel<X, Y, false>);
+}
+
+} // namespace gvxd
+
+using namespace gvxd;
+
+namespace gvxb_impl {
+
+/// gvxb_edge's Gaussian variants (called from edge.cu).
+int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a) {
+    const gvxb_image& s = a->src;
+    const bool ox = a->gx.data, oy = a->gy.data, om = a->mag.data;
+    void* fn = ox ? (oy ? pick_e8<true, true>(om) : pick_e8<true, false>(om))
+                  : (oy ? pick_e8<false, true>(om) : pick_e8<false, false>(om));
+    const int rows = a->band.row1 - a->band.row0;
+    const int frames = s.frames > 0 ? s.frames : 1;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kE8Threads, 0);
+    const long long strips = static_cast<long long>(frames) * ((s.width + kE8Cols - 1) / kE8Cols);
+    Edge8Params p;
+    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, kE8THMax,
+                              4);
+    if (const char* e = std::getenv("GVX_EDGE8_TH")) p.th = std::max(8, std::atoi(e)); // tuning experiments
+    CUtensorMap map;
+    if (int rc = make_u8_tensor_map(&map, s, kE8SW, kE8Chunk)) return rc;
+    p.width = s.width;
+    p.band = Band{a->band.row0, a->band.row1, a->band.global_h, a->band.src_row0, a->band.dst_row0};
+    auto plane = [](const gvxb_image& img) {
+        E8Plane o;
+        o.data = static_cast<int16_t*>(img.data);
+        o.pitch = img.pitch;
+        o.frame_stride = img.frames > 1 ? img.frame_stride : img.pitch * img.height;
+        return o;
+    };
+    p.gx = plane(a->gx);
+    p.gy = plane(a->gy);
+    p.mag = plane(a->mag);
+    dim3 grid((s.width + kE8Cols - 1) / kE8Cols, (rows + p.th - 1) / p.th, frames);
+    void* args[] = {&map, &p};
+    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kE8Threads), args, 0, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "edge8 kernel launch");
+    return check_launch(ctx, "edge8 kernel");
+}
+
+} // namespace gvxb_impl

@@ -106,10 +106,6 @@ __device__ __forceinline__ uint32_t sign_bytes(float a, float b) {
     return r;
 }
 
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
 template <bool kResp>
 #ifndef GVX_HARRIS_MINB
 #define GVX_HARRIS_MINB 12 // resident one-warp CTAs per SM: 3 per scheduler at <= 168 registers
