@@ -310,8 +310,11 @@ struct SepParams {
     Band band;
     int th;
     float u[7], v[7];
-    float bias;     // d / 2 (0 for d == 1)
+    float bias;     // d / 2 (0 for d == 1); fractional form: (d / 2) / 2^15
     float inv_d;    // 1 / (d << shift), exact power of two
+    float qscale;   // quotient FMA: 1.5*2^23 + q = rd(acc * qscale + qbase)
+    float qbase;    //   magic form: inv_d, 1.5*2^23; fractional: 2^15 inv_d, 1.5*2^23 - 2^15 W inv_d
+    int frac;       // columns in fractional form (kernel variant kFrac)
     int clamp255;   // q may exceed 255: 1 saturate to 255, 2 wrap (low byte)
     uint8_t* dst;   // K3 output, or K4's converted image (may be null)
     int64_t dst_pitch, dst_fstride;
@@ -358,6 +361,22 @@ __device__ __forceinline__ SepRow<R> sep_load(const uint8_t* row, int off) {
     return r;
 }
 
+/// As sep_load, with every column in fractional form 1 + x / 2^15 (byte
+/// permutes only, no de-biasing adds): weighted sums W + s / 2^15 stay exact
+/// while W (2^15 + 255) < 2^24 (checked on the host).
+template <int R>
+__device__ __forceinline__ SepRow<R> sep_load_frac(const uint8_t* row, int off) {
+    const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
+    auto col = [&](int j) -> float {
+        const uint32_t w = j < 0 ? wl : (j < 4 ? wc : wr);
+        return __uint_as_float(__byte_perm(w, 0x3F800000u, 0x7604u | (static_cast<unsigned>(j & 3) << 4)));
+    };
+    SepRow<R> r;
+#pragma unroll
+    for (int j = -R; j <= R + 1; ++j) r.p[j + R] = f2(col(j), col(j + 2));
+    return r;
+}
+
 template <int K>
 __device__ __forceinline__ Q4 sep_horizontal(const SepRow<K / 2>& r, const float* v) {
     Q4 h;
@@ -372,8 +391,8 @@ __device__ __forceinline__ Q4 sep_horizontal(const SepRow<K / 2>& r, const float
 }
 
 /// Division epilogue: 1.5*2^23 + min(q, 255) per column.
-__device__ __forceinline__ Q4 sep_quotient(Q4 acc, float inv_d, int clamp255) {
-    const float2 M = f2(12582912.f, 12582912.f), id = f2(inv_d, inv_d);
+__device__ __forceinline__ Q4 sep_quotient(Q4 acc, float qscale, float qbase, int clamp255) {
+    const float2 M = f2(qbase, qbase), id = f2(qscale, qscale);
     Q4 q{__ffma2_rd(acc.e, id, M), __ffma2_rd(acc.o, id, M)};
     if (clamp255) {
         const float top = 12582912.f + 255.f;
@@ -383,8 +402,8 @@ __device__ __forceinline__ Q4 sep_quotient(Q4 acc, float inv_d, int clamp255) {
     return q;
 }
 
-__device__ __forceinline__ Q4 sep_neg_quotient(Q4 acc, float inv_d, int clamp255) {
-    const float2 M = f2(-12582912.f, -12582912.f), id = f2(-inv_d, -inv_d);
+__device__ __forceinline__ Q4 sep_neg_quotient(Q4 acc, float qscale, float qbase, int clamp255) {
+    const float2 M = f2(-qbase, -qbase), id = f2(-qscale, -qscale);
     Q4 q{__ffma2_ru(acc.e, id, M), __ffma2_ru(acc.o, id, M)};
     if (clamp255) {
         const float bot = -12582912.f - 255.f;
@@ -427,7 +446,7 @@ __device__ __forceinline__ void store4(uint8_t* dp, uint32_t w, int c, int width
 /// kMode 0: U8 stencil output; 1: unsharp chain sat_u8(2x - blur);
 /// 2: Convolve -> ConvertDepth -> per-CTA value histogram; 3: as 2 and also
 /// store the converted image.
-template <int K, int kMode, bool kClamp>
+template <int K, int kMode, bool kClamp, bool kFrac>
 __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
     constexpr int R = K / 2;
     constexpr int SH = (kMode >= 2 ? kSepHistTH : kSepTHMax) + 2 * R;
@@ -490,7 +509,7 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
             if (kMode == 1) {
                 // -(1.5*2^23 + b) by round-up of the negated product, then
                 // 2(2^23 + x) - (1.5*2^23 + b) = 2^22 + (2x - b), clamped to U8
-                const Q4 q = sep_neg_quotient(acc, p.inv_d, kClamp);
+                const Q4 q = sep_neg_quotient(acc, p.qscale, p.qbase, kClamp);
                 const uint32_t w = *reinterpret_cast<const uint32_t*>(crow);
                 const float2 xe = f2(magic_byte(w, 0), magic_byte(w, 2)), xo = f2(magic_byte(w, 1), magic_byte(w, 3));
                 const float2 two = f2(2.f, 2.f), lift = f2(8388608.f, 8388608.f);
@@ -502,10 +521,10 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
                 crow += kSepSW;
                 drow += p.dst_pitch;
             } else if (kMode == 0) {
-                store(sep_pack(sep_quotient(acc, p.inv_d, kClamp)));
+                store(sep_pack(sep_quotient(acc, p.qscale, p.qbase, kClamp)));
                 drow += p.dst_pitch;
             } else {
-                const Q4 q = sep_quotient(acc, p.inv_d, kClamp && p.clamp255 == 1);
+                const Q4 q = sep_quotient(acc, p.qscale, p.qbase, kClamp && p.clamp255 == 1);
                 if (kMode == 3) {
                     store(sep_pack(q));
                     drow += p.dst_pitch;
@@ -526,7 +545,9 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
         // into output o = j - i; output o is complete after row j = o + K - 1.
         Q4 acc[K];
         auto row = [&](int j, int slot0) { // slot0 = j mod K
-            const Q4 h = sep_horizontal<K>(sep_load<R>(tile + j * kSepSW, off), v);
+            const Q4 h = sep_horizontal<K>(kFrac ? sep_load_frac<R>(tile + j * kSepSW, off)
+                                                 : sep_load<R>(tile + j * kSepSW, off),
+                                           v);
 #pragma unroll
             for (int i = 0; i < K; ++i) {
                 Q4& a = acc[(slot0 - i + 2 * K) % K];
@@ -639,21 +660,34 @@ bool sep_setup(const int32_t* mask, int K, long long d, int shift, SepParams& p,
     for (int t = 0; t < 7; ++t) p.u[t] = t < K ? static_cast<float>(u[t]) : 0.f, p.v[t] = t < K ? static_cast<float>(v[t]) : 0.f;
     p.bias = static_cast<float>(d / 2);
     p.inv_d = 1.0f / static_cast<float>(d << shift);
+    p.qscale = p.inv_d;
+    p.qbase = 12582912.f;
+    // fractional form (columns as 1 + x / 2^15, no de-biasing adds): exact
+    // while W (2^15 + 255) + d/2 < 2^24 and 2^15 W / (d << shift) is an integer
+    const long long W = su * sv, D = d << shift;
+    p.frac = W * (32768 + 255) + d / 2 < (1LL << 24) && (W * 32768) % D == 0 ? 1 : 0;
+    if (std::getenv("GVX_SEP_NOFRAC")) p.frac = 0; // A/B tests
+    if (p.frac) {
+        p.bias = static_cast<float>(d / 2) / 32768.f;
+        p.qscale = 32768.f / static_cast<float>(D);
+        p.qbase = static_cast<float>(12582912LL - W * 32768 / D);
+    }
     qmax = smax / d;
     return true;
 }
 
-template <int K, int M>
+template <int K, int M, bool F>
 void* sep_fn(bool clamp) {
-    return clamp ? reinterpret_cast<void*>(&sep_kernel<K, M, true>) : reinterpret_cast<void*>(&sep_kernel<K, M, false>);
+    return clamp ? reinterpret_cast<void*>(&sep_kernel<K, M, true, F>)
+                 : reinterpret_cast<void*>(&sep_kernel<K, M, false, F>);
 }
 
 template <int M>
-void* sep_fn_k(int k, bool clamp) {
+void* sep_fn_k(int k, bool clamp, bool frac) {
     switch (k) {
-    case 3: return sep_fn<3, M>(clamp);
-    case 5: return sep_fn<5, M>(clamp);
-    case 7: return sep_fn<7, M>(clamp);
+    case 3: return frac ? sep_fn<3, M, true>(clamp) : sep_fn<3, M, false>(clamp);
+    case 5: return frac ? sep_fn<5, M, true>(clamp) : sep_fn<5, M, false>(clamp);
+    case 7: return frac ? sep_fn<7, M, true>(clamp) : sep_fn<7, M, false>(clamp);
     default: return nullptr;
     }
 }
@@ -714,7 +748,7 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
             sp.dst = static_cast<uint8_t*>(a->dst.data);
             sp.dst_pitch = a->dst.pitch;
             sp.dst_fstride = a->dst.frames > 1 ? a->dst.frame_stride : a->dst.pitch * a->dst.height;
-            void* fn = a->mode == 0 ? sep_fn_k<0>(a->ksize, sp.clamp255) : sep_fn_k<1>(a->ksize, sp.clamp255);
+            void* fn = a->mode == 0 ? sep_fn_k<0>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<1>(a->ksize, sp.clamp255, sp.frac);
             if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0);
         }
     }
@@ -799,7 +833,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
         long long qmax = 0;
         int lo = 0, hi = 0;
         range_of(a->conv_format, lo, hi);
-        if (sep_setup(a->mask, a->ksize, a->scale, a->shift, sp, qmax) && qmax <= hi && sep_fn_k<2>(a->ksize, false)) {
+        if (sep_setup(a->mask, a->ksize, a->scale, a->shift, sp, qmax) && qmax <= hi && sep_fn_k<2>(a->ksize, false, false)) {
             sp.width = s.width;
             sp.band = Band{0, s.height, s.height, 0, 0};
             sp.clamp255 = (qmax >> a->shift) > 255 ? (a->wrap ? 2 : 1) : 0;
@@ -813,7 +847,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
             sp.identity = p.identity_bins;
             sp.sum = p.sum;
             sp.sumsq = p.sumsq;
-            void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255) : sep_fn_k<2>(a->ksize, sp.clamp255);
+            void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<2>(a->ksize, sp.clamp255, sp.frac);
             if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes))
                 return rc;
             return meanstd(ctx, a, p, frames, s);
