@@ -295,6 +295,12 @@ __global__ void meanstd_finalize_kernel(const unsigned long long* sum, const uns
 constexpr int kSepThreads = 96;
 constexpr int kSepTW = 4 * kSepThreads; // 384 columns: 4K / 8K / 1080p split evenly
 constexpr int kSepSW = kSepTW + 32;     // tile origin x0 - 16 (16-byte aligned TMA start)
+#ifndef GVX_SEP_HIST_THREADS
+#define GVX_SEP_HIST_THREADS 96
+#endif
+/// Threads per CTA: the histogram modes may use all four counter bytes of a
+/// (value, lane) word with four warps.
+__host__ __device__ constexpr int sep_threads(int mode) { return mode >= 2 ? GVX_SEP_HIST_THREADS : kSepThreads; }
 #ifndef GVX_SEP_TH_MAX
 #define GVX_SEP_TH_MAX 48
 #endif
@@ -447,34 +453,35 @@ __device__ __forceinline__ void store4(uint8_t* dp, uint32_t w, int c, int width
 /// 2: Convolve -> ConvertDepth -> per-CTA value histogram; 3: as 2 and also
 /// store the converted image.
 template <int K, int kMode, bool kClamp, bool kFrac>
-__global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
+__global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
+    constexpr int NT = sep_threads(kMode), TW = 4 * NT, SW = TW + 32;
     constexpr int R = K / 2;
     constexpr int SH = (kMode >= 2 ? kSepHistTH : kSepTHMax) + 2 * R;
-    __shared__ alignas(128) uint8_t tile[SH * kSepSW];
+    __shared__ alignas(128) uint8_t tile[SH * SW];
     __shared__ uint64_t bar;
     extern __shared__ uint4 hist_dyn[]; // kMode 2: [bin][lane][warp] u8 counters
     uint8_t* hist = reinterpret_cast<uint8_t*>(hist_dyn);
 
     const int tid = static_cast<int>(threadIdx.x);
-    const int x0 = blockIdx.x * kSepTW;
+    const int x0 = blockIdx.x * TW;
     const int y0 = p.band.row0 + blockIdx.y * p.th;
     const int n = min(y0 + p.th, p.band.row1) - y0;
     const int frame = blockIdx.z;
     if (kMode >= 2) {
-        for (int i = tid; i < kSepHistBytes / 16; i += kSepThreads) hist_dyn[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < kSepHistBytes / 16; i += NT) hist_dyn[i] = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_barrier_init();
     }
     __syncthreads();
-    stage_tile_u8<kSepSW, SH>(tile, &map, &bar, x0 - 16, y0 - R, frame, p.width, p.band, p.th + 2 * R);
+    stage_tile_u8<SW, SH>(tile, &map, &bar, x0 - 16, y0 - R, frame, p.width, p.band, p.th + 2 * R);
 
     const int c = x0 + 4 * tid;
     const int off = 16 + 4 * tid;
     const int dy0 = kMode >= 2 ? y0 : y0 - p.band.dst_row0;
     uint8_t* drow = p.dst ? p.dst + frame * p.dst_fstride + static_cast<int64_t>(dy0) * p.dst_pitch + c : nullptr;
-    const uint8_t* crow = tile + R * kSepSW + off; // kMode 1: centre pixels of output row o
+    const uint8_t* crow = tile + R * SW + off; // kMode 1: centre pixels of output row o
     // kMode 2 counter of (value, lane, warp): value * 128 + lane * 4 + warp
     const uint32_t hbase = smem_u32(hist_dyn) + (((tid & 31) << 2) | (tid >> 5));
     const uint32_t hcnt = hbase - (0x4B400000u << 7);
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
                 re = f2(fminf(fmaxf(re.x, lo), hi), fminf(fmaxf(re.y, lo), hi));
                 ro = f2(fminf(fmaxf(ro.x, lo), hi), fminf(fmaxf(ro.y, lo), hi));
                 store(sep_pack(Q4{add2(re, lift), add2(ro, lift)})); // 1.5*2^23 + y
-                crow += kSepSW;
+                crow += SW;
                 drow += p.dst_pitch;
             } else if (kMode == 0) {
                 store(sep_pack(sep_quotient(acc, p.qscale, p.qbase, kClamp)));
@@ -545,8 +552,8 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
         // into output o = j - i; output o is complete after row j = o + K - 1.
         Q4 acc[K];
         auto row = [&](int j, int slot0) { // slot0 = j mod K
-            const Q4 h = sep_horizontal<K>(kFrac ? sep_load_frac<R>(tile + j * kSepSW, off)
-                                                 : sep_load<R>(tile + j * kSepSW, off),
+            const Q4 h = sep_horizontal<K>(kFrac ? sep_load_frac<R>(tile + j * SW, off)
+                                                 : sep_load<R>(tile + j * SW, off),
                                            v);
 #pragma unroll
             for (int i = 0; i < K; ++i) {
@@ -572,7 +579,7 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
             count(pend.o.y, 3);
         }
     };
-    if (x0 + kSepTW > p.width) body(std::true_type{});
+    if (x0 + TW > p.width) body(std::true_type{});
     else body(std::false_type{});
 
     if (kMode < 2) return;
@@ -580,7 +587,7 @@ __global__ void __launch_bounds__(kSepThreads) sep_kernel(const __grid_constant_
     // merge: thread t owns values t, t + 96, t + 192 (< 256); the 128 counter
     // bytes of a value are read as 8 uint4 in a rotated order (bank spread)
     long long s1 = 0, s2 = 0;
-    for (int val = tid; val < 256; val += kSepThreads) {
+    for (int val = tid; val < 256; val += NT) {
         const uint4* rowp = hist_dyn + val * 8;
         unsigned cnt = 0;
 #pragma unroll
@@ -692,24 +699,27 @@ void* sep_fn_k(int k, bool clamp, bool frac) {
     }
 }
 
-int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K, int rows, int th_max, size_t dyn) {
+int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K, int rows, int th_max, size_t dyn,
+               int ch_threads) {
     using namespace gvxb_impl;
     if (dyn > 0) { // static tile + dynamic histogram exceed the 48 KB default
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
         if (e != cudaSuccess) return cuda_fail(e, "separable stencil smem attribute");
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSepThreads, dyn);
+    const int nt = ch_threads;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, dyn);
     const int frames = s.frames > 0 ? s.frames : 1;
-    const long long strips = static_cast<long long>((s.width + kSepTW - 1) / kSepTW) * frames;
+    const int tw = 4 * nt, sw = tw + 32;
+    const long long strips = static_cast<long long>((s.width + tw - 1) / tw) * frames;
     p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, th_max,
                               K - 1);
     if (const char* e = std::getenv("GVX_SEP_TH")) p.th = std::max(8, std::min(th_max, std::atoi(e))); // tuning experiments
     CUtensorMap map;
-    if (int rc = make_u8_tensor_map(&map, s, kSepSW, p.th + K - 1)) return rc;
-    dim3 grid((s.width + kSepTW - 1) / kSepTW, (rows + p.th - 1) / p.th, frames);
+    if (int rc = make_u8_tensor_map(&map, s, sw, p.th + K - 1)) return rc;
+    dim3 grid((s.width + tw - 1) / tw, (rows + p.th - 1) / p.th, frames);
     void* args[] = {&map, &p};
-    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kSepThreads), args, dyn, ctx->stream);
+    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(nt), args, dyn, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "separable stencil launch");
     return check_launch(ctx, "separable stencil kernel");
 }
@@ -749,7 +759,7 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
             sp.dst_pitch = a->dst.pitch;
             sp.dst_fstride = a->dst.frames > 1 ? a->dst.frame_stride : a->dst.pitch * a->dst.height;
             void* fn = a->mode == 0 ? sep_fn_k<0>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<1>(a->ksize, sp.clamp255, sp.frac);
-            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0);
+            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0, sep_threads(0));
         }
     }
     StencilParams p;
@@ -848,7 +858,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
             sp.sum = p.sum;
             sp.sumsq = p.sumsq;
             void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<2>(a->ksize, sp.clamp255, sp.frac);
-            if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes))
+            if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2)))
                 return rc;
             return meanstd(ctx, a, p, frames, s);
         }
