@@ -58,6 +58,13 @@ struct P8 {
 struct P12 {
     float2 v[6];
 };
+/// A Gaussian row around the lane: its 8 columns and the neighbour columns
+/// c-1 / c+8 as scalars (pairs mixing them with own columns would each cost
+/// a register move; the boundary terms are scalar adds instead).
+struct GRow {
+    P8 g;
+    float l, r;
+};
 
 __device__ __forceinline__ float e8_sqrt_approx(float x) {
     float r;
@@ -226,13 +233,13 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
             }
             if (x == 0 && lane == 0) g.v[3].x = g.v[0].y;
         };
-        /// Gaussian row pairs for i = -1 .. 4 (columns c-1 / c+8 from the
-        /// neighbour lanes; clamped at the image border).
+        /// Gaussian row with columns c-1 / c+8 from the neighbour lanes
+        /// (clamped at the image border).
         auto neighbourhood = [&](const P8& g) {
             const float L = __shfl_up_sync(0xffffffffu, g.v[3].y, 1);
             float R = __shfl_down_sync(0xffffffffu, g.v[0].x, 1);
             if (kEdge) R = last <= 7 ? g.v[3].y : R;
-            return P12{{f2(L, g.v[3].x), g.v[0], g.v[1], g.v[2], g.v[3], f2(g.v[0].y, R)}};
+            return GRow{g, L, R};
         };
         auto emit = [&](const P8& gx, const P8& gy) {
             const bool full = !kEdge || c + 7 < W;
@@ -275,7 +282,7 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
         struct State {
             P8 Hp, Rp;  // Hg(j-1), Hg(j-2) + Hg(j-1)
             P8 Dp, Qp;  // D(m), Q(m) of the newest Gaussian row
-            P12 Gn;     // Gaussian neighbourhood of the row this copy last produced
+            GRow Gn;    // Gaussian row this copy last produced
         };
         State A, B;
         // 16 + (S + 8) / 2^15 -> 1.5*2^23 + floor((S + 8) / 16): exact scaling by
@@ -294,17 +301,24 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
             clamp_cols(g);
             return neighbourhood(g);
         };
-        auto diff = [&](const P12& n) {
+        /// D = G(x+1) - G(x-1) for the lane's 8 columns.
+        auto diff = [&](const GRow& n) {
+            const P8& g = n.g;
             P8 d;
-#pragma unroll
-            for (int t = 0; t < 4; ++t) d.v[t] = sub2(n.v[t + 2], n.v[t]);
+            d.v[0] = f2(g.v[1].x - n.l, g.v[1].y - g.v[3].x);
+            d.v[1] = sub2(g.v[2], g.v[0]);
+            d.v[2] = sub2(g.v[3], g.v[1]);
+            d.v[3] = f2(g.v[0].y - g.v[2].x, n.r - g.v[2].y);
             return d;
         };
-        /// gy of the row between Gaussian rows n (newer) and m (two older).
-        auto grad_y = [&](const P12& n, const P12& m) {
+        /// gy of the row between Gaussian rows n (newer) and m (two older):
+        /// vertical differences, then the 1-2-1 across columns.
+        auto grad_y = [&](const GRow& n, const GRow& m) {
             float2 d[6];
+            d[0] = f2(n.l - m.l, n.g.v[3].x - m.g.v[3].x);
 #pragma unroll
-            for (int t = 0; t < 6; ++t) d[t] = sub2(n.v[t], m.v[t]);
+            for (int t = 0; t < 4; ++t) d[t + 1] = sub2(n.g.v[t], m.g.v[t]);
+            d[5] = f2(n.g.v[0].y - m.g.v[0].y, n.r - m.r);
             P8 g;
 #pragma unroll
             for (int t = 0; t < 4; ++t) g.v[t] = fma2(two, d[t + 1], add2(d[t], d[t + 2]));
@@ -317,8 +331,8 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
             for (int t = 0; t < 4; ++t) A.Rp.v[t] = add2(h0.v[t], h1.v[t]);
             A.Hp = h1;
         }
-        P12 G1 = gauss_step(2, A, B); // Gaussian row y0-1
-        P12 G2 = gauss_step(3, B, A); // Gaussian row y0
+        GRow G1 = gauss_step(2, A, B); // Gaussian row y0-1
+        GRow G2 = gauss_step(3, B, A); // Gaussian row y0
         if (y0 == 0) G1 = G2;          // Gaussian row -1 clamps to row 0
         {
             const P8 D1 = diff(G1), D2 = diff(G2);
@@ -331,7 +345,7 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
         /// Step j: Gaussian row j-1 -> Sobel / outputs of row j-4 (global).
         /// `bottom`: Gaussian row j-1 is row H, which clamps to row H-1.
         auto full_step = [&](int j, State& i, State& o, bool bottom) {
-            P12 Gn = gauss_step(j, i, o);
+            GRow Gn = gauss_step(j, i, o);
             if (bottom) Gn = i.Gn;
             const P8 D = diff(Gn);
             const P8 gy = grad_y(Gn, o.Gn); // o.Gn = Gaussian row j-3

@@ -260,7 +260,9 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
             float R = __shfl_down_sync(0xffffffffu, q.v[0].x, 1);     // right lane's A0 = my c+8
             if (kEdge) R = last <= 7 ? q.v[3].y : R;
             const float2 sa = add2(q.v[0], q.v[1]), sb = add2(q.v[2], q.v[3]);
-            return Q8{{add2(f2(L, q.v[3].x), sa), add2(sa, q.v[2]), add2(q.v[1], sb), add2(sb, f2(q.v[0].y, R))}};
+            // the two boundary outputs as scalar adds: assembling the pairs
+            // (L, A3) and (B0, R) cost a register move each (measured +2.8%)
+            return Q8{{f2(L + sa.x, q.v[3].x + sa.y), add2(sa, q.v[2]), add2(q.v[1], sb), f2(sb.x + q.v[0].y, sb.y + R)}};
         };
         /// Products of one Sobel row and their horizontal box sums.
         auto products = [&](const Q8& gx, const Q8& gy) {
