@@ -139,22 +139,35 @@ struct Emitter {
     Emitter(const std::vector<SlotInfo>& i, const std::vector<SlotInfo>& o)
         : ins(i), outs(o), n_in(static_cast<int>(i.size())) {}
 
+    // Several emitters may share one kernel (fused local chains): this one's
+    // input slot s lives at parameter slot `slot_base + s`, its outputs after
+    // `n_in_total` inputs, its helpers are named with `prefix`, and reads of
+    // input slot `smem_slot` go to `smem_loader` (a shared-memory tile).
+    int slot_base = 0;
+    int n_in_total = -1;
+    std::string prefix;
+    int smem_slot = -1;
+    std::string smem_loader;
+    int fin(int slot) const { return field_in(slot_base + slot); }
+    int fout(int o) const { return field_in((n_in_total >= 0 ? n_in_total : n_in) + o); }
+
     std::string in_base(int slot) const {
         std::ostringstream s;
-        s << "((const unsigned char*)p.f[" << field_in(slot) << "] + (u64)fr * p.f[" << field_in(slot) + 2 << "])";
+        s << "((const unsigned char*)p.f[" << fin(slot) << "] + (u64)fr * p.f[" << fin(slot) + 2 << "])";
         return s.str();
     }
 
     /// Image load function name for (slot, channel, clamp flavour); emitted once.
     std::string image_loader(int slot, Channel ch) {
+        if (slot == smem_slot) return smem_loader;
         const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
-        std::string name = "ld" + std::to_string(slot) + "_" + std::to_string(static_cast<int>(ch));
+        std::string name = "ld" + prefix + std::to_string(slot) + "_" + std::to_string(static_cast<int>(ch));
         for (const std::string& d : defined)
             if (d == name) return name;
         defined.push_back(name);
         std::ostringstream f;
         f << "__device__ __forceinline__ V " << name << "(const P& p, int fr, int x, int y, u64& rd) {\n"
-          << "  rd++;\n  const unsigned char* row = " << in_base(slot) << " + (u64)y * p.f[" << field_in(slot) + 1
+          << "  rd++;\n  const unsigned char* row = " << in_base(slot) << " + (u64)y * p.f[" << fin(slot) + 1
           << "];\n";
         switch (s.desc.format) {
         case ImageFormat::U8: f << "  return vi(row[x]);\n"; break;
@@ -181,8 +194,8 @@ struct Emitter {
 
     std::string scalar_load(int slot) const {
         std::ostringstream s;
-        s << "ld_val((const i64*)((const unsigned char*)p.f[" << field_in(slot) << "] + (u64)fr * p.f["
-          << field_in(slot) + 2 << "]))";
+        s << "ld_val((const i64*)((const unsigned char*)p.f[" << fin(slot) << "] + (u64)fr * p.f["
+          << fin(slot) + 2 << "]))";
         return s.str();
     }
 
@@ -213,10 +226,10 @@ struct Emitter {
         if (s.kind != SlotKind::Array && s.kind != SlotKind::Matrix)
             return "(raise_st(p, 2u), vi(0))";
         std::ostringstream o;
-        o << "[&]() -> V { i64 at = vl(" << idx << "); u64 n = p.f[" << field_in(slot) + 1
+        o << "[&]() -> V { i64 at = vl(" << idx << "); u64 n = p.f[" << fin(slot) + 1
           << "]; if (at < 0 || (u64)at >= n) { raise_st(p, 2u); return vi(0); } return ld_val((const i64*)((const "
              "unsigned char*)p.f["
-          << field_in(slot) << "] + (u64)fr * p.f[" << field_in(slot) + 2 << "]) + 2 * at); }()";
+          << fin(slot) << "] + (u64)fr * p.f[" << fin(slot) + 2 << "]) + 2 * at); }()";
         return o.str();
     }
 
@@ -300,7 +313,7 @@ struct Emitter {
     /// Store statement of V `val` into output slot `o`, channel c (RGB).
     std::string store(int o, const std::string& val, int channel, const std::string& x, const std::string& y) const {
         const SlotInfo& s = outs[static_cast<std::size_t>(o)];
-        const int f = field_in(n_in + o);
+        const int f = fout(o);
         std::ostringstream r;
         r << "{ unsigned char* row = (unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2 << "] + (u64)(" << y
           << ") * p.f[" << f + 1 << "]; V sv = " << val << "; ";
@@ -318,7 +331,7 @@ struct Emitter {
     }
 
     std::string out_slot_ptr(int o) const {
-        const int f = field_in(n_in + o);
+        const int f = fout(o);
         return "((i64*)((unsigned char*)p.f[" + std::to_string(f) + "] + (u64)fr * p.f[" + std::to_string(f + 2) +
                "]))";
     }
@@ -608,6 +621,130 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     prog.kernels.push_back(std::move(ks));
     return prog;
 }
+
+// ------------------------------------------------------- fused local chain
+
+namespace {
+
+/// C type holding a stored pixel of an integer / F32 image format, and the
+/// V -> storage conversion of Emitter::store.
+bool storage_of(ImageFormat f, std::string& ctype, std::string& conv, std::string& load) {
+    switch (f) {
+    case ImageFormat::U8: ctype = "unsigned char"; conv = "(unsigned char)sv.i"; load = "vi((i64)v)"; return true;
+    case ImageFormat::U16: ctype = "unsigned short"; conv = "(unsigned short)sv.i"; load = "vi((i64)v)"; return true;
+    case ImageFormat::S16: ctype = "short"; conv = "(short)sv.i"; load = "vi((i64)v)"; return true;
+    case ImageFormat::S32: ctype = "int"; conv = "(int)sv.i"; load = "vi((i64)v)"; return true;
+    case ImageFormat::F32: ctype = "float"; conv = "(float)vd(sv)"; load = "vf((double)v)"; return true;
+    default: return false;
+    }
+}
+
+/// Generic (Value-typed) tap loop + post body of a local node at (px, py):
+/// statements defining `V pv` (the value before its store).
+std::string local_value(Emitter& em, const LocalKernel& lk) {
+    std::ostringstream b;
+    const int hw = lk.window_w / 2, hh = lk.window_h / 2;
+    em.mode = Emitter::Mode::Tap;
+    const char* comb = lk.combine == CombineMode::Sum ? "v_add" : lk.combine == CombineMode::Min ? "v_min" : "v_max";
+    bool first = true;
+    for (int dy = -hh; dy <= hh; ++dy)
+        for (int dx = -hw; dx <= hw; ++dx) {
+            em.tdx = dx;
+            em.tdy = dy;
+            const std::string v = em.emit(*lk.tap_body);
+            if (first) {
+                b << "    V cmb = " << v << ";\n";
+                first = false;
+            } else {
+                b << "    cmb = " << comb << "(cmb, " << v << ");\n";
+            }
+        }
+    em.tdx = em.tdy = 0;
+    em.mode = Emitter::Mode::Post;
+    b << "    V pv = " << (lk.post_body ? em.emit(*lk.post_body) : std::string("cmb")) << ";\n";
+    return b.str();
+}
+
+} // namespace
+} // namespace (lowering helpers)
+
+bool local_chain_fusible(const AbstractionKernel& producer, const AbstractionKernel& consumer, ImageFormat mid) {
+    if (producer.kind != AbstractionKind::Local || consumer.kind != AbstractionKind::Local) return false;
+    const LocalKernel& a = producer.local();
+    const LocalKernel& b = consumer.local();
+    if (a.median3x3 || b.median3x3 || !a.tap_body || !b.tap_body) return false;
+    if (a.boundary == BoundaryMode::Undefined || b.boundary != BoundaryMode::Clamp) return false;
+    if (b.window_w > 7 || b.window_h > 7 || a.window_w > 7 || a.window_h > 7) return false;
+    std::string t, c, l;
+    return storage_of(mid, t, c, l);
+}
+
+NodeProgram lower_local_chain(const AbstractionKernel& producer, const std::vector<SlotInfo>& p_ins,
+                              const std::vector<Value>& p_matrix, const SlotInfo& mid,
+                              const AbstractionKernel& consumer, const std::vector<SlotInfo>& c_ins, int c_mid_slot,
+                              const std::vector<SlotInfo>& c_outs, const std::vector<Value>& c_matrix) {
+    const LocalKernel& pk = producer.local();
+    const LocalKernel& ck = consumer.local();
+    std::string ctype, conv, load;
+    if (!storage_of(mid.desc.format, ctype, conv, load)) throw Error(ErrorCode::BadFormat, "fused chain format");
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(p_ins.size() + c_ins.size());
+    prog.n_outputs = static_cast<int>(c_outs.size());
+    prog.dims_from = -1;
+    prog.counts_reads = false; // static windows: the host counts both nodes' reads
+    constexpr int TX = 32, TY = 8;
+    const int RX = ck.window_w / 2, RY = ck.window_h / 2;
+    const int RW = TX + 2 * RX, RH = TY + 2 * RY;
+
+    std::vector<SlotInfo> p_outs{mid};
+    Emitter pe(p_ins, p_outs);
+    pe.local = &pk;
+    pe.mask = pk.mask.empty() ? &p_matrix : &pk.mask;
+    pe.prefix = "P";
+    pe.n_in_total = prog.n_inputs;
+    Emitter ce(c_ins, c_outs);
+    ce.local = &ck;
+    ce.mask = ck.mask.empty() ? &c_matrix : &ck.mask;
+    ce.prefix = "C";
+    ce.slot_base = static_cast<int>(p_ins.size());
+    ce.n_in_total = prog.n_inputs;
+    ce.smem_slot = c_mid_slot;
+    ce.smem_loader = "ld_mid";
+
+    const std::string pbody = local_value(pe, pk);
+    const std::string cbody = local_value(ce, ck);
+    std::ostringstream src;
+    src << "__shared__ " << ctype << " gvx_mid[" << RH * RW << "];\n"
+        << "__device__ __forceinline__ V ld_mid(const P& p, int fr, int x, int y, u64& rd) {\n"
+        << "  const " << ctype << " v = gvx_mid[(y - ((int)blockIdx.y * " << TY << " - " << RY << ")) * " << RW
+        << " + (x - ((int)blockIdx.x * " << TX << " - " << RX << "))];\n  return " << load << ";\n}\n"
+        << "extern \"C\" __global__ void gvx_lchain(const P p) {\n"
+        << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
+        << "  const int x0 = (int)blockIdx.x * " << TX << " - " << RX << ", y0 = (int)blockIdx.y * " << TY << " - "
+        << RY << ";\n"
+        << "  // the intermediate at every (clamped) position the tile's windows read\n"
+        << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << RH * RW
+        << "; e += blockDim.x * blockDim.y) {\n"
+        << "    const int px = clampi(x0 + e % " << RW << ", 0, W - 1), py = clampi(y0 + e / " << RW
+        << ", 0, H - 1);\n"
+        << pbody << "    V sv = pv;\n    gvx_mid[e] = " << conv << ";\n  }\n  __syncthreads();\n"
+        << "  const int px = blockIdx.x * " << TX << " + threadIdx.x, py = blockIdx.y * " << TY << " + threadIdx.y;\n"
+        << "  if (px < W && py < H) {\n"
+        << cbody << "    " << ce.store(0, "pv", 0, "px", "py") << "  }\n}\n";
+    KernelSpec ks;
+    ks.name = "gvx_lchain";
+    ks.block_x = TX;
+    ks.block_y = TY;
+    ks.cols = 1;
+    std::string pre = kPrelude;
+    const std::string key = "NFIELDS";
+    pre.replace(pre.find(key), key.size(), std::to_string(prog.fields()));
+    ks.source = pre + pe.helpers.str() + ce.helpers.str() + src.str();
+    prog.kernels.push_back(std::move(ks));
+    return prog;
+}
+
+namespace {
 
 // ---------------------------------------------------------------- reduce
 

@@ -49,3 +49,17 @@ def test_corpus_graph_matches_reference(path, gvx):
                                               "transfers_executed")][1:] == gold["counters"][1:]
             launches[naive] = counters["kernel_launches"]
         assert launches[False] <= launches[True], (path.stem, variant, launches)
+
+
+@pytest.mark.parametrize("stem", ["sobel", "edge_fig1"])
+def test_generic_local_chain_runs_on_chip(stem, gvx):
+    """Local -> local pairs outside the hand-written groups (Sobel-y feeding
+    Sobel-x + Magnitude, the Gaussian feeding Sobel + Magnitude + Threshold
+    after the reference fuser's merges) run as one NVRTC kernel whose
+    intermediate stays in shared memory, bit-exact with the reference."""
+    gold = GOLDEN[stem]
+    g = gvx.GraphFile((REPO / "examples" / f"{stem}.json").read_text())
+    assert " -> " in g.describe(), g.describe()
+    outs, counters = g.run(naive=False, seed=gold["seed"])
+    assert hashlib.sha256(blob(outs)).hexdigest() == gold["sha256"]
+    assert counters["kernel_launches"] == 1
