@@ -401,7 +401,9 @@ struct RandomGraph {
 TEST_CASE("gpu: fusion soundness on random DAGs (run_plan == run_naive, bit exact)") {
     GPU_ONLY();
     int checked = 0;
-    for (std::uint64_t seed = 1; seed <= 40; ++seed) {
+    // 100 graphs: local -> local pairs with virtual intermediates (the generic
+    // on-chip chains) appear in most of them
+    for (std::uint64_t seed = 1; seed <= 100; ++seed) {
         const int w = 5 + static_cast<int>(seed * 37 % 120), h = 3 + static_cast<int>(seed * 11 % 50);
         RandomGraph rg(seed, w, h);
         VerifyResult vr = verify(*rg.g);
@@ -418,7 +420,7 @@ TEST_CASE("gpu: fusion soundness on random DAGs (run_plan == run_naive, bit exac
         CHECK(b.counters.transfers_executed <= a.counters.transfers_executed);
         ++checked;
     }
-    CHECK(checked >= 30);
+    CHECK(checked >= 75);
 }
 
 TEST_CASE("gpu: frame batches through a DeviceSession equal per-frame run_plan") {
