@@ -642,9 +642,12 @@ std::shared_ptr<Program> build_plan(const OptimizedPlan& plan, const std::map<Ob
     for (Unit& u : aot) p->units.push_back(std::move(u));
     // generic local -> local chains among the remaining executed nodes: a
     // virtual intermediate written by a local and read only by one local
-    // stays on chip (jit::lower_local_chain); GVX_NO_LOCAL_CHAINS disables
-    static const bool no_chains = std::getenv("GVX_NO_LOCAL_CHAINS") != nullptr;
-    if (!no_chains) {
+    // stays on chip (jit::lower_local_chain).  Opt-in (GVX_LOCAL_CHAINS=1):
+    // the pair kernel moves 4x fewer DRAM bytes but its Value-typed post
+    // bodies run one pixel per thread, and on the corpus pairs it measured
+    // slower than the two per-node kernels (profiles/chain_probe)
+    const bool chains = std::getenv("GVX_LOCAL_CHAINS") != nullptr;
+    if (chains) {
         std::map<ObjectId, std::vector<ObjectId>> fg_readers; // object -> reading executed nodes
         std::map<ObjectId, ObjectId> fg_writer;
         for (const OperatorNode& n : fg.nodes()) {

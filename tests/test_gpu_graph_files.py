@@ -52,11 +52,12 @@ def test_corpus_graph_matches_reference(path, gvx):
 
 
 @pytest.mark.parametrize("stem", ["sobel", "edge_fig1"])
-def test_generic_local_chain_runs_on_chip(stem, gvx):
+def test_generic_local_chain_runs_on_chip(stem, gvx, monkeypatch):
     """Local -> local pairs outside the hand-written groups (Sobel-y feeding
     Sobel-x + Magnitude, the Gaussian feeding Sobel + Magnitude + Threshold
     after the reference fuser's merges) run as one NVRTC kernel whose
     intermediate stays in shared memory, bit-exact with the reference."""
+    monkeypatch.setenv("GVX_LOCAL_CHAINS", "1")  # opt-in pass (see DESIGN.md §3)
     gold = GOLDEN[stem]
     g = gvx.GraphFile((REPO / "examples" / f"{stem}.json").read_text())
     assert " -> " in g.describe(), g.describe()

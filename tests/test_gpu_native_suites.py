@@ -10,8 +10,8 @@ pytestmark = pytest.mark.gpu
 REPO = pathlib.Path(__file__).resolve().parent.parent
 
 
-def _run(exe, timeout=900):
-    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=timeout)
+def _run(exe, timeout=900, env=None):
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=timeout, env=env)
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-4000:]
     assert "failed: 0" in out.stdout
 
@@ -32,3 +32,10 @@ def test_reference_expr_and_graph_tests():
 
 def test_cpp_fusion_soundness_and_boundaries():
     _run(REPO / "tests" / "cpp" / "bin" / "test_graphvx")
+
+
+def test_cpp_fusion_soundness_with_local_chains():
+    """The same suite with the opt-in generic local -> local chains: the
+    random DAGs then run their local pairs as single on-chip kernels."""
+    import os
+    _run(REPO / "tests" / "cpp" / "bin" / "test_graphvx", env=dict(os.environ, GVX_LOCAL_CHAINS="1"))
