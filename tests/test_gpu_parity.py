@@ -1,6 +1,7 @@
 """GPU parity: every BASELINE config through the public API on the B200,
 bit-exact against the reference (golden fixtures from the unmodified
 reference) and the C restatement at full size."""
+import pathlib
 import numpy as np
 import pytest
 
@@ -191,3 +192,20 @@ def test_host_pipeline_pinned_inputs(cfg, gvx, oracle_mod):
         assert _same(cfg, r, oracle_mod.port_run(cfg, f))
     with pytest.raises(gvx.GraphvxError):
         pl.submit(gvx.random_u8(w, h, 7), pinned=True)
+
+
+@pytest.mark.parametrize("size", [(1920, 1080), (77, 41), (481, 37)])
+def test_edge_v2_kernel_still_bit_exact(size):
+    """The 4-warp tiled edge kernel (kept behind GVX_EDGE_V2=1 for A/B runs
+    against edge8) in a fresh process: bit-exact with the C restatement."""
+    import os
+    import subprocess
+    import sys
+    repo = pathlib.Path(__file__).resolve().parent.parent
+    code = ("import sys; sys.path.insert(0, '.'); import numpy as np, paper_2008_11476_b200 as gvx, oracle; "
+            f"w, h = {size[0]}, {size[1]}; img = gvx.random_u8(w, h, 3); "
+            "got, _ = gvx.ConfigGraph(1, w, h).run_host(img); "
+            "print('EQUAL' if np.array_equal(got, oracle.port_run(1, img)) else 'DIFF')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=repo, capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ, GVX_EDGE_V2="1"))
+    assert "EQUAL" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
