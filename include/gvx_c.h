@@ -94,6 +94,14 @@ int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stat
 /* As gvxc_pipeline_next for image-output graphs, without the copy: *view
  * points at the result in page-locked staging until the next submit. */
 int gvxc_pipeline_next_view(gvxc_pipeline p, const void** view, size_t* bytes, long long counters[4]);
+/* A stream of n host frames through the pipeline in one call (image-output
+ * graphs): keeps `depth` frames in flight and hands every result, in order,
+ * to on_result (may be NULL) while it is still in page-locked staging;
+ * counters = sums over the frames.  `pinned`: frames are page-locked
+ * (gvxc_host_register) and DMAed without the staging copy. */
+int gvxc_pipeline_stream(gvxc_pipeline p, const uint8_t* const* frames, int n, int pinned,
+                         void (*on_result)(const void* view, size_t bytes, void* user), void* user,
+                         long long counters[4]);
 
 /* ---- graph description files (graph_io.hpp, ref:src/graph_io.cpp) -------- */
 typedef struct gvxc_json_s* gvxc_json;

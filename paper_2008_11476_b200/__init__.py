@@ -120,6 +120,7 @@ def _declare(c, g):
     g.gvxc_pipeline_pending.argtypes = [P]
     g.gvxc_pipeline_next.argtypes = [P, P, ctypes.POINTER(L), ctypes.POINTER(D), ctypes.POINTER(L)]
     g.gvxc_pipeline_next_view.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(L)]
+    g.gvxc_pipeline_stream.argtypes = [P, ctypes.POINTER(P), I, I, P, P, ctypes.POINTER(L)]
     g.gvxc_graph_input_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_graph_output_ptr.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
     g.gvxc_launch_count.restype = ctypes.c_longlong
@@ -347,6 +348,33 @@ class Pipeline:
             views[key] = raw.view(dt).reshape(self.graph.height, self.graph.width)
         cnt = dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(counters)))
         return views[key], cnt
+
+    _ON_RESULT = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+    def stream(self, frames, pinned: bool = False, on_result=None) -> dict:
+        """All `frames` through the pipeline in one native call (results are
+        taken in order from page-locked staging, `depth` frames in flight);
+        returns the summed counters.  `on_result(view)` (optional) sees each
+        result plane while it is valid.  With `pinned` every frame must be
+        page-locked (PinnedHost)."""
+        ptrs = (ctypes.c_void_p * len(frames))()
+        for i, f in enumerate(frames):
+            assert f.dtype == np.uint8 and f.flags.c_contiguous and f.shape == (self.graph.height, self.graph.width)
+            ptrs[i] = f.ctypes.data
+        cb = None
+        if on_result is not None:
+            dt = np.dtype(CONFIG_OUTPUT[self.graph.cfg])
+
+            def _cb(view, nbytes, _user):
+                raw = np.ctypeslib.as_array(ctypes.cast(view, ctypes.POINTER(ctypes.c_uint8)), shape=(nbytes,))
+                on_result(raw.view(dt).reshape(self.graph.height, self.graph.width))
+
+            cb = self._ON_RESULT(_cb)
+        counters = (ctypes.c_longlong * 4)()
+        _check_graph(_graph.gvxc_pipeline_stream(self._h, ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)),
+                                                 len(frames), int(pinned), ctypes.cast(cb, ctypes.c_void_p) if cb
+                                                 else None, None, counters))
+        return dict(zip(["kernel_launches", "pixels_read", "pixels_written", "transfers_executed"], list(counters)))
 
     def next(self, out: np.ndarray = None):
         """Oldest frame's result: (output plane, counters), or

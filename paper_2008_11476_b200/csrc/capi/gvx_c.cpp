@@ -308,6 +308,7 @@ int gvxc_random_u8(int w, int h, unsigned long long seed, uint8_t* out) {
 struct gvxc_pipeline_s {
     gvxc_graph g = nullptr;
     std::unique_ptr<gvx::HostPipeline> p;
+    int depth = 1;
 };
 
 extern "C" {
@@ -316,6 +317,7 @@ int gvxc_pipeline_create(gvxc_graph g, int naive, int depth, gvxc_pipeline* out)
     return guarded([&] {
         auto pl = std::make_unique<gvxc_pipeline_s>();
         pl->g = g;
+        pl->depth = depth < 1 ? 1 : depth;
         pl->p = naive ? std::make_unique<gvx::HostPipeline>(g->impl, depth)
                       : std::make_unique<gvx::HostPipeline>(g->plan, depth);
         *out = pl.release();
@@ -364,6 +366,36 @@ int gvxc_pipeline_next_view(gvxc_pipeline p, const void** view, size_t* bytes, l
             counters[2] = r.counters.pixels_written;
             counters[3] = r.counters.transfers_executed;
         }
+    });
+}
+
+int gvxc_pipeline_stream(gvxc_pipeline p, const uint8_t* const* frames, int n, int pinned,
+                         void (*on_result)(const void* view, size_t bytes, void* user), void* user,
+                         long long counters[4]) {
+    return guarded([&] {
+        gvxc_graph g = p->g;
+        if (g->cfg == 4) throw gvx::Error(gvx::ErrorCode::UnknownObject, "config 4 has no image output");
+        const std::size_t px = static_cast<std::size_t>(g->width) * static_cast<std::size_t>(g->height);
+        const std::size_t out_bytes = (g->cfg == 1 || g->cfg == 5 ? 2u : 1u) * px;
+        const gvx::ObjectId in_id = g->cg.input, out_id = g->cg.outputs.at(0);
+        long long acc[4] = {0, 0, 0, 0};
+        auto take = [&] {
+            const void* view = nullptr;
+            const gvx::ExecutionReport r = p->p->next_view(out_id, &view);
+            if (on_result) on_result(view, out_bytes, user); // before the next submit reuses the staging
+            acc[0] += r.counters.kernel_launches;
+            acc[1] += r.counters.pixels_read;
+            acc[2] += r.counters.pixels_written;
+            acc[3] += r.counters.transfers_executed;
+        };
+        for (int i = 0; i < n; ++i) {
+            if (p->p->pending() >= p->depth) take();
+            if (pinned) p->p->submit_pinned(in_id, frames[i], px);
+            else p->p->submit(in_id, frames[i], px);
+        }
+        while (p->p->pending() > 0) take();
+        if (counters)
+            for (int k = 0; k < 4; ++k) counters[k] = acc[k];
     });
 }
 

@@ -172,6 +172,28 @@ def test_host_pipeline_views(gvx, oracle_mod):
         assert np.array_equal(r, oracle_mod.port_run(2, f))
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_pipeline_stream(pinned, gvx, oracle_mod):
+    """gvxc_pipeline_stream: a whole stream in one native call, every result
+    handed over in order; counters are the per-frame sums."""
+    w, h = 517, 333
+    g = gvx.ConfigGraph(1, w, h)
+    stack = np.stack([gvx.random_u8(w, h, 150 + i) for i in range(7)])
+    pl = gvx.Pipeline(g, depth=3)
+    got = []
+    if pinned:
+        with gvx.PinnedHost([stack]):
+            cnt = pl.stream(list(stack), pinned=True, on_result=lambda v: got.append(np.array(v)))
+    else:
+        cnt = pl.stream(list(stack), on_result=lambda v: got.append(np.array(v)))
+    assert len(got) == len(stack)
+    for r, f in zip(got, stack):
+        assert np.array_equal(r, oracle_mod.port_run(1, f))
+    _, one = g.run_host(stack[0])
+    assert cnt["pixels_read"] == len(stack) * one["pixels_read"]
+    assert cnt["kernel_launches"] == len(stack) * one["kernel_launches"]
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 4])
 def test_host_pipeline_pinned_inputs(cfg, gvx, oracle_mod):
     """submit(pinned=True): frames DMAed straight from registered host memory
