@@ -320,7 +320,7 @@ struct SepParams {
     float inv_d;    // 1 / (d << shift), exact power of two
     float qscale;   // quotient FMA: 1.5*2^23 + q = rd(acc * qscale + qbase)
     float qbase;    //   magic form: inv_d, 1.5*2^23; fractional: 2^15 inv_d, 1.5*2^23 - 2^15 W inv_d
-    int frac;       // columns in fractional form (kernel variant kFrac)
+    int frac;       // 0 magic-form columns; 1 fractional form; 2 fractional + symmetric unit-end row mask
     int clamp255;   // q may exceed 255: 1 saturate to 255, 2 wrap (low byte)
     uint8_t* dst;   // K3 output, or K4's converted image (may be null)
     int64_t dst_pitch, dst_fstride;
@@ -381,6 +381,23 @@ __device__ __forceinline__ SepRow<R> sep_load_frac(const uint8_t* row, int off) 
 #pragma unroll
     for (int j = -R; j <= R + 1; ++j) r.p[j + R] = f2(col(j), col(j + 2));
     return r;
+}
+
+/// Horizontal pass of a symmetric row mask with unit ends (v[t] = v[K-1-t],
+/// v[0] = 1: the binomials): outer pairs added first, K - 1 instead of K
+/// packed ops per column pair.
+template <int K>
+__device__ __forceinline__ Q4 sep_horizontal_sym(const SepRow<K / 2>& r, const float* v) {
+    constexpr int R = K / 2;
+    Q4 h{add2(r.p[0], r.p[K - 1]), add2(r.p[1], r.p[K])};
+#pragma unroll
+    for (int t = 1; t < R; ++t) {
+        h.e = fma2(f2(v[t], v[t]), add2(r.p[t], r.p[K - 1 - t]), h.e);
+        h.o = fma2(f2(v[t], v[t]), add2(r.p[t + 1], r.p[K - t]), h.o);
+    }
+    h.e = fma2(f2(v[R], v[R]), r.p[R], h.e);
+    h.o = fma2(f2(v[R], v[R]), r.p[R + 1], h.o);
+    return h;
 }
 
 template <int K>
@@ -452,7 +469,7 @@ __device__ __forceinline__ void store4(uint8_t* dp, uint32_t w, int c, int width
 /// kMode 0: U8 stencil output; 1: unsharp chain sat_u8(2x - blur);
 /// 2: Convolve -> ConvertDepth -> per-CTA value histogram; 3: as 2 and also
 /// store the converted image.
-template <int K, int kMode, bool kClamp, bool kFrac>
+template <int K, int kMode, bool kClamp, int kLoad>
 __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
     constexpr int NT = sep_threads(kMode), TW = 4 * NT, SW = TW + 32;
     constexpr int R = K / 2;
@@ -552,9 +569,11 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         // into output o = j - i; output o is complete after row j = o + K - 1.
         Q4 acc[K];
         auto row = [&](int j, int slot0) { // slot0 = j mod K
-            const Q4 h = sep_horizontal<K>(kFrac ? sep_load_frac<R>(tile + j * SW, off)
-                                                 : sep_load<R>(tile + j * SW, off),
-                                           v);
+            // kLoad 0: magic form; 1: fractional form; 2: fractional + symmetric mask
+            const Q4 h = kLoad == 2 ? sep_horizontal_sym<K>(sep_load_frac<R>(tile + j * SW, off), v)
+                                    : sep_horizontal<K>(kLoad == 1 ? sep_load_frac<R>(tile + j * SW, off)
+                                                                   : sep_load<R>(tile + j * SW, off),
+                                                        v);
 #pragma unroll
             for (int i = 0; i < K; ++i) {
                 Q4& a = acc[(slot0 - i + 2 * K) % K];
@@ -674,6 +693,9 @@ bool sep_setup(const int32_t* mask, int K, long long d, int shift, SepParams& p,
     const long long W = su * sv, D = d << shift;
     p.frac = W * (32768 + 255) + d / 2 < (1LL << 24) && (W * 32768) % D == 0 ? 1 : 0;
     if (std::getenv("GVX_SEP_NOFRAC")) p.frac = 0; // A/B tests
+    bool sym = v[0] == 1 && !std::getenv("GVX_SEP_NOSYM");
+    for (int t = 0; t < K; ++t) sym = sym && v[t] == v[K - 1 - t];
+    if (p.frac && sym) p.frac = 2;
     if (p.frac) {
         p.bias = static_cast<float>(d / 2) / 32768.f;
         p.qscale = 32768.f / static_cast<float>(D);
@@ -683,18 +705,23 @@ bool sep_setup(const int32_t* mask, int K, long long d, int shift, SepParams& p,
     return true;
 }
 
-template <int K, int M, bool F>
+template <int K, int M, int F>
 void* sep_fn(bool clamp) {
     return clamp ? reinterpret_cast<void*>(&sep_kernel<K, M, true, F>)
                  : reinterpret_cast<void*>(&sep_kernel<K, M, false, F>);
 }
 
+template <int K, int M>
+void* sep_fn_f(bool clamp, int frac) {
+    return frac == 2 ? sep_fn<K, M, 2>(clamp) : frac == 1 ? sep_fn<K, M, 1>(clamp) : sep_fn<K, M, 0>(clamp);
+}
+
 template <int M>
-void* sep_fn_k(int k, bool clamp, bool frac) {
+void* sep_fn_k(int k, bool clamp, int frac) {
     switch (k) {
-    case 3: return frac ? sep_fn<3, M, true>(clamp) : sep_fn<3, M, false>(clamp);
-    case 5: return frac ? sep_fn<5, M, true>(clamp) : sep_fn<5, M, false>(clamp);
-    case 7: return frac ? sep_fn<7, M, true>(clamp) : sep_fn<7, M, false>(clamp);
+    case 3: return sep_fn_f<3, M>(clamp, frac);
+    case 5: return sep_fn_f<5, M>(clamp, frac);
+    case 7: return sep_fn_f<7, M>(clamp, frac);
     default: return nullptr;
     }
 }
@@ -843,7 +870,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
         long long qmax = 0;
         int lo = 0, hi = 0;
         range_of(a->conv_format, lo, hi);
-        if (sep_setup(a->mask, a->ksize, a->scale, a->shift, sp, qmax) && qmax <= hi && sep_fn_k<2>(a->ksize, false, false)) {
+        if (sep_setup(a->mask, a->ksize, a->scale, a->shift, sp, qmax) && qmax <= hi && sep_fn_k<2>(a->ksize, false, 0)) {
             sp.width = s.width;
             sp.band = Band{0, s.height, s.height, 0, 0};
             sp.clamp255 = (qmax >> a->shift) > 255 ? (a->wrap ? 2 : 1) : 0;
