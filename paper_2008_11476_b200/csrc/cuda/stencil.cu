@@ -370,12 +370,15 @@ __device__ __forceinline__ SepRow<R> sep_load(const uint8_t* row, int off) {
 /// As sep_load, with every column in fractional form 1 + x / 2^15 (byte
 /// permutes only, no de-biasing adds): weighted sums W + s / 2^15 stay exact
 /// while W (2^15 + 255) < 2^24 (checked on the host).
-template <int R>
+template <int R, bool kHalf = false>
 __device__ __forceinline__ SepRow<R> sep_load_frac(const uint8_t* row, int off) {
     const uint32_t wl = lds32(row, off - 4), wc = lds32(row, off), wr = lds32(row, off + 4);
+    // kHalf: 1 + (x + 1/2) / 2^15 (bit 7 of the constant), the rounding bias
+    // riding in the sources (see sep_kernel kLoad 3)
+    constexpr uint32_t kBase = kHalf ? 0x3F800080u : 0x3F800000u;
     auto col = [&](int j) -> float {
         const uint32_t w = j < 0 ? wl : (j < 4 ? wc : wr);
-        return __uint_as_float(__byte_perm(w, 0x3F800000u, 0x7604u | (static_cast<unsigned>(j & 3) << 4)));
+        return __uint_as_float(__byte_perm(w, kBase, 0x7604u | (static_cast<unsigned>(j & 3) << 4)));
     };
     SepRow<R> r;
 #pragma unroll
@@ -568,18 +571,40 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         // push accumulation: smem row j (global row y0 - R + j) adds u[i] * h(j)
         // into output o = j - i; output o is complete after row j = o + K - 1.
         Q4 acc[K];
+        Q4 hq[K]; // kLoad 3: the last K rows' horizontal sums (slot = row mod K)
         auto row = [&](int j, int slot0) { // slot0 = j mod K
-            // kLoad 0: magic form; 1: fractional form; 2: fractional + symmetric mask
-            const Q4 h = kLoad == 2 ? sep_horizontal_sym<K>(sep_load_frac<R>(tile + j * SW, off), v)
-                                    : sep_horizontal<K>(kLoad == 1 ? sep_load_frac<R>(tile + j * SW, off)
-                                                                   : sep_load<R>(tile + j * SW, off),
-                                                        v);
+            // kLoad 0: magic form; 1: fractional form; 2: fractional + symmetric
+            // row mask; 3: as 2 with symmetric column mask and the rounding
+            // bias in the sources: rows kept, outputs summed symmetrically
+            const Q4 h = kLoad == 3 ? sep_horizontal_sym<K>(sep_load_frac<R, true>(tile + j * SW, off), v)
+                         : kLoad == 2 ? sep_horizontal_sym<K>(sep_load_frac<R>(tile + j * SW, off), v)
+                                      : sep_horizontal<K>(kLoad == 1 ? sep_load_frac<R>(tile + j * SW, off)
+                                                                     : sep_load<R>(tile + j * SW, off),
+                                                          v);
+            if constexpr (kLoad == 3) {
+                hq[slot0] = h;
+                return;
+            }
 #pragma unroll
             for (int i = 0; i < K; ++i) {
                 Q4& a = acc[(slot0 - i + 2 * K) % K];
                 if (i == 0) a = Q4{fma2(f2(u[0], u[0]), h.e, bias), fma2(f2(u[0], u[0]), h.o, bias)};
                 else a = Q4{fma2(f2(u[i], u[i]), h.e, a.e), fma2(f2(u[i], u[i]), h.o, a.o)};
             }
+        };
+        /// kLoad 3: output o from rows o .. o+K-1 (row o+K-1 in slot `last`):
+        /// (h0 + h_{K-1}) + sum u_i (h_i + h_{K-1-i}) + u_R h_R.
+        auto vsum = [&](int last) {
+            auto at = [&](int i) -> const Q4& { return hq[(last + 1 + i) % K]; };
+            Q4 a{add2(at(0).e, at(K - 1).e), add2(at(0).o, at(K - 1).o)};
+#pragma unroll
+            for (int i = 1; i < R; ++i) {
+                a.e = fma2(f2(u[i], u[i]), add2(at(i).e, at(K - 1 - i).e), a.e);
+                a.o = fma2(f2(u[i], u[i]), add2(at(i).o, at(K - 1 - i).o), a.o);
+            }
+            a.e = fma2(f2(u[R], u[R]), at(R).e, a.e);
+            a.o = fma2(f2(u[R], u[R]), at(R).o, a.o);
+            return a;
         };
 #pragma unroll
         for (int j = 0; j < K - 1; ++j) row(j, j);
@@ -588,7 +613,8 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
             for (int t = 0; t < K; ++t) {
                 if (O + t >= n) break;
                 row(O + t + K - 1, (t + K - 1) % K); // O is a multiple of K
-                emit(acc[t]);                        // output o = O + t
+                if constexpr (kLoad == 3) emit(vsum((t + K - 1) % K));
+                else emit(acc[t]);                   // output o = O + t
             }
         }
         if (kMode >= 2 && have_pend) {
@@ -696,8 +722,14 @@ bool sep_setup(const int32_t* mask, int K, long long d, int shift, SepParams& p,
     bool sym = v[0] == 1 && !std::getenv("GVX_SEP_NOSYM");
     for (int t = 0; t < K; ++t) sym = sym && v[t] == v[K - 1 - t];
     if (p.frac && sym) p.frac = 2;
+    // both masks symmetric with unit ends, even sums and d == W: the bias d/2
+    // = W/2 rides in the sources as +1/2 each, so no output needs a bias add
+    // and every partial sum stays a multiple of 2^-15 (exact)
+    bool usym = u[0] == 1 && su % 2 == 0 && sv % 2 == 0 && W == d && !std::getenv("GVX_SEP_NOVSYM");
+    for (int t = 0; t < K; ++t) usym = usym && u[t] == u[K - 1 - t];
+    if (p.frac == 2 && usym) p.frac = 3;
     if (p.frac) {
-        p.bias = static_cast<float>(d / 2) / 32768.f;
+        p.bias = p.frac == 3 ? 0.f : static_cast<float>(d / 2) / 32768.f;
         p.qscale = 32768.f / static_cast<float>(D);
         p.qbase = static_cast<float>(12582912LL - W * 32768 / D);
     }
@@ -713,7 +745,12 @@ void* sep_fn(bool clamp) {
 
 template <int K, int M>
 void* sep_fn_f(bool clamp, int frac) {
-    return frac == 2 ? sep_fn<K, M, 2>(clamp) : frac == 1 ? sep_fn<K, M, 1>(clamp) : sep_fn<K, M, 0>(clamp);
+    switch (frac) {
+    case 3: return sep_fn<K, M, 3>(clamp);
+    case 2: return sep_fn<K, M, 2>(clamp);
+    case 1: return sep_fn<K, M, 1>(clamp);
+    default: return sep_fn<K, M, 0>(clamp);
+    }
 }
 
 template <int M>
