@@ -442,6 +442,14 @@ __device__ __forceinline__ Q4 sep_neg_quotient(Q4 acc, float qscale, float qbase
 /// ++ of a u8 shared-memory counter.  Volatile asm keeps the increments of
 /// one thread in program order (two may hit the same counter) while leaving
 /// the tile loads free to be scheduled around them.
+/// Counter increment as one shared-memory reduction on the (value, lane)
+/// word: each warp owns one byte of it (inc = 1 << 8 warp), at most 4 px x
+/// 48 rows = 192 counts per byte between merges, so no carry crosses bytes.
+/// No load -> add -> store dependency chain per pixel.
+__device__ __forceinline__ void smem_red_u32(uint32_t addr, uint32_t inc) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(inc) : "memory");
+}
+
 __device__ __forceinline__ void smem_inc_u8(uint32_t addr) {
     asm volatile(
         "{\n"
@@ -505,6 +513,9 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
     // kMode 2 counter of (value, lane, warp): value * 128 + lane * 4 + warp
     const uint32_t hbase = smem_u32(hist_dyn) + (((tid & 31) << 2) | (tid >> 5));
     const uint32_t hcnt = hbase - (0x4B400000u << 7);
+    const uint32_t hword = smem_u32(hist_dyn) + ((tid & 31) << 2); // the (value 0, lane) word
+    const uint32_t hwcnt = hword - (0x4B400000u << 7);
+    const uint32_t hinc = 1u << (8 * (tid >> 5));                  // this warp's byte
     float u[K], v[K];
 #pragma unroll
     for (int t = 0; t < K; ++t) u[t] = p.u[t], v[t] = p.v[t];
@@ -527,8 +538,13 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         // multiply-add gives the counter address hbase + value * 128
         auto count = [&](float qv, int i) {
             if (kEdge && i >= nv) return;
+#ifdef GVX_SEP_HIST_LDST
             if (kClamp && p.clamp255 == 2) smem_inc_u8(hbase + ((__float_as_uint(qv) & 0xFFu) << 7)); // Wrap
             else smem_inc_u8(hcnt + (__float_as_uint(qv) << 7));
+#else
+            if (kClamp && p.clamp255 == 2) smem_red_u32(hword + ((__float_as_uint(qv) & 0xFFu) << 7), hinc); // Wrap
+            else smem_red_u32(hwcnt + (__float_as_uint(qv) << 7), hinc);
+#endif
         };
         Q4 pend{};
         bool have_pend = false;
