@@ -296,7 +296,7 @@ constexpr int kSepThreads = 96;
 constexpr int kSepTW = 4 * kSepThreads; // 384 columns: 4K / 8K / 1080p split evenly
 constexpr int kSepSW = kSepTW + 32;     // tile origin x0 - 16 (16-byte aligned TMA start)
 #ifndef GVX_SEP_HIST_THREADS
-#define GVX_SEP_HIST_THREADS 96
+#define GVX_SEP_HIST_THREADS 128 // 4 warps: every byte of a (value, lane) counter word used (+2% with red increments)
 #endif
 /// Threads per CTA: the histogram modes may use all four counter bytes of a
 /// (value, lane) word with four warps.
@@ -306,7 +306,7 @@ __host__ __device__ constexpr int sep_threads(int mode) { return mode >= 2 ? GVX
 #endif
 constexpr int kSepTHMax = GVX_SEP_TH_MAX; // measured best of 32 / 48 / 64 (cfg3)
 #ifndef GVX_SEP_HIST_TH
-#define GVX_SEP_HIST_TH 48
+#define GVX_SEP_HIST_TH 40 // 4 CTAs / SM with 4-warp tiles
 #endif
 constexpr int kSepHistTH = GVX_SEP_HIST_TH; // u8 counters: 4 px * rows <= 255; measured best (24..60): 4 CTAs / SM
 constexpr int kSepHistBytes = 256 * 32 * 4;
