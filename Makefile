@@ -28,7 +28,7 @@ build/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(wildcard $(PKG)/csrc/cuda/*.cuh) include
 
 $(LIB)/libgvx_cuda.so: $(CUDA_OBJ)
 	@mkdir -p $(LIB)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $^ -o $@ -L$(CUDA_HOME)/lib64 -lnvrtc \
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC $^ -o $@ -L$(CUDA_HOME)/lib64 -lnvrtc -ldl \
 	    -Xlinker -rpath,$(CUDA_HOME)/lib64
 
 build/host/%.o: $(PKG)/csrc/host/%.cpp $(wildcard include/graphvx/*.hpp) $(wildcard $(PKG)/csrc/host/*.hpp) include/gvxb.h

@@ -1,13 +1,13 @@
 #!/usr/bin/env python
 """graphvx-b200 benchmark (driver contract, see task README / DESIGN.md §6).
 
-Default workload = BASELINE.json configs[1]: the Harris corner graph on
-3840x2160 U8 frames, executed through the optimized plan (fused sm_100a
-kernel) on device-resident frame batches.  One *step* = one graph execution
-over a batch of `--frames` frames.  Inputs rotate over two batches
-(footprint > L2).  `--config k` selects another BASELINE config (1..5);
-config 5 (16384^2 edge graph) runs as row bands with NVLink halo exchange
-when launched with N > 1 ranks.
+Default workload = BASELINE.json's headline configuration, configs[4]: the
+Gaussian3x3 -> Sobel3x3 -> Magnitude graph on one 16384^2 U8 image, run as
+N row bands (one per GPU / rank) through the library's BandedSession with
+the halo rows exchanged over NCCL every step.  One *step* = one execution
+of the graph over the whole image.  `--config k` selects the other BASELINE
+configs (1..4: frame batches through DeviceSession, N ranks = N frame
+replicas).
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the reference CPU
 engine (oracle/_ref, built unmodified from the reference sources) on bounded
@@ -40,8 +40,8 @@ CONFIG_NAME = {
 }
 # algorithmic HBM bytes per output pixel of the fused program
 ALGO_BYTES = {1: 3, 2: 2, 3: 2, 4: 1, 5: 3}
-KERNEL_NAME = {1: "edge_kernel", 2: "harris_kernel", 3: "sep_kernel<5,1> (separable stencil, unsharp epilogue)", 4: "sep_kernel<5,2> (separable conv + value histogram)",
-               5: "edge_kernel"}
+KERNEL_NAME = {1: "edge8_kernel", 2: "harris_kernel", 3: "sep_kernel<5,1> (separable stencil, unsharp epilogue)", 4: "sep_kernel<5,2> (separable conv + value histogram)",
+               5: "edge8_kernel"}
 # frames per launch: each step is one fused launch over a batch of frames; the
 # two rotating batches (inputs + outputs) span >= 4x the 126 MB L2 (SURVEY.md
 # §8d), which also amortises the ~20 us fixed cost of a launch (ramp + tail)
@@ -317,158 +317,117 @@ def run_frames(args, cfg, rank, world, local_rank):
 
 # --------------------------------------------------------------- banded cfg5
 
-class GvxbImage(ctypes.Structure):
-    _fields_ = [("data", ctypes.c_void_p), ("pitch", ctypes.c_int64), ("width", ctypes.c_int32),
-                ("height", ctypes.c_int32), ("format", ctypes.c_int32), ("frames", ctypes.c_int32),
-                ("frame_stride", ctypes.c_int64)]
-
-
-class GvxbBand(ctypes.Structure):
-    _fields_ = [("row0", ctypes.c_int32), ("row1", ctypes.c_int32), ("global_h", ctypes.c_int32),
-                ("src_row0", ctypes.c_int32), ("dst_row0", ctypes.c_int32)]
-
-
-class GvxbEdgeArgs(ctypes.Structure):
-    _fields_ = [("src", GvxbImage), ("gx", GvxbImage), ("gy", GvxbImage), ("mag", GvxbImage),
-                ("with_gauss", ctypes.c_int32), ("band", GvxbBand)]
-
-
-HALO = 2  # Gaussian radius 1 + Sobel radius 1
+def fullsize_fixture(cfg):
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "fullsize.json")) as f:
+            return json.load(f).get(str(cfg))
+    except Exception:
+        return None
 
 
 def run_banded(args, rank, world, local_rank):
-    """cfg5: 16384^2 edge graph as row bands; halo rows exchanged over NCCL."""
-    import torch
+    """cfg5: the 16384^2 edge graph as `world` row bands through the library
+    (gvx::BandedSession via gvx_c.h).  Each rank holds its owned input rows;
+    every step the band's 2 halo rows per neighbour arrive over NCCL
+    (gvxb_halo_start, issued by the library) while the interior rows run,
+    then the edge rows.  No torch on this path."""
+    import hashlib
     import paper_2008_11476_b200 as gvx
-    c, _ = gvx.libraries()
-    c.gvxb_edge.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbEdgeArgs)]
     W = H = args.size or 16384
-    r0, r1 = gvx.band_rows(H, world, rank)
-    s0, s1 = max(0, r0 - HALO), min(H, r1 + HALO)
+    comm = gvx.Comm(rank, world, local_rank) if world > 1 else None
+    global _comm
+    _comm = comm
     dev = gvx.Device(local_rank)
-    torch.cuda.set_device(local_rank)
-    stream = torch.cuda.Stream()  # a real stream: the legacy default stream does not order with ours
-    torch.cuda.set_stream(stream)
-    c.gvxb_ctx_set_stream(dev.h, ctypes.c_void_p(stream.cuda_stream))
-    src = torch.empty((s1 - s0, W), dtype=torch.uint8, device="cuda")
-    gen = torch.Generator(device="cuda").manual_seed(5 + rank)
-    src.random_(0, 256, generator=gen)
-    mag = torch.empty((r1 - r0, W), dtype=torch.int16, device="cuda")
-
-    import torch.distributed as dist
-    from paper_2008_11476_b200.bands import band_pieces, halo_exchange_start
-
-    def band_args(a0, a1):  # output rows [a0, a1) of my band
-        a = GvxbEdgeArgs()
-        a.src = GvxbImage(src.data_ptr(), W, W, s1 - s0, 0, 1, 0)
-        a.mag = GvxbImage(mag.data_ptr(), W * 2, W, r1 - r0, 2, 1, 0)
-        a.with_gauss = 1
-        a.band = GvxbBand(a0, a1, H, s0, r0)
-        return a
-
-    # interior rows need only owned source rows: computed while the halo rows
-    # are in flight; the <= 2 x HALO edge rows run once they have arrived
-    interior, edges = band_pieces(r0, r1, rank, world, HALO)
-    interior_args = band_args(*interior) if interior else None
-    edge_args = [band_args(*e) for e in edges]
-
-    def launch(a):
-        rc = c.gvxb_edge(dev.h, ctypes.byref(a))
-        if rc:
-            raise RuntimeError(c.gvxb_last_error().decode())
-
-    def step():
-        # posted first: NCCL orders after the previous step's kernels only
-        works = halo_exchange_start(dist, src, r0, r1, s0, s1, rank, world, HALO)
-        if interior_args is not None:
-            launch(interior_args)
-        for w in works:
-            w.wait()  # the stream waits for the halo rows
-        for a in edge_args:
-            launch(a)
-
+    graph = gvx.ConfigGraph(5, W, H, True)
+    band = gvx.Band(graph, rank, world, comm, device=local_rank)
+    band.set_stream(dev.stream)
+    L = band.layout
+    r0, r1, s0, s1 = L["row0"], L["row1"], L["src_row0"], L["src_row1"]
+    # the reference's random_buffer input (seed 5, SURVEY.md §8d); this rank
+    # uploads only the rows it owns: its halo rows come from the exchange
+    img = gvx.random_u8(W, H, 5)
+    band.upload(0, img[r0:r1], r0)
     for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        band.launch()
+    band.sync()
+    checked = None
+    if not args.no_check:
+        # bit-exact vs the reference: SHA-256 digests of oracle/_ref run_naive
+        # over the same input (tests/golden/fullsize.json), per 2048-row block
+        fx = fullsize_fixture(5)
+        if fx and fx["width"] == W and fx["height"] == H and r0 % fx["block_rows"] == 0 and \
+                (r1 % fx["block_rows"] == 0 or r1 == H):
+            out = band.download(1, r0, r1 - r0, np.int16)
+            br = fx["block_rows"]
+            ok = all(hashlib.sha256(out[a - r0:a - r0 + br].tobytes()).hexdigest() == fx["block_sha256"][a // br]
+                     for a in range(r0, r1, br))
+            checked = bool(allreduce_max(0.0 if ok else 1.0) == 0.0)
+            del out
+    ev = [dev.event() for _ in range(2)]
     barrier()
-    torch.cuda.synchronize()
+    dev.sync()
     with ClockSampler(local_rank) as clk:
         t_end = time.perf_counter() + args.clock_window
+        i = 0
         while time.perf_counter() < t_end:
-            step()
-            torch.cuda.synchronize()
-        launches0 = dev.launch_count()
-        e0.record(stream)
+            band.launch()
+            i += 1
+            if i % 20 == 0:
+                dev.sync()
+        dev.sync()
+        barrier()
+        launches0 = gvx.launch_count()  # every context of the process (the band has its own)
+        dev.record(ev[0])
         for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+            band.launch()
+        dev.record(ev[1])
+        dev.sync()
+    ms = dev.elapsed_ms(ev[0], ev[1])
     ms_max = allreduce_max(ms)
     value = W * H * args.steps / (ms_max / 1e3) / 1e6
-    launches = dev.launch_count() - launches0
-    # e2e: the rank's source rows (band + halo) in page-locked host memory,
-    # magnitude rows back to page-locked host memory, through the C-ABI:
-    # row chunks pipelined over three streams (upload of chunk i+1, kernel of
-    # chunk i, download of chunk i-1 overlap).  The halo rows come from the
-    # host image, so no exchange is needed on this path.
-    host_in = torch.from_numpy(np.random.default_rng(rank).integers(0, 256, size=(s1 - s0, W), dtype=np.uint8))
-    host_in = host_in.pin_memory()
-    host_out = torch.empty((r1 - r0, W), dtype=torch.int16).pin_memory()
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    chunk = 1024  # output rows per piece (measured: 512 / 1024 / 2048 within 3%)
-    pieces = [(a, min(r1, a + chunk)) for a in range(r0, r1, chunk)]
-    piece_args = [band_args(a0, a1) for a0, a1 in pieces]
-
-    def e2e_pass():
-        up = s0  # source rows [s0, up) uploaded
-        for (a0, a1), a in zip(pieces, piece_args):
-            hi = min(s1, a1 + HALO)
-            with torch.cuda.stream(s_in):
-                src[up - s0:hi - s0].copy_(host_in[up - s0:hi - s0], non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(s_in)
-            up = hi
-            stream.wait_event(ev_in)
-            launch(a)
-            ev_k = torch.cuda.Event()
-            ev_k.record(stream)
-            s_out.wait_event(ev_k)
-            with torch.cuda.stream(s_out):
-                host_out[a0 - r0:a1 - r0].copy_(mag[a0 - r0:a1 - r0], non_blocking=True)
-        s_out.synchronize()
-
-    e2e_pass()  # warm-up
+    launches = gvx.launch_count() - launches0
+    # e2e through the same API: BandedSession::run_host streams the rank's
+    # input slab (owned + halo rows, page-locked) up and its magnitude rows
+    # down in 1024-row pieces (upload, kernel, download overlapped on three
+    # streams); the halo rows come with the host slab, so no exchange
+    src = gvx.HostBuffer((s1 - s0, W), np.uint8)
+    src.array[:] = img[s0:s1]
+    dst = gvx.HostBuffer((r1 - r0, W), np.int16)
+    del img
+    band.run_host(src.ptr, W, 1, dst.ptr, 2 * W, 1024)  # warm-up
     n_e2e = max(3, min(args.steps, 5))
     barrier()
     t0 = time.perf_counter()
     for _ in range(n_e2e):
-        e2e_pass()
+        band.run_host(src.ptr, W, 1, dst.ptr, 2 * W, 1024)
     e2e_s = allreduce_max(time.perf_counter() - t0)
-    # the piecewise host result equals one whole-band launch over the same rows
     e2e_ok = None
-    if world == 1:
-        launch(band_args(r0, r1))
-        torch.cuda.synchronize()
-        e2e_ok = bool(torch.equal(mag.cpu(), host_out))
+    if not args.no_check:
+        want = band.download(1, r0, r1 - r0, np.int16)
+        e2e_ok = bool(np.array_equal(want, dst.array))
     e2e = {"value": W * H * n_e2e / e2e_s / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": (s1 - s0) * W,
-           "d2h_bytes_per_step": (r1 - r0) * W * 2, "checked_vs_whole_band": e2e_ok,
-           "path": "gvxb_edge C-ABI on 1024-row pieces of the band: page-locked host rows in / magnitude out, "
-                   "upload, kernel and download of consecutive pieces overlapped on three streams"}
+           "d2h_bytes_per_step": (r1 - r0) * W * 2, "checked_vs_device_result": e2e_ok,
+           "path": "gvx::BandedSession::run_host via gvx_c.h (gvxc_band_run_host): page-locked input slab rows in, "
+                   "magnitude rows out, 1024-row pieces with upload / kernel / download overlapped on three streams"}
+    src.close()
+    dst.close()
     return dict(value=value, ms_per_step=ms_max / args.steps, clocks=clk.summary(), launches=launches, e2e=e2e,
-                frames=1, kernel_ms=ms / args.steps if world == 1 else None, checked=None, w=W, h=H,
-                px_step=W * H, launches_per_step=1, describe=f"row band {r0}:{r1} of {H}, halo {HALO}")
+                frames=1, kernel_ms=ms / args.steps if world == 1 else None, checked=checked, w=W, h=H,
+                px_step=W * H, launches_per_step=band.launches(), describe=band.describe())
 
 
 # ------------------------------------------------------------- distributed
 
 _dist = None
+_comm = None  # gvx.Comm (library NCCL communicator) on the banded path
 
 
-def init_dist(world, local_rank):
+def init_dist(world, local_rank, cfg):
+    """Frame replicas (cfg1-4) use torch.distributed for the barrier and the
+    max-over-ranks timing; the banded cfg5 path uses the library's own NCCL
+    communicator (created in run_banded) and never imports torch."""
     global _dist
-    if world <= 1:
+    if world <= 1 or cfg == 5:
         return
     import torch
     import torch.distributed as dist
@@ -478,11 +437,15 @@ def init_dist(world, local_rank):
 
 
 def barrier():
-    if _dist is not None:
+    if _comm is not None:
+        _comm.barrier()
+    elif _dist is not None:
         _dist.barrier()
 
 
 def allreduce_max(x: float) -> float:
+    if _comm is not None:
+        return _comm.allreduce_max(x)
     if _dist is None:
         return x
     import torch
@@ -497,7 +460,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="graphvx-b200", choices=["graphvx-b200", "ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--frames", type=int, default=0)
     ap.add_argument("--size", type=int, default=0, help="cfg5 image side (default 16384)")
     ap.add_argument("--e2e-frames", type=int, default=48)
@@ -517,7 +480,8 @@ def main():
         r = cpu_reference_run(cfg, args.steps, args.warmup)
         line = {"metric": "graph Mpixel/s", "value": r["value"], "unit": "Mpixel/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": r["seconds"] / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": r["seconds"] / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong" if cfg == 5 else "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference random_buffer)",
                 "config": {"workload": CONFIG_NAME[cfg], "width": w, "height": h},
                 "impl": "reference", "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -527,7 +491,7 @@ def main():
         return 0
 
     os.environ.setdefault("GVX_DEVICE", str(local_rank))
-    init_dist(world, local_rank)
+    init_dist(world, local_rank, cfg)
     if cfg == 5:
         res = run_banded(args, rank, world, local_rank)
         scaling = "strong"
@@ -568,14 +532,18 @@ def main():
     line = {"metric": "graph Mpixel/s", "value": res["value"], "unit": "Mpixel/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (reference random_buffer frame + derived frames)",
+            "data": "synthetic (reference random_buffer, seed 5)" if cfg == 5 else
+                    "synthetic (reference random_buffer frame + derived frames)",
             "config": {"workload": CONFIG_NAME[cfg], "width": res["w"], "height": res["h"],
                        "frames_per_step": res["frames"], "l2": "inputs/outputs rotate over 2 batches spanning >= 4x L2"
                        if cfg != 5 else "16384^2 input > L2",
                        "parallelism": f"{'row bands' if cfg == 5 else 'frame replicas'} x{world}"},
             "e2e": res["e2e"], "roofline": roof, "cpu_baseline": cpu, "clocks": res["clocks"],
             "gpu_launches": res["launches"], "launches_per_step": res["launches_per_step"],
-            "checked_vs_oracle": res["checked"], "program": res["describe"]}
+            "checked_vs_oracle": res["checked"],
+            "checked_against": "SHA-256 of oracle/_ref run_naive (unmodified reference) per 2048-row block"
+                               if cfg == 5 else "oracle/gvx_oracle.c restatement, frame 0",
+            "program": res["describe"]}
     print(json.dumps(line), flush=True)
     return 0
 

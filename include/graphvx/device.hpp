@@ -9,6 +9,7 @@
 
 #include <memory>
 #include <string>
+#include <vector>
 
 namespace gvx {
 
@@ -99,6 +100,85 @@ public:
 
 private:
     std::unique_ptr<Impl> impl_;
+};
+
+/// Row-band geometry of one band (global rows; see gvxb_band_plan).
+struct BandLayout {
+    int rank = 0, world = 1;
+    int width = 0, height = 0; ///< the whole image
+    int row0 = 0, row1 = 0;    ///< owned output rows
+    int src_row0 = 0, src_row1 = 0; ///< rows of the input slab (owned + halo)
+    int halo = 0;              ///< total stencil radius of the program's input
+};
+
+class BandGroup;
+
+/// Row-band execution of an optimized plan (additive; no reference
+/// counterpart — the reference splits rows over <= 4 host threads,
+/// ref:src/execute.cpp:392-419).  Band `rank` of `world` computes output
+/// rows [row0, row1) of every image of the plan's device program.  Before
+/// each fused stencil group, the halo rows of the group's input that the
+/// band does not own come from its neighbours: over NCCL (`comm`, a
+/// gvxb_comm, one process per GPU) or by peer copies inside a BandGroup;
+/// Clamp borders use global rows, so the union of the bands equals the
+/// single-image result bit for bit.  The exchange overlaps the interior rows,
+/// which read owned rows only.  Programs must consist of hand-written
+/// stencil groups over images of one size (Error(UnsupportedKind) otherwise).
+class BandedSession {
+public:
+    BandedSession(const OptimizedPlan& plan, int rank, int world, void* comm = nullptr, int device = -1,
+                  int frames = 1);
+    ~BandedSession();
+    BandedSession(const BandedSession&) = delete;
+    BandedSession& operator=(const BandedSession&) = delete;
+
+    BandLayout layout() const;
+    /// Band storage of image `id`: its pointer addresses global row `first_row`
+    /// (the slab's first row: src_row0 for an input, row0 for an output).
+    DeviceTensor tensor(ObjectId id, int* first_row = nullptr, int* rows = nullptr);
+    void set_stream(void* cuda_stream);
+    /// Global rows [first_row, first_row + rows) of image `id` from / to host
+    /// memory (`pitch` bytes per host row); must lie inside the band storage.
+    void upload_rows(ObjectId id, const void* host, std::size_t pitch, int first_row, int rows, int frame = 0);
+    void download_rows(ObjectId id, void* host, std::size_t pitch, int first_row, int rows, int frame = 0);
+    /// Enqueue one execution (halo exchanges + all groups, all frames).
+    void launch();
+    void synchronize();
+    /// End to end from host memory, frame 0, single-group programs: `src` holds
+    /// the input slab rows [src_row0, src_row1), `dst` receives output rows
+    /// [row0, row1) of `output`.  Pieces of `piece_rows` output rows are
+    /// pipelined over three streams (upload of piece i+1, kernel of piece i,
+    /// download of piece i-1).  Returns when `dst` is complete.  Page-locked
+    /// host memory (gvxb_host_alloc / gvxb_host_register) DMAs at full rate.
+    void run_host(const void* src, std::size_t src_pitch, ObjectId output, void* dst, std::size_t dst_pitch,
+                  int piece_rows = 1024);
+    int launches_per_run() const;
+    std::string describe() const;
+
+    struct Impl;
+
+private:
+    friend class BandGroup;
+    std::unique_ptr<Impl> impl_;
+};
+
+/// `devices.size()` bands of one image driven from one process: band g runs
+/// on devices[g] (entries may repeat: several bands on one GPU), halo rows
+/// move as strided peer copies (NVLink P2P between GPUs) on an exchange
+/// stream, ordered by events, overlapping the interior rows.
+class BandGroup {
+public:
+    BandGroup(const OptimizedPlan& plan, const std::vector<int>& devices, int frames = 1);
+    ~BandGroup();
+    BandGroup(const BandGroup&) = delete;
+    BandGroup& operator=(const BandGroup&) = delete;
+    int size() const;
+    BandedSession& band(int g);
+    void launch();
+    void synchronize();
+
+private:
+    std::vector<std::unique_ptr<BandedSession>> bands_;
 };
 
 /// Number of CUDA devices visible (0 on a host without GPUs).

@@ -103,6 +103,39 @@ int gvxc_pipeline_stream(gvxc_pipeline p, const uint8_t* const* frames, int n, i
                          void (*on_result)(const void* view, size_t bytes, void* user), void* user,
                          long long counters[4]);
 
+/* ---- row bands across GPUs (gvx::BandedSession / gvx::BandGroup) ---------
+ * Slots as for sessions (0 = the input image, k >= 1 = config output k-1).
+ * comm: a gvxb_comm (NCCL, one process per GPU) or NULL for world == 1;
+ * device -1 = the library's device.  Rows are global image rows. */
+typedef struct gvxc_band_s* gvxc_band;
+typedef struct gvxc_group_s* gvxc_group;
+int gvxc_band_create(gvxc_graph g, int rank, int world, void* comm, int device, int frames, gvxc_band* out);
+int gvxc_band_destroy(gvxc_band b);
+/* {rank, world, width, height, row0, row1, src_row0, src_row1, halo} */
+int gvxc_band_layout(gvxc_band b, int32_t out[9]);
+int gvxc_band_tensor(gvxc_band b, int slot, void** dptr, int64_t* pitch, int64_t* fstride, int32_t* first_row,
+                     int32_t* rows);
+int gvxc_band_upload(gvxc_band b, int slot, const void* host, size_t pitch, int first_row, int rows, int frame);
+int gvxc_band_download(gvxc_band b, int slot, void* host, size_t pitch, int first_row, int rows, int frame);
+int gvxc_band_set_stream(gvxc_band b, void* stream);
+int gvxc_band_launch(gvxc_band b);
+int gvxc_band_sync(gvxc_band b);
+int gvxc_band_launches(gvxc_band b);
+/* End to end from host memory: src = input slab rows [src_row0, src_row1),
+ * dst = output rows [row0, row1) of `slot`; pieces pipelined (upload, kernel,
+ * download on three streams); returns when dst is complete. */
+int gvxc_band_run_host(gvxc_band b, const void* src, size_t src_pitch, int slot, void* dst, size_t dst_pitch,
+                       int piece_rows);
+int gvxc_band_describe(gvxc_band b, char* buf, size_t cap);
+/* n bands of one image in this process, band i on devices[i] (entries may
+ * repeat); halo rows move by strided peer copies.  gvxc_group_band returns a
+ * borrowed handle (destroyed with the group). */
+int gvxc_group_create(gvxc_graph g, int n, const int* devices, int frames, gvxc_group* out);
+int gvxc_group_destroy(gvxc_group gr);
+int gvxc_group_band(gvxc_group gr, int i, gvxc_band* out);
+int gvxc_group_launch(gvxc_group gr);
+int gvxc_group_sync(gvxc_group gr);
+
 /* ---- graph description files (graph_io.hpp, ref:src/graph_io.cpp) -------- */
 typedef struct gvxc_json_s* gvxc_json;
 /* save_graph_json(load_graph_json(text)); *len = bytes needed (incl. NUL). */

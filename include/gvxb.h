@@ -234,14 +234,63 @@ int gvxb_jit_launch(gvxb_ctx ctx, gvxb_module m, int kernel_index, const unsigne
 /* NVRTC log of the last failed build on this thread. */
 const char* gvxb_jit_log(void);
 
-/* ---- multi-GPU row bands ------------------------------------------------- */
+/* ---- multi-GPU row bands -------------------------------------------------
+ * No reference counterpart: the reference splits rows over <= 4 host
+ * threads (ref:src/execute.cpp:392-419).  Band g of G owns global output
+ * rows [row0, row1); a stencil group of radius R reads source rows
+ * [row0 - R, row1 + R) clipped to the image (its "slab"); the R rows on each
+ * side that it does not own come from its neighbours once per group
+ * execution. */
+
 /* Rows of band `rank` of `world` for an image of height h (balanced split). */
 int gvxb_band_rows(int32_t h, int32_t world, int32_t rank, int32_t* row0, int32_t* row1);
+
+/* One band's rows, overlap split and exchange schedule.  Side 0 is the
+ * upper neighbour (rank - 1), side 1 the lower (rank + 1); peer[s] = -1 when
+ * absent.  Interior rows read owned source rows only (computed while the
+ * halo rows are in flight); the edge rows read halo rows.  For world > 1
+ * every band must be at least `halo` rows tall (neighbours supply the whole
+ * halo). */
+typedef struct gvxb_band_plan {
+    int32_t height, world, rank, halo;
+    int32_t row0, row1;                   /* owned output rows */
+    int32_t src_row0, src_row1;           /* slab rows (owned + halo, clipped) */
+    int32_t interior_row0, interior_row1; /* empty when interior_row0 == interior_row1 */
+    int32_t n_edges;
+    int32_t edge_row0[2], edge_row1[2];
+    int32_t peer[2];
+    int32_t send_row0[2], send_rows[2];   /* my owned rows sent to peer[s] */
+    int32_t recv_row0[2], recv_rows[2];   /* halo rows received from peer[s] */
+} gvxb_band_plan;
+int gvxb_band_plan_make(int32_t height, int32_t world, int32_t rank, int32_t halo, gvxb_band_plan* out);
+
 /* Enable peer access from ctx's device to `peer_device` (NVLink P2P). */
 int gvxb_enable_peer(gvxb_ctx ctx, int peer_device);
-/* Copy `rows` rows of `row_bytes` from a peer device buffer (P2P over NVLink). */
+/* Copy `rows` rows of `row_bytes` between (possibly different) devices as
+ * one strided DMA (cudaMemcpy3DPeerAsync) on ctx's stream. */
 int gvxb_copy_peer_rows(gvxb_ctx ctx, void* dst, size_t dpitch, int dst_device, const void* src,
                         size_t spitch, int src_device, size_t row_bytes, size_t rows);
+/* ctx's stream waits for `ev` (recorded on any stream / device). */
+int gvxb_stream_wait_event(gvxb_ctx ctx, void* ev);
+
+/* NCCL communicator for the halo exchange between processes (one rank per
+ * GPU).  NCCL is loaded at first use (dlopen "libnccl.so.2");
+ * gvxb_comm_available() reports whether it could be. */
+#define GVXB_COMM_ID_BYTES 128
+typedef struct gvxb_comm_s* gvxb_comm;
+int gvxb_comm_available(void);
+int gvxb_comm_unique_id(uint8_t id[GVXB_COMM_ID_BYTES]);
+int gvxb_comm_create(int device, int rank, int world, const uint8_t id[GVXB_COMM_ID_BYTES], gvxb_comm* out);
+int gvxb_comm_destroy(gvxb_comm c);
+/* Posts the halo exchange of `plan` for every frame of `slab` (an image
+ * holding global rows [plan->src_row0, plan->src_row1)) on the
+ * communicator's stream, ordered after ctx's enqueued work; returns at
+ * once.  gvxb_halo_wait makes ctx's stream wait for it (sends included). */
+int gvxb_halo_start(gvxb_ctx ctx, gvxb_comm c, const gvxb_band_plan* plan, const gvxb_image* slab);
+int gvxb_halo_wait(gvxb_ctx ctx, gvxb_comm c);
+/* Host-value max over ranks (blocking); barrier = an all-reduce. */
+int gvxb_comm_allreduce_max(gvxb_comm c, double* value);
+int gvxb_comm_barrier(gvxb_comm c);
 
 #ifdef __cplusplus
 }

@@ -132,6 +132,32 @@ def _declare(c, g):
     g.gvxc_json_run.argtypes = [P, I, ctypes.c_ulonglong, U8P, SZ, ctypes.POINTER(SZ), ctypes.POINTER(L)]
     g.gvxc_json_pass_stats.argtypes = [P, ctypes.POINTER(L)]
     g.gvxc_json_describe.argtypes = [P, I, ctypes.c_char_p, ctypes.c_size_t]
+    I32P = ctypes.POINTER(ctypes.c_int32)
+    c.gvxb_band_plan_make.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_void_p]
+    c.gvxb_comm_available.restype = I
+    c.gvxb_comm_unique_id.argtypes = [ctypes.c_void_p]
+    c.gvxb_comm_create.argtypes = [I, I, I, ctypes.c_void_p, ctypes.POINTER(P)]
+    c.gvxb_comm_destroy.argtypes = [P]
+    c.gvxb_comm_allreduce_max.argtypes = [P, ctypes.POINTER(D)]
+    c.gvxb_comm_barrier.argtypes = [P]
+    g.gvxc_band_create.argtypes = [P, I, I, P, I, I, ctypes.POINTER(P)]
+    g.gvxc_band_destroy.argtypes = [P]
+    g.gvxc_band_layout.argtypes = [P, I32P]
+    g.gvxc_band_tensor.argtypes = [P, I, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.POINTER(ctypes.c_int64), I32P, I32P]
+    g.gvxc_band_upload.argtypes = [P, I, P, SZ, I, I, I]
+    g.gvxc_band_download.argtypes = [P, I, P, SZ, I, I, I]
+    g.gvxc_band_set_stream.argtypes = [P, P]
+    g.gvxc_band_launch.argtypes = [P]
+    g.gvxc_band_sync.argtypes = [P]
+    g.gvxc_band_launches.argtypes = [P]
+    g.gvxc_band_run_host.argtypes = [P, P, SZ, I, P, SZ, I]
+    g.gvxc_band_describe.argtypes = [P, ctypes.c_char_p, SZ]
+    g.gvxc_group_create.argtypes = [P, I, ctypes.POINTER(I), I, ctypes.POINTER(P)]
+    g.gvxc_group_destroy.argtypes = [P]
+    g.gvxc_group_band.argtypes = [P, I, ctypes.POINTER(P)]
+    g.gvxc_group_launch.argtypes = [P]
+    g.gvxc_group_sync.argtypes = [P]
 
 
 def _check_graph(rc: int):
@@ -697,6 +723,231 @@ def band_rows(height: int, world: int, rank: int):
     return r0.value, r1.value
 
 
+class GvxbBandPlan(ctypes.Structure):
+    """include/gvxb.h gvxb_band_plan."""
+    _fields_ = [(n, ctypes.c_int32) for n in ("height", "world", "rank", "halo", "row0", "row1", "src_row0",
+                                              "src_row1", "interior_row0", "interior_row1", "n_edges")] + [
+        ("edge_row0", ctypes.c_int32 * 2), ("edge_row1", ctypes.c_int32 * 2), ("peer", ctypes.c_int32 * 2),
+        ("send_row0", ctypes.c_int32 * 2), ("send_rows", ctypes.c_int32 * 2), ("recv_row0", ctypes.c_int32 * 2),
+        ("recv_rows", ctypes.c_int32 * 2)]
+
+
+def band_plan(height: int, world: int, rank: int, halo: int) -> dict:
+    """gvxb_band_plan_make: rows, overlap split and exchange schedule of one band."""
+    c, _ = _load()
+    p = GvxbBandPlan()
+    _check_cuda(c.gvxb_band_plan_make(height, world, rank, halo, ctypes.byref(p)))
+    d = {n: getattr(p, n) for n, _ in GvxbBandPlan._fields_[:11]}
+    d["edges"] = [(p.edge_row0[i], p.edge_row1[i]) for i in range(p.n_edges)]
+    d["peers"] = [None if p.peer[s] < 0 else {"peer": p.peer[s], "send": (p.send_row0[s], p.send_row0[s] + p.send_rows[s]),
+                                               "recv": (p.recv_row0[s], p.recv_row0[s] + p.recv_rows[s])}
+                  for s in range(2)]
+    return d
+
+
+class Comm:
+    """NCCL communicator of the C-ABI (gvxb_comm_*): the halo exchange and
+    the max-over-ranks timing of row bands, one process per GPU.  The
+    128-byte unique id travels from rank 0 through a file named after the
+    launcher (torchrun agent pid + MASTER_PORT) so no Python collective
+    library is needed."""
+
+    def __init__(self, rank: int, world: int, device: int, uid: bytes | None = None, timeout: float = 120.0):
+        c, _ = _load()
+        self.c, self.rank, self.world = c, rank, world
+        if uid is None:
+            uid = self._exchange_id(rank, timeout)
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        _check_cuda(c.gvxb_comm_create(device, rank, world, buf, ctypes.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        c, _ = _load()
+        buf = (ctypes.c_uint8 * 128)()
+        _check_cuda(c.gvxb_comm_unique_id(buf))
+        return bytes(buf)
+
+    def _exchange_id(self, rank: int, timeout: float) -> bytes:
+        import tempfile
+        import time
+        key = f"{os.getppid()}_{os.environ.get('MASTER_PORT', '0')}_{os.environ.get('TORCHELASTIC_RUN_ID', '')}"
+        path = pathlib.Path(tempfile.gettempdir()) / f"gvx_nccl_id_{key}"
+        if rank == 0:
+            uid = self.unique_id()
+            tmp = path.with_suffix(".tmp")
+            tmp.write_bytes(uid)
+            os.replace(tmp, path)
+            self._id_path = path
+            return uid
+        t_end = time.time() + timeout
+        while time.time() < t_end:
+            if path.exists():
+                data = path.read_bytes()
+                if len(data) == 128:
+                    return data
+            time.sleep(0.01)
+        raise TimeoutError(f"NCCL unique id not published at {path}")
+
+    def allreduce_max(self, x: float) -> float:
+        v = ctypes.c_double(x)
+        _check_cuda(self.c.gvxb_comm_allreduce_max(self.h, ctypes.byref(v)))
+        return v.value
+
+    def barrier(self):
+        _check_cuda(self.c.gvxb_comm_barrier(self.h))
+
+    def close(self):
+        if getattr(self, "_id_path", None) is not None:
+            try:
+                self._id_path.unlink()
+            except OSError:
+                pass
+            self._id_path = None
+        if getattr(self, "h", None):
+            self.c.gvxb_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Band:
+    """One row band of a ConfigGraph's plan (gvx::BandedSession through
+    gvx_c.h).  Slots: 0 = input image, k >= 1 = config output k - 1."""
+
+    def __init__(self, graph: "ConfigGraph", rank: int = 0, world: int = 1, comm: Comm | None = None,
+                 device: int = -1, frames: int = 1, _handle=None):
+        self.graph = graph
+        if _handle is not None:
+            self._h, self._own = _handle, False
+        else:
+            h = ctypes.c_void_p()
+            _check_graph(_graph.gvxc_band_create(graph.handle, rank, world, comm.h if comm else None, device, frames,
+                                                 ctypes.byref(h)))
+            self._h, self._own = h, True
+        v = (ctypes.c_int32 * 9)()
+        _check_graph(_graph.gvxc_band_layout(self._h, v))
+        self.layout = dict(zip(["rank", "world", "width", "height", "row0", "row1", "src_row0", "src_row1", "halo"],
+                               list(v)))
+
+    def close(self):
+        if getattr(self, "_own", False) and getattr(self, "_h", None):
+            _graph.gvxc_band_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def tensor(self, slot: int):
+        """(device pointer, pitch, frame stride, first global row, rows)."""
+        p, pitch, fs = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
+        r0, n = ctypes.c_int32(), ctypes.c_int32()
+        _check_graph(_graph.gvxc_band_tensor(self._h, slot, ctypes.byref(p), ctypes.byref(pitch), ctypes.byref(fs),
+                                             ctypes.byref(r0), ctypes.byref(n)))
+        return p.value, pitch.value, fs.value, r0.value, n.value
+
+    def upload(self, slot: int, rows: np.ndarray, first_row: int, frame: int = 0):
+        a = np.ascontiguousarray(rows)
+        _check_graph(_graph.gvxc_band_upload(self._h, slot, a.ctypes.data, a.strides[0], first_row, a.shape[0], frame))
+
+    def download(self, slot: int, first_row: int, rows: int, dtype, frame: int = 0) -> np.ndarray:
+        out = np.empty((rows, self.layout["width"]), dtype)
+        _check_graph(_graph.gvxc_band_download(self._h, slot, out.ctypes.data, out.strides[0], first_row, rows, frame))
+        return out
+
+    def set_stream(self, stream: int | None):
+        _check_graph(_graph.gvxc_band_set_stream(self._h, ctypes.c_void_p(stream or 0)))
+
+    def launch(self):
+        _check_graph(_graph.gvxc_band_launch(self._h))
+
+    def sync(self):
+        _check_graph(_graph.gvxc_band_sync(self._h))
+
+    def launches(self) -> int:
+        return _graph.gvxc_band_launches(self._h)
+
+    def run_host(self, src: int, src_pitch: int, slot: int, dst: int, dst_pitch: int, piece_rows: int = 1024):
+        """Host pointers (ints): src = input slab rows, dst = output rows of the band."""
+        _check_graph(_graph.gvxc_band_run_host(self._h, ctypes.c_void_p(src), src_pitch, slot, ctypes.c_void_p(dst),
+                                               dst_pitch, piece_rows))
+
+    def describe(self) -> str:
+        buf = ctypes.create_string_buffer(8192)
+        _check_graph(_graph.gvxc_band_describe(self._h, buf, len(buf)))
+        return buf.value.decode()
+
+
+class BandGroup:
+    """n row bands of one image in this process (gvx::BandGroup): band i on
+    devices[i]; halo rows by strided peer copies."""
+
+    def __init__(self, graph: "ConfigGraph", devices, frames: int = 1):
+        self.graph = graph
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        _check_graph(_graph.gvxc_group_create(graph.handle, len(devices), devs, frames, ctypes.byref(h)))
+        self._h = h
+        self.bands = []
+        for i in range(len(devices)):
+            bh = ctypes.c_void_p()
+            _check_graph(_graph.gvxc_group_band(h, i, ctypes.byref(bh)))
+            self.bands.append(Band(graph, _handle=bh))
+
+    def launch(self):
+        _check_graph(_graph.gvxc_group_launch(self._h))
+
+    def sync(self):
+        _check_graph(_graph.gvxc_group_sync(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            for b in self.bands:
+                b._h = None
+            _graph.gvxc_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HostBuffer:
+    """Page-locked host memory (gvxb_host_alloc) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        c, _ = _load()
+        self.c = c
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = ctypes.c_void_p()
+        _check_cuda(c.gvxb_host_alloc(max(n, 1), ctypes.byref(p)))
+        self.ptr = p.value
+        buf = (ctypes.c_uint8 * n).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.array = None
+            self.c.gvxb_host_free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 __all__ = ["GraphvxError", "ConfigGraph", "Session", "Device", "build", "device_count", "random_u8",
            "stencil_point", "conv_stats", "harris", "GraphFile", "json_roundtrip", "parse_outputs", "Pipeline",
-           "band_rows", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]
+           "band_rows", "band_plan", "Band", "BandGroup", "Comm", "HostBuffer", "libraries", "CONFIG_SIZE", "CONFIG_SEED", "CONFIG_FRAMES"]

@@ -388,12 +388,24 @@ int gvxc_pipeline_stream(gvxc_pipeline p, const uint8_t* const* frames, int n, i
             acc[2] += r.counters.pixels_written;
             acc[3] += r.counters.transfers_executed;
         };
-        for (int i = 0; i < n; ++i) {
-            if (p->p->pending() >= p->depth) take();
-            if (pinned) p->p->submit_pinned(in_id, frames[i], px);
-            else p->p->submit(in_id, frames[i], px);
+        try {
+            for (int i = 0; i < n; ++i) {
+                if (p->p->pending() >= p->depth) take();
+                if (pinned) p->p->submit_pinned(in_id, frames[i], px);
+                else p->p->submit(in_id, frames[i], px);
+            }
+            while (p->p->pending() > 0) take();
+        } catch (...) {
+            // no DMA may still read the caller's (possibly page-locked) frames
+            // after we return, and no stale result may reach the next call
+            while (p->p->pending() > 0) {
+                try {
+                    p->p->next();
+                } catch (...) {
+                }
+            }
+            throw;
         }
-        while (p->p->pending() > 0) take();
         if (counters)
             for (int k = 0; k < 4; ++k) counters[k] = acc[k];
     });
@@ -418,6 +430,141 @@ int gvxc_pipeline_next(gvxc_pipeline p, void* out, long long* hist, double* stat
             counters[3] = r.counters.transfers_executed;
         }
     });
+}
+
+} // extern "C"
+
+// ------------------------------------------------------------ row bands
+
+struct gvxc_band_s {
+    gvxc_graph g = nullptr;
+    std::unique_ptr<gvx::BandedSession> own;
+    gvx::BandedSession* s = nullptr;
+};
+
+struct gvxc_group_s {
+    gvxc_graph g = nullptr;
+    std::unique_ptr<gvx::BandGroup> group;
+    std::vector<std::unique_ptr<gvxc_band_s>> bands;
+};
+
+namespace {
+gvx::ObjectId band_slot(gvxc_graph g, int slot) {
+    if (slot == 0) return g->cg.input;
+    if (slot < 1 || slot > static_cast<int>(g->cg.outputs.size()))
+        throw gvx::Error(gvx::ErrorCode::UnknownObject, "bad slot");
+    return g->cg.outputs[static_cast<std::size_t>(slot - 1)];
+}
+} // namespace
+
+extern "C" {
+
+int gvxc_band_create(gvxc_graph g, int rank, int world, void* comm, int device, int frames, gvxc_band* out) {
+    return guarded([&] {
+        auto b = std::make_unique<gvxc_band_s>();
+        b->g = g;
+        b->own = std::make_unique<gvx::BandedSession>(g->plan, rank, world, comm, device, frames);
+        b->s = b->own.get();
+        *out = b.release();
+    });
+}
+
+int gvxc_band_destroy(gvxc_band b) {
+    if (b && b->own) delete b; // group members belong to their group
+    return 0;
+}
+
+int gvxc_band_layout(gvxc_band b, int32_t out[9]) {
+    return guarded([&] {
+        const gvx::BandLayout l = b->s->layout();
+        const int32_t v[9] = {l.rank, l.world, l.width, l.height, l.row0, l.row1, l.src_row0, l.src_row1, l.halo};
+        std::memcpy(out, v, sizeof(v));
+    });
+}
+
+int gvxc_band_tensor(gvxc_band b, int slot, void** dptr, int64_t* pitch, int64_t* fstride, int32_t* first_row,
+                     int32_t* rows) {
+    return guarded([&] {
+        int r0 = 0, n = 0;
+        const gvx::DeviceTensor t = b->s->tensor(band_slot(b->g, slot), &r0, &n);
+        *dptr = t.data;
+        if (pitch) *pitch = t.pitch;
+        if (fstride) *fstride = t.frame_stride;
+        if (first_row) *first_row = r0;
+        if (rows) *rows = n;
+    });
+}
+
+int gvxc_band_upload(gvxc_band b, int slot, const void* host, size_t pitch, int first_row, int rows, int frame) {
+    return guarded([&] { b->s->upload_rows(band_slot(b->g, slot), host, pitch, first_row, rows, frame); });
+}
+
+int gvxc_band_download(gvxc_band b, int slot, void* host, size_t pitch, int first_row, int rows, int frame) {
+    return guarded([&] { b->s->download_rows(band_slot(b->g, slot), host, pitch, first_row, rows, frame); });
+}
+
+int gvxc_band_set_stream(gvxc_band b, void* stream) {
+    return guarded([&] { b->s->set_stream(stream); });
+}
+
+int gvxc_band_launch(gvxc_band b) {
+    return guarded([&] { b->s->launch(); });
+}
+
+int gvxc_band_sync(gvxc_band b) {
+    return guarded([&] { b->s->synchronize(); });
+}
+
+int gvxc_band_launches(gvxc_band b) { return b->s->launches_per_run(); }
+
+int gvxc_band_run_host(gvxc_band b, const void* src, size_t src_pitch, int slot, void* dst, size_t dst_pitch,
+                       int piece_rows) {
+    return guarded([&] { b->s->run_host(src, src_pitch, band_slot(b->g, slot), dst, dst_pitch, piece_rows); });
+}
+
+int gvxc_band_describe(gvxc_band b, char* buf, size_t cap) {
+    return guarded([&] {
+        const std::string d = b->s->describe();
+        if (cap) {
+            std::strncpy(buf, d.c_str(), cap - 1);
+            buf[cap - 1] = '\0';
+        }
+    });
+}
+
+int gvxc_group_create(gvxc_graph g, int n, const int* devices, int frames, gvxc_group* out) {
+    return guarded([&] {
+        auto gr = std::make_unique<gvxc_group_s>();
+        gr->g = g;
+        gr->group = std::make_unique<gvx::BandGroup>(g->plan, std::vector<int>(devices, devices + n), frames);
+        for (int i = 0; i < n; ++i) {
+            auto b = std::make_unique<gvxc_band_s>();
+            b->g = g;
+            b->s = &gr->group->band(i);
+            gr->bands.push_back(std::move(b));
+        }
+        *out = gr.release();
+    });
+}
+
+int gvxc_group_destroy(gvxc_group gr) {
+    delete gr;
+    return 0;
+}
+
+int gvxc_group_band(gvxc_group gr, int i, gvxc_band* out) {
+    return guarded([&] {
+        if (i < 0 || i >= static_cast<int>(gr->bands.size())) throw gvx::Error(gvx::ErrorCode::UnknownObject, "bad band");
+        *out = gr->bands[static_cast<std::size_t>(i)].get();
+    });
+}
+
+int gvxc_group_launch(gvxc_group gr) {
+    return guarded([&] { gr->group->launch(); });
+}
+
+int gvxc_group_sync(gvxc_group gr) {
+    return guarded([&] { gr->group->synchronize(); });
 }
 
 } // extern "C"

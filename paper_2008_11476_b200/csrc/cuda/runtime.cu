@@ -374,38 +374,4 @@ int gvxb_jit_launch(gvxb_ctx ctx, gvxb_module m, int k, const unsigned grid[3], 
     return GVXB_OK;
 }
 
-// --------------------------------------------------------------- row bands
-
-int gvxb_band_rows(int32_t h, int32_t world, int32_t rank, int32_t* row0, int32_t* row1) {
-    if (world < 1 || rank < 0 || rank >= world || h < 0) return fail(GVXB_ERR_INVALID, "bad band query");
-    const int64_t base = h / world, extra = h % world;
-    *row0 = static_cast<int32_t>(rank * base + (rank < extra ? rank : extra));
-    *row1 = static_cast<int32_t>(*row0 + base + (rank < extra ? 1 : 0));
-    return GVXB_OK;
-}
-
-int gvxb_enable_peer(gvxb_ctx ctx, int peer) {
-    int can = 0;
-    cudaDeviceCanAccessPeer(&can, ctx->device, peer);
-    if (!can) return fail(GVXB_ERR_UNSUPPORTED, "peer access not possible");
-    cudaSetDevice(ctx->device);
-    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
-    if (e == cudaErrorPeerAccessAlreadyEnabled) {
-        cudaGetLastError();
-        return GVXB_OK;
-    }
-    return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
-}
-
-int gvxb_copy_peer_rows(gvxb_ctx ctx, void* dst, size_t dpitch, int dst_dev, const void* src, size_t spitch,
-                        int src_dev, size_t row_bytes, size_t rows) {
-    for (size_t r = 0; r < rows; ++r) {
-        cudaError_t e = cudaMemcpyPeerAsync(static_cast<char*>(dst) + r * dpitch, dst_dev,
-                                            static_cast<const char*>(src) + r * spitch, src_dev, row_bytes,
-                                            ctx->stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyPeerAsync");
-    }
-    return GVXB_OK;
-}
-
 } // extern "C"

@@ -309,6 +309,10 @@ constexpr int kSepTHMax = GVX_SEP_TH_MAX; // measured best of 32 / 48 / 64 (cfg3
 #define GVX_SEP_HIST_TH 40 // 4 CTAs / SM with 4-warp tiles
 #endif
 constexpr int kSepHistTH = GVX_SEP_HIST_TH; // u8 counters: 4 px * rows <= 255; measured best (24..60): 4 CTAs / SM
+// each warp owns one byte of a (value, lane) counter word: at most 4 warps,
+// and a tile's 4 px x kSepHistTH rows per lane must not carry out of a byte
+static_assert(GVX_SEP_HIST_THREADS % 32 == 0 && GVX_SEP_HIST_THREADS <= 128, "one counter byte per warp");
+static_assert(4 * kSepHistTH <= 255, "u8 histogram counters would wrap");
 constexpr int kSepHistBytes = 256 * 32 * 4;
 
 struct SepParams {
@@ -439,17 +443,18 @@ __device__ __forceinline__ Q4 sep_neg_quotient(Q4 acc, float qscale, float qbase
     return q;
 }
 
-/// ++ of a u8 shared-memory counter.  Volatile asm keeps the increments of
-/// one thread in program order (two may hit the same counter) while leaving
-/// the tile loads free to be scheduled around them.
 /// Counter increment as one shared-memory reduction on the (value, lane)
-/// word: each warp owns one byte of it (inc = 1 << 8 warp), at most 4 px x
-/// 48 rows = 192 counts per byte between merges, so no carry crosses bytes.
-/// No load -> add -> store dependency chain per pixel.
+/// word: each warp owns one byte of it (inc = 1 << 8 warp), at most
+/// 4 px x kSepHistTH rows counts per byte between merges (static_assert
+/// below), so no carry crosses bytes.  No load -> add -> store dependency
+/// chain per pixel.
 __device__ __forceinline__ void smem_red_u32(uint32_t addr, uint32_t inc) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(inc) : "memory");
 }
 
+/// ++ of a u8 shared-memory counter.  Volatile asm keeps the increments of
+/// one thread in program order (two may hit the same counter) while leaving
+/// the tile loads free to be scheduled around them.
 __device__ __forceinline__ void smem_inc_u8(uint32_t addr) {
     asm volatile(
         "{\n"
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
 
     if (kMode < 2) return;
     __syncthreads();
-    // merge: thread t owns values t, t + 96, t + 192 (< 256); the 128 counter
+    // merge: thread t owns values t, t + NT, ... (< 256); the 128 counter
     // bytes of a value are read as 8 uint4 in a rotated order (bank spread)
     long long s1 = 0, s2 = 0;
     for (int val = tid; val < 256; val += NT) {
@@ -667,8 +672,8 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
             if (!p.identity) {
                 const long long t = (static_cast<long long>(val) - p.offset) * p.bins;
                 bin = t / p.range;
-                if (bin < 0 || bin >= p.bins) continue;
             }
+            if (bin < 0 || bin >= p.bins) continue; // out of range: skipped (ref:src/execute.cpp:717-724)
             atomicAdd(reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + bin].bits),
                       static_cast<unsigned long long>(cnt));
         }

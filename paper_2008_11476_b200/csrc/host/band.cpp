@@ -1,0 +1,489 @@
+// Row-band execution of an optimized plan over several GPUs (device.hpp:
+// BandedSession, BandGroup).  No reference counterpart: the reference
+// splits rows over <= 4 host threads of one process
+// (ref:src/execute.cpp:392-419); here each band is a GPU, one halo exchange
+// per fused stencil group, all device work through the
+// C-ABI (include/gvxb.h).
+//
+// Storage: every image object of the program is held as a slab of global
+// rows [row0 - R, row1 + R) clipped to the image, R = the largest radius of
+// the groups reading it (0 for outputs).  A group's launch writes rows
+// [row0, row1) of its outputs; before it runs, the R rows of its input that
+// the band does not own are received from the neighbours (the interior rows
+// run meanwhile: they read owned rows only).
+#include "graphvx/device.hpp"
+#include "graphvx/error.hpp"
+#include "program.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+
+namespace gvx {
+
+namespace {
+
+using dev::check;
+
+int unit_radius(const dev::Unit& u) {
+    switch (u.kind) {
+    case dev::Unit::Kind::Edge: return u.with_gauss ? 2 : 1; // Gaussian3x3 + Sobel3x3
+    case dev::Unit::Kind::Harris: return 2;                  // Sobel3x3 + Box3x3
+    case dev::Unit::Kind::Stencil: return u.ksize / 2;
+    default: return -1;
+    }
+}
+
+struct Slab {
+    void* ptr = nullptr;
+    std::int64_t pitch = 0, fstride = 0;
+    int row0 = 0, rows = 0; ///< global rows held
+    int halo = 0;           ///< rows beyond the band on each side (clipped)
+    int bpp = 1, format = 0;
+    bool owned = false;
+};
+
+} // namespace
+
+struct BandedSession::Impl {
+    std::shared_ptr<dev::Program> prog;
+    int rank = 0, world = 1, device = 0, frames = 1;
+    int W = 0, H = 0;
+    gvxb_ctx ctx = nullptr;  ///< compute stream
+    gvxb_ctx xctx = nullptr; ///< exchange stream (peer copies in a group)
+    gvxb_comm comm = nullptr;
+    gvxb_band_plan band{};   ///< rows of this band (halo 0)
+    std::map<ObjectId, Slab> slabs;
+    std::vector<gvxb_band_plan> unit_plan; ///< per unit: split by its radius
+    std::vector<gvxb_band_plan> src_plan;  ///< per unit: exchange of its input's whole slab halo
+    int input_halo = 0;
+    ObjectId input = kInvalidId;
+
+    // BandGroup wiring (peer copies)
+    std::vector<Impl*>* group = nullptr;
+    int index = 0;
+    void* ev_ready = nullptr; ///< compute stream reached the exchange point
+    void* ev_xdone = nullptr; ///< exchange stream finished pulling
+    bool pulled = false;
+
+    // run_host pipeline
+    gvxb_ctx up = nullptr, dn = nullptr;
+    std::vector<void*> ev_up, ev_k;
+
+    ~Impl() {
+        if (ctx) gvxb_sync(ctx);
+        if (xctx) gvxb_sync(xctx);
+        if (up) gvxb_sync(up);
+        if (dn) gvxb_sync(dn);
+        for (auto& kv : slabs)
+            if (kv.second.owned) gvxb_free(ctx, kv.second.ptr);
+        for (void* e : ev_up) gvxb_event_destroy(e);
+        for (void* e : ev_k) gvxb_event_destroy(e);
+        if (ev_ready) gvxb_event_destroy(ev_ready);
+        if (ev_xdone) gvxb_event_destroy(ev_xdone);
+        for (gvxb_ctx c : {up, dn, xctx, ctx})
+            if (c) gvxb_ctx_destroy(c);
+    }
+
+    void init(const OptimizedPlan& plan, int rank_, int world_, void* comm_, int device_, int frames_) {
+        prog = dev::program_of(plan);
+        rank = rank_;
+        world = world_;
+        frames = std::max(1, frames_);
+        comm = static_cast<gvxb_comm>(comm_);
+        if (world < 1 || rank < 0 || rank >= world) throw Error(ErrorCode::BadKernel, "bad band rank / world");
+        std::map<ObjectId, int> radius_in; // object -> largest radius of the groups reading it
+        for (const dev::Unit& u : prog->units) {
+            const int r = unit_radius(u);
+            if (r < 0)
+                throw Error(ErrorCode::UnsupportedKind,
+                            "row-band execution needs a program of hand-written stencil groups; '" + u.label +
+                                "' is not one (run it with DeviceSession per frame instead)");
+            radius_in[u.src] = std::max(radius_in[u.src], r);
+        }
+        if (prog->units.empty()) throw Error(ErrorCode::UnsupportedKind, "row-band execution of an empty program");
+        for (const auto& [id, oi] : prog->objects) {
+            if (oi.desc.kind != ObjKind::Image)
+                throw Error(ErrorCode::UnsupportedKind, "row-band execution: non-image object in the program", id);
+            if (W == 0) W = oi.desc.width, H = oi.desc.height;
+            if (oi.desc.width != W || oi.desc.height != H)
+                throw Error(ErrorCode::UnsupportedKind, "row-band execution needs images of one size", id);
+        }
+        device = device_ >= 0 ? device_ : gvxb_ctx_device(dev::context());
+        ctx = dev::own_context(device);
+        check(gvxb_band_plan_make(H, world, rank, 0, &band), "band plan");
+        for (const auto& [id, oi] : prog->objects) {
+            auto it = radius_in.find(id);
+            const int R = it == radius_in.end() ? 0 : it->second;
+            gvxb_band_plan p{};
+            check(gvxb_band_plan_make(H, world, rank, R, &p), "band plan");
+            Slab s;
+            s.row0 = p.src_row0;
+            s.rows = p.src_row1 - p.src_row0;
+            s.halo = R;
+            s.bpp = bytes_per_pixel(oi.desc.format);
+            s.format = static_cast<int>(oi.desc.format);
+            const std::int64_t row = static_cast<std::int64_t>(W) * s.bpp;
+            s.pitch = std::max<std::int64_t>(128, (row + 127) / 128 * 128);
+            s.fstride = s.pitch * std::max(1, s.rows);
+            s.owned = true;
+            const std::size_t bytes = static_cast<std::size_t>(s.fstride) * frames;
+            check(gvxb_alloc(ctx, bytes, &s.ptr), "band allocation");
+            check(gvxb_memset(ctx, s.ptr, 0, bytes), "band clear");
+            slabs[id] = s;
+            if (!oi.produced && R > 0 && input == kInvalidId) input = id, input_halo = R;
+        }
+        if (input == kInvalidId) input = prog->units.front().src, input_halo = radius_in[input];
+        for (const dev::Unit& u : prog->units) {
+            gvxb_band_plan p{}, q{};
+            check(gvxb_band_plan_make(H, world, rank, unit_radius(u), &p), "band plan");
+            check(gvxb_band_plan_make(H, world, rank, slabs.at(u.src).halo, &q), "band plan");
+            unit_plan.push_back(p);
+            src_plan.push_back(q);
+        }
+    }
+
+    gvxb_image image(ObjectId id, bool at_band_row0) {
+        gvxb_image im{};
+        if (id == kInvalidId) return im;
+        const Slab& s = slabs.at(id);
+        const int skip = at_band_row0 ? band.row0 - s.row0 : 0;
+        im.data = static_cast<char*>(s.ptr) + static_cast<std::int64_t>(skip) * s.pitch;
+        im.pitch = s.pitch;
+        im.width = W;
+        im.height = s.rows - skip;
+        im.format = s.format;
+        im.frames = frames;
+        im.frame_stride = s.fstride;
+        return im;
+    }
+
+    /// Output rows [r0, r1) of unit `u` (its input halo rows must be present).
+    void compute(const dev::Unit& u, int r0, int r1, gvxb_ctx on) {
+        if (r1 <= r0) return;
+        const Slab& src = slabs.at(u.src);
+        const gvxb_band b{r0, r1, H, src.row0, band.row0};
+        switch (u.kind) {
+        case dev::Unit::Kind::Edge: {
+            gvxb_edge_args a{};
+            a.src = image(u.src, false);
+            a.gx = image(u.out[0], true);
+            a.gy = image(u.out[1], true);
+            a.mag = image(u.out[2], true);
+            a.with_gauss = u.with_gauss ? 1 : 0;
+            a.band = b;
+            check(gvxb_edge(on, &a), "gvxb_edge (band)");
+            return;
+        }
+        case dev::Unit::Kind::Harris: {
+            gvxb_harris_args a{};
+            a.src = image(u.src, false);
+            a.mask = image(u.out[0], true);
+            a.response = image(u.out[1], true);
+            a.k = u.k_param;
+            a.threshold = u.threshold;
+            a.band = b;
+            check(gvxb_harris(on, &a), "gvxb_harris (band)");
+            return;
+        }
+        case dev::Unit::Kind::Stencil: {
+            gvxb_stencil_args a{};
+            a.src = image(u.src, false);
+            a.dst = image(u.out[0], true);
+            a.ksize = u.ksize;
+            std::memcpy(a.mask, u.mask, sizeof(a.mask));
+            a.div_num = 1;
+            a.div_den = u.divisor;
+            a.mode = u.mode;
+            a.band = b;
+            check(gvxb_stencil_point(on, &a), "gvxb_stencil_point (band)");
+            return;
+        }
+        default: throw Error(ErrorCode::UnsupportedKind, "row-band execution: unsupported group");
+        }
+    }
+
+    bool needs_exchange(std::size_t i) const {
+        const gvxb_band_plan& q = src_plan[i];
+        return world > 1 && (q.peer[0] >= 0 || q.peer[1] >= 0);
+    }
+
+    /// Posts unit i's input halo exchange (NCCL).  Peer mode: BandGroup.
+    void exchange_nccl(std::size_t i) {
+        if (!comm) throw Error(ErrorCode::UnsupportedKind, "row bands with world > 1 need a communicator or a BandGroup");
+        gvxb_image slab = image(prog->units[i].src, false);
+        check(gvxb_halo_start(ctx, comm, &src_plan[i], &slab), "halo exchange");
+    }
+
+    /// Peer mode, phase 2: pull unit i's input halo rows from the neighbours
+    /// on the exchange stream once both sides reached the exchange point.
+    void exchange_peer(std::size_t i) {
+        const gvxb_band_plan& q = src_plan[i];
+        const ObjectId id = prog->units[i].src;
+        const Slab& me = slabs.at(id);
+        check(gvxb_stream_wait_event(xctx, ev_ready), "exchange ordering");
+        for (int side = 0; side < 2; ++side) {
+            if (q.peer[side] < 0) continue;
+            Impl* nb = (*group)[static_cast<std::size_t>(q.peer[side])];
+            check(gvxb_stream_wait_event(xctx, nb->ev_ready), "exchange ordering");
+            const Slab& ns = nb->slabs.at(id);
+            for (int f = 0; f < frames; ++f) {
+                char* dst = static_cast<char*>(me.ptr) + f * me.fstride +
+                            static_cast<std::int64_t>(q.recv_row0[side] - me.row0) * me.pitch;
+                const char* src = static_cast<const char*>(ns.ptr) + f * ns.fstride +
+                                  static_cast<std::int64_t>(q.recv_row0[side] - ns.row0) * ns.pitch;
+                check(gvxb_copy_peer_rows(xctx, dst, static_cast<std::size_t>(me.pitch), device, src,
+                                          static_cast<std::size_t>(ns.pitch), nb->device,
+                                          static_cast<std::size_t>(W) * me.bpp,
+                                          static_cast<std::size_t>(q.recv_rows[side])),
+                      "halo peer copy");
+            }
+        }
+        check(gvxb_event_record(xctx, ev_xdone), "exchange event");
+        pulled = true;
+    }
+
+    void wait_exchange() {
+        if (group) check(gvxb_stream_wait_event(ctx, ev_xdone), "halo wait");
+        else check(gvxb_halo_wait(ctx, comm), "halo wait");
+    }
+
+    /// Unit i after its exchange was posted: interior rows, wait, edge rows.
+    void run_unit(std::size_t i, bool exchanged) {
+        const dev::Unit& u = prog->units[i];
+        if (!exchanged) {
+            compute(u, band.row0, band.row1, ctx);
+            return;
+        }
+        const gvxb_band_plan& p = unit_plan[i];
+        compute(u, p.interior_row0, p.interior_row1, ctx);
+        wait_exchange();
+        for (int e = 0; e < p.n_edges; ++e) compute(u, p.edge_row0[e], p.edge_row1[e], ctx);
+    }
+
+    void launch_standalone() {
+        for (std::size_t i = 0; i < prog->units.size(); ++i) {
+            const bool x = needs_exchange(i);
+            if (x) exchange_nccl(i);
+            run_unit(i, x);
+        }
+    }
+
+    void ensure_pipeline(std::size_t pieces) {
+        if (!up) up = dev::own_context(device), dn = dev::own_context(device);
+        while (ev_up.size() < pieces) {
+            void* a = nullptr;
+            void* b = nullptr;
+            check(gvxb_event_create(&a), "event");
+            check(gvxb_event_create(&b), "event");
+            ev_up.push_back(a);
+            ev_k.push_back(b);
+        }
+    }
+
+    void run_host(const void* src, std::size_t spitch, ObjectId output, void* dst, std::size_t dpitch, int piece) {
+        if (prog->units.size() != 1)
+            throw Error(ErrorCode::UnsupportedKind, "BandedSession::run_host needs a single-group program");
+        const dev::Unit& u = prog->units[0];
+        const Slab& in = slabs.at(u.src);
+        const Slab& out = slabs.at(output);
+        const int R = unit_radius(u);
+        piece = std::max(piece, 1);
+        std::vector<std::pair<int, int>> pieces;
+        for (int a = band.row0; a < band.row1; a += piece) pieces.emplace_back(a, std::min(band.row1, a + piece));
+        ensure_pipeline(pieces.size());
+        const std::size_t in_row = static_cast<std::size_t>(W) * in.bpp, out_row = static_cast<std::size_t>(W) * out.bpp;
+        int uploaded = in.row0; // source rows [in.row0, uploaded) are on the device
+        const int in_end = in.row0 + in.rows;
+        for (std::size_t k = 0; k < pieces.size(); ++k) {
+            const auto [a0, a1] = pieces[k];
+            const int hi = std::min(in_end, a1 + R);
+            if (hi > uploaded) {
+                check(gvxb_upload_2d(up, static_cast<char*>(in.ptr) + static_cast<std::int64_t>(uploaded - in.row0) * in.pitch,
+                                     static_cast<std::size_t>(in.pitch),
+                                     static_cast<const char*>(src) + static_cast<std::size_t>(uploaded - in.row0) * spitch,
+                                     spitch, in_row, static_cast<std::size_t>(hi - uploaded)),
+                      "band piece upload");
+                uploaded = hi;
+            }
+            check(gvxb_event_record(up, ev_up[k]), "event");
+            check(gvxb_stream_wait_event(ctx, ev_up[k]), "event wait");
+            compute(u, a0, a1, ctx);
+            check(gvxb_event_record(ctx, ev_k[k]), "event");
+            check(gvxb_stream_wait_event(dn, ev_k[k]), "event wait");
+            check(gvxb_download_2d(dn, static_cast<char*>(dst) + static_cast<std::size_t>(a0 - band.row0) * dpitch, dpitch,
+                                   static_cast<const char*>(out.ptr) + static_cast<std::int64_t>(a0 - out.row0) * out.pitch,
+                                   static_cast<std::size_t>(out.pitch), out_row, static_cast<std::size_t>(a1 - a0)),
+                  "band piece download");
+        }
+        check(gvxb_sync(dn), "band download sync");
+        check(gvxb_sync(ctx), "band compute sync");
+    }
+
+    void synchronize() {
+        check(gvxb_sync(ctx), "band sync");
+        std::uint32_t status = 0;
+        check(gvxb_status_read(ctx, &status), "status read");
+        if (status & GVXB_STATUS_DIV_BY_ZERO) {
+            gvxb_status_reset(ctx);
+            throw Error(ErrorCode::DivByZero, "division by zero in a device kernel");
+        }
+    }
+};
+
+// ------------------------------------------------------------ BandedSession
+
+BandedSession::BandedSession(const OptimizedPlan& plan, int rank, int world, void* comm, int device, int frames)
+    : impl_(std::make_unique<Impl>()) {
+    impl_->init(plan, rank, world, comm, device, frames);
+}
+
+BandedSession::~BandedSession() = default;
+
+BandLayout BandedSession::layout() const {
+    BandLayout l;
+    l.rank = impl_->rank;
+    l.world = impl_->world;
+    l.width = impl_->W;
+    l.height = impl_->H;
+    l.row0 = impl_->band.row0;
+    l.row1 = impl_->band.row1;
+    const Slab& in = impl_->slabs.at(impl_->input);
+    l.src_row0 = in.row0;
+    l.src_row1 = in.row0 + in.rows;
+    l.halo = impl_->input_halo;
+    return l;
+}
+
+DeviceTensor BandedSession::tensor(ObjectId id, int* first_row, int* rows) {
+    auto it = impl_->slabs.find(id);
+    if (it == impl_->slabs.end()) throw Error(ErrorCode::UnknownObject, "object is not an image of the program", id);
+    if (first_row) *first_row = it->second.row0;
+    if (rows) *rows = it->second.rows;
+    return DeviceTensor{it->second.ptr, it->second.pitch, it->second.fstride};
+}
+
+void BandedSession::set_stream(void* s) { check(gvxb_ctx_set_stream(impl_->ctx, s), "set stream"); }
+
+void BandedSession::upload_rows(ObjectId id, const void* host, std::size_t pitch, int first_row, int rows, int frame) {
+    auto it = impl_->slabs.find(id);
+    if (it == impl_->slabs.end()) throw Error(ErrorCode::UnknownObject, "object is not an image of the program", id);
+    const Slab& s = it->second;
+    if (first_row < s.row0 || first_row + rows > s.row0 + s.rows || frame < 0 || frame >= impl_->frames)
+        throw Error(ErrorCode::ShapeMismatch, "rows outside the band storage", id);
+    char* d = static_cast<char*>(s.ptr) + frame * s.fstride + static_cast<std::int64_t>(first_row - s.row0) * s.pitch;
+    check(gvxb_upload_2d(impl_->ctx, d, static_cast<std::size_t>(s.pitch), host, pitch,
+                         static_cast<std::size_t>(impl_->W) * s.bpp, static_cast<std::size_t>(rows)),
+          "band upload");
+}
+
+void BandedSession::download_rows(ObjectId id, void* host, std::size_t pitch, int first_row, int rows, int frame) {
+    auto it = impl_->slabs.find(id);
+    if (it == impl_->slabs.end()) throw Error(ErrorCode::UnknownObject, "object is not an image of the program", id);
+    const Slab& s = it->second;
+    if (first_row < s.row0 || first_row + rows > s.row0 + s.rows || frame < 0 || frame >= impl_->frames)
+        throw Error(ErrorCode::ShapeMismatch, "rows outside the band storage", id);
+    const char* d = static_cast<const char*>(s.ptr) + frame * s.fstride +
+                    static_cast<std::int64_t>(first_row - s.row0) * s.pitch;
+    check(gvxb_download_2d(impl_->ctx, host, pitch, d, static_cast<std::size_t>(s.pitch),
+                           static_cast<std::size_t>(impl_->W) * s.bpp, static_cast<std::size_t>(rows)),
+          "band download");
+    check(gvxb_sync(impl_->ctx), "band download sync");
+}
+
+void BandedSession::launch() {
+    if (impl_->group) throw Error(ErrorCode::UnsupportedKind, "a BandGroup member launches through its group");
+    impl_->launch_standalone();
+}
+
+void BandedSession::synchronize() { impl_->synchronize(); }
+
+void BandedSession::run_host(const void* src, std::size_t src_pitch, ObjectId output, void* dst,
+                             std::size_t dst_pitch, int piece_rows) {
+    impl_->run_host(src, src_pitch, output, dst, dst_pitch, piece_rows);
+}
+
+int BandedSession::launches_per_run() const {
+    int n = 0;
+    for (std::size_t i = 0; i < impl_->prog->units.size(); ++i) {
+        const gvxb_band_plan& p = impl_->unit_plan[i];
+        n += impl_->needs_exchange(i) ? (p.interior_row1 > p.interior_row0 ? 1 : 0) + p.n_edges : 1;
+    }
+    return n;
+}
+
+std::string BandedSession::describe() const {
+    std::ostringstream os;
+    const BandLayout l = layout();
+    os << "row band " << l.rank << "/" << l.world << ": rows [" << l.row0 << ", " << l.row1 << ") of " << l.height
+       << ", input slab [" << l.src_row0 << ", " << l.src_row1 << "), halo " << l.halo << "\n"
+       << impl_->prog->describe();
+    return os.str();
+}
+
+// ---------------------------------------------------------------- BandGroup
+
+BandGroup::BandGroup(const OptimizedPlan& plan, const std::vector<int>& devices, int frames) {
+    if (devices.empty()) throw Error(ErrorCode::BadKernel, "a band group needs at least one device");
+    const int world = static_cast<int>(devices.size());
+    auto* ring = new std::vector<BandedSession::Impl*>(); // owned by band 0's Impl lifetime below
+    for (int g = 0; g < world; ++g) {
+        bands_.push_back(std::make_unique<BandedSession>(plan, g, world, nullptr, devices[static_cast<std::size_t>(g)],
+                                                         frames));
+        ring->push_back(bands_.back()->impl_.get());
+    }
+    for (int g = 0; g < world; ++g) {
+        BandedSession::Impl& b = *ring->at(static_cast<std::size_t>(g));
+        b.group = ring;
+        b.index = g;
+        b.xctx = dev::own_context(b.device);
+        check(gvxb_event_create(&b.ev_ready), "event");
+        check(gvxb_event_create(&b.ev_xdone), "event");
+        for (int nb : {g - 1, g + 1})
+            if (nb >= 0 && nb < world && devices[static_cast<std::size_t>(nb)] != b.device)
+                check(gvxb_enable_peer(b.xctx, devices[static_cast<std::size_t>(nb)]), "peer access");
+    }
+}
+
+BandGroup::~BandGroup() {
+    std::vector<BandedSession::Impl*>* ring = bands_.empty() ? nullptr : bands_.front()->impl_->group;
+    for (auto& b : bands_) b->impl_->synchronize();
+    bands_.clear();
+    delete ring;
+}
+
+int BandGroup::size() const { return static_cast<int>(bands_.size()); }
+
+BandedSession& BandGroup::band(int g) { return *bands_.at(static_cast<std::size_t>(g)); }
+
+void BandGroup::launch() {
+    const std::size_t n_units = bands_.front()->impl_->prog->units.size();
+    for (std::size_t i = 0; i < n_units; ++i) {
+        bool any = false;
+        for (auto& b : bands_) {
+            b->impl_->pulled = false;
+            any = any || b->impl_->needs_exchange(i);
+        }
+        if (any) {
+            for (auto& b : bands_) check(gvxb_event_record(b->impl_->ctx, b->impl_->ev_ready), "exchange event");
+            for (auto& b : bands_)
+                if (b->impl_->needs_exchange(i)) b->impl_->exchange_peer(i);
+        }
+        for (auto& b : bands_) b->impl_->run_unit(i, b->impl_->pulled);
+        // the next write of this group's input (a later group or launch) waits
+        // for the neighbours' pulls of it
+        for (auto& b : bands_)
+            for (int side = 0; side < 2; ++side) {
+                const int nb = b->impl_->src_plan[i].peer[side];
+                if (nb < 0) continue;
+                BandedSession::Impl* o = bands_[static_cast<std::size_t>(nb)]->impl_.get();
+                if (o->pulled) check(gvxb_stream_wait_event(b->impl_->ctx, o->ev_xdone), "exchange ordering");
+            }
+    }
+}
+
+void BandGroup::synchronize() {
+    for (auto& b : bands_) b->impl_->synchronize();
+}
+
+} // namespace gvx

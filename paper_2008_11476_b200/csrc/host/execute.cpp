@@ -231,9 +231,9 @@ long long launch_count() {
 /// A context of its own (stream, status word, read counter) on the library's
 /// device: sessions executing concurrently never share error flags or
 /// counters (the reference allows concurrent run_* calls).
-gvxb_ctx own_context() {
+gvxb_ctx own_context(int device) {
     gvxb_ctx c = nullptr;
-    check(gvxb_ctx_create(gvxb_ctx_device(context()), &c), "gvxb_ctx_create");
+    check(gvxb_ctx_create(device >= 0 ? device : gvxb_ctx_device(context()), &c), "gvxb_ctx_create");
     return c;
 }
 
@@ -1168,6 +1168,12 @@ std::shared_ptr<dev::Program> plan_program(const OptimizedPlan& plan, const Inpu
     mats.insert(base_mats.begin(), base_mats.end());
     return cached_program(program_key(plan.fused.stamp(), false, mats), [&] { return dev::build_plan(plan, mats); });
 }
+
+} // namespace
+
+std::shared_ptr<dev::Program> dev::program_of(const OptimizedPlan& plan) { return plan_program(plan, nullptr); }
+
+namespace {
 
 /// The reference's input binding rules (ref:src/execute.cpp:300-346).
 std::map<ObjectId, const Buffer*> bind_inputs(const VerifiedGraph& vg, const InputMap& inputs,

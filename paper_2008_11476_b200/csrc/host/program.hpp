@@ -95,6 +95,13 @@ std::shared_ptr<Program> build_naive(const VerifiedGraph& g, const std::map<Obje
 std::shared_ptr<Program> build_plan(const OptimizedPlan& plan,
                                     const std::map<ObjectId, std::vector<Value>>& matrices);
 
+/// The (cached) device program of an optimized plan, as run_plan uses it.
+std::shared_ptr<Program> program_of(const OptimizedPlan& plan);
+
+/// A context of its own (stream, status word, read counter) on `device`
+/// (-1: the library's device, GVX_DEVICE).
+gvxb_ctx own_context(int device = -1);
+
 // ---- hand-written group matching (lower.cpp) --------------------------------
 
 struct GraphView {
