@@ -262,6 +262,60 @@ TEST_CASE("gpu: boundary modes through fused plans equal run_naive") {
     }
 }
 
+TEST_CASE("gpu: host API error contract of run_plan / run_naive (ref:src/execute.cpp:300-346, 880-897)") {
+    GPU_ONLY();
+    Context ctx;
+    auto cg = gvx_configs::build_config(ctx, 1, 40, 30, true);
+    VerifiedGraph impl = impl_of(ctx, *cg.graph);
+    OptimizedPlan plan = optimize(impl, ctx);
+    auto code_of = [](auto&& fn) {
+        try {
+            fn();
+        } catch (const Error& e) {
+            return static_cast<int>(e.code());
+        }
+        return -1;
+    };
+    const Buffer good = random_buffer(img_desc(40, 30, ImageFormat::U8), 3);
+    for (bool naive : {false, true}) {
+        auto run = [&](const InputMap& in) { return naive ? run_naive(impl, in) : run_plan(plan, in); };
+        CAPTURE(naive);
+        // MissingInput: a consumed input without a buffer (ref:src/execute.cpp:344)
+        CHECK(code_of([&] { run(InputMap{}); }) == static_cast<int>(ErrorCode::MissingInput));
+        // ShapeMismatch: declared 40x30 U8, got 41x30 / S16 (ref:src/execute.cpp:321)
+        InputMap wrong;
+        wrong[cg.input] = random_buffer(img_desc(41, 30, ImageFormat::U8), 3);
+        CHECK(code_of([&] { run(wrong); }) == static_cast<int>(ErrorCode::ShapeMismatch));
+        wrong[cg.input] = random_buffer(img_desc(40, 30, ImageFormat::S16), 3);
+        CHECK(code_of([&] { run(wrong); }) == static_cast<int>(ErrorCode::ShapeMismatch));
+        // UnknownObject: a buffer for an id the context does not know (ref:src/execute.cpp:304)
+        InputMap unknown;
+        unknown[cg.input] = good;
+        unknown[987654] = good;
+        CHECK(code_of([&] { run(unknown); }) == static_cast<int>(ErrorCode::UnknownObject));
+        // AccessDenied: writing a virtual intermediate from the host (ref:src/execute.cpp:306)
+        ObjectId virt = kInvalidId;
+        for (ObjectId id : cg.graph->data())
+            if (ctx.find(id) && ctx.find(id)->is_virtual) virt = id;
+        REQUIRE(virt != kInvalidId);
+        InputMap denied;
+        denied[cg.input] = good;
+        denied[virt] = good;
+        CHECK(code_of([&] { run(denied); }) == static_cast<int>(ErrorCode::AccessDenied));
+        // the good run still works after every failure (no poisoned device state)
+        InputMap ok;
+        ok[cg.input] = good;
+        CHECK(run(ok).outputs.size() == 1);
+    }
+    // UnstampedGraph: an unverified graph / plan (ref:src/execute.cpp:881, 891)
+    VerifiedGraph blank;
+    OptimizedPlan blank_plan;
+    InputMap ok;
+    ok[cg.input] = good;
+    CHECK(code_of([&] { run_naive(blank, ok); }) == static_cast<int>(ErrorCode::UnstampedGraph));
+    CHECK(code_of([&] { run_plan(blank_plan, ok); }) == static_cast<int>(ErrorCode::UnstampedGraph));
+}
+
 TEST_CASE("gpu: runtime division by zero surfaces as DivByZero") {
     GPU_ONLY();
     std::vector<SignatureParam> ps(3);
