@@ -1,4 +1,4 @@
-// K1 v3 — fused Gaussian3x3 -> Sobel3x3 -> {gx, gy, Magnitude} (U8 -> S16)
+// K1 v4 — fused Gaussian3x3 -> Sobel3x3 -> {gx, gy, Magnitude} (U8 -> S16)
 // in the layout of the Harris kernel: one warp per CTA, 8 columns per lane,
 // source rows streamed through a TMA row ring, long row bands.
 //
@@ -9,21 +9,25 @@
 //   Clamp of the intermediate: the Gaussian at an out-of-image position is
 //   the Gaussian of the clamped position (ref:src/execute.cpp:242-245).
 //
+// The work is split across the SM sub-partition's two arithmetic pipes: the
+// Gaussian runs as 16-bit SWAR integer arithmetic on the ALU pipe (PRMT /
+// LEA / IADD3 / LOP3, two columns per 32-bit register), the Sobel and the
+// magnitude as packed FP32 (FFMA2 / FADD2 / FMUL2) on the FMA pipe.
+//
 // Layout: a strip of 248 output columns per warp; lane L holds columns
-// c = x - 4 + 8L .. c + 7 as four float2 pairs (A_i, B_i) = (c+i, c+4+i), so
-// every 3-tap step is a packed op on register pairs; only lane 0's A half
-// and lane 31's B half are halo.  Per source row j (virtual row j <-> global
-// row y0 - 2 + j):
-//   Hg(j)       horizontal 1-2-1 of the source bytes, each held as the float
-//               1 + (x + 1/2) / 2^15 straight from a byte permute (the
-//               half-biases carry the +8 of the rounding through the sums)
-//   G(j-1)      = fma_rd(Hg(j-2) + 2 Hg(j-1) + Hg(j), 2^11, 1.5*2^23 - 2^15)
-//               = 1.5*2^23 + floor((S + 8) / 16), kept in this magic form
-//               (running sums R = Hg(j-1) + Hg(j))
+// c = x - 4 + 8L .. c + 7; only lane 0's first half and lane 31's second
+// half are halo.  Per source row j (virtual row j <-> global row y0 - 2 + j):
+//   h(j)        horizontal 1-2-1 of the source bytes as SWAR words of the
+//               column pairs E1 = (c, c+2), O1 = (c+1, c+3), E2 = (c+4, c+6),
+//               O2 = (c+5, c+7) (byte permutes of the ring words)
+//   G(j-1)      = (h(j-2) + 2 h(j-1) + h(j) + 8) & ~15 = 16 floor((S + 8) / 16)
+//               (running sums R = h(j-1) + h(j)); each 16-bit lane becomes the
+//               float 2^23 + 16 g by one byte permute, as pairs (c+i, c+4+i)
 //   gx(j-2)     = Q(j-2) + Q(j-1), Q(m) = D(m-1) + D(m), D = G(x+1) - G(x-1)
-//   gy(j-2)     = horizontal 1-2-1 of G(j-1) - G(j-3) (the magic cancels)
-// so output row j - 4 is emitted at step j.  Every quantity is an integer
-// (or, before rounding, a half-integer) below 2^24: exact in fp32.
+//   gy(j-2)     = horizontal 1-2-1 of G(j-1) - G(j-3) (the 2^23 cancels)
+// so output row j - 4 is emitted at step j, gx and gy scaled by 16.  Every
+// quantity is an integer times 16 below 2^24 (squares: times 256 below
+// 2^30 with <= 21 significant bits): exact in fp32.
 #include "packed.cuh"
 
 #include <algorithm>
@@ -72,32 +76,31 @@ __device__ __forceinline__ float e8_sqrt_approx(float x) {
     return r;
 }
 
-/// round(sqrt(n)) half away from zero for integer-valued 0 <= n < 2^22, in
-/// magic form 1.5*2^23 + k (low 16 bits = k): k0 = rn(s - 0.01) is k* or
-/// k* - 1 for the approximate root s, and k* = k0 + (n > k0^2 + k0).
-__device__ __forceinline__ float2 e8_round_sqrt(float2 n) {
-    const float2 M = f2(12582912.f, 12582912.f), nM = f2(-12582912.f, -12582912.f);
-    const float2 d = f2(-0.01f, -0.01f);
-    const float2 s = f2(e8_sqrt_approx(n.x), e8_sqrt_approx(n.y));
-    float2 km = add2(add2(s, d), M); // 1.5*2^23 + k0
-    const float2 k = add2(km, nM);
-    const float2 kk = fma2(k, k, k);
-    km.x += n.x > kk.x ? 1.f : 0.f;
-    km.y += n.y > kk.y ? 1.f : 0.f;
-    return km;
+/// round(sqrt(n)) half away from zero, in magic form 1.5*2^23 + k (low 16
+/// bits = k), from n16 = 256 n (integer-valued, n < 2^21; gx, gy carry a
+/// factor 16).  s = sqrt~(n16) = 16 sqrt(n) (1 + e), |e| < 2^-21, so
+/// k0 = floor(s / 16) (one FFMA2 rounding down into the magic range) is
+/// k* or k* - 1, and k* = k0 + (n > k0 (k0 + 1)): u = 256 k0 (k0 + 1) - n16 is
+/// exact and negative exactly when the increment applies; its sign bit is
+/// added to the magic form's low bits (an ALU op).
+__device__ __forceinline__ float2 e8_round_sqrt16(float2 n16) {
+    const float2 s = f2(e8_sqrt_approx(n16.x), e8_sqrt_approx(n16.y));
+    const float2 km = __ffma2_rd(s, f2(0.0625f, 0.0625f), f2(12582912.f, 12582912.f)); // 1.5*2^23 + k0
+    const float2 k16 = __ffma2_rn(km, f2(16.f, 16.f), f2(-201326592.f, -201326592.f));  // 16 k0
+    const float2 u = __ffma2_rn(k16, add2(k16, f2(16.f, 16.f)), f2(-n16.x, -n16.y));
+    return f2(__uint_as_float(__float_as_uint(km.x) + (__float_as_uint(u.x) >> 31)),
+              __uint_as_float(__float_as_uint(km.y) + (__float_as_uint(u.y) >> 31)));
 }
 
-/// 1 + (byte k of w + 1/2) / 2^15: the byte lands in mantissa bits 8..15 and
-/// the constant supplies exponent 0 and the half (bit 7).  Sums of up to 2^8
-/// such values stay exact (all multiples of 2^-16 below 2^8).
-__device__ __forceinline__ float frac_byte(uint32_t w, int k) {
-    return __uint_as_float(__byte_perm(w, 0x3F800080u, 0x7604u | (static_cast<unsigned>(k) << 4)));
+/// 16-bit lane `hi` of a SWAR word as the float 2^23 + lane (one permute).
+__device__ __forceinline__ float e8_lane(uint32_t w, int hi) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, hi ? 0x7632u : 0x7610u));
 }
 
-/// Integer-valued floats |v| < 2^22 as two int16 in a u32.
-__device__ __forceinline__ uint32_t e8_pack(float lo, float hi) {
+/// 16 x (integer-valued floats |v| < 2^18) as two int16 v in a u32.
+__device__ __forceinline__ uint32_t e8_pack16(float lo, float hi) {
     const float m = 12582912.f;
-    return __byte_perm(__float_as_uint(lo + m), __float_as_uint(hi + m), 0x5410);
+    return __byte_perm(__float_as_uint(fmaf(lo, 0.0625f, m)), __float_as_uint(fmaf(hi, 0.0625f, m)), 0x5410);
 }
 /// Magic-form values (1.5*2^23 + v) as two int16 in a u32.
 __device__ __forceinline__ uint32_t e8_pack_magic(float lo, float hi) {
@@ -192,28 +195,24 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
 
     auto body = [&](auto edge_tag) {
         constexpr bool kEdge = decltype(edge_tag)::value;
-        /// Source row j in fractional form 1 + (x + 1/2) / 2^15 (byte permutes
-        /// only): pairs for i = -1 .. 4.
-        auto src_pairs = [&](int j) {
+        /// Horizontal 1-2-1 of source row j as SWAR words {E1, O1, E2, O2}
+        /// (16-bit lanes, sums <= 1020).  L / R are the neighbour-column pairs
+        /// built by permutes with a zero lane from the unpacked words.
+        auto hsum = [&](int j, uint32_t* h) {
             const uint8_t* row = ring + (j % kE8Ring) * kE8SW + off;
             const uint2 lo = *reinterpret_cast<const uint2*>(row - 4), hi = *reinterpret_cast<const uint2*>(row + 4);
-            P12 r;
-            r.v[0] = f2(frac_byte(lo.x, 3), frac_byte(lo.y, 3));
-            r.v[1] = f2(frac_byte(lo.y, 0), frac_byte(hi.x, 0));
-            r.v[2] = f2(frac_byte(lo.y, 1), frac_byte(hi.x, 1));
-            r.v[3] = f2(frac_byte(lo.y, 2), frac_byte(hi.x, 2));
-            r.v[4] = f2(frac_byte(lo.y, 3), frac_byte(hi.x, 3));
-            r.v[5] = f2(frac_byte(hi.x, 0), frac_byte(hi.y, 0));
-            return r;
+            const uint32_t E1 = __byte_perm(lo.y, 0, 0x4240), O1 = __byte_perm(lo.y, 0, 0x4341);
+            const uint32_t E2 = __byte_perm(hi.x, 0, 0x4240), O2 = __byte_perm(hi.x, 0, 0x4341);
+            const uint32_t LE1 = __byte_perm(lo.x, O1, 0x5453); // (c-1, c+1)
+            const uint32_t RO1 = __byte_perm(E1, hi.x, 0x1412); // (c+2, c+4)
+            const uint32_t LE2 = __byte_perm(O1, O2, 0x1412);   // (c+3, c+5)
+            const uint32_t RO2 = __byte_perm(E2, hi.y, 0x1412); // (c+6, c+8)
+            h[0] = (E1 << 1) + LE1 + O1;
+            h[1] = (O1 << 1) + E1 + RO1;
+            h[2] = (E2 << 1) + LE2 + O2;
+            h[3] = (O2 << 1) + E2 + RO2;
         };
         const float2 two = f2(2.f, 2.f);
-        /// Horizontal 1-2-1: 4 + (s + 2) / 2^15 (the four half-biases).
-        auto smooth = [&](const P12& q) {
-            P8 h;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) h.v[i] = fma2(two, q.v[i + 1], add2(q.v[i], q.v[i + 2]));
-            return h;
-        };
         /// Gaussian columns beyond W-1 take column W-1's value; column -1
         /// (lane 0's A3 in the first strip) takes column 0's (B0).
         auto clamp_cols = [&](P8& g) {
@@ -258,19 +257,19 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
                 }
             };
             if (kGx) {
-                put(pgx, e8_pack(gx.v[0].x, gx.v[1].x), e8_pack(gx.v[2].x, gx.v[3].x), e8_pack(gx.v[0].y, gx.v[1].y),
-                    e8_pack(gx.v[2].y, gx.v[3].y));
+                put(pgx, e8_pack16(gx.v[0].x, gx.v[1].x), e8_pack16(gx.v[2].x, gx.v[3].x), e8_pack16(gx.v[0].y, gx.v[1].y),
+                    e8_pack16(gx.v[2].y, gx.v[3].y));
                 pgx += p.gx.pitch;
             }
             if (kGy) {
-                put(pgy, e8_pack(gy.v[0].x, gy.v[1].x), e8_pack(gy.v[2].x, gy.v[3].x), e8_pack(gy.v[0].y, gy.v[1].y),
-                    e8_pack(gy.v[2].y, gy.v[3].y));
+                put(pgy, e8_pack16(gy.v[0].x, gy.v[1].x), e8_pack16(gy.v[2].x, gy.v[3].x), e8_pack16(gy.v[0].y, gy.v[1].y),
+                    e8_pack16(gy.v[2].y, gy.v[3].y));
                 pgy += p.gy.pitch;
             }
             if (kMag) {
                 float2 m[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) m[i] = e8_round_sqrt(fma2(gx.v[i], gx.v[i], mul2(gy.v[i], gy.v[i])));
+                for (int i = 0; i < 4; ++i) m[i] = e8_round_sqrt16(fma2(gx.v[i], gx.v[i], mul2(gy.v[i], gy.v[i])));
                 put(pmag, e8_pack_magic(m[0].x, m[1].x), e8_pack_magic(m[2].x, m[3].x), e8_pack_magic(m[0].y, m[1].y),
                     e8_pack_magic(m[2].y, m[3].y));
                 pmag += p.mag.pitch;
@@ -280,24 +279,26 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
         // State of the running sums; two alternating copies (A, B) so the
         // 2x-unrolled loop renames instead of moving registers.
         struct State {
-            P8 Hp, Rp;  // Hg(j-1), Hg(j-2) + Hg(j-1)
-            P8 Dp, Qp;  // D(m), Q(m) of the newest Gaussian row
-            GRow Gn;    // Gaussian row this copy last produced
+            uint32_t hp[4], rp[4]; // h(j-1), h(j-2) + h(j-1) (SWAR)
+            P8 Dp, Qp;             // D(m), Q(m) of the newest Gaussian row
+            GRow Gn;               // Gaussian row this copy last produced
         };
         State A, B;
-        // 16 + (S + 8) / 2^15 -> 1.5*2^23 + floor((S + 8) / 16): exact scaling by
-        // 2^11, one rounding (down) of the sum with 1.5*2^23 - 2^15
-        const float2 sc = f2(2048.f, 2048.f), M = f2(12550144.f, 12550144.f);
-        /// Source row j -> Gaussian row j-1 (magic form, clamped columns).
+        /// Source row j -> Gaussian row j-1 (2^23 + 16 g, clamped columns).
         auto gauss_step = [&](int j, const State& i, State& o) {
-            const P8 h = smooth(src_pairs(j));
-            P8 g;
+            uint32_t h[4], g16[4];
+            hsum(j, h);
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                o.Rp.v[t] = add2(i.Hp.v[t], h.v[t]);
-                g.v[t] = __ffma2_rd(add2(i.Rp.v[t], o.Rp.v[t]), sc, M);
+                o.rp[t] = i.hp[t] + h[t];
+                g16[t] = (i.rp[t] + o.rp[t] + 0x00080008u) & 0xFFF0FFF0u;
+                o.hp[t] = h[t];
             }
-            o.Hp = h;
+            P8 g; // pairs (c+i, c+4+i): E1 = (c, c+2), O1 = (c+1, c+3), E2, O2 = +4
+            g.v[0] = f2(e8_lane(g16[0], 0), e8_lane(g16[2], 0));
+            g.v[1] = f2(e8_lane(g16[1], 0), e8_lane(g16[3], 0));
+            g.v[2] = f2(e8_lane(g16[0], 1), e8_lane(g16[2], 1));
+            g.v[3] = f2(e8_lane(g16[1], 1), e8_lane(g16[3], 1));
             clamp_cols(g);
             return neighbourhood(g);
         };
@@ -324,12 +325,13 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
             for (int t = 0; t < 4; ++t) g.v[t] = fma2(two, d[t + 1], add2(d[t], d[t + 2]));
             return g;
         };
-        // prologue: Hg rows 0, 1; Gaussian rows y0-1 (j = 2) and y0 (j = 3)
+        // prologue: h rows 0, 1; Gaussian rows y0-1 (j = 2) and y0 (j = 3)
         {
-            const P8 h0 = smooth(src_pairs(0)), h1 = smooth(src_pairs(1));
+            uint32_t h0[4];
+            hsum(0, h0);
+            hsum(1, A.hp);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) A.Rp.v[t] = add2(h0.v[t], h1.v[t]);
-            A.Hp = h1;
+            for (int t = 0; t < 4; ++t) A.rp[t] = h0[t] + A.hp[t];
         }
         GRow G1 = gauss_step(2, A, B); // Gaussian row y0-1
         GRow G2 = gauss_step(3, B, A); // Gaussian row y0
