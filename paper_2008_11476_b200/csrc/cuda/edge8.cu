@@ -62,12 +62,11 @@ struct P8 {
 struct P12 {
     float2 v[6];
 };
-/// A Gaussian row around the lane: its 8 columns and the neighbour columns
-/// c-1 / c+8 as scalars (pairs mixing them with own columns would each cost
-/// a register move; the boundary terms are scalar adds instead).
+/// A Gaussian row around the lane: its 8 columns and the two neighbour
+/// pairs lp = (c-1, c+3), rp = (c+4, c+8), so every 3-tap step is packed.
 struct GRow {
     P8 g;
-    float l, r;
+    float2 lp, rp;
 };
 
 __device__ __forceinline__ float e8_sqrt_approx(float x) {
@@ -76,18 +75,20 @@ __device__ __forceinline__ float e8_sqrt_approx(float x) {
     return r;
 }
 
-/// round(sqrt(n)) half away from zero, in magic form 1.5*2^23 + k (low 16
-/// bits = k), from n16 = 256 n (integer-valued, n < 2^21; gx, gy carry a
-/// factor 16).  s = sqrt~(n16) = 16 sqrt(n) (1 + e), |e| < 2^-21, so
-/// k0 = floor(s / 16) (one FFMA2 rounding down into the magic range) is
-/// k* or k* - 1, and k* = k0 + (n > k0 (k0 + 1)): u = 256 k0 (k0 + 1) - n16 is
-/// exact and negative exactly when the increment applies; its sign bit is
-/// added to the magic form's low bits (an ALU op).
-__device__ __forceinline__ float2 e8_round_sqrt16(float2 n16) {
-    const float2 s = f2(e8_sqrt_approx(n16.x), e8_sqrt_approx(n16.y));
-    const float2 km = __ffma2_rd(s, f2(0.0625f, 0.0625f), f2(12582912.f, 12582912.f)); // 1.5*2^23 + k0
-    const float2 k16 = __ffma2_rn(km, f2(16.f, 16.f), f2(-201326592.f, -201326592.f));  // 16 k0
-    const float2 u = __ffma2_rn(k16, add2(k16, f2(16.f, 16.f)), f2(-n16.x, -n16.y));
+/// round(sqrt(n)) half away from zero, in magic form 2^23 + k (low 16 bits
+/// = k), from n64 = 256 n + 64 = 64 (4 n + 1) (gx, gy carry a factor 16;
+/// the caller folds in the 64).  s = sqrt~(n64) = 16 sqrt(n + 1/4) (1 + e),
+/// |e| < 2^-21, and sqrt(n + 1/4) lies in [k* - 1/2, k* + 1/2] for the
+/// rounded root k*, so k0 = floor(s / 16) (one FFMA2 rounding down into the
+/// magic range) is k* or k* - 1, and k* = k0 + (n > k0 (k0 + 1)).  With
+/// v = 16 k0 + 8, u = v^2 - n64 = 256 (k0 (k0 + 1) - n) is exact (multiples
+/// of 64 below 2^30) and negative exactly when the increment applies; its
+/// sign bit is added to the magic form's low bits (an ALU op).
+__device__ __forceinline__ float2 e8_round_sqrt16(float2 n64) {
+    const float2 s = f2(e8_sqrt_approx(n64.x), e8_sqrt_approx(n64.y));
+    const float2 km = __ffma2_rd(s, f2(0.0625f, 0.0625f), f2(8388608.f, 8388608.f)); // 2^23 + k0
+    const float2 v = __ffma2_rn(km, f2(16.f, 16.f), f2(-134217720.f, -134217720.f)); // 16 k0 + 8 (2^27 - 8 is exact)
+    const float2 u = __ffma2_rn(v, v, f2(-n64.x, -n64.y));
     return f2(__uint_as_float(__float_as_uint(km.x) + (__float_as_uint(u.x) >> 31)),
               __uint_as_float(__float_as_uint(km.y) + (__float_as_uint(u.y) >> 31)));
 }
@@ -107,6 +108,9 @@ __device__ __forceinline__ uint32_t e8_pack_magic(float lo, float hi) {
     return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x5410);
 }
 
+#ifndef GVX_EDGE8_UNROLL
+#define GVX_EDGE8_UNROLL 4 // rows per loop iteration of interior strips (2 or 4)
+#endif
 template <bool kGx, bool kGy, bool kMag>
 #ifndef GVX_EDGE8_MINB
 #define GVX_EDGE8_MINB 1
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
             const float L = __shfl_up_sync(0xffffffffu, g.v[3].y, 1);
             float R = __shfl_down_sync(0xffffffffu, g.v[0].x, 1);
             if (kEdge) R = last <= 7 ? g.v[3].y : R;
-            return GRow{g, L, R};
+            return GRow{g, f2(L, g.v[3].x), f2(g.v[0].y, R)};
         };
         auto emit = [&](const P8& gx, const P8& gy) {
             const bool full = !kEdge || c + 7 < W;
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
             if (kMag) {
                 float2 m[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) m[i] = e8_round_sqrt16(fma2(gx.v[i], gx.v[i], mul2(gy.v[i], gy.v[i])));
+                for (int i = 0; i < 4; ++i) m[i] = e8_round_sqrt16(fma2(gx.v[i], gx.v[i], fma2(gy.v[i], gy.v[i], f2(64.f, 64.f))));
                 put(pmag, e8_pack_magic(m[0].x, m[1].x), e8_pack_magic(m[2].x, m[3].x), e8_pack_magic(m[0].y, m[1].y),
                     e8_pack_magic(m[2].y, m[3].y));
                 pmag += p.mag.pitch;
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
         struct State {
             uint32_t hp[4], rp[4]; // h(j-1), h(j-2) + h(j-1) (SWAR)
             P8 Dp, Qp;             // D(m), Q(m) of the newest Gaussian row
-            GRow Gn;               // Gaussian row this copy last produced
+            P8 Hn;                 // H of the Gaussian row this copy last produced
         };
         State A, B;
         /// Source row j -> Gaussian row j-1 (2^23 + 16 g, clamped columns).
@@ -304,26 +308,21 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
         };
         /// D = G(x+1) - G(x-1) for the lane's 8 columns.
         auto diff = [&](const GRow& n) {
-            const P8& g = n.g;
             P8 d;
-            d.v[0] = f2(g.v[1].x - n.l, g.v[1].y - g.v[3].x);
-            d.v[1] = sub2(g.v[2], g.v[0]);
-            d.v[2] = sub2(g.v[3], g.v[1]);
-            d.v[3] = f2(g.v[0].y - g.v[2].x, n.r - g.v[2].y);
+            d.v[0] = sub2(n.g.v[1], n.lp);
+            d.v[1] = sub2(n.g.v[2], n.g.v[0]);
+            d.v[2] = sub2(n.g.v[3], n.g.v[1]);
+            d.v[3] = sub2(n.rp, n.g.v[2]);
             return d;
         };
-        /// gy of the row between Gaussian rows n (newer) and m (two older):
-        /// vertical differences, then the 1-2-1 across columns.
-        auto grad_y = [&](const GRow& n, const GRow& m) {
-            float2 d[6];
-            d[0] = f2(n.l - m.l, n.g.v[3].x - m.g.v[3].x);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) d[t + 1] = sub2(n.g.v[t], m.g.v[t]);
-            d[5] = f2(n.g.v[0].y - m.g.v[0].y, n.r - m.r);
-            P8 g;
-#pragma unroll
-            for (int t = 0; t < 4; ++t) g.v[t] = fma2(two, d[t + 1], add2(d[t], d[t + 2]));
-            return g;
+        /// Horizontal 1-2-1 of a Gaussian row: gy(r) = H(r+1) - H(r-1).
+        auto hsmooth = [&](const GRow& n) {
+            P8 h;
+            h.v[0] = fma2(two, n.g.v[0], add2(n.lp, n.g.v[1]));
+            h.v[1] = fma2(two, n.g.v[1], add2(n.g.v[0], n.g.v[2]));
+            h.v[2] = fma2(two, n.g.v[2], add2(n.g.v[1], n.g.v[3]));
+            h.v[3] = fma2(two, n.g.v[3], add2(n.g.v[2], n.rp));
+            return h;
         };
         // prologue: h rows 0, 1; Gaussian rows y0-1 (j = 2) and y0 (j = 3)
         {
@@ -341,28 +340,40 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
 #pragma unroll
             for (int t = 0; t < 4; ++t) A.Qp.v[t] = add2(D1.v[t], D2.v[t]);
             A.Dp = D2;
-            A.Gn = G2; // newest row
-            B.Gn = G1; // the copy read at the next step holds the row two back
+            A.Hn = hsmooth(G2); // newest row
+            B.Hn = hsmooth(G1); // the copy read at the next step holds the row two back
         }
         /// Step j: Gaussian row j-1 -> Sobel / outputs of row j-4 (global).
         /// `bottom`: Gaussian row j-1 is row H, which clamps to row H-1.
         auto full_step = [&](int j, State& i, State& o, bool bottom) {
-            GRow Gn = gauss_step(j, i, o);
-            if (bottom) Gn = i.Gn;
-            const P8 D = diff(Gn);
-            const P8 gy = grad_y(Gn, o.Gn); // o.Gn = Gaussian row j-3
-            P8 Q, gx;
+            const GRow Gn = gauss_step(j, i, o);
+            P8 D = diff(Gn), Hn = hsmooth(Gn);
+            if (bottom) D = i.Dp, Hn = i.Hn; // Gaussian row H clamps to row H-1
+            P8 Q, gx, gy;
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 Q.v[t] = add2(i.Dp.v[t], D.v[t]);
                 gx.v[t] = add2(i.Qp.v[t], Q.v[t]);
+                gy.v[t] = sub2(Hn.v[t], o.Hn.v[t]); // o.Hn = H of Gaussian row j-3
             }
             o.Qp = Q;
             o.Dp = D;
-            o.Gn = Gn;
+            o.Hn = Hn;
             emit(gx, gy);
         };
         int j = 4;
+        // 4 rows per iteration (j % 4 == 0: one chunk check per iteration;
+        // the state's loop-carried copies are re-aligned once per 4 rows)
+        // (interior strips only: the border variant, with its column clamps,
+        // runs faster 2x-unrolled)
+        if (!kEdge && GVX_EDGE8_UNROLL >= 4)
+        for (; j + 4 < steps; j += 4) {
+            if (j % kE8Chunk == 0) next_chunk(j / kE8Chunk);
+            full_step(j, A, B, false);
+            full_step(j + 1, B, A, false);
+            full_step(j + 2, A, B, false);
+            full_step(j + 3, B, A, false);
+        }
         for (; j + 2 < steps; j += 2) {
             if (j % kE8Chunk == 0) next_chunk(j / kE8Chunk);
             full_step(j, A, B, false);
@@ -400,6 +411,19 @@ int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a) {
                   : (oy ? pick_e8<false, true>(om) : pick_e8<false, false>(om));
     const int rows = a->band.row1 - a->band.row0;
     const int frames = s.frames > 0 ? s.frames : 1;
+#ifndef GVX_EDGE8_CARVEOUT
+#define GVX_EDGE8_CARVEOUT 1
+#endif
+    static bool carveout = !GVX_EDGE8_CARVEOUT; // one-warp CTAs: shared memory must not cap residency
+    if (!carveout) {
+        for (bool X : {false, true})
+            for (bool Y : {false, true})
+                for (bool M : {false, true})
+                    cudaFuncSetAttribute(X ? (Y ? pick_e8<true, true>(M) : pick_e8<true, false>(M))
+                                           : (Y ? pick_e8<false, true>(M) : pick_e8<false, false>(M)),
+                                         cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        carveout = true;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kE8Threads, 0);
     const long long strips = static_cast<long long>(frames) * ((s.width + kE8Cols - 1) / kE8Cols);

@@ -18,6 +18,26 @@ METRICS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "sm__cycles_elapsed.avg.per_second",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smsp__warps_issue_stalled_math_pipe_throttle_per_warp_active.pct",
+    "smsp__warps_issue_stalled_wait_per_warp_active.pct",
+    "smsp__warps_issue_stalled_short_scoreboard_per_warp_active.pct",
+    "smsp__warps_issue_stalled_long_scoreboard_per_warp_active.pct",
+    "smsp__warps_issue_stalled_barrier_per_warp_active.pct",
+    "smsp__warps_issue_stalled_no_instruction_per_warp_active.pct",
+    "smsp__warps_issue_stalled_not_selected_per_warp_active.pct",
+    "smsp__warps_issue_stalled_selected_per_warp_active.pct",
+    "smsp__warps_issue_stalled_dispatch_stall_per_warp_active.pct",
+    "smsp__warps_issue_stalled_lg_throttle_per_warp_active.pct",
+    "smsp__warps_issue_stalled_mio_throttle_per_warp_active.pct",
+    "smsp__warps_issue_stalled_drain_per_warp_active.pct",
+    "smsp__warps_issue_stalled_sleeping_per_warp_active.pct",
+    "smsp__warps_issue_stalled_branch_resolving_per_warp_active.pct",
+    "smsp__warps_issue_stalled_membar_per_warp_active.pct",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -48,7 +68,7 @@ def update_traffic(tag, res):
     import os
     sys.path.insert(0, os.getcwd())
     from bench import DEFAULT_FRAMES
-    size = {1: (1920, 1080), 2: (3840, 2160), 3: (7680, 4320), 4: (3840, 2160)}
+    size = {1: (1920, 1080), 2: (3840, 2160), 3: (7680, 4320), 4: (3840, 2160), 5: (16384, 16384)}
     path = "profiles/ncu_traffic.json"
     try:
         table = json.load(open(path))
