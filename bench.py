@@ -304,6 +304,56 @@ def run_frames(args, cfg, rank, world, local_rank):
     px_step = w * h * F
     value = px_step * args.steps * world / (ms_max / 1e3) / 1e6
 
+    # one frame per launch (vxProcessGraph semantics: one graph execution per
+    # call), device time per execution over distinct frames (> 4x L2 in turn)
+    single = None
+    if not args.no_single:
+        s1 = gvx.Session(graph, frames=1)
+        s1.set_stream(dev.stream)
+        fstride = pitch * h
+        ofs = out_pitch * h
+
+        def bind1(i):
+            b, f = (i // F) % 2, i % F
+            din, dout = pools[b]
+            s1.bind(0, din + f * fstride, pitch, fstride)
+            if dout is not None:
+                s1.bind(1, dout + f * ofs, out_pitch, ofs)
+
+        n1 = max(2 * F, 64)
+        for i in range(8):
+            bind1(i)
+            s1.launch()
+        dev.sync()
+        dev.record(ev[0])
+        for i in range(n1):
+            bind1(i)
+            s1.launch()
+        dev.record(ev[1])
+        dev.sync()
+        ms1 = dev.elapsed_ms(ev[0], ev[1]) / n1
+        single = {"ms_per_frame": round(ms1, 5), "value": round(w * h / (ms1 / 1e3) / 1e6, 1), "unit": "Mpixel/s",
+                  "launches_per_frame": s1.launches(), "frames_timed": n1,
+                  "note": "one graph execution (one fused launch) per frame, as vxProcessGraph / run_plan "
+                          "execute; inputs rotate over the same two batches"}
+        s1.close()
+
+    # the drop-in host entry point itself: run_plan(plan, InputMap) on pageable
+    # host buffers, one call per frame (copies in and out inside each call)
+    run_plan_e2e = None
+    if not args.no_single:
+        g2 = gvx.ConfigGraph(cfg, w, h, True)
+        g2.run_host(host[0])
+        n2 = 8
+        t0 = time.perf_counter()
+        for i in range(n2):
+            g2.run_host(host[i % F])
+        dt = time.perf_counter() - t0
+        run_plan_e2e = {"value": round(w * h * n2 / dt / 1e6, 1), "unit": "Mpixel/s", "frames": n2,
+                        "path": "gvx::run_plan(plan, InputMap) via gvxc_graph_run_host: pageable numpy frame in, "
+                                "output copied to a numpy array, one synchronous call per frame"}
+        g2.close()
+
     # one fused launch per step (F frames in grid.z); cfg4's step also holds
     # the scratch-clear and MeanStdDev-finalize micro-kernels (counted in, so
     # the roofline fraction is a lower bound for the conv/histogram kernel)
@@ -312,7 +362,8 @@ def run_frames(args, cfg, rank, world, local_rank):
         kernel_ms = None
     return dict(value=value, ms_per_step=ms_max / args.steps, clocks=clk.summary(), launches=launches,
                 e2e=e2e, frames=F, kernel_ms=kernel_ms, checked=checked, w=w, h=h, px_step=px_step,
-                launches_per_step=sess.launches(), describe=graph.describe())
+                launches_per_step=sess.launches(), describe=graph.describe(), single_frame=single,
+                run_plan_e2e=run_plan_e2e)
 
 
 # --------------------------------------------------------------- banded cfg5
@@ -393,6 +444,19 @@ def run_banded(args, rank, world, local_rank):
     src = gvx.HostBuffer((s1 - s0, W), np.uint8)
     src.array[:] = img[s0:s1]
     dst = gvx.HostBuffer((r1 - r0, W), np.int16)
+    # the drop-in host entry point at N=1: run_plan(plan, InputMap) with the
+    # whole 16384^2 frame in pageable host memory, one synchronous call
+    run_plan_e2e = None
+    if world == 1 and not args.no_single:
+        graph.run_host(img)
+        n2 = 3
+        t0 = time.perf_counter()
+        for _ in range(n2):
+            graph.run_host(img)
+        dt = time.perf_counter() - t0
+        run_plan_e2e = {"value": round(W * H * n2 / dt / 1e6, 1), "unit": "Mpixel/s", "frames": n2,
+                        "path": "gvx::run_plan(plan, InputMap) via gvxc_graph_run_host: pageable 268 MB frame in, "
+                                "537 MB magnitude copied out, one synchronous call per frame"}
     del img
     band.run_host(src.ptr, W, 1, dst.ptr, 2 * W, 1024)  # warm-up
     n_e2e = max(3, min(args.steps, 5))
@@ -413,7 +477,8 @@ def run_banded(args, rank, world, local_rank):
     dst.close()
     return dict(value=value, ms_per_step=ms_max / args.steps, clocks=clk.summary(), launches=launches, e2e=e2e,
                 frames=1, kernel_ms=ms / args.steps if world == 1 else None, checked=checked, w=W, h=H,
-                px_step=W * H, launches_per_step=band.launches(), describe=band.describe())
+                px_step=W * H, launches_per_step=band.launches(), describe=band.describe(),
+                run_plan_e2e=run_plan_e2e)
 
 
 # ------------------------------------------------------------- distributed
@@ -466,6 +531,7 @@ def main():
     ap.add_argument("--e2e-frames", type=int, default=48)
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single", action="store_true", help="skip the one-frame-per-launch and run_plan legs")
     ap.add_argument("--clock-window", type=float, default=1.0, help="seconds of identical load sampled before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -540,6 +606,7 @@ def main():
                        "parallelism": f"{'row bands' if cfg == 5 else 'frame replicas'} x{world}"},
             "e2e": res["e2e"], "roofline": roof, "cpu_baseline": cpu, "clocks": res["clocks"],
             "gpu_launches": res["launches"], "launches_per_step": res["launches_per_step"],
+            "single_frame": res.get("single_frame"), "run_plan_e2e": res.get("run_plan_e2e"),
             "checked_vs_oracle": res["checked"],
             "checked_against": "SHA-256 of oracle/_ref run_naive (unmodified reference) per 2048-row block"
                                if cfg == 5 else "oracle/gvx_oracle.c restatement, frame 0",
