@@ -195,6 +195,7 @@ def run_frames(args, cfg, rank, world, local_rank):
     graph = gvx.ConfigGraph(cfg, w, h, True)
     sess = gvx.Session(graph, frames=F)
     sess.set_stream(dev.stream)
+    sess.set_overlap(1)  # only this session launches kernels on dev.stream
     pitch = (w + 127) // 128 * 128
     in_bytes = pitch * h * F
     out_pitch = pitch * (2 if cfg in (1, 5) else 1)
@@ -310,6 +311,7 @@ def run_frames(args, cfg, rank, world, local_rank):
     if not args.no_single:
         s1 = gvx.Session(graph, frames=1)
         s1.set_stream(dev.stream)
+        s1.set_overlap(1)
         fstride = pitch * h
         ofs = out_pitch * h
 

@@ -41,6 +41,11 @@ public:
 
     /// Launch stream (a cudaStream_t); nullptr = the runtime's own stream.
     void set_stream(void* cuda_stream);
+    /// Programmatic dependent launch between consecutive executions whose
+    /// bound buffers do not alias (gvxb_ctx_set_overlap): -1 (default) only
+    /// on the session's own stream, 0 off, 1 on (the caller guarantees no
+    /// other kernels are launched on the stream set with set_stream).
+    void set_overlap(int mode);
     /// Enqueue one execution of the program over all frames (asynchronous).
     void launch();
     /// Wait, then raise the reference's errors (DivByZero, ShapeMismatch)

@@ -54,6 +54,9 @@ int gvxc_session_destroy(gvxc_session s);
 /* slot 0 = the input image; slot k >= 1 = config output k-1. */
 int gvxc_session_bind(gvxc_session s, int slot, void* dptr, int64_t pitch, int64_t frame_stride);
 int gvxc_session_set_stream(gvxc_session s, void* cuda_stream);
+/* Programmatic dependent launch of consecutive non-aliasing executions:
+ * -1 own stream only (default), 0 off, 1 on (DeviceSession::set_overlap). */
+int gvxc_session_set_overlap(gvxc_session s, int mode);
 int gvxc_session_launch(gvxc_session s);
 int gvxc_session_sync(gvxc_session s);
 int gvxc_session_launches(gvxc_session s);

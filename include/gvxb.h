@@ -101,6 +101,15 @@ int gvxb_ctx_create(int device, gvxb_ctx* out);
 int gvxb_ctx_destroy(gvxb_ctx ctx);
 /* Launch on an external stream (e.g. a framework's); NULL = own stream. */
 int gvxb_ctx_set_stream(gvxb_ctx ctx, void* cuda_stream);
+/* Programmatic dependent launch of the hand-written kernels: a kernel whose
+ * read / write ranges do not touch the previous kernel's (on this context's
+ * stream, with nothing else enqueued in between) is launched so that it
+ * starts while the previous one drains; a dependent one still starts early
+ * but waits for it (griddepcontrol.wait) before touching memory.  mode
+ * -1 (default) = only while the context launches on its own stream (then no
+ * foreign work can sit between two of its kernels), 0 = off, 1 = on (the
+ * caller guarantees that nothing else launches kernels on the stream). */
+int gvxb_ctx_set_overlap(gvxb_ctx ctx, int mode);
 void* gvxb_ctx_stream(gvxb_ctx ctx);
 int gvxb_ctx_device(gvxb_ctx ctx);
 int gvxb_ctx_sm_count(gvxb_ctx ctx);

@@ -106,6 +106,7 @@ def _declare(c, g):
     g.gvxc_session_bind.argtypes = [P, I, P, ctypes.c_int64, ctypes.c_int64]
     g.gvxc_session_set_stream.argtypes = [P, P]
     g.gvxc_session_launch.argtypes = [P]
+    g.gvxc_session_set_overlap.argtypes = [P, I]
     g.gvxc_session_sync.argtypes = [P]
     g.gvxc_session_launches.argtypes = [P]
     g.gvxc_session_upload_input.argtypes = [P, I, U8P]
@@ -475,6 +476,9 @@ class Session:
 
     def set_stream(self, stream: int | None):
         _check_graph(_graph.gvxc_session_set_stream(self._h, ctypes.c_void_p(stream or 0)))
+
+    def set_overlap(self, mode: int):
+        _check_graph(_graph.gvxc_session_set_overlap(self._h, mode))
 
     def launch(self):
         _check_graph(_graph.gvxc_session_launch(self._h))

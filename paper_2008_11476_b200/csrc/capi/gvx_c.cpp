@@ -245,6 +245,10 @@ int gvxc_session_set_stream(gvxc_session s, void* stream) {
     return guarded([&] { s->s->set_stream(stream); });
 }
 
+int gvxc_session_set_overlap(gvxc_session s, int mode) {
+    return guarded([&] { s->s->set_overlap(mode); });
+}
+
 int gvxc_session_launch(gvxc_session s) {
     return guarded([&] { s->s->launch(); });
 }

@@ -151,6 +151,7 @@ int gvxb_enable_peer(gvxb_ctx ctx, int peer) {
 
 int gvxb_copy_peer_rows(gvxb_ctx ctx, void* dst, size_t dpitch, int dst_dev, const void* src, size_t spitch,
                         int src_dev, size_t row_bytes, size_t rows) {
+    gvxb_impl::untracked_op(ctx);
     if (!rows || !row_bytes) return GVXB_OK;
     cudaError_t e;
     if (dst_dev == src_dev) {
@@ -169,6 +170,7 @@ int gvxb_copy_peer_rows(gvxb_ctx ctx, void* dst, size_t dpitch, int dst_dev, con
 }
 
 int gvxb_stream_wait_event(gvxb_ctx ctx, void* ev) {
+    gvxb_impl::untracked_op(ctx);
     cudaError_t e = cudaStreamWaitEvent(ctx->stream, static_cast<cudaEvent_t>(ev), 0);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaStreamWaitEvent");
 }
@@ -226,6 +228,7 @@ int gvxb_comm_destroy(gvxb_comm c) {
 }
 
 int gvxb_halo_start(gvxb_ctx ctx, gvxb_comm c, const gvxb_band_plan* p, const gvxb_image* slab) {
+    gvxb_impl::untracked_op(ctx);
     if (!c || !p || !slab) return fail(GVXB_ERR_INVALID, "halo exchange: null argument");
     if (p->world != c->world || p->rank != c->rank) return fail(GVXB_ERR_INVALID, "band plan / communicator mismatch");
     cudaError_t e = cudaEventRecord(c->ready, ctx->stream);
@@ -261,6 +264,7 @@ int gvxb_halo_start(gvxb_ctx ctx, gvxb_comm c, const gvxb_band_plan* p, const gv
 }
 
 int gvxb_halo_wait(gvxb_ctx ctx, gvxb_comm c) {
+    gvxb_impl::untracked_op(ctx);
     if (!c) return fail(GVXB_ERR_INVALID, "halo wait: null communicator");
     if (!c->posted) return GVXB_OK;
     cudaError_t e = cudaStreamWaitEvent(ctx->stream, c->done, 0);

@@ -12,6 +12,11 @@
 #include <cstdint>
 #include <string>
 
+/// Device byte range [lo, hi) a kernel reads or writes.
+struct gvxb_range {
+    uintptr_t lo = 0, hi = 0;
+};
+
 struct gvxb_ctx_s {
     int device = 0;
     int sm_count = 148;
@@ -20,13 +25,57 @@ struct gvxb_ctx_s {
     unsigned* status = nullptr;            // GVXB_STATUS_* bits
     unsigned long long* counter = nullptr; // pixel-read events of generated kernels
     int64_t launches = 0;
+    // Programmatic dependent launch between consecutive hand-written kernels
+    // (gvxb_ctx_set_overlap): the ranges the previous kernel on the stream
+    // read / wrote, valid only while nothing else was enqueued after it.
+    int overlap = -1; // -1 auto (own stream only), 0 off, 1 on
+    bool prev_kernel = false;
+    gvxb_range prev_r[4], prev_w[4];
+    int prev_nr = 0, prev_nw = 0;
 };
 
 namespace gvxb_impl {
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int check_launch(gvxb_ctx ctx, const char* what);
+
+/// Bytes an image (all its frames) spans; empty for a null image.
+inline gvxb_range image_range(const gvxb_image& im) {
+    gvxb_range r;
+    if (!im.data || im.height <= 0) return r;
+    const int64_t frames = im.frames > 1 ? im.frames : 1;
+    const int64_t span = (frames > 1 ? im.frame_stride * (frames - 1) : 0) + im.pitch * im.height;
+    r.lo = reinterpret_cast<uintptr_t>(im.data);
+    r.hi = r.lo + static_cast<uintptr_t>(span);
+    return r;
+}
+
+/// Whether a kernel reading `r` and writing `w` may overlap the previous
+/// kernel on ctx's stream: no read-after-write, write-after-read or
+/// write-after-write through any of the ranges.  Returns the value of the
+/// kernel's `pdl_wait` parameter: 1 = must wait for the previous grid.
+int pdl_must_wait(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw);
+
+/// Launches `fn` on ctx's stream, as a programmatic dependent launch when
+/// the context allows it and the previous stream operation was a tracked
+/// kernel, and records this kernel's ranges for the next one.
+int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                   const gvxb_range* r, int nr, const gvxb_range* w, int nw, const char* what);
+
+/// Any other stream operation (copies, memsets, generated kernels).
+inline void untracked_op(gvxb_ctx ctx) { ctx->prev_kernel = false; }
 } // namespace gvxb_impl
+
+namespace gvxd {
+/// Kernel prologue for programmatic dependent launch: let the next grid on
+/// the stream be scheduled as this one's CTAs retire, and, when this grid
+/// may read what the previous one wrote (pdl_wait), wait for it first.  Both
+/// are no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_prologue(int pdl_wait) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+} // namespace gvxd
 
 namespace gvxd {
 

@@ -330,6 +330,7 @@ extern "C" int gvxb_edge(gvxb_ctx ctx, const gvxb_edge_args* a) {
     p.mag = plane(a->mag);
     dim3 grid((s.width + kEdgeTW - 1) / kEdgeTW, (rows + p.th - 1) / p.th, frames);
     void* args[] = {&map, &p};
+    untracked_op(ctx);
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kEdgeThreads), args, 0, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "edge kernel launch");
     return check_launch(ctx, "edge kernel");

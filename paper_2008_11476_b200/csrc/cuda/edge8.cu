@@ -51,6 +51,7 @@ struct E8Plane {
 struct Edge8Params {
     int width;
     int th;
+    int pdl_wait; // the previous grid on the stream may have written what this one touches
     Band band;
     E8Plane gx, gy, mag;
 };
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kE8Threads, GVX_EDGE8_MINB) edge8_kernel(const
     const int steps = (y1 - y0) + 4;
     const int nchunks = (steps + kE8Chunk - 1) / kE8Chunk;
 
+    pdl_prologue(p.pdl_wait);
     if (lane == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -446,10 +448,11 @@ int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a) {
     p.gy = plane(a->gy);
     p.mag = plane(a->mag);
     dim3 grid((s.width + kE8Cols - 1) / kE8Cols, (rows + p.th - 1) / p.th, frames);
+    const gvxb_range r[1] = {image_range(s)};
+    const gvxb_range w[3] = {image_range(a->gx), image_range(a->gy), image_range(a->mag)};
+    p.pdl_wait = pdl_must_wait(ctx, r, 1, w, 3);
     void* args[] = {&map, &p};
-    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kE8Threads), args, 0, ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "edge8 kernel launch");
-    return check_launch(ctx, "edge8 kernel");
+    return launch_tracked(ctx, fn, grid, dim3(kE8Threads), args, 0, r, 1, w, 3, "edge8 kernel");
 }
 
 } // namespace gvxb_impl

@@ -52,6 +52,7 @@ constexpr int kHarTHMax = 64; // measured (4K x32): band heights 54..72 within 1
 
 struct HarrisParams {
     int width;
+    int pdl_wait; // the previous grid on the stream may have written what this one touches
     int th; // output rows per band (<= kHarTHMax), chosen to fill whole waves
     Band band;
     uint8_t* mask;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
     const int steps = (y1 - y0) + 4; // virtual rows j <-> global row y0 - 2 + j
     const int nchunks = (steps + kHarChunk - 1) / kHarChunk;
 
+    pdl_prologue(p.pdl_wait);
     if (lane == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -494,8 +496,9 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     p.c_tt = static_cast<float>((c_tt + c_tr / (2.0 * a_tr)) * 1.001);
     p.c0 = static_cast<float>((c_0 + c_tr * a_tr / 2.0) * 1.001 + 1.0);
     dim3 grid((s.width + kHarCols - 1) / kHarCols, (rows + p.th - 1) / p.th, frames);
+    const gvxb_range r[1] = {image_range(s)};
+    const gvxb_range w[2] = {image_range(a->mask), image_range(a->response)};
+    p.pdl_wait = pdl_must_wait(ctx, r, 1, w, 2);
     void* args[] = {&map, &p};
-    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kHarThreads), args, 0, ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "harris kernel launch");
-    return check_launch(ctx, "harris kernel");
+    return launch_tracked(ctx, fn, grid, dim3(kHarThreads), args, 0, r, 1, w, 2, "harris kernel");
 }

@@ -41,6 +41,49 @@ int check_launch(gvxb_ctx ctx, const char* what) {
     return GVXB_OK;
 }
 
+namespace {
+bool overlaps(const gvxb_range& a, const gvxb_range& b) { return a.lo < b.hi && b.lo < a.hi && a.lo < a.hi && b.lo < b.hi; }
+} // namespace
+
+int pdl_must_wait(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw) {
+    if (!ctx->prev_kernel) return 1;
+    for (int i = 0; i < nr; ++i)
+        for (int k = 0; k < ctx->prev_nw; ++k)
+            if (overlaps(r[i], ctx->prev_w[k])) return 1; // RAW
+    for (int i = 0; i < nw; ++i) {
+        for (int k = 0; k < ctx->prev_nw; ++k)
+            if (overlaps(w[i], ctx->prev_w[k])) return 1; // WAW
+        for (int k = 0; k < ctx->prev_nr; ++k)
+            if (overlaps(w[i], ctx->prev_r[k])) return 1; // WAR
+    }
+    return 0;
+}
+
+int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                   const gvxb_range* r, int nr, const gvxb_range* w, int nw, const char* what) {
+    const bool allowed = ctx->overlap > 0 || (ctx->overlap < 0 && ctx->stream == ctx->own_stream);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    if (allowed && ctx->prev_kernel) {
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    ctx->prev_nr = nr < 4 ? nr : 4;
+    ctx->prev_nw = nw < 4 ? nw : 4;
+    for (int i = 0; i < ctx->prev_nr; ++i) ctx->prev_r[i] = r[i];
+    for (int i = 0; i < ctx->prev_nw; ++i) ctx->prev_w[i] = w[i];
+    ctx->prev_kernel = nr <= 4 && nw <= 4;
+    return check_launch(ctx, what);
+}
+
 } // namespace gvxb_impl
 
 using namespace gvxb_impl;
@@ -136,8 +179,16 @@ int gvxb_ctx_destroy(gvxb_ctx ctx) {
     return GVXB_OK;
 }
 
+int gvxb_ctx_set_overlap(gvxb_ctx ctx, int mode) {
+    ctx->overlap = mode < 0 ? -1 : (mode > 0 ? 1 : 0);
+    untracked_op(ctx);
+    return GVXB_OK;
+}
+
 int gvxb_ctx_set_stream(gvxb_ctx ctx, void* s) {
-    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    cudaStream_t to = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    if (to != ctx->stream) untracked_op(ctx);
+    ctx->stream = to;
     return GVXB_OK;
 }
 
@@ -197,12 +248,14 @@ int gvxb_host_is_pinned(const void* p, int* pinned) {
 }
 
 int gvxb_memset(gvxb_ctx ctx, void* p, int v, size_t bytes) {
+    untracked_op(ctx);
     cudaError_t e = cudaMemsetAsync(p, v, bytes, ctx->stream);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemsetAsync");
 }
 
 int gvxb_upload_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
                    size_t row_bytes, size_t rows) {
+    untracked_op(ctx);
     if (!rows || !row_bytes) return GVXB_OK;
     // dense on both sides: one linear copy (the DMA engines stream it faster)
     cudaError_t e = dpitch == row_bytes && spitch == row_bytes
@@ -214,6 +267,7 @@ int gvxb_upload_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size
 
 int gvxb_download_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, size_t spitch,
                      size_t row_bytes, size_t rows) {
+    untracked_op(ctx);
     if (!rows || !row_bytes) return GVXB_OK;
     cudaError_t e = dpitch == row_bytes && spitch == row_bytes
                         ? cudaMemcpyAsync(dst, src, row_bytes * rows, cudaMemcpyDeviceToHost, ctx->stream)
@@ -223,6 +277,7 @@ int gvxb_download_2d(gvxb_ctx ctx, void* dst, size_t dpitch, const void* src, si
 }
 
 int gvxb_copy_d2d(gvxb_ctx ctx, void* dst, const void* src, size_t bytes) {
+    untracked_op(ctx);
     cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMemcpyAsync(D2D)");
 }
@@ -240,6 +295,7 @@ int gvxb_event_destroy(void* ev) {
 }
 
 int gvxb_event_record(gvxb_ctx ctx, void* ev) {
+    untracked_op(ctx);
     cudaError_t r = cudaEventRecord(static_cast<cudaEvent_t>(ev), ctx->stream);
     return r == cudaSuccess ? GVXB_OK : cuda_fail(r, "cudaEventRecord");
 }
@@ -257,6 +313,7 @@ int gvxb_event_sync(void* ev) {
 }
 
 int gvxb_status_reset(gvxb_ctx ctx) {
+    untracked_op(ctx);
     cudaError_t e = cudaMemsetAsync(ctx->status, 0, sizeof(unsigned) + 2 * sizeof(unsigned long long),
                                     ctx->stream);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "status reset");
@@ -363,6 +420,7 @@ int gvxb_jit_free(gvxb_module m) {
 
 int gvxb_jit_launch(gvxb_ctx ctx, gvxb_module m, int k, const unsigned grid[3], const unsigned block[3],
                     size_t smem, void** args) {
+    untracked_op(ctx);
     if (k < 0 || k >= static_cast<int>(m->functions.size())) return fail(GVXB_ERR_INVALID, "bad kernel index");
     if (grid[0] == 0 || grid[1] == 0 || grid[2] == 0) return GVXB_OK;
     CUresult r = driver().launch_kernel(m->functions[static_cast<std::size_t>(k)], grid[0], grid[1], grid[2],

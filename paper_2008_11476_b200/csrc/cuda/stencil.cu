@@ -319,6 +319,7 @@ struct SepParams {
     int width;
     Band band;
     int th;
+    int pdl_wait; // the previous grid on the stream may have written what this one touches
     float u[7], v[7];
     float bias;     // d / 2 (0 for d == 1); fractional form: (d / 2) / 2^15
     float inv_d;    // 1 / (d << shift), exact power of two
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
     __shared__ uint64_t bar;
     extern __shared__ uint4 hist_dyn[]; // kMode 2: [bin][lane][warp] u8 counters
     uint8_t* hist = reinterpret_cast<uint8_t*>(hist_dyn);
+    pdl_prologue(p.pdl_wait);
 
     const int tid = static_cast<int>(threadIdx.x);
     const int x0 = blockIdx.x * TW;
@@ -785,7 +787,7 @@ void* sep_fn_k(int k, bool clamp, int frac) {
 }
 
 int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K, int rows, int th_max, size_t dyn,
-               int ch_threads) {
+               int ch_threads, const gvxb_range* wr, int nw) {
     using namespace gvxb_impl;
     if (dyn > 0) { // static tile + dynamic histogram exceed the 48 KB default
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
@@ -803,10 +805,10 @@ int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K,
     CUtensorMap map;
     if (int rc = make_u8_tensor_map(&map, s, sw, p.th + K - 1)) return rc;
     dim3 grid((s.width + tw - 1) / tw, (rows + p.th - 1) / p.th, frames);
+    const gvxb_range r[1] = {image_range(s)};
+    p.pdl_wait = pdl_must_wait(ctx, r, 1, wr, nw);
     void* args[] = {&map, &p};
-    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(nt), args, dyn, ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "separable stencil launch");
-    return check_launch(ctx, "separable stencil kernel");
+    return launch_tracked(ctx, fn, grid, dim3(nt), args, dyn, r, 1, wr, nw, "separable stencil kernel");
 }
 
 template <int K>
@@ -844,7 +846,8 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
             sp.dst_pitch = a->dst.pitch;
             sp.dst_fstride = a->dst.frames > 1 ? a->dst.frame_stride : a->dst.pitch * a->dst.height;
             void* fn = a->mode == 0 ? sep_fn_k<0>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<1>(a->ksize, sp.clamp255, sp.frac);
-            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0, sep_threads(0));
+            const gvxb_range w[1] = {image_range(a->dst)};
+            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0, sep_threads(0), w, 1);
         }
     }
     StencilParams p;
@@ -870,6 +873,7 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
     const int frames = s.frames > 0 ? s.frames : 1;
     dim3 grid((s.width + kStTW - 1) / kStTW, (rows + kStTH - 1) / kStTH, frames);
     void* args[] = {&map, &p};
+    untracked_op(ctx);
     cudaError_t e = cudaLaunchKernel(fn, grid, dim3(kStThreads), args, 0, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "stencil kernel launch");
     return check_launch(ctx, "stencil kernel");
@@ -878,6 +882,7 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
 static int meanstd(gvxb_ctx ctx, const gvxb_conv_stats_args* a, const ConvStatsParams& p, int frames, const gvxb_image& s) {
     if (a->mean || a->stddev) {
         const long long n = static_cast<long long>(s.width) * s.height;
+        gvxb_impl::untracked_op(ctx);
         meanstd_finalize_kernel<<<(frames + 63) / 64, 64, 0, ctx->stream>>>(p.sum, p.sumsq, n, frames, a->mean,
                                                                               a->stddev);
         return gvxb_impl::check_launch(ctx, "meanstd finalize");
@@ -917,6 +922,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
         const long long nh = a->hist ? static_cast<long long>(frames) * p.bins * 2 : 0;
         const long long total = nh + 2LL * frames;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 1024));
+        untracked_op(ctx);
         zero_scratch_kernel<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<unsigned long long*>(a->hist), nh,
                                                              p.sum, p.sumsq, frames);
         if (int rc = check_launch(ctx, "conv_stats scratch clear")) return rc;
@@ -943,7 +949,8 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
             sp.sum = p.sum;
             sp.sumsq = p.sumsq;
             void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<2>(a->ksize, sp.clamp255, sp.frac);
-            if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2)))
+            const gvxb_range w[1] = {image_range(a->converted)}; // after the (untracked) scratch clear: waits anyway
+            if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2), w, 1))
                 return rc;
             return meanstd(ctx, a, p, frames, s);
         }
@@ -965,6 +972,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
     }
     dim3 grid((s.width + kStTW - 1) / kStTW, (s.height + kStTH - 1) / kStTH, frames);
     void* args[] = {&map, &p};
+    untracked_op(ctx);
     e = cudaLaunchKernel(fn, grid, dim3(kStThreads), args, dyn, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "conv_stats kernel launch");
     if (int rc = check_launch(ctx, "conv_stats kernel")) return rc;

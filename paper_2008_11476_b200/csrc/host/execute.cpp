@@ -1393,20 +1393,21 @@ DeviceTensor DeviceSession::tensor(ObjectId id) {
     return DeviceTensor{s.ptr, s.pitch, s.fstride};
 }
 
-void DeviceSession::set_stream(void* s) { impl_->stream = s; }
+void DeviceSession::set_stream(void* s) {
+    impl_->stream = s;
+    gvxb_ctx_set_stream(impl_->ctx, s); // the session's own context: kept until changed
+}
+
+void DeviceSession::set_overlap(int mode) { dev::check(gvxb_ctx_set_overlap(impl_->ctx, mode), "set overlap"); }
 
 void DeviceSession::launch() {
     if (impl_->scratch.size() != impl_->prog->units.size()) impl_->prepare();
-    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
     impl_->run_all();
-    gvxb_ctx_set_stream(impl_->ctx, nullptr);
 }
 
 void DeviceSession::synchronize() {
-    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
     std::uint32_t status = 0;
     const int rc = gvxb_status_read(impl_->ctx, &status);
-    gvxb_ctx_set_stream(impl_->ctx, nullptr);
     dev::check(rc, "device status");
     if (status & GVXB_STATUS_DIV_BY_ZERO) throw Error(ErrorCode::DivByZero, "division by zero");
     if (status & GVXB_STATUS_INDEX_RANGE) throw Error(ErrorCode::ShapeMismatch, "array index out of range");
@@ -1414,16 +1415,12 @@ void DeviceSession::synchronize() {
 
 void DeviceSession::upload(ObjectId id, const Buffer& b, int frame) {
     if (!impl_->prog->objects.count(id)) return;
-    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
     impl_->upload(id, b, frame);
-    gvxb_ctx_set_stream(impl_->ctx, nullptr);
 }
 
 Buffer DeviceSession::download(ObjectId id, int frame) {
     if (!impl_->prog->objects.count(id)) throw Error(ErrorCode::UnknownObject, "object not produced on the device", id);
-    gvxb_ctx_set_stream(impl_->ctx, impl_->stream);
     Buffer b = impl_->download(id, frame);
-    gvxb_ctx_set_stream(impl_->ctx, nullptr);
     return b;
 }
 
