@@ -107,6 +107,9 @@ __device__ __forceinline__ uint32_t sign_bytes(float a, float b) {
     return r;
 }
 
+#ifndef GVX_HARRIS_UNROLL
+#define GVX_HARRIS_UNROLL 2 // rows per loop iteration of interior strips (measured: 4 rows -16%, 163 registers)
+#endif
 template <bool kResp>
 #ifndef GVX_HARRIS_MINB
 #define GVX_HARRIS_MINB 12 // resident one-warp CTAs per SM: 3 per scheduler at <= 168 registers
@@ -227,7 +230,8 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
             return Q8{{sub2(q.v[2], q.v[0]), sub2(q.v[3], q.v[1]), sub2(q.v[4], q.v[2]), sub2(q.v[5], q.v[3])}};
         };
         /// Sobel-y of the row between source rows j and j-2: vertical
-        /// difference first, then the 1-2-1 smoothing across columns.
+        /// difference first (the 2^23 cancels exactly), then the 1-2-1
+        /// smoothing across columns.
         auto sobel_y = [&](const Raw8& q, const Raw8& m) {
             float2 d[6];
 #pragma unroll
@@ -423,6 +427,16 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
             emit(padd(i.P, (y1 == H) ? i.Hp : Hn));
         };
         int j = 4;
+        // 4 rows per iteration on interior strips (loop-carried copies
+        // re-aligned once per 4 rows; j % 4 == 0: one chunk check)
+        if (!kEdge && GVX_HARRIS_UNROLL >= 4)
+            for (; j + 4 < steps; j += 4) {
+                if (j % kHarChunk == 0) next_chunk(j / kHarChunk);
+                full_step(j, A, B);
+                full_step(j + 1, B, A);
+                full_step(j + 2, A, B);
+                full_step(j + 3, B, A);
+            }
         for (; j + 2 < steps; j += 2) {
             if (j % kHarChunk == 0) next_chunk(j / kHarChunk);
             full_step(j, A, B);
