@@ -400,8 +400,22 @@ def run_banded(args, rank, world, local_rank):
     # uploads only the rows it owns: its halo rows come from the exchange
     img = gvx.random_u8(W, H, 5)
     band.upload(0, img[r0:r1], r0)
-    for _ in range(args.warmup):
+    # results alternate between two output buffers (double buffering, as the
+    # frame configs rotate two batches): consecutive executions then touch
+    # disjoint outputs and may overlap (programmatic dependent launch; only
+    # this band's work runs on dev.stream)
+    band.set_overlap(1)
+    out_pitch = (2 * W + 127) // 128 * 128
+    outs = [dev.alloc(out_pitch * (r1 - r0)) for _ in range(2)]
+
+    def launch(i):
+        band.bind(1, outs[i % 2], out_pitch, out_pitch * (r1 - r0))
         band.launch()
+
+    for i in range(args.warmup):
+        launch(i)
+    band.sync()
+    launch(0)
     band.sync()
     checked = None
     if not args.no_check:
@@ -423,7 +437,7 @@ def run_banded(args, rank, world, local_rank):
         t_end = time.perf_counter() + args.clock_window
         i = 0
         while time.perf_counter() < t_end:
-            band.launch()
+            launch(i)
             i += 1
             if i % 20 == 0:
                 dev.sync()
@@ -431,8 +445,8 @@ def run_banded(args, rank, world, local_rank):
         barrier()
         launches0 = gvx.launch_count()  # every context of the process (the band has its own)
         dev.record(ev[0])
-        for _ in range(args.steps):
-            band.launch()
+        for i in range(args.steps):
+            launch(i)
         dev.record(ev[1])
         dev.sync()
     ms = dev.elapsed_ms(ev[0], ev[1])

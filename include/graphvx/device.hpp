@@ -142,6 +142,12 @@ public:
     /// (the slab's first row: src_row0 for an input, row0 for an output).
     DeviceTensor tensor(ObjectId id, int* first_row = nullptr, int* rows = nullptr);
     void set_stream(void* cuda_stream);
+    /// As DeviceSession::set_overlap.
+    void set_overlap(int mode);
+    /// Use caller memory for image `id`'s band storage (same rows as
+    /// tensor(id) reports; pitch a multiple of 16 and >= the row bytes),
+    /// e.g. to alternate output buffers between executions.
+    void bind(ObjectId id, DeviceTensor t);
     /// Global rows [first_row, first_row + rows) of image `id` from / to host
     /// memory (`pitch` bytes per host row); must lie inside the band storage.
     void upload_rows(ObjectId id, const void* host, std::size_t pitch, int first_row, int rows, int frame = 0);

@@ -121,6 +121,9 @@ int gvxc_band_tensor(gvxc_band b, int slot, void** dptr, int64_t* pitch, int64_t
 int gvxc_band_upload(gvxc_band b, int slot, const void* host, size_t pitch, int first_row, int rows, int frame);
 int gvxc_band_download(gvxc_band b, int slot, void* host, size_t pitch, int first_row, int rows, int frame);
 int gvxc_band_set_stream(gvxc_band b, void* stream);
+int gvxc_band_set_overlap(gvxc_band b, int mode);
+/* Caller storage for a slot's band rows (as gvxc_band_tensor reports them). */
+int gvxc_band_bind(gvxc_band b, int slot, void* dptr, int64_t pitch, int64_t fstride);
 int gvxc_band_launch(gvxc_band b);
 int gvxc_band_sync(gvxc_band b);
 int gvxc_band_launches(gvxc_band b);

@@ -149,6 +149,8 @@ def _declare(c, g):
     g.gvxc_band_upload.argtypes = [P, I, P, SZ, I, I, I]
     g.gvxc_band_download.argtypes = [P, I, P, SZ, I, I, I]
     g.gvxc_band_set_stream.argtypes = [P, P]
+    g.gvxc_band_set_overlap.argtypes = [P, I]
+    g.gvxc_band_bind.argtypes = [P, I, P, ctypes.c_int64, ctypes.c_int64]
     g.gvxc_band_launch.argtypes = [P]
     g.gvxc_band_sync.argtypes = [P]
     g.gvxc_band_launches.argtypes = [P]
@@ -869,6 +871,12 @@ class Band:
 
     def set_stream(self, stream: int | None):
         _check_graph(_graph.gvxc_band_set_stream(self._h, ctypes.c_void_p(stream or 0)))
+
+    def set_overlap(self, mode: int):
+        _check_graph(_graph.gvxc_band_set_overlap(self._h, mode))
+
+    def bind(self, slot: int, dptr: int, pitch: int, frame_stride: int = 0):
+        _check_graph(_graph.gvxc_band_bind(self._h, slot, ctypes.c_void_p(dptr), pitch, frame_stride))
 
     def launch(self):
         _check_graph(_graph.gvxc_band_launch(self._h))

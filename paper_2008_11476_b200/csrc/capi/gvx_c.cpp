@@ -507,6 +507,14 @@ int gvxc_band_download(gvxc_band b, int slot, void* host, size_t pitch, int firs
     return guarded([&] { b->s->download_rows(band_slot(b->g, slot), host, pitch, first_row, rows, frame); });
 }
 
+int gvxc_band_set_overlap(gvxc_band b, int mode) {
+    return guarded([&] { b->s->set_overlap(mode); });
+}
+
+int gvxc_band_bind(gvxc_band b, int slot, void* dptr, int64_t pitch, int64_t fstride) {
+    return guarded([&] { b->s->bind(band_slot(b->g, slot), gvx::DeviceTensor{dptr, pitch, fstride}); });
+}
+
 int gvxc_band_set_stream(gvxc_band b, void* stream) {
     return guarded([&] { b->s->set_stream(stream); });
 }

@@ -365,6 +365,27 @@ DeviceTensor BandedSession::tensor(ObjectId id, int* first_row, int* rows) {
 
 void BandedSession::set_stream(void* s) { check(gvxb_ctx_set_stream(impl_->ctx, s), "set stream"); }
 
+void BandedSession::set_overlap(int mode) { check(gvxb_ctx_set_overlap(impl_->ctx, mode), "set overlap"); }
+
+void BandedSession::bind(ObjectId id, DeviceTensor t) {
+    auto it = impl_->slabs.find(id);
+    if (it == impl_->slabs.end()) throw Error(ErrorCode::UnknownObject, "object is not an image of the program", id);
+    Slab& s = it->second;
+    const std::int64_t row = static_cast<std::int64_t>(impl_->W) * s.bpp;
+    if (!t.data || t.pitch % 16 != 0 || t.pitch < row)
+        throw Error(ErrorCode::ShapeMismatch, "band tensor: pitch must be a multiple of 16 and hold a row", id);
+    if (impl_->frames > 1 && t.frame_stride < t.pitch * s.rows)
+        throw Error(ErrorCode::ShapeMismatch, "band tensor: frame stride too small", id);
+    if (s.owned) {
+        gvxb_sync(impl_->ctx);
+        gvxb_free(impl_->ctx, s.ptr);
+    }
+    s.ptr = t.data;
+    s.pitch = t.pitch;
+    s.fstride = impl_->frames > 1 ? t.frame_stride : t.pitch * std::max(1, s.rows);
+    s.owned = false;
+}
+
 void BandedSession::upload_rows(ObjectId id, const void* host, std::size_t pitch, int first_row, int rows, int frame) {
     auto it = impl_->slabs.find(id);
     if (it == impl_->slabs.end()) throw Error(ErrorCode::UnknownObject, "object is not an image of the program", id);
