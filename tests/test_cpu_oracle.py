@@ -1,5 +1,7 @@
 """The CPU oracle is pinned before it is trusted (tests/golden/ were produced
 by the unmodified reference, see tests/golden/make_golden.py)."""
+import pathlib
+
 import numpy as np
 import pytest
 
@@ -67,3 +69,14 @@ def test_generalised_oracle_agrees_with_pinned_configs(oracle_mod):
     assert (oracle_mod.port_stencil(c, b5, 256, 0) == 200).all()
     assert (oracle_mod.port_stencil(c, np.ones((3, 3)), 8, 0) == 225).all()   # 1800/8 = 225
     assert (oracle_mod.port_stencil(c, np.ones((3, 3)), 4, 0) == 255).all()   # saturates
+
+
+def test_edge8_magnitude_rounding_is_exact(tmp_path):
+    """The fp32 rounding sequence of edge8's magnitude equals the reference's
+    llround(sqrt(n)) for every reachable n (tests/cpp/round_sqrt16.c)."""
+    import subprocess
+    src = pathlib.Path(__file__).resolve().parent / "cpp" / "round_sqrt16.c"
+    exe = tmp_path / "rs"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", str(src), "-o", str(exe), "-lm"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert "bad=0" in out, out

@@ -76,3 +76,55 @@ def test_random_dags_match_reference(block, gvx, oracle_mod):
         compare(doc, gvx, oracle_mod, seed=seed)
         ran += 1
     assert ran >= 20
+
+
+def _harris_doc(w, h, k, t, observable_resp=False):
+    doc = json.loads((REPO / "examples" / "cfg2_harris.json").read_text())
+    for im in doc["images"]:
+        im["width"], im["height"] = w, h
+        if observable_resp and im["name"] == "resp":
+            im.pop("virtual", None)
+    if observable_resp:
+        doc["outputs"] = ["resp", "mask"]
+
+    def patch(e):
+        if isinstance(e, dict):
+            if e.get("op") == "const_f":
+                e["value"] = k if e["value"] == 0.04 else t
+            for v in e.values():
+                patch(v)
+        elif isinstance(e, list):
+            for v in e:
+                patch(v)
+    patch(doc["custom_kernels"])
+    return doc
+
+
+@pytest.mark.parametrize("k", [0.04, 0.15, -0.05])
+def test_harris_certified_threshold_matches_reference(k, gvx, oracle_mod):
+    """The fused Harris kernel decides `resp > T` with a certified fp32
+    estimate and falls back to the reference's int64/double expression only
+    where the estimate is undecided.  Pin that decision to the UNMODIFIED
+    reference at thresholds placed ON response values of the image (ties:
+    resp == T gives 0) and at response quantiles, for several k."""
+    import numpy as np
+    if not oracle_mod.have_ref_graph_io():
+        pytest.skip("reference graph_io not built")
+    w, h, seed = 211, 97, 3
+    blob, _ = oracle_mod.ref_json_run(json.dumps(rg.reference_form(_harris_doc(w, h, k, 1e9, True))), seed)
+    outs = gvx.parse_outputs(blob)
+    resp = np.frombuffer(outs[0][1], np.float32)
+    vals = np.unique(resp)
+    picks = [float(vals[i]) for i in np.linspace(0, len(vals) - 1, 9).astype(int)]
+    picks += [float(np.quantile(resp, q)) for q in (0.5, 0.9, 0.99)] + [0.0, -1.0]
+    for t in picks:
+        doc = _harris_doc(w, h, k, t)
+        g = gvx.GraphFile(json.dumps(doc))
+        assert "harris" in g.describe()  # the fused kernel decides
+        want, _ = oracle_mod.ref_json_run(json.dumps(rg.reference_form(doc)), seed)
+        got, _ = g.run(naive=False, seed=seed)
+        assert blob_of(got) == want, (k, t)
+
+
+def blob_of(outs):
+    return blob(outs)
