@@ -157,6 +157,12 @@ int gvxc_json_run(gvxc_json g, int naive, unsigned long long seed, uint8_t* out,
                   long long counters[4]);
 /* PassStats of the plan (same layout as gvxc_graph_pass_stats). */
 int gvxc_json_pass_stats(gvxc_json g, long long st[8]);
+/* Device benchmark of the graph through DeviceSession (plan or naive):
+ * `frames` frames per execution (random_buffer inputs, seed + id), `iters`
+ * timed executions.  out = {ms per execution, algorithmic HBM bytes per
+ * execution (non-virtual source images read + produced images written),
+ * kernel launches per execution, frames}. */
+int gvxc_json_bench(gvxc_json g, int naive, int frames, int iters, unsigned long long seed, double out[4]);
 /* Device program summary (naive = 1: per-node program, else the plan's). */
 int gvxc_json_describe(gvxc_json g, int naive, char* buf, size_t cap);
 

@@ -133,6 +133,7 @@ def _declare(c, g):
     g.gvxc_json_run.argtypes = [P, I, ctypes.c_ulonglong, U8P, SZ, ctypes.POINTER(SZ), ctypes.POINTER(L)]
     g.gvxc_json_pass_stats.argtypes = [P, ctypes.POINTER(L)]
     g.gvxc_json_describe.argtypes = [P, I, ctypes.c_char_p, ctypes.c_size_t]
+    g.gvxc_json_bench.argtypes = [P, I, I, I, ctypes.c_ulonglong, ctypes.POINTER(D)]
     I32P = ctypes.POINTER(ctypes.c_int32)
     c.gvxb_band_plan_make.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_void_p]
     c.gvxb_comm_available.restype = I
@@ -247,6 +248,12 @@ class GraphFile:
         buf = ctypes.create_string_buffer(8192)
         _check_graph(self._g.gvxc_json_describe(self._h, int(naive), buf, 8192))
         return buf.value.decode()
+
+    def bench(self, naive: bool = False, frames: int = 1, iters: int = 20, seed: int = 1) -> dict:
+        """Device time of one execution over `frames` frames (DeviceSession)."""
+        out = (ctypes.c_double * 4)()
+        _check_graph(self._g.gvxc_json_bench(self._h, int(naive), frames, iters, seed, out))
+        return {"ms": out[0], "bytes": out[1], "launches": out[2], "frames": int(out[3])}
 
     def pass_stats(self) -> dict:
         st = (ctypes.c_longlong * 8)()

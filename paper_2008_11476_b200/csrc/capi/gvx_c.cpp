@@ -639,6 +639,51 @@ int gvxc_json_describe(gvxc_json g, int naive, char* buf, size_t cap) {
     });
 }
 
+int gvxc_json_bench(gvxc_json g, int naive, int frames, int iters, unsigned long long seed, double out[4]) {
+    return guarded([&] {
+        const gvx::AppGraph& app = *g->L->lg.graph;
+        const gvx::Context& ctx = *g->L->lg.ctx;
+        gvx::DeviceSession s = naive ? gvx::DeviceSession(g->L->impl, frames) : gvx::DeviceSession(*g->L->plan, frames);
+        double bytes = 0; // algorithmic HBM bytes per execution: source images in, observable images out
+        for (gvx::ObjectId id : app.data()) {
+            const gvx::DataObject* o = ctx.find(id);
+            if (!o || o->is_virtual || o->kind != gvx::ObjKind::Image) continue;
+            const gvx::ResolvedDesc d = o->desc();
+            const double b = static_cast<double>(d.width) * d.height * gvx::bytes_per_pixel(d.format) * frames;
+            if (app.producer(id) == gvx::kInvalidId) {
+                if (app.consumers(id).empty()) continue;
+                gvx::Buffer in = gvx::random_buffer(d, seed + static_cast<std::uint64_t>(id));
+                for (int f = 0; f < frames; ++f) s.upload(id, in, f);
+            }
+            bytes += b;
+        }
+        for (int i = 0; i < 3; ++i) s.launch();
+        s.synchronize();
+        void* ev[2];
+        gvxb_event_create(&ev[0]);
+        gvxb_event_create(&ev[1]);
+        gvxb_ctx c = nullptr;
+        gvxb_ctx_create(gvxb_ctx_device(gvx::dev::context()), &c);
+        s.set_stream(gvxb_ctx_stream(c));
+        s.launch();
+        gvxb_event_record(c, ev[0]);
+        const long long l0 = gvxb_total_launch_count();
+        for (int i = 0; i < iters; ++i) s.launch();
+        gvxb_event_record(c, ev[1]);
+        s.synchronize();
+        float ms = 0;
+        gvxb_event_elapsed_ms(ev[0], ev[1], &ms);
+        out[0] = ms / iters;
+        out[1] = bytes;
+        out[2] = static_cast<double>(gvxb_total_launch_count() - l0) / iters;
+        out[3] = frames;
+        s.set_stream(nullptr);
+        gvxb_event_destroy(ev[0]);
+        gvxb_event_destroy(ev[1]);
+        gvxb_ctx_destroy(c);
+    });
+}
+
 int gvxc_json_pass_stats(gvxc_json g, long long st[8]) {
     const gvx::PassStats& p = g->L->plan->stats;
     const long long v[8] = {p.nodes_before, p.nodes_alive, p.nodes_removed, p.transfers_naive,

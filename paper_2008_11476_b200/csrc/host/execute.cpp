@@ -416,6 +416,267 @@ bool chain_unit(const OperatorNode& pn, const OperatorNode& cn, ObjectId mid, co
     return true;
 }
 
+/// Generic fused regions (jit::lower_region): maximal convex DAG regions of
+/// the remaining executed point / local nodes over images of one size, each
+/// one kernel with its intermediates in shared memory.  Returns the units
+/// and the executed nodes they cover; a region that cannot be lowered
+/// (run-time typed bodies, shared memory) falls back to per-node kernels.
+std::vector<Unit> region_units(const AppGraph& fg, const VerifiedGraph& fused, const std::set<ObjectId>& taken,
+                               const std::map<ObjectId, std::vector<Value>>& matrices, std::set<ObjectId>& covered) {
+    std::vector<Unit> units;
+    if (std::getenv("GVX_NO_REGIONS")) return units;
+    const Context& ctx = fused.context();
+    std::map<ObjectId, std::vector<ObjectId>> readers;
+    std::map<ObjectId, ObjectId> writer;
+    for (const OperatorNode& n : fg.nodes())
+        for (const Binding& b : n.bindings) {
+            if (b.direction == Direction::Input) readers[b.object].push_back(n.id);
+            else writer[b.object] = n.id;
+        }
+    auto img_dims = [&](ObjectId id, int& w, int& h) {
+        if (id == kInvalidId) return true;
+        const ResolvedDesc& d = fused.desc(id);
+        if (d.kind != ObjKind::Image) return true;
+        if (w < 0) w = d.width, h = d.height;
+        return d.width == w && d.height == h;
+    };
+    // candidates
+    std::map<ObjectId, std::pair<int, int>> dims;
+    std::vector<ObjectId> order = fg.topo_sort();
+    std::set<ObjectId> cand;
+    for (ObjectId nid : order) {
+        if (taken.count(nid)) continue;
+        const OperatorNode* n = fg.node(nid);
+        if (!n || !n->abstraction) continue;
+        const AbstractionKind kk = n->abstraction->kind;
+        if (kk != AbstractionKind::Point && kk != AbstractionKind::Local) continue;
+        if (kk == AbstractionKind::Local && (n->abstraction->local().median3x3 || n->abstraction->local().window_w > 9 ||
+                                             n->abstraction->local().window_h > 9))
+            continue;
+        std::int64_t r = 0, w = 0;
+        if (!static_counts(*n, fused, r, w)) continue;
+        int W = -1, H = -1;
+        bool ok = true;
+        for (const Binding& b : n->bindings) {
+            ok = ok && img_dims(b.object, W, H);
+            if (b.direction == Direction::Output) {
+                const ResolvedDesc& d = fused.desc(b.object);
+                ok = ok && d.kind == ObjKind::Image &&
+                     (d.format == ImageFormat::U8 || d.format == ImageFormat::U16 || d.format == ImageFormat::S16 ||
+                      d.format == ImageFormat::S32 || d.format == ImageFormat::F32);
+            }
+        }
+        if (!ok || W < 0) continue;
+        cand.insert(nid);
+        dims[nid] = {W, H};
+    }
+    // reachability over the executed graph (small graphs)
+    std::map<ObjectId, std::set<ObjectId>> succ;
+    for (const OperatorNode& n : fg.nodes())
+        for (const Binding& b : n.bindings)
+            if (b.direction == Direction::Output)
+                for (ObjectId c : readers[b.object]) succ[n.id].insert(c);
+    auto reaches = [&](ObjectId from, const std::set<ObjectId>& targets, const std::set<ObjectId>& avoid) {
+        std::vector<ObjectId> st{from};
+        std::set<ObjectId> seen{from};
+        while (!st.empty()) {
+            const ObjectId x = st.back();
+            st.pop_back();
+            for (ObjectId y : succ[x]) {
+                if (targets.count(y)) return true;
+                if (avoid.count(y) || !seen.insert(y).second) continue;
+                st.push_back(y);
+            }
+        }
+        return false;
+    };
+    auto convex = [&](const std::set<ObjectId>& S) {
+        for (const OperatorNode& m : fg.nodes()) {
+            if (S.count(m.id)) continue;
+            bool from_s = false;
+            for (ObjectId x : S) from_s = from_s || succ[x].count(m.id) || reaches(x, {m.id}, S);
+            if (from_s && reaches(m.id, S, {})) return false;
+        }
+        return true;
+    };
+    // grow regions along candidate producer -> consumer edges, topo order
+    std::map<ObjectId, int> region_of;
+    std::vector<std::set<ObjectId>> regions;
+    for (ObjectId nid : order) {
+        if (!cand.count(nid)) continue;
+        const OperatorNode* n = fg.node(nid);
+        // join every producer region it can (merging them) while the union stays convex
+        std::set<ObjectId> S{nid};
+        std::set<int> merged;
+        for (const Binding& b : n->bindings) {
+            if (b.direction != Direction::Input) continue;
+            auto w = writer.find(b.object);
+            if (w == writer.end() || !region_of.count(w->second)) continue;
+            const int r = region_of[w->second];
+            if (merged.count(r) || regions[static_cast<std::size_t>(r)].empty()) continue;
+            if (dims[*regions[static_cast<std::size_t>(r)].begin()] != dims[nid]) continue;
+            std::set<ObjectId> T = S;
+            T.insert(regions[static_cast<std::size_t>(r)].begin(), regions[static_cast<std::size_t>(r)].end());
+            if (!convex(T)) continue;
+            S = std::move(T);
+            merged.insert(r);
+        }
+        for (int r : merged) regions[static_cast<std::size_t>(r)].clear();
+        regions.push_back(S);
+        for (ObjectId m : S) region_of[m] = static_cast<int>(regions.size()) - 1;
+    }
+    for (const std::set<ObjectId>& S : regions) {
+        if (S.size() < 2) continue; // merged-away (empty) or single nodes: per-node kernels
+        // members in topological order
+        std::vector<const OperatorNode*> mem;
+        for (ObjectId nid : order)
+            if (S.count(nid)) mem.push_back(fg.node(nid));
+        // region objects: images produced by members, and the single-channel
+        // images they read from outside (staged into shared memory); halos backwards
+        std::map<ObjectId, int> obj_index;
+        std::vector<jit::RegionObject> objs;
+        std::vector<ObjectId> obj_ids;
+        std::set<ObjectId> produced;
+        for (const OperatorNode* n : mem)
+            for (const Binding& b : n->bindings)
+                if (b.direction == Direction::Output) produced.insert(b.object);
+        auto staged_format = [](ImageFormat f) {
+            return f == ImageFormat::U8 || f == ImageFormat::U16 || f == ImageFormat::S16 || f == ImageFormat::S32 ||
+                   f == ImageFormat::F32;
+        };
+        for (const OperatorNode* n : mem)
+            for (const Binding& b : n->bindings) {
+                if (obj_index.count(b.object) || b.object == kInvalidId) continue;
+                const ResolvedDesc& d = fused.desc(b.object);
+                if (d.kind != ObjKind::Image) continue;
+                if (b.direction == Direction::Input && !produced.count(b.object) && !staged_format(d.format)) continue;
+                obj_index[b.object] = static_cast<int>(objs.size());
+                jit::RegionObject ro;
+                ro.format = d.format;
+                objs.push_back(ro);
+                obj_ids.push_back(b.object);
+            }
+        bool ok = true;
+        for (auto it = mem.rbegin(); it != mem.rend(); ++it) {
+            const OperatorNode* n = *it;
+            int hx = 0, hy = 0; // halo of this node's outputs
+            for (const Binding& b : n->bindings)
+                if (b.direction == Direction::Output) {
+                    hx = std::max(hx, objs[static_cast<std::size_t>(obj_index[b.object])].halo_x);
+                    hy = std::max(hy, objs[static_cast<std::size_t>(obj_index[b.object])].halo_y);
+                }
+            const bool local = n->abstraction->kind == AbstractionKind::Local;
+            const int rx = local ? n->abstraction->local().window_w / 2 : 0;
+            const int ry = local ? n->abstraction->local().window_h / 2 : 0;
+            const auto& ps = n->abstraction->signature.params;
+            int slot = 0;
+            for (std::size_t i = 0; i < ps.size(); ++i) {
+                if (ps[i].direction != Direction::Input) continue;
+                const int in_slot = slot++;
+                const Binding* b = n->binding_for(static_cast<int>(i));
+                if (!b || !obj_index.count(b->object)) continue;
+                // the window radius applies to inputs the taps read through a window
+                const bool win = local && n->abstraction->local().tap_body &&
+                                 jit::reads_window(*n->abstraction->local().tap_body, in_slot);
+                jit::RegionObject& ro = objs[static_cast<std::size_t>(obj_index[b->object])];
+                ro.halo_x = std::max(ro.halo_x, hx + (win ? rx : 0));
+                ro.halo_y = std::max(ro.halo_y, hy + (win ? ry : 0));
+            }
+        }
+        for (const jit::RegionObject& ro : objs) ok = ok && ro.halo_x <= 8 && ro.halo_y <= 8;
+        if (!ok) continue;
+        Unit u;
+        u.kind = Unit::Kind::Jit;
+        u.k = mem.back()->abstraction;
+        u.label = "region";
+        // stored objects: consumed outside the region or observable
+        std::vector<jit::SlotInfo> outs;
+        for (std::size_t o = 0; o < objs.size(); ++o) {
+            const ObjectId id = obj_ids[o];
+            if (!produced.count(id)) continue;
+            bool outside = false;
+            for (ObjectId r : readers[id]) outside = outside || !S.count(r);
+            const DataObject* ob = ctx.find(id);
+            if (outside || !ob || !ob->is_virtual) {
+                objs[o].store = static_cast<int>(outs.size());
+                outs.push_back(slot_of(fused, id));
+                u.out_ids.push_back(id);
+                u.writes.push_back(id);
+            }
+        }
+        std::vector<jit::RegionNode> rnodes;
+        std::map<ObjectId, int> param_of;
+        std::vector<jit::SlotInfo> ins;
+        std::int64_t reads = 0, writes = 0;
+        for (const OperatorNode* n : mem) {
+            jit::RegionNode rn;
+            rn.k = n->abstraction.get();
+            const auto& ps = rn.k->signature.params;
+            Unit tmp;
+            for (std::size_t i = 0; i < ps.size(); ++i) {
+                const Binding* b = n->binding_for(static_cast<int>(i));
+                const ObjectId id = b ? b->object : kInvalidId;
+                if (ps[i].direction == Direction::Input) {
+                    rn.in_slots.push_back(slot_of(fused, id));
+                    tmp.in_ids.push_back(id);
+                    const bool image = id != kInvalidId && fused.desc(id).kind == ObjKind::Image;
+                    if (image && obj_index.count(id)) {
+                        rn.in_obj.push_back(obj_index[id]);
+                        rn.in_param.push_back(-1);
+                        if (!produced.count(id) && !param_of.count(id)) { // staged region input
+                            param_of[id] = static_cast<int>(ins.size());
+                            ins.push_back(slot_of(fused, id));
+                            u.in_ids.push_back(id);
+                            u.reads.push_back(id);
+                            objs[static_cast<std::size_t>(obj_index[id])].load = param_of[id];
+                        }
+                    } else if (image) {
+                        if (!param_of.count(id)) {
+                            param_of[id] = static_cast<int>(ins.size());
+                            ins.push_back(slot_of(fused, id));
+                            u.in_ids.push_back(id);
+                            u.reads.push_back(id);
+                        }
+                        rn.in_obj.push_back(-1);
+                        rn.in_param.push_back(param_of[id]);
+                    } else {
+                        rn.in_obj.push_back(-1);
+                        rn.in_param.push_back(-1); // matrices are baked in; scalars make the body run-time typed
+                    }
+                } else {
+                    rn.out_obj.push_back(id != kInvalidId && obj_index.count(id) ? obj_index[id] : -1);
+                }
+            }
+            rn.matrix = matrix_for(tmp, ctx, matrices);
+            std::int64_t r = 0, w = 0;
+            static_counts(*n, fused, r, w);
+            reads += r;
+            writes += w;
+            rnodes.push_back(std::move(rn));
+        }
+        u.in_slots = ins;
+        u.out_slots = outs;
+        try {
+            u.prog = jit::lower_region(rnodes, objs, ins, outs);
+        } catch (const Error& e) {
+            if (std::getenv("GVX_TRACE_REGIONS"))
+                std::fprintf(stderr, "[gvx region] %zu nodes not fused: %s\n", mem.size(), e.what());
+            continue; // run-time typed parts: per-node kernels
+        }
+        u.width = dims[mem.front()->id].first;
+        u.height = dims[mem.front()->id].second;
+        u.static_reads = reads;
+        u.static_writes = writes;
+        u.device_counts_reads = false;
+        for (const OperatorNode* n : mem) {
+            u.covers.push_back(n->id);
+            covered.insert(n->id);
+        }
+        units.push_back(std::move(u));
+    }
+    return units;
+}
+
 void record_objects(Program& p, const VerifiedGraph& vg) {
     const Context& ctx = vg.context();
     for (const Unit& u : p.units) {
@@ -682,6 +943,11 @@ std::shared_ptr<Program> build_plan(const OptimizedPlan& plan, const std::map<Ob
                 break;
             }
         }
+    }
+    {
+        std::set<ObjectId> rcov;
+        for (Unit& u : region_units(fg, fused, covered_fused, matrices, rcov)) p->units.push_back(std::move(u));
+        covered_fused.insert(rcov.begin(), rcov.end());
     }
     for (ObjectId nid : fg.topo_sort())
         if (!covered_fused.count(nid)) p->units.push_back(jit_unit(*fg.node(nid), fused, matrices));
@@ -950,7 +1216,7 @@ struct DeviceSession::Impl {
             case jit::KernelSpec::Grid::Pixels:
             case jit::KernelSpec::Grid::OutPixels:
                 grid[0] = static_cast<unsigned>((u.width + ks.block_x * ks.cols - 1) / (ks.block_x * ks.cols));
-                grid[1] = static_cast<unsigned>((u.height + ks.block_y - 1) / ks.block_y);
+                grid[1] = static_cast<unsigned>((u.height + ks.block_y * ks.rows - 1) / (ks.block_y * ks.rows));
                 break;
             case jit::KernelSpec::Grid::Strided: {
                 grid[0] = static_cast<unsigned>((u.width + ks.block_x - 1) / ks.block_x);

@@ -9,6 +9,10 @@
 //   scan / scale / table            src/execute.cpp:729-843
 #include "jit.hpp"
 
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -99,6 +103,38 @@ __device__ __forceinline__ void flush_reads(const P& p, u64 rd) {
   if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0 && rd) atomicAdd((u64*)p.f[1], rd);
 }
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// ---- typed forms (Emitter::temit): the same semantics on statically typed
+// values, used where a range analysis proves int32 / int64 / double suffice
+__device__ __forceinline__ i64 t_cast_d(double r, i64 lo, i64 hi, int pol) {
+  if (r != r) return 0;
+  if (pol == 0) { if (r >= (double)hi) return hi; if (r <= (double)lo) return lo; return llround(r); }
+  i64 x = (i64)fmod(trunc(r), 18446744073709551616.0);
+  u64 width = (u64)(hi - lo) + 1ull; u64 low = (u64)x & (width - 1ull);
+  return (lo < 0 && low > (u64)hi) ? (i64)low - (i64)width : (i64)low;
+}
+__device__ __forceinline__ i64 t_sat(i64 x, i64 lo, i64 hi) { return x < lo ? lo : (x > hi ? hi : x); }
+// llround(sqrt((double)n)) for integer 0 <= n < 2^24: fp32 estimate, then
+// the integer correction k* = largest k with k*k - k < n (no n is a half
+// square, so half-away rounding never ties)
+__device__ __forceinline__ int t_round_sqrt(int n) {
+  int k = __float2int_rn(sqrtf(__int2float_rn(n)));
+  k -= (k * k - k >= n && k > 0) ? 1 : 0;
+  k += (n > k * k + k) ? 1 : 0;
+  return k;
+}
+__device__ __forceinline__ i64 t_wrap(i64 x, i64 lo, i64 hi) {
+  u64 width = (u64)(hi - lo) + 1ull; u64 low = (u64)x & (width - 1ull);
+  return (lo < 0 && low > (u64)hi) ? (i64)low - (i64)width : (i64)low;
+}
+__device__ __forceinline__ i64 t_div(const P& p, i64 a, i64 b) {
+  if (b == 0) { raise_st(p, 1u); return 0; }
+  if (b == -1) return (i64)(0ull - (u64)a);
+  return a / b;
+}
+__device__ __forceinline__ double t_ddiv(const P& p, double a, double d) {
+  if (d == 0.0) { raise_st(p, 1u); return 0.0; }
+  return __ddiv_rn(a, d);
+}
 )CUDA";
 
 std::string hex_i64(std::int64_t v) {
@@ -122,6 +158,12 @@ int type_code(ScalarType t) { return static_cast<int>(t); }
 int field_in(int k) { return 5 + 3 * k; }
 
 // ------------------------------------------------------------ node emitter
+
+/// Static type of a value held in shared memory by a region kernel.
+struct TVproto {
+    char t = 'i';
+    long long lo = 0, hi = 0;
+};
 
 struct Emitter {
     const std::vector<SlotInfo>& ins;
@@ -148,7 +190,18 @@ struct Emitter {
     std::string prefix;
     int smem_slot = -1;
     std::string smem_loader;
-    int fin(int slot) const { return field_in(slot_base + slot); }
+    /// Region kernels (lower_region): input slot -> parameter slot of the
+    /// region kernel, and input slot -> region object held in shared memory
+    /// (-1: read from global memory).
+    std::vector<int> slot_param;
+    std::vector<int> slot_obj;
+    /// Shared-memory access of region object o at global (x, y): entry
+    /// expression builder set by lower_region.
+    std::function<std::string(int, int, int)> obj_entry; ///< (object, dx, dy) from the current entry
+    std::function<bool(int, TVproto&)> obj_type;
+    int fin(int slot) const {
+        return field_in(slot_param.empty() ? slot_base + slot : slot_param[static_cast<std::size_t>(slot)]);
+    }
     int fout(int o) const { return field_in((n_in_total >= 0 ? n_in_total : n_in) + o); }
 
     std::string in_base(int slot) const {
@@ -310,6 +363,413 @@ struct Emitter {
         return std::string(un[i]) + "(" + emit(*e.a) + ")";
     }
 
+    // ------------------------------------------------------------ typed
+    // A statically typed form of an expression: 'i' int32, 'l' int64, 'd'
+    // double, with the integer value range.  temit() fails (returns false)
+    // for anything whose type is only known at run time (scalars / arrays,
+    // mixed-type Select, bit ops on reals); callers then use emit().
+    struct TV {
+        std::string c;
+        char t = 'i';
+        __int128 lo = 0, hi = 0;
+    };
+    static constexpr __int128 kI32Lo = -2147483648LL, kI32Hi = 2147483647LL;
+    static constexpr __int128 kI64Lo = static_cast<__int128>(INT64_MIN), kI64Hi = static_cast<__int128>(INT64_MAX);
+    /// Typed value of the combined tap value in Post mode (slot 0), if any.
+    bool cmb_typed = false;
+    TV cmb_tv;
+
+    static TV tint(std::string c, __int128 lo, __int128 hi) {
+        TV v;
+        v.c = std::move(c);
+        v.lo = lo;
+        v.hi = hi;
+        v.t = (lo >= kI32Lo && hi <= kI32Hi) ? 'i' : 'l';
+        return v;
+    }
+    static TV tdbl(std::string c) {
+        TV v;
+        v.c = std::move(c);
+        v.t = 'd';
+        return v;
+    }
+    static std::string as_i64(const TV& v) { return "((i64)(" + v.c + "))"; }
+    static std::string as_dbl(const TV& v) { return v.t == 'd' ? v.c : "__ll2double_rn((i64)(" + v.c + "))"; }
+    static std::string i128s(__int128 x) {
+        // literal of an int64-range bound
+        char buf[48];
+        std::snprintf(buf, sizeof buf, "((i64)0x%llxull)", static_cast<unsigned long long>(static_cast<long long>(x)));
+        return buf;
+    }
+    static std::string tlit_i(std::int64_t v) {
+        char buf[48];
+        if (v >= -2147483647LL && v <= 2147483647LL) std::snprintf(buf, sizeof buf, "(%lld)", static_cast<long long>(v));
+        else std::snprintf(buf, sizeof buf, "((i64)0x%llxull)", static_cast<unsigned long long>(v));
+        return buf;
+    }
+    static std::string tlit_d(double d) {
+        std::uint64_t bits;
+        std::memcpy(&bits, &d, 8);
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "__longlong_as_double((i64)0x%llxull)", static_cast<unsigned long long>(bits));
+        return buf;
+    }
+    static TV tvalue(const Value& v) {
+        return v.real ? tdbl(tlit_d(v.f)) : tint(tlit_i(v.i), v.i, v.i);
+    }
+
+    /// Typed load of image slot `slot` (int formats -> int, F32 -> double).
+    bool typed_loader(int slot, Channel ch, std::string& name, TV& proto) {
+        const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
+        std::int64_t lo = 0, hi = 255;
+        bool real = false;
+        const char* expr = nullptr;
+        switch (s.desc.format) {
+        case ImageFormat::U8: expr = "row[x]"; break;
+        case ImageFormat::U16: lo = 0, hi = 65535, expr = "((const unsigned short*)row)[x]"; break;
+        case ImageFormat::S16: lo = -32768, hi = 32767, expr = "((const short*)row)[x]"; break;
+        case ImageFormat::S32: lo = INT32_MIN, hi = INT32_MAX, expr = "((const int*)row)[x]"; break;
+        case ImageFormat::F32: real = true, expr = "(double)((const float*)row)[x]"; break;
+        case ImageFormat::RGB:
+            expr = ch == Channel::G ? "row[3 * x + 1]" : ch == Channel::B ? "row[3 * x + 2]" : "row[3 * x]";
+            break;
+        case ImageFormat::UYVY:
+            expr = ch == Channel::U ? "row[4 * (x / 2)]" : ch == Channel::V ? "row[4 * (x / 2) + 2]" : "row[2 * x + 1]";
+            break;
+        default: return false;
+        }
+        name = "tld" + prefix + std::to_string(slot) + "_" + std::to_string(static_cast<int>(ch));
+        proto = real ? tdbl("") : tint("", lo, hi);
+        for (const std::string& d : defined)
+            if (d == name) return true;
+        defined.push_back(name);
+        helpers << "__device__ __forceinline__ " << (real ? "double " : "int ") << name
+                << "(const P& p, int fr, int x, int y, u64& rd) {\n  rd++;\n  const unsigned char* row = " << in_base(slot)
+                << " + (u64)y * p.f[" << fin(slot) + 1 << "];\n  return " << expr << ";\n}\n";
+        return true;
+    }
+
+    int region_obj(int slot) const {
+        return slot_obj.empty() ? -1 : slot_obj[static_cast<std::size_t>(slot)];
+    }
+    bool tobj(int o, int dx, int dy, TV& out) {
+        TVproto pr;
+        if (!obj_type || !obj_type(o, pr)) return false;
+        const std::string c = obj_entry(o, dx, dy);
+        out = pr.t == 'd' ? tdbl("(double)" + c) : tint("(int)" + c, pr.lo, pr.hi);
+        return true;
+    }
+
+    bool tpointwise(int slot, Channel ch, const std::string& x, const std::string& y, TV& out) {
+        if (slot < 0 || slot >= n_in) return false;
+        if (region_obj(slot) >= 0) return ch == Channel::C0 && x == "px" && y == "py" && tobj(region_obj(slot), 0, 0, out);
+        const SlotInfo& s = ins[static_cast<std::size_t>(slot)];
+        if (s.kind != SlotKind::Image || slot == smem_slot) return false;
+        if (ch == Channel::C0 && x == "px" && y == "py" && static_cast<std::size_t>(slot) < preloaded.size() &&
+            preloaded[static_cast<std::size_t>(slot)]) {
+            TV proto;
+            std::string name;
+            if (!typed_loader(slot, ch, name, proto)) return false;
+            const std::string r = "in" + std::to_string(slot) + "[i]";
+            out = proto.t == 'd' ? tdbl("(double)" + r) : tint("(int)" + r, proto.lo, proto.hi);
+            return true;
+        }
+        std::string name;
+        TV proto;
+        if (!typed_loader(slot, ch, name, proto)) return false;
+        proto.c = name + "(p, fr, " + x + ", " + y + ", rd)";
+        out = proto;
+        return true;
+    }
+
+    bool twindow(const Expr& e, TV& out) {
+        const int slot = e.input;
+        if (slot < 0 || slot >= n_in || ins[static_cast<std::size_t>(slot)].kind != SlotKind::Image) return false;
+        if (slot == smem_slot) return false;
+        const int ox = tdx + e.dx, oy = tdy + e.dy;
+        const std::string x = "(px + (" + std::to_string(ox) + "))", y = "(py + (" + std::to_string(oy) + "))";
+        if (region_obj(slot) >= 0) {
+            // region entries hold the intermediate at the CLAMPED position
+            // (Clamp semantics of a virtual intermediate, SURVEY.md §8a rule 2)
+            if (e.channel != Channel::C0) return false;
+            TV v;
+            if (!tobj(region_obj(slot), ox, oy, v)) return false;
+            if (local->boundary != BoundaryMode::Constant) {
+                out = v;
+                return true;
+            }
+            const Value& bv = local->boundary_value;
+            if (bv.real != (v.t == 'd')) return false;
+            const std::string ty = v.t == 'd' ? "double" : "i64";
+            out = v;
+            out.c = "([&]() -> " + ty + " { int xx = " + x + ", yy = " + y +
+                    "; if (xx < 0 || yy < 0 || xx >= W || yy >= H) return " + (bv.real ? tlit_d(bv.f) : tlit_i(bv.i)) +
+                    "; return " + v.c + "; }())";
+            if (!bv.real) {
+                out = tint(out.c, std::min<__int128>(v.lo, bv.i), std::max<__int128>(v.hi, bv.i));
+                if (out.t == 'i') out.c = "((int)" + out.c + ")";
+            }
+            return true;
+        }
+        std::string name;
+        TV proto;
+        if (!typed_loader(slot, e.channel, name, proto)) return false;
+        if (local->boundary == BoundaryMode::Constant) {
+            const Value& bv = local->boundary_value;
+            if (bv.real != (proto.t == 'd')) return false; // mixed int / real: run-time tags
+            const std::string ty = proto.t == 'd' ? "double" : "i64";
+            out = proto;
+            out.c = "([&]() -> " + ty + " { int xx = " + x + ", yy = " + y +
+                    "; if (xx < 0 || yy < 0 || xx >= W || yy >= H) return " +
+                    (bv.real ? tlit_d(bv.f) : tlit_i(bv.i)) + "; return " + name + "(p, fr, xx, yy, rd); }())";
+            if (!bv.real) {
+                out = tint(out.c, std::min<__int128>(proto.lo, bv.i), std::max<__int128>(proto.hi, bv.i));
+                if (out.t == 'i') out.c = "((int)" + out.c + ")";
+            }
+            return true;
+        }
+        out = proto;
+        out.c = name + "(p, fr, clampi(" + x + ", 0, W - 1), clampi(" + y + ", 0, H - 1), rd)";
+        return true;
+    }
+
+    bool tinput(const Expr& e, TV& out) {
+        switch (mode) {
+        case Mode::Point:
+        case Mode::Tap:
+        case Mode::BinOf: return tpointwise(e.input, e.channel, "px", "py", out);
+        case Mode::Post:
+            if (e.input == 0) {
+                if (!cmb_typed) return false;
+                out = cmb_tv;
+                return true;
+            }
+            return tpointwise(e.input, e.channel, "px", "py", out);
+        default: return false;
+        }
+    }
+
+    static TV tbin_int(const std::string& op, const TV& a, const TV& b, __int128 lo, __int128 hi) {
+        if (lo >= kI64Lo && hi <= kI64Hi) {
+            TV r = tint("", lo, hi);
+            r.c = r.t == 'i' && a.t == 'i' && b.t == 'i' ? "(" + a.c + " " + op + " " + b.c + ")"
+                                                         : "(" + as_i64(a) + " " + op + " " + as_i64(b) + ")";
+            return r;
+        }
+        // may leave int64: the reference's wrapping int64 arithmetic
+        TV r = tint("(i64)((u64)" + as_i64(a) + " " + op + " (u64)" + as_i64(b) + ")", kI64Lo, kI64Hi);
+        r.t = 'l';
+        return r;
+    }
+
+    bool temit(const Expr& e, TV& out) {
+        switch (e.op) {
+        case ExprOp::ConstI: out = tint(tlit_i(e.ival), e.ival, e.ival); return true;
+        case ExprOp::ConstF: out = tdbl(tlit_d(e.fval)); return true;
+        case ExprOp::InputPixel: return tinput(e, out);
+        case ExprOp::WindowPixel: return mode == Mode::Tap && twindow(e, out);
+        case ExprOp::MaskCoef: {
+            if (mode != Mode::Tap || !mask) return false;
+            const int mw = local->window_w, mh = local->window_h;
+            const int ix = std::min(std::max(tdx + e.dx + mw / 2, 0), mw - 1);
+            const int iy = std::min(std::max(tdy + e.dy + mh / 2, 0), mh - 1);
+            const std::size_t at = static_cast<std::size_t>(iy * mw + ix);
+            if (at >= mask->size()) return false;
+            out = tvalue((*mask)[at]);
+            return true;
+        }
+        case ExprOp::ArrayAt: return false;
+        case ExprOp::Select: {
+            TV c, x, y;
+            if (!temit(*e.a, c) || c.t == 'd' || !temit(*e.b, x) || !temit(*e.c, y)) return false;
+            if ((x.t == 'd') != (y.t == 'd')) return false; // the result's tag depends on the branch
+            if (x.t == 'd') {
+                out = tdbl("((" + c.c + ") != 0 ? " + x.c + " : " + y.c + ")");
+                return true;
+            }
+            out = tint("", std::min(x.lo, y.lo), std::max(x.hi, y.hi));
+            out.c = out.t == 'i' ? "((" + c.c + ") != 0 ? " + x.c + " : " + y.c + ")"
+                                 : "((" + c.c + ") != 0 ? " + as_i64(x) + " : " + as_i64(y) + ")";
+            return true;
+        }
+        case ExprOp::Cast: {
+            TV a;
+            if (!temit(*e.a, a)) return false;
+            const ScalarType to = e.cast_to;
+            if (to == ScalarType::F64) {
+                out = tdbl(as_dbl(a));
+                return true;
+            }
+            if (to == ScalarType::F32) {
+                if (a.t != 'd' && a.lo >= -16777216 && a.hi <= 16777216) out = tdbl(as_dbl(a)); // exact in float
+                else out = tdbl("(double)__double2float_rn(" + as_dbl(a) + ")");
+                return true;
+            }
+            if (to == ScalarType::I64) {
+                if (a.t == 'd') out = tint("((i64)(" + a.c + "))", kI64Lo, kI64Hi), out.t = 'l';
+                else out = a;
+                return true;
+            }
+            std::int64_t lo = 0, hi = 0;
+            switch (to) {
+            case ScalarType::U8: lo = 0, hi = 255; break;
+            case ScalarType::U16: lo = 0, hi = 65535; break;
+            case ScalarType::S16: lo = -32768, hi = 32767; break;
+            default: lo = INT32_MIN, hi = INT32_MAX; break;
+            }
+            const int pol = e.policy == CastPolicy::Wrap ? 1 : 0;
+            if (pol == 0 && e.a->op == ExprOp::Sqrt) {
+                // cast(int, sqrt(n)) for an integer n in [0, 2^24): exact in fp32
+                // plus an integer correction (the reference rounds llround(sqrt(double)))
+                TV n;
+                if (temit(*e.a->a, n) && n.t != 'd' && n.lo >= 0 && n.hi < (1 << 24)) {
+                    const long long kmax = static_cast<long long>(std::sqrt(static_cast<double>(n.hi))) + 1;
+                    out = tint("(int)t_sat((i64)t_round_sqrt(" + n.c + "), " + tlit_i(lo) + ", " + tlit_i(hi) + ")",
+                               std::max<std::int64_t>(lo, 0), std::min<std::int64_t>(hi, kmax));
+                    return true;
+                }
+            }
+            if (a.t == 'd') {
+                out = tint("(int)t_cast_d(" + a.c + ", " + tlit_i(lo) + ", " + tlit_i(hi) + ", " + std::to_string(pol) + ")",
+                           lo, hi);
+                return true;
+            }
+            if (a.lo >= lo && a.hi <= hi) { // already in range: the cast is the identity
+                out = a;
+                return true;
+            }
+            if (pol == 0) {
+                out = tint("(int)t_sat(" + as_i64(a) + ", " + tlit_i(lo) + ", " + tlit_i(hi) + ")", lo, hi);
+            } else {
+                out = tint("(int)t_wrap(" + as_i64(a) + ", " + tlit_i(lo) + ", " + tlit_i(hi) + ")", lo, hi);
+            }
+            return true;
+        }
+        default: break;
+        }
+        if (is_binary(e.op)) {
+            TV a, b;
+            if (!temit(*e.a, a) || !temit(*e.b, b)) return false;
+            const bool real = a.t == 'd' || b.t == 'd';
+            switch (e.op) {
+            case ExprOp::Add:
+                if (real) { out = tdbl("__dadd_rn(" + as_dbl(a) + ", " + as_dbl(b) + ")"); return true; }
+                out = tbin_int("+", a, b, a.lo + b.lo, a.hi + b.hi);
+                return true;
+            case ExprOp::Sub:
+                if (real) { out = tdbl("__dsub_rn(" + as_dbl(a) + ", " + as_dbl(b) + ")"); return true; }
+                out = tbin_int("-", a, b, a.lo - b.hi, a.hi - b.lo);
+                return true;
+            case ExprOp::Mul: {
+                if (real) { out = tdbl("__dmul_rn(" + as_dbl(a) + ", " + as_dbl(b) + ")"); return true; }
+                const __int128 p[4] = {a.lo * b.lo, a.lo * b.hi, a.hi * b.lo, a.hi * b.hi};
+                __int128 lo = std::min({p[0], p[1], p[2], p[3]}), hi = std::max({p[0], p[1], p[2], p[3]});
+                if (a.c == b.c && a.t == b.t) lo = (a.lo <= 0 && a.hi >= 0) ? 0 : std::min(p[0], p[3]); // a square
+                out = tbin_int("*", a, b, lo, hi);
+                return true;
+            }
+            case ExprOp::Div: {
+                if (real) { out = tdbl("t_ddiv(p, " + as_dbl(a) + ", " + as_dbl(b) + ")"); return true; }
+                const __int128 m = std::max(a.lo < 0 ? -a.lo : a.lo, a.hi < 0 ? -a.hi : a.hi);
+                out = tint("t_div(p, " + as_i64(a) + ", " + as_i64(b) + ")", -m, m);
+                if (out.t == 'i') out.c = "(int)" + out.c;
+                return true;
+            }
+            case ExprOp::Min:
+            case ExprOp::Max: {
+                const bool mn = e.op == ExprOp::Min;
+                if (real) {
+                    const std::string x = as_dbl(a), y = as_dbl(b);
+                    // v_min / v_max: y < x ? y : x  /  x < y ? y : x
+                    out = tdbl("([&]() -> double { double x = " + x + ", y = " + y + "; return " +
+                               (mn ? "y < x ? y : x" : "x < y ? y : x") + "; }())");
+                    return true;
+                }
+                out = tint("", mn ? std::min(a.lo, b.lo) : std::max(a.lo, b.lo), mn ? std::min(a.hi, b.hi) : std::max(a.hi, b.hi));
+                out.c = std::string(mn ? "min" : "max") + "(" + as_i64(a) + ", " + as_i64(b) + ")";
+                if (out.t == 'i') out.c = "(int)" + out.c;
+                return true;
+            }
+            case ExprOp::And:
+            case ExprOp::Or:
+            case ExprOp::Xor: {
+                if (real) return false;
+                const char* op = e.op == ExprOp::And ? "&" : e.op == ExprOp::Or ? "|" : "^";
+                __int128 lo = kI64Lo, hi = kI64Hi;
+                if (a.lo >= 0 && b.lo >= 0) {
+                    __int128 m = 1;
+                    while (m <= std::max(a.hi, b.hi)) m <<= 1;
+                    lo = 0, hi = e.op == ExprOp::And ? std::min(a.hi, b.hi) : m - 1;
+                }
+                out = tint("(" + as_i64(a) + " " + op + " " + as_i64(b) + ")", lo, hi);
+                if (out.t == 'i') out.c = "(int)" + out.c;
+                return true;
+            }
+            case ExprOp::Shl:
+                if (real) return false;
+                out = tint("(i64)((u64)" + as_i64(a) + " << shcnt(" + as_i64(b) + "))", kI64Lo, kI64Hi);
+                out.t = 'l';
+                return true;
+            case ExprOp::Shr:
+                if (real) return false;
+                out = tint("(" + as_i64(a) + " >> shcnt(" + as_i64(b) + "))", std::min<__int128>(a.lo, 0),
+                           std::max<__int128>(a.hi, 0));
+                if (out.t == 'i') out.c = "(int)" + out.c;
+                return true;
+            case ExprOp::Lt:
+            case ExprOp::Gt:
+            case ExprOp::Eq: {
+                const char* op = e.op == ExprOp::Lt ? "<" : e.op == ExprOp::Gt ? ">" : "==";
+                out = real ? tint("(int)(" + as_dbl(a) + " " + op + " " + as_dbl(b) + ")", 0, 1)
+                           : tint("(int)(" + as_i64(a) + " " + op + " " + as_i64(b) + ")", 0, 1);
+                return true;
+            }
+            case ExprOp::Atan2: out = tdbl("atan2(" + as_dbl(a) + ", " + as_dbl(b) + ")"); return true;
+            default: return false;
+            }
+        }
+        TV a;
+        if (!temit(*e.a, a)) return false;
+        switch (e.op) {
+        case ExprOp::Not:
+            if (a.t == 'd') return false;
+            out = tint("(~" + as_i64(a) + ")", -a.hi - 1, -a.lo - 1);
+            if (out.t == 'i') out.c = "(int)" + out.c;
+            return true;
+        case ExprOp::Neg:
+            if (a.t == 'd') { out = tdbl("(-(" + a.c + "))"); return true; }
+            if (a.lo <= kI64Lo) out = tint("(i64)(0ull - (u64)" + as_i64(a) + ")", kI64Lo, kI64Hi), out.t = 'l';
+            else out = tint("(-" + as_i64(a) + ")", -a.hi, -a.lo);
+            if (out.t == 'i') out.c = "(int)" + out.c;
+            return true;
+        case ExprOp::Abs:
+            if (a.t == 'd') { out = tdbl("fabs(" + a.c + ")"); return true; }
+            if (a.lo <= kI64Lo) return false;
+            out = tint("", a.lo >= 0 ? a.lo : (a.hi <= 0 ? -a.hi : 0), std::max(a.lo < 0 ? -a.lo : a.lo, a.hi < 0 ? -a.hi : a.hi));
+            out.c = "([&]() -> i64 { i64 v = " + as_i64(a) + "; return v < 0 ? -v : v; }())";
+            if (out.t == 'i') out.c = "(int)" + out.c;
+            return true;
+        case ExprOp::Sqrt: out = tdbl("__dsqrt_rn(" + as_dbl(a) + ")"); return true;
+        default: return false;
+        }
+    }
+
+    /// V-typed expression of `e`: the typed form boxed when the analysis
+    /// succeeds (the boxes fold away in the compiled code), else emit().
+    std::string emit_any(const Expr& e) {
+        TV t;
+        const std::size_t mark = helpers.tellp();
+        const std::size_t ndef = defined.size();
+        if (temit(e, t)) return t.t == 'd' ? "vf(" + t.c + ")" : "vi((i64)(" + t.c + "))";
+        // drop typed loaders this failed attempt registered
+        std::string h = helpers.str();
+        h.resize(mark);
+        helpers.str(h);
+        helpers.seekp(0, std::ios_base::end);
+        defined.resize(ndef);
+        return emit(e);
+    }
+
     /// Store statement of V `val` into output slot `o`, channel c (RGB).
     std::string store(int o, const std::string& val, int channel, const std::string& x, const std::string& y) const {
         const SlotInfo& s = outs[static_cast<std::size_t>(o)];
@@ -426,20 +886,20 @@ NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>&
         std::string t, vt;
         int bytes = 0;
         if (bodies.size() == 3 && outs[o].desc.format == ImageFormat::RGB) {
-            for (int c = 0; c < 3; ++c) b << "  " << em.store(static_cast<int>(o), em.emit(*bodies[static_cast<std::size_t>(c)]), c, "px", "py");
+            for (int c = 0; c < 3; ++c) b << "  " << em.store(static_cast<int>(o), em.emit_any(*bodies[static_cast<std::size_t>(c)]), c, "px", "py");
         } else if (vector_io && vec_types(outs[o].desc.format, t, vt, bytes)) {
             // the four results gather in registers and leave as one vector store
             const int f = field_in(static_cast<int>(ins.size() + o));
             pre << "    " << t << " out" << o << "[4];\n";
             const std::string cvt = outs[o].desc.format == ImageFormat::F32 ? "(float)vd(sv)" : "(" + t + ")sv.i";
-            b << "      { V sv = " << em.emit(*bodies[0]) << "; out" << o << "[i] = " << cvt << "; }\n";
+            b << "      { V sv = " << em.emit_any(*bodies[0]) << "; out" << o << "[i] = " << cvt << "; }\n";
             post << "    { " << t << "* r = (" << t << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
                  << "] + (u64)py * p.f[" << f + 1 << "]) + px4;\n"
                  << "      if (px4 + 3 < W && ((u64)r & " << 4 * bytes - 1 << ") == 0) *(" << vt << "*)r = make_" << vt
                  << "(out" << o << "[0], out" << o << "[1], out" << o << "[2], out" << o << "[3]);\n"
                  << "      else { for (int i = 0; i < 4 && px4 + i < W; ++i) r[i] = out" << o << "[i]; } }\n";
         } else {
-            b << "  " << em.store(static_cast<int>(o), em.emit(*bodies[0]), 0, "px", "py");
+            b << "  " << em.store(static_cast<int>(o), em.emit_any(*bodies[0]), 0, "px", "py");
         }
     }
     KernelSpec ks;
@@ -548,6 +1008,210 @@ std::string int_tap_loop(const LocalKernel& lk, const std::vector<SlotInfo>& ins
     return b.str();
 }
 
+/// The tap loop with every tap in its static type (Emitter::temit): int32
+/// accumulation when every partial sum's range fits, int64 when it may not
+/// (exact: the reference's int64 arithmetic, wrapping alike), double for real
+/// taps (same operation order, no contraction).  Returns statements defining
+/// `V cmb` and records its typed form for the post body, or "" when some tap
+/// has a run-time type (mixed int / real taps included).
+std::string typed_combine(Emitter& em, const LocalKernel& lk, const std::vector<Emitter::TV>& taps);
+
+std::string typed_taps(Emitter& em, const LocalKernel& lk) {
+    if (!lk.tap_body || lk.median3x3) return "";
+    const int hw = lk.window_w / 2, hh = lk.window_h / 2;
+    std::vector<Emitter::TV> taps;
+    for (int dy = -hh; dy <= hh; ++dy)
+        for (int dx = -hw; dx <= hw; ++dx) {
+            em.tdx = dx;
+            em.tdy = dy;
+            Emitter::TV t;
+            if (!em.temit(*lk.tap_body, t)) return "";
+            taps.push_back(t);
+        }
+    return typed_combine(em, lk, taps);
+}
+
+/// Sum / Min / Max of typed tap values in row-major order (see typed_taps).
+std::string typed_combine(Emitter& em, const LocalKernel& lk, const std::vector<Emitter::TV>& all_taps) {
+    if (all_taps.empty()) return "";
+    // integer sums: a tap that is identically 0 (a zero mask coefficient)
+    // adds nothing (its reads are counted by the host)
+    std::vector<Emitter::TV> taps;
+    for (const Emitter::TV& t : all_taps)
+        if (!(lk.combine == CombineMode::Sum && t.t != 'd' && t.lo == 0 && t.hi == 0)) taps.push_back(t);
+    if (taps.empty()) taps.push_back(Emitter::tint("0", 0, 0));
+    const bool real = taps[0].t == 'd';
+    for (const Emitter::TV& t : taps)
+        if ((t.t == 'd') != real) return "";
+    std::ostringstream b;
+    Emitter::TV acc;
+    if (real) {
+        b << "    double cmbt = " << taps[0].c << ";\n";
+        for (std::size_t k = 1; k < taps.size(); ++k) {
+            if (lk.combine == CombineMode::Sum) b << "    cmbt = __dadd_rn(cmbt, " << taps[k].c << ");\n";
+            else b << "    { double y = " << taps[k].c << "; cmbt = " << (lk.combine == CombineMode::Min ? "y < cmbt ? y : cmbt" : "cmbt < y ? y : cmbt") << "; }\n";
+        }
+        acc = Emitter::tdbl("cmbt");
+        b << "    V cmb = vf(cmbt);\n";
+    } else {
+        __int128 lo = taps[0].lo, hi = taps[0].hi, plo = lo, phi = hi;
+        for (std::size_t k = 1; k < taps.size(); ++k) {
+            if (lk.combine == CombineMode::Sum) lo += taps[k].lo, hi += taps[k].hi;
+            else if (lk.combine == CombineMode::Min) lo = std::min(lo, taps[k].lo), hi = std::min(hi, taps[k].hi);
+            else lo = std::max(lo, taps[k].lo), hi = std::max(hi, taps[k].hi);
+            plo = std::min(plo, lo), phi = std::max(phi, hi);
+        }
+        const bool i32 = plo >= Emitter::kI32Lo && phi <= Emitter::kI32Hi;
+        const bool wraps = plo < Emitter::kI64Lo || phi > Emitter::kI64Hi;
+        const char* ty = i32 ? "int" : "i64";
+        auto term = [&](const Emitter::TV& t) { return i32 ? t.c : Emitter::as_i64(t); };
+        b << "    " << ty << " cmbt = " << term(taps[0]) << ";\n";
+        for (std::size_t k = 1; k < taps.size(); ++k) {
+            if (lk.combine == CombineMode::Sum) {
+                if (wraps) b << "    cmbt = (i64)((u64)cmbt + (u64)" << term(taps[k]) << ");\n";
+                else b << "    cmbt += " << term(taps[k]) << ";\n";
+            } else {
+                b << "    cmbt = " << (lk.combine == CombineMode::Min ? "min" : "max") << "(cmbt, " << term(taps[k]) << ");\n";
+            }
+        }
+        acc = wraps ? Emitter::tint("cmbt", Emitter::kI64Lo, Emitter::kI64Hi) : Emitter::tint("cmbt", lo, hi);
+        if (!i32) acc.t = 'l';
+        b << "    V cmb = vi((i64)cmbt);\n";
+    }
+    em.cmb_typed = true;
+    em.cmb_tv = acc;
+    return b.str();
+}
+
+namespace {
+bool uses_op(const Expr& e, ExprOp op) {
+    if (e.op == op) return true;
+    for (const ExprPtr* c : {&e.a, &e.b, &e.c})
+        if (*c && uses_op(**c, op)) return true;
+    return false;
+}
+} // namespace
+
+/// Local node as a shared-memory tile program (when the host counts its
+/// reads statically): the tap body factors as `mask(dx, dy) * g` or `g`,
+/// with g a function of the tap position alone (window reads, constants; no
+/// pointwise reads of the output pixel, no mask).  g is evaluated ONCE per
+/// source position of a 128 x 8 output tile plus its halo, in its static
+/// type, into shared memory — a point body the reference fuser inlined into
+/// the taps (Multiply -> Box3x3) then costs one evaluation per source pixel
+/// instead of one per tap — and each output pixel combines the window from
+/// there (row-major, the reference's order and types).  Each window read
+/// inside g keeps its own border handling, so the tabulated values are
+/// exactly what every tap would compute; only positions some output's window
+/// uses are evaluated (no extra DivByZero).  Empty program when the node
+/// does not qualify.
+NodeProgram lower_local_tiled(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
+                              const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values) {
+    NodeProgram none;
+    const LocalKernel& lk = k.local();
+    if (lk.median3x3 || !lk.tap_body || outs.empty() || outs[0].kind != SlotKind::Image) return none;
+    const Expr& t = *lk.tap_body;
+    const Expr* g = &t;
+    const Expr* mc = nullptr;
+    if (t.op == ExprOp::Mul && t.a && t.b) {
+        if (t.a->op == ExprOp::MaskCoef && !uses_op(*t.b, ExprOp::MaskCoef)) mc = t.a.get(), g = t.b.get();
+        else if (t.b->op == ExprOp::MaskCoef && !uses_op(*t.a, ExprOp::MaskCoef)) mc = t.b.get(), g = t.a.get();
+    }
+    if (mc && (mc->dx != 0 || mc->dy != 0)) return none;
+    if (uses_op(*g, ExprOp::MaskCoef) || uses_op(*g, ExprOp::InputPixel) || uses_op(*g, ExprOp::ArrayAt)) return none;
+    // a plain window read is cheaper straight from L1 with the per-thread
+    // register reuse of int_tap_loop: tabulate only real computations
+    if (g->op == ExprOp::WindowPixel || (g->op == ExprOp::Cast && g->a && g->a->op == ExprOp::WindowPixel)) return none;
+    const std::vector<Value>& mask = lk.mask.empty() ? matrix_values : lk.mask;
+    const int ww = lk.window_w, wh = lk.window_h, hw = ww / 2, hh = wh / 2;
+    if (ww > 9 || wh > 9) return none;
+    if (mc && mask.size() != static_cast<std::size_t>(ww * wh)) return none;
+
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = -1;
+    prog.counts_reads = false;
+    Emitter em(ins, outs);
+    em.local = &lk;
+    em.mask = &mask;
+    em.mode = Emitter::Mode::Tap;
+    em.tdx = em.tdy = 0;
+    Emitter::TV gv;
+    if (!em.temit(*g, gv)) return none;
+    const char* gty = gv.t == 'd' ? "double" : gv.t == 'l' ? "i64" : "int";
+    constexpr int TX = 32, TY = 8, PX = 4;
+    const int RW = TX * PX + 2 * hw, RH = TY + 2 * hh;
+    const bool undef = lk.boundary == BoundaryMode::Undefined;
+
+    // the combine over the tile: tap (dx, dy) of output (threadIdx.x + 32 i, threadIdx.y)
+    std::vector<Emitter::TV> taps;
+    for (int dy = -hh; dy <= hh; ++dy)
+        for (int dx = -hw; dx <= hw; ++dx) {
+            Emitter::TV gt = gv;
+            gt.c = "gs[(threadIdx.y + " + std::to_string(dy + hh) + ") * " + std::to_string(RW) +
+                   " + threadIdx.x + 32 * i + " + std::to_string(dx + hw) + "]";
+            if (!mc) {
+                taps.push_back(gt);
+                continue;
+            }
+            const Value& cv = mask[static_cast<std::size_t>((dy + hh) * ww + dx + hw)];
+            const Emitter::TV cf = Emitter::tvalue(cv);
+            if (cv.real || gt.t == 'd') {
+                taps.push_back(Emitter::tdbl("__dmul_rn(" + Emitter::as_dbl(cf) + ", " + Emitter::as_dbl(gt) + ")"));
+            } else {
+                const __int128 pr[4] = {cf.lo * gt.lo, cf.lo * gt.hi, cf.hi * gt.lo, cf.hi * gt.hi};
+                taps.push_back(Emitter::tbin_int("*", cf, gt, std::min({pr[0], pr[1], pr[2], pr[3]}),
+                                                 std::max({pr[0], pr[1], pr[2], pr[3]})));
+            }
+        }
+    // integer Sum: zero coefficients add nothing (exact); real sums keep every term
+    std::vector<Emitter::TV> used;
+    for (std::size_t q = 0; q < taps.size(); ++q) {
+        const bool zero = mc && lk.combine == CombineMode::Sum && taps[q].t != 'd' && taps[q].lo == 0 && taps[q].hi == 0;
+        if (!zero) used.push_back(taps[q]);
+    }
+    if (used.empty()) return none;
+    const std::string comb = typed_combine(em, lk, used);
+    if (comb.empty()) return none;
+    em.tdx = em.tdy = 0;
+    em.mode = Emitter::Mode::Post;
+    const std::string pv = lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb");
+    const ScalarType out_t = scalar_of(outs.at(0).desc.format);
+
+    std::ostringstream src;
+    src << "extern \"C\" __global__ void gvx_ltile(const P p) {\n"
+        << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
+        << "  const int x0 = (int)blockIdx.x * " << TX * PX << ", y0 = (int)blockIdx.y * " << TY << ";\n"
+        << "  __shared__ " << gty << " gs[" << RW * RH << "];\n"
+        << "  for (int ry = threadIdx.y; ry < " << RH << "; ry += " << TY << ")\n"
+        << "  for (int rx = threadIdx.x; rx < " << RW << "; rx += " << TX << ") {\n"
+        << "    const int e = ry * " << RW << " + rx;\n"
+        << "    const int px = x0 - " << hw << " + rx, py = y0 - " << hh << " + ry;\n";
+    if (undef)
+        src << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
+    else
+        src << "    if (px < -" << hw << " || py < -" << hh << " || px >= W + " << hw << " || py >= H + " << hh << ") continue;\n";
+    src << "    gs[e] = (" << gty << ")(" << gv.c << ");\n  }\n  __syncthreads();\n"
+        << "  const int py = y0 + (int)threadIdx.y;\n  if (py >= H) return;\n"
+        << "#pragma unroll\n  for (int i = 0; i < " << PX << "; ++i) {\n"
+        << "    const int px = x0 + (int)threadIdx.x + " << TX << " * i;\n    if (px >= W) break;\n";
+    if (undef)
+        src << "    if (px < " << hw << " || py < " << hh << " || px >= W - " << hw << " || py >= H - " << hh << ") {\n"
+            << "      " << em.store(0, "v_cast(vi(0), " + std::to_string(type_code(out_t)) + ", 0)", 0, "px", "py")
+            << "      continue;\n    }\n";
+    src << comb << "    " << em.store(0, pv, 0, "px", "py") << "  }\n  (void)rd;\n}\n";
+    KernelSpec ks;
+    ks.name = "gvx_ltile";
+    ks.grid = KernelSpec::Grid::Pixels;
+    ks.block_x = TX;
+    ks.block_y = TY;
+    ks.cols = PX;
+    ks.source = assemble(em, src.str(), prog.fields());
+    prog.kernels.push_back(std::move(ks));
+    return prog;
+}
+
 NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
                         const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values) {
     NodeProgram prog;
@@ -569,10 +1233,15 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     }
     em.mode = Emitter::Mode::Tap;
     const std::string fast = int_tap_loop(lk, ins, *em.mask, em);
+    const std::string typed = fast.empty() ? typed_taps(em, lk) : std::string();
     if (!fast.empty()) {
         pre << fast;
         b << "    V cmb = vi((i64)acc[i]);\n";
         prog.counts_reads = false; // the host counts these reads (static window)
+        em.cmb_typed = true;
+        em.cmb_tv = Emitter::tint("acc[i]", -2147483647LL, 2147483647LL);
+    } else if (!typed.empty()) {
+        b << typed;
     } else if (lk.median3x3) {
         b << "    V t[9];\n";
         int idx = 0;
@@ -607,7 +1276,7 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     em.tdx = em.tdy = 0;
     if (lk.post_body) {
         em.mode = Emitter::Mode::Post;
-        b << "    " << em.store(0, em.emit(*lk.post_body), 0, "px", "py");
+        b << "    " << em.store(0, em.emit_any(*lk.post_body), 0, "px", "py");
     } else {
         b << "    " << em.store(0, "cmb", 0, "px", "py");
     }
@@ -732,10 +1401,19 @@ std::string local_value(Emitter& em, const LocalKernel& lk, const std::vector<Sl
     if (!fast.empty()) {
         em.tdx = em.tdy = 0;
         em.mode = Emitter::Mode::Post;
-        b << fast << "    V pv = " << (lk.post_body ? em.emit(*lk.post_body) : std::string("cmb")) << ";\n";
+        em.cmb_typed = true;
+        em.cmb_tv = Emitter::tint("cacc", -2147483647LL, 2147483647LL);
+        b << fast << "    V pv = " << (lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb")) << ";\n";
         return b.str();
     }
     em.mode = Emitter::Mode::Tap;
+    const std::string typed = typed_taps(em, lk);
+    if (!typed.empty()) {
+        em.tdx = em.tdy = 0;
+        em.mode = Emitter::Mode::Post;
+        b << typed << "    V pv = " << (lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb")) << ";\n";
+        return b.str();
+    }
     const char* comb = lk.combine == CombineMode::Sum ? "v_add" : lk.combine == CombineMode::Min ? "v_min" : "v_max";
     bool first = true;
     for (int dy = -hh; dy <= hh; ++dy)
@@ -752,7 +1430,7 @@ std::string local_value(Emitter& em, const LocalKernel& lk, const std::vector<Sl
         }
     em.tdx = em.tdy = 0;
     em.mode = Emitter::Mode::Post;
-    b << "    V pv = " << (lk.post_body ? em.emit(*lk.post_body) : std::string("cmb")) << ";\n";
+    b << "    V pv = " << (lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb")) << ";\n";
     return b.str();
 }
 
@@ -1171,13 +1849,242 @@ NodeProgram lower_table(const std::vector<SlotInfo>& ins, const std::vector<Slot
 
 } // namespace
 
+namespace {
+const char* storage_ctype(ImageFormat f) {
+    switch (f) {
+    case ImageFormat::U8: return "unsigned char";
+    case ImageFormat::U16: return "unsigned short";
+    case ImageFormat::S16: return "short";
+    case ImageFormat::S32: return "int";
+    case ImageFormat::F32: return "float";
+    default: return nullptr;
+    }
+}
+} // namespace
+
+bool reads_window(const Expr& e, int slot) {
+    if (e.op == ExprOp::WindowPixel && e.input == slot) return true;
+    for (const ExprPtr* c : {&e.a, &e.b, &e.c})
+        if (*c && reads_window(**c, slot)) return true;
+    return false;
+}
+
+NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector<RegionObject>& objs,
+                         const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs) {
+    auto unsupported = [](const std::string& why) { return Error(ErrorCode::UnsupportedKind, "region: " + why); };
+    for (const RegionObject& o : objs)
+        if (!storage_ctype(o.format)) throw unsupported("intermediate format");
+    // tile: 64 x 16 outputs per 256-thread block, halved while the shared
+    // memory of the intermediates exceeds 40 KB
+    int TW = 64, TH = 16;
+    auto smem_bytes = [&] {
+        std::size_t b = 0;
+        for (const RegionObject& o : objs)
+            b += static_cast<std::size_t>(TW + 2 * o.halo_x) * (TH + 2 * o.halo_y) *
+                 static_cast<std::size_t>(bytes_per_pixel(o.format));
+        return b;
+    };
+    while (smem_bytes() > 40 * 1024 && (TW > 32 || TH > 8)) (TH > 8 ? TH : TW) /= 2;
+    if (smem_bytes() > 40 * 1024) throw unsupported("intermediates exceed shared memory");
+
+    NodeProgram prog;
+    prog.n_inputs = static_cast<int>(ins.size());
+    prog.n_outputs = static_cast<int>(outs.size());
+    prog.dims_from = -1;
+    prog.counts_reads = false;
+    auto rw = [&](int o) { return TW + 2 * objs[static_cast<std::size_t>(o)].halo_x; };
+    auto rh = [&](int o) { return TH + 2 * objs[static_cast<std::size_t>(o)].halo_y; };
+    // a node's code reads object o relative to the entry being evaluated:
+    // index base b<o> (set per entry) + dy * row length + dx
+    std::vector<bool> used_obj(objs.size());
+    auto entry = [&](int o, int dx, int dy) {
+        used_obj[static_cast<std::size_t>(o)] = true;
+        return "ro" + std::to_string(o) + "[b" + std::to_string(o) + " + (" + std::to_string(dy * rw(o) + dx) + ")]";
+    };
+    // value ranges of the entries: the format's, narrowed to the producing
+    // node's static range when it stores without narrowing
+    std::vector<TVproto> orange(objs.size());
+    for (std::size_t o = 0; o < objs.size(); ++o) {
+        std::int64_t lo = 0, hi = 0;
+        if (objs[o].format == ImageFormat::F32) orange[o].t = 'd';
+        else if (int_format_range(objs[o].format, lo, hi)) orange[o].lo = lo, orange[o].hi = hi;
+    }
+    auto otype = [&](int o, TVproto& pr) {
+        pr = orange[static_cast<std::size_t>(o)];
+        return true;
+    };
+
+    std::ostringstream helpers, body;
+    body << "extern \"C\" __global__ void gvx_region(const P p) {\n"
+         << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
+         << "  const int tx0 = (int)blockIdx.x * " << TW << ", ty0 = (int)blockIdx.y * " << TH << ";\n";
+    for (std::size_t o = 0; o < objs.size(); ++o)
+        body << "  __shared__ " << storage_ctype(objs[o].format) << " ro" << o << "["
+             << rw(static_cast<int>(o)) * rh(static_cast<int>(o)) << "];\n";
+    // region inputs staged once: entry = input at the CLAMPED position
+    bool staged = false;
+    for (std::size_t o = 0; o < objs.size(); ++o) {
+        if (objs[o].load < 0) continue;
+        staged = true;
+        const int f = field_in(objs[o].load);
+        const char* ct = storage_ctype(objs[o].format);
+        body << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << rw(static_cast<int>(o)) * rh(static_cast<int>(o))
+             << "; e += blockDim.x * blockDim.y) {\n"
+             << "    const int ry = e / " << rw(static_cast<int>(o)) << ", rx = e - ry * " << rw(static_cast<int>(o)) << ";\n"
+             << "    const int x = clampi(tx0 - " << objs[o].halo_x << " + rx, 0, W - 1), y = clampi(ty0 - "
+             << objs[o].halo_y << " + ry, 0, H - 1);\n"
+             << "    ro" << o << "[e] = ((const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
+             << f + 2 << "] + (u64)y * p.f[" << f + 1 << "]))[x];\n  }\n";
+    }
+    if (staged) body << "  __syncthreads();\n";
+    for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
+        const RegionNode& rn = nodes[ni];
+        const AbstractionKernel& k = *rn.k;
+        std::vector<SlotInfo> no_outs;
+        Emitter em(rn.in_slots, no_outs);
+        em.prefix = "N" + std::to_string(ni) + "_";
+        em.slot_obj = rn.in_obj;
+        em.slot_param.resize(rn.in_param.size());
+        for (std::size_t i = 0; i < rn.in_param.size(); ++i) em.slot_param[i] = rn.in_param[i] < 0 ? 0 : rn.in_param[i];
+        em.obj_entry = entry;
+        em.obj_type = otype;
+        // outputs of this node (all share one region: the largest halo)
+        int oref = -1;
+        for (int o : rn.out_obj)
+            if (o >= 0 && (oref < 0 || objs[static_cast<std::size_t>(o)].halo_x > objs[static_cast<std::size_t>(oref)].halo_x ||
+                           objs[static_cast<std::size_t>(o)].halo_y > objs[static_cast<std::size_t>(oref)].halo_y))
+                oref = o;
+        if (oref < 0) throw unsupported("node without a region output");
+        const RegionObject& R = objs[static_cast<std::size_t>(oref)];
+        // in-image entries only (their taps then sit at constant offsets from
+        // the entry); out-of-image entries replicate the clamped one below
+        std::ostringstream nb;
+        std::fill(used_obj.begin(), used_obj.end(), false);
+        auto put = [&](int o, const Emitter::TV& v) {
+            if (v.t != 'd' && orange[static_cast<std::size_t>(o)].t != 'd') {
+                TVproto& r = orange[static_cast<std::size_t>(o)];
+                if (v.lo >= r.lo && v.hi <= r.hi) r.lo = static_cast<long long>(v.lo), r.hi = static_cast<long long>(v.hi);
+            }
+            const ImageFormat f = objs[static_cast<std::size_t>(o)].format;
+            std::string val;
+            if (f == ImageFormat::F32) val = "(float)" + Emitter::as_dbl(v);
+            else val = v.t == 'd' ? std::string("0") : "(" + std::string(storage_ctype(f)) + ")(" + v.c + ")";
+            // every output entry of this node at the entry's position (a
+            // smaller-halo output covers a sub-rectangle of the reference one)
+            const RegionObject& O = objs[static_cast<std::size_t>(o)];
+            if (O.halo_x == R.halo_x && O.halo_y == R.halo_y) {
+                nb << "    ro" << o << "[e] = " << val << ";\n";
+            } else {
+                nb << "    { const int ox = rx - " << R.halo_x - O.halo_x << ", oy = ry - " << R.halo_y - O.halo_y
+                   << "; if (ox >= 0 && oy >= 0 && ox < " << rw(o) << " && oy < " << rh(o) << ") ro" << o
+                   << "[oy * " << rw(o) << " + ox] = " << val << "; }\n";
+            }
+        };
+        if (k.kind == AbstractionKind::Point) {
+            const PointKernel& pk = k.point();
+            em.mode = Emitter::Mode::Point;
+            for (std::size_t j = 0; j < rn.out_obj.size() && j < pk.outputs.size(); ++j) {
+                if (rn.out_obj[j] < 0) continue;
+                if (pk.outputs[j].channel_bodies.size() != 1) throw unsupported("multi-channel point output");
+                Emitter::TV v;
+                if (!em.temit(*pk.outputs[j].channel_bodies[0], v)) throw unsupported("run-time typed point body");
+                put(rn.out_obj[j], v);
+            }
+        } else if (k.kind == AbstractionKind::Local) {
+            const LocalKernel& lk = k.local();
+            if (lk.median3x3) throw unsupported("median");
+            em.local = &lk;
+            em.mask = lk.mask.empty() ? &rn.matrix : &lk.mask;
+            em.mode = Emitter::Mode::Tap;
+            const int hw = lk.window_w / 2, hh = lk.window_h / 2;
+            if (lk.boundary == BoundaryMode::Undefined) {
+                Emitter::TV z = Emitter::tint("0", 0, 0);
+                nb << "    if (px < " << hw << " || py < " << hh << " || px >= W - " << hw << " || py >= H - " << hh
+                     << ") {\n";
+                for (int o : rn.out_obj)
+                    if (o >= 0) put(o, z);
+                nb << "      continue;\n    }\n";
+            }
+            const std::string taps = typed_taps(em, lk);
+            if (taps.empty()) throw unsupported("run-time typed tap body");
+            em.tdx = em.tdy = 0;
+            em.mode = Emitter::Mode::Post;
+            Emitter::TV v = em.cmb_tv;
+            if (lk.post_body && !em.temit(*lk.post_body, v)) throw unsupported("run-time typed post body");
+            nb << taps;
+            for (int o : rn.out_obj)
+                if (o >= 0) put(o, v);
+        } else {
+            throw unsupported("node kind");
+        }
+        body << "  // node " << ni << ": " << k.name << "\n"
+             << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << rw(oref) * rh(oref)
+             << "; e += blockDim.x * blockDim.y) {\n"
+             << "    const int ry = e / " << rw(oref) << ", rx = e - ry * " << rw(oref) << ";\n"
+             << "    const int px = tx0 - " << R.halo_x << " + rx, py = ty0 - " << R.halo_y << " + ry;\n"
+             << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
+        for (std::size_t o = 0; o < objs.size(); ++o)
+            if (used_obj[o])
+                body << "    const int b" << o << " = (ry + " << objs[o].halo_y - R.halo_y << ") * " << rw(static_cast<int>(o))
+                     << " + rx + " << objs[o].halo_x - R.halo_x << ";\n";
+        body << nb.str() << "  }\n  __syncthreads();\n";
+        // out-of-image entries = the entry at the clamped position (border tiles)
+        for (int o : rn.out_obj) {
+            if (o < 0) continue;
+            const RegionObject& O = objs[static_cast<std::size_t>(o)];
+            body << "  if (tx0 - " << O.halo_x << " < 0 || ty0 - " << O.halo_y << " < 0 || tx0 + " << TW + O.halo_x
+                 << " > W || ty0 + " << TH + O.halo_y << " > H) {\n"
+                 << "    for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << rw(o) * rh(o)
+                 << "; e += blockDim.x * blockDim.y) {\n"
+                 << "      const int ry = e / " << rw(o) << ", rx = e - ry * " << rw(o) << ";\n"
+                 << "      const int x = tx0 - " << O.halo_x << " + rx, y = ty0 - " << O.halo_y << " + ry;\n"
+                 << "      if (x >= 0 && y >= 0 && x < W && y < H) continue;\n"
+                 << "      ro" << o << "[e] = ro" << o << "[(clampi(y, 0, H - 1) - ty0 + " << O.halo_y << ") * " << rw(o)
+                 << " + clampi(x, 0, W - 1) - tx0 + " << O.halo_x << "];\n    }\n    __syncthreads();\n  }\n";
+        }
+        // per-node helper functions (typed loaders of global inputs)
+        std::string h = em.helpers.str();
+        helpers << h;
+    }
+    // stores of the objects consumed outside the region (or observable)
+    for (std::size_t o = 0; o < objs.size(); ++o) {
+        if (objs[o].store < 0) continue;
+        const int f = field_in(static_cast<int>(ins.size()) + objs[o].store);
+        body << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << TW * TH
+             << "; e += blockDim.x * blockDim.y) {\n"
+             << "    const int ry = e / " << TW << ", rx = e - ry * " << TW << ";\n"
+             << "    const int gx = tx0 + rx, gy = ty0 + ry;\n    if (gx >= W || gy >= H) continue;\n"
+             << "    " << storage_ctype(objs[o].format) << "* row = (" << storage_ctype(objs[o].format)
+             << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2 << "] + (u64)gy * p.f[" << f + 1
+             << "]);\n    row[gx] = ro" << o << "[(ry + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))
+             << " + rx + " << objs[o].halo_x << "];\n  }\n";
+    }
+    body << "  (void)rd;\n}\n";
+    KernelSpec ks;
+    ks.name = "gvx_region";
+    ks.grid = KernelSpec::Grid::Pixels;
+    ks.block_x = 32;
+    ks.block_y = 8;
+    ks.cols = TW / 32;
+    ks.rows = TH / 8;
+    std::string pre = kPrelude;
+    const std::string key = "NFIELDS";
+    pre.replace(pre.find(key), key.size(), std::to_string(prog.fields()));
+    ks.source = pre + helpers.str() + body.str();
+    prog.kernels.push_back(std::move(ks));
+    return prog;
+}
+
 NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
                        const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values,
                        bool count_reads) {
     NodeProgram p;
     switch (k.kind) {
     case AbstractionKind::Point: p = lower_point(k, ins, outs, /*vector_io=*/!count_reads); break;
-    case AbstractionKind::Local: p = lower_local(k, ins, outs, matrix_values); break;
+    case AbstractionKind::Local:
+        if (!count_reads && !std::getenv("GVX_NO_LTILE")) p = lower_local_tiled(k, ins, outs, matrix_values);
+        if (p.kernels.empty()) p = lower_local(k, ins, outs, matrix_values);
+        break;
     case AbstractionKind::Reduce: p = lower_reduce(k, ins, outs); break;
     case AbstractionKind::Histogram: p = lower_histogram(k, ins, outs); break;
     case AbstractionKind::Scan: p = lower_scan(ins, outs); break;

@@ -38,6 +38,7 @@ struct KernelSpec {
     enum class Grid : std::uint8_t { Pixels, OutPixels, Single, Rows, Cols, Strided } grid = Grid::Pixels;
     int block_x = 32, block_y = 8;
     int cols = 1; ///< pixels per thread along x (Pixels grids)
+    int rows = 1; ///< pixels per thread along y (Pixels grids)
 };
 
 /// A node lowered to one or more generated kernels.
@@ -81,5 +82,42 @@ NodeProgram lower_local_chain(const AbstractionKernel& producer, const std::vect
                               const std::vector<Value>& p_matrix, const SlotInfo& mid,
                               const AbstractionKernel& consumer, const std::vector<SlotInfo>& c_ins, int c_mid_slot,
                               const std::vector<SlotInfo>& c_outs, const std::vector<Value>& c_matrix);
+
+/// One node of a fused region (lower_region).
+struct RegionNode {
+    const AbstractionKernel* k = nullptr;
+    std::vector<SlotInfo> in_slots;  ///< per INPUT parameter
+    std::vector<int> in_obj;         ///< per INPUT parameter: region object (shared memory) or -1
+    std::vector<int> in_param;       ///< per INPUT parameter: kernel input slot (global) or -1
+    std::vector<int> out_obj;        ///< per OUTPUT parameter: region object or -1 (unbound)
+    std::vector<Value> matrix;       ///< mask values of a matrix-driven local
+};
+
+/// An image produced inside a region: held in shared memory over the tile
+/// plus `halo` on each side; `store` >= 0: also written to kernel output
+/// slot `store` (consumed outside the region, or observable).
+struct RegionObject {
+    ImageFormat format = ImageFormat::U8;
+    int halo_x = 0, halo_y = 0;
+    int store = -1;
+    int load = -1; ///< >= 0: an input of the region staged from kernel input slot `load`
+};
+
+/// Whether `e` reads input `slot` through a window (WindowPixel).
+bool reads_window(const Expr& e, int slot);
+
+/// A DAG region of point and local nodes over images of one size as ONE
+/// kernel (the generic local -> local / point -> local / local -> point
+/// fusion): each tile evaluates every node, in topological order, at every
+/// position its consumers' windows reach (tile + accumulated halo) into
+/// shared memory, each value narrowed to its image's storage format exactly
+/// as its store would (SURVEY.md §8a fusion contract rule 1) and taken at
+/// the CLAMPED position (rule 2), so every evaluated value is a pixel the
+/// reference also computes.  Inputs from outside the region are read from
+/// global memory with each reader's border mode.  Nodes are evaluated in
+/// their static types (Emitter::temit); throws Error(UnsupportedKind) when a
+/// node has run-time-typed parts.  The host counts the events statically.
+NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector<RegionObject>& objs,
+                         const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs);
 
 } // namespace gvx::jit
