@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <set>
 #include <sstream>
 
 namespace gvx {
@@ -25,13 +26,37 @@ namespace {
 
 using dev::check;
 
-int unit_radius(const dev::Unit& u) {
+/// Image inputs of a unit with the rows beyond its output rows it reads
+/// them at, or false when the unit cannot run on a row band.
+bool band_inputs(const dev::Unit& u, const std::map<ObjectId, dev::ObjInfo>& objects,
+                 std::vector<std::pair<ObjectId, int>>& out) {
+    out.clear();
     switch (u.kind) {
-    case dev::Unit::Kind::Edge: return u.with_gauss ? 2 : 1; // Gaussian3x3 + Sobel3x3
-    case dev::Unit::Kind::Harris: return 2;                  // Sobel3x3 + Box3x3
-    case dev::Unit::Kind::Stencil: return u.ksize / 2;
-    default: return -1;
+    case dev::Unit::Kind::Edge: out.push_back({u.src, u.with_gauss ? 2 : 1}); return true; // Gaussian + Sobel
+    case dev::Unit::Kind::Harris: out.push_back({u.src, 2}); return true;                  // Sobel + Box3x3
+    case dev::Unit::Kind::Stencil: out.push_back({u.src, u.ksize / 2}); return true;
+    case dev::Unit::Kind::Jit: {
+        if (u.prog.in_halo.size() != u.in_ids.size()) return false; // global ops, scans, scaling
+        for (const jit::KernelSpec& ks : u.prog.kernels)
+            if (ks.grid != jit::KernelSpec::Grid::Pixels && ks.grid != jit::KernelSpec::Grid::OutPixels) return false;
+        for (std::size_t i = 0; i < u.in_ids.size(); ++i) {
+            const ObjectId id = u.in_ids[i];
+            if (id == kInvalidId) continue;
+            auto it = objects.find(id);
+            if (it == objects.end()) continue;
+            if (it->second.desc.kind == ObjKind::Image) out.push_back({id, u.prog.in_halo[i]});
+            else if (it->second.desc.kind != ObjKind::Matrix) return false; // run-time scalars / arrays
+        }
+        return true;
     }
+    default: return false;
+    }
+}
+
+int unit_halo(const std::vector<std::pair<ObjectId, int>>& ins) {
+    int r = 0;
+    for (const auto& kv : ins) r = std::max(r, kv.second);
+    return r;
 }
 
 struct Slab {
@@ -54,8 +79,10 @@ struct BandedSession::Impl {
     gvxb_comm comm = nullptr;
     gvxb_band_plan band{};   ///< rows of this band (halo 0)
     std::map<ObjectId, Slab> slabs;
-    std::vector<gvxb_band_plan> unit_plan; ///< per unit: split by its radius
-    std::vector<gvxb_band_plan> src_plan;  ///< per unit: exchange of its input's whole slab halo
+    std::vector<gvxb_band_plan> unit_plan; ///< per unit: split by its largest input halo
+    std::vector<std::vector<std::pair<ObjectId, int>>> unit_ins; ///< per unit: image inputs and halos
+    std::map<ObjectId, gvxb_band_plan> obj_plan;  ///< exchange of an object's whole slab halo
+    std::set<ObjectId> exchanged;                 ///< objects exchanged in the current launch
     int input_halo = 0;
     ObjectId input = kInvalidId;
 
@@ -92,17 +119,20 @@ struct BandedSession::Impl {
         frames = std::max(1, frames_);
         comm = static_cast<gvxb_comm>(comm_);
         if (world < 1 || rank < 0 || rank >= world) throw Error(ErrorCode::BadKernel, "bad band rank / world");
-        std::map<ObjectId, int> radius_in; // object -> largest radius of the groups reading it
+        std::map<ObjectId, int> radius_in; // object -> largest halo of the units reading it
         for (const dev::Unit& u : prog->units) {
-            const int r = unit_radius(u);
-            if (r < 0)
+            std::vector<std::pair<ObjectId, int>> ins;
+            if (!band_inputs(u, prog->objects, ins))
                 throw Error(ErrorCode::UnsupportedKind,
-                            "row-band execution needs a program of hand-written stencil groups; '" + u.label +
-                                "' is not one (run it with DeviceSession per frame instead)");
-            radius_in[u.src] = std::max(radius_in[u.src], r);
+                            "row-band execution needs stencil / point programs; '" + u.label +
+                                "' is a global operation or reads run-time scalars (run it with DeviceSession per frame "
+                                "instead)");
+            for (const auto& [id, r] : ins) radius_in[id] = std::max(radius_in[id], r);
+            unit_ins.push_back(std::move(ins));
         }
         if (prog->units.empty()) throw Error(ErrorCode::UnsupportedKind, "row-band execution of an empty program");
         for (const auto& [id, oi] : prog->objects) {
+            if (oi.desc.kind == ObjKind::Matrix) continue; // baked into the generated code
             if (oi.desc.kind != ObjKind::Image)
                 throw Error(ErrorCode::UnsupportedKind, "row-band execution: non-image object in the program", id);
             if (W == 0) W = oi.desc.width, H = oi.desc.height;
@@ -113,6 +143,7 @@ struct BandedSession::Impl {
         ctx = dev::own_context(device);
         check(gvxb_band_plan_make(H, world, rank, 0, &band), "band plan");
         for (const auto& [id, oi] : prog->objects) {
+            if (oi.desc.kind != ObjKind::Image) continue;
             auto it = radius_in.find(id);
             const int R = it == radius_in.end() ? 0 : it->second;
             gvxb_band_plan p{};
@@ -133,13 +164,18 @@ struct BandedSession::Impl {
             slabs[id] = s;
             if (!oi.produced && R > 0 && input == kInvalidId) input = id, input_halo = R;
         }
-        if (input == kInvalidId) input = prog->units.front().src, input_halo = radius_in[input];
-        for (const dev::Unit& u : prog->units) {
-            gvxb_band_plan p{}, q{};
-            check(gvxb_band_plan_make(H, world, rank, unit_radius(u), &p), "band plan");
-            check(gvxb_band_plan_make(H, world, rank, slabs.at(u.src).halo, &q), "band plan");
+        if (input == kInvalidId && !unit_ins.front().empty())
+            input = unit_ins.front().front().first, input_halo = radius_in[input];
+        for (std::size_t i = 0; i < prog->units.size(); ++i) {
+            gvxb_band_plan p{};
+            check(gvxb_band_plan_make(H, world, rank, unit_halo(unit_ins[i]), &p), "band plan");
             unit_plan.push_back(p);
-            src_plan.push_back(q);
+            for (const auto& kv : unit_ins[i]) {
+                if (obj_plan.count(kv.first)) continue;
+                gvxb_band_plan q{};
+                check(gvxb_band_plan_make(H, world, rank, slabs.at(kv.first).halo, &q), "band plan");
+                obj_plan[kv.first] = q;
+            }
         }
     }
 
@@ -161,6 +197,10 @@ struct BandedSession::Impl {
     /// Output rows [r0, r1) of unit `u` (its input halo rows must be present).
     void compute(const dev::Unit& u, int r0, int r1, gvxb_ctx on) {
         if (r1 <= r0) return;
+        if (u.kind == dev::Unit::Kind::Jit) {
+            compute_jit(u, r0, r1, on);
+            return;
+        }
         const Slab& src = slabs.at(u.src);
         const gvxb_band b{r0, r1, H, src.row0, band.row0};
         switch (u.kind) {
@@ -199,29 +239,98 @@ struct BandedSession::Impl {
             check(gvxb_stencil_point(on, &a), "gvxb_stencil_point (band)");
             return;
         }
+        case dev::Unit::Kind::Jit: compute_jit(u, r0, r1, on); return;
         default: throw Error(ErrorCode::UnsupportedKind, "row-band execution: unsupported group");
         }
     }
 
-    bool needs_exchange(std::size_t i) const {
-        const gvxb_band_plan& q = src_plan[i];
-        return world > 1 && (q.peer[0] >= 0 || q.peer[1] >= 0);
+    /// A generated kernel set on output rows [r0, r1): image slots get the
+    /// address of their global row 0 inside the slab (rows outside the slab
+    /// are never read: its halo covers the kernel's windows).
+    void compute_jit(const dev::Unit& u, int r0, int r1, gvxb_ctx on) {
+        const jit::NodeProgram& np = u.prog;
+        std::vector<std::uint64_t> f(static_cast<std::size_t>(np.fields()), 0);
+        unsigned long long* counter = nullptr;
+        std::uint32_t* status = nullptr;
+        gvxb_counter_ptr(on, &counter);
+        gvxb_status_ptr(on, &status);
+        f[0] = reinterpret_cast<std::uint64_t>(status);
+        f[1] = reinterpret_cast<std::uint64_t>(counter);
+        f[2] = static_cast<std::uint64_t>(W);
+        f[3] = static_cast<std::uint64_t>(H);
+        f[4] = static_cast<std::uint64_t>(frames);
+        auto put = [&](int slot, ObjectId id) {
+            if (id == kInvalidId) return;
+            auto it = slabs.find(id);
+            if (it == slabs.end()) return; // matrices: baked into the code
+            const Slab& sl = it->second;
+            const std::size_t b = static_cast<std::size_t>(5 + 3 * slot);
+            f[b] = reinterpret_cast<std::uint64_t>(static_cast<char*>(sl.ptr) - static_cast<std::int64_t>(sl.row0) * sl.pitch);
+            f[b + 1] = static_cast<std::uint64_t>(sl.pitch);
+            f[b + 2] = static_cast<std::uint64_t>(sl.fstride);
+        };
+        for (std::size_t i = 0; i < u.in_ids.size(); ++i) put(static_cast<int>(i), u.in_ids[i]);
+        for (std::size_t o = 0; o < u.out_ids.size(); ++o) put(static_cast<int>(u.in_ids.size() + o), u.out_ids[o]);
+        f[f.size() - 4] = static_cast<std::uint64_t>(r0);
+        f[f.size() - 3] = static_cast<std::uint64_t>(r1);
+        void* args[] = {f.data()};
+        for (std::size_t ki = 0; ki < np.kernels.size(); ++ki) {
+            const jit::KernelSpec& ks = np.kernels[ki];
+            const unsigned grid[3] = {static_cast<unsigned>((W + ks.block_x * ks.cols - 1) / (ks.block_x * ks.cols)),
+                                      static_cast<unsigned>((r1 - r0 + ks.block_y * ks.rows - 1) / (ks.block_y * ks.rows)),
+                                      static_cast<unsigned>(frames)};
+            const unsigned block[3] = {static_cast<unsigned>(ks.block_x), static_cast<unsigned>(ks.block_y), 1};
+            check(gvxb_jit_launch(on, u.module, static_cast<int>(ki), grid, block, 0, args), "generated kernel (band)");
+        }
     }
 
-    /// Posts unit i's input halo exchange (NCCL).  Peer mode: BandGroup.
+    /// Inputs of unit i whose halo rows must come from the neighbours (not
+    /// yet exchanged in this launch).
+    std::vector<ObjectId> pending_exchange(std::size_t i) const {
+        std::vector<ObjectId> v;
+        if (world <= 1) return v;
+        for (const auto& kv : unit_ins[i]) {
+            const gvxb_band_plan& q = obj_plan.at(kv.first);
+            if ((q.peer[0] >= 0 || q.peer[1] >= 0) && !exchanged.count(kv.first)) v.push_back(kv.first);
+        }
+        return v;
+    }
+    bool needs_exchange(std::size_t i) const { return !pending_exchange(i).empty(); }
+    /// Whether unit i's inputs have halo rows from neighbours at all.
+    bool has_exchange(std::size_t i) const {
+        if (world <= 1) return false;
+        for (const auto& kv : unit_ins[i]) {
+            const gvxb_band_plan& q = obj_plan.at(kv.first);
+            if (q.peer[0] >= 0 || q.peer[1] >= 0) return true;
+        }
+        return false;
+    }
+
+    /// Posts the halo exchange of unit i's inputs (NCCL).  Peer mode: BandGroup.
     void exchange_nccl(std::size_t i) {
         if (!comm) throw Error(ErrorCode::UnsupportedKind, "row bands with world > 1 need a communicator or a BandGroup");
-        gvxb_image slab = image(prog->units[i].src, false);
-        check(gvxb_halo_start(ctx, comm, &src_plan[i], &slab), "halo exchange");
+        for (ObjectId id : pending_exchange(i)) {
+            gvxb_image slab = image(id, false);
+            check(gvxb_halo_start(ctx, comm, &obj_plan.at(id), &slab), "halo exchange");
+            exchanged.insert(id);
+        }
     }
 
-    /// Peer mode, phase 2: pull unit i's input halo rows from the neighbours
+    /// Peer mode, phase 2: pull unit i's inputs' halo rows from the neighbours
     /// on the exchange stream once both sides reached the exchange point.
     void exchange_peer(std::size_t i) {
-        const gvxb_band_plan& q = src_plan[i];
-        const ObjectId id = prog->units[i].src;
-        const Slab& me = slabs.at(id);
         check(gvxb_stream_wait_event(xctx, ev_ready), "exchange ordering");
+        for (ObjectId id : pending_exchange(i)) {
+            exchange_peer_object(id);
+            exchanged.insert(id);
+        }
+        check(gvxb_event_record(xctx, ev_xdone), "exchange event");
+        pulled = true;
+    }
+
+    void exchange_peer_object(ObjectId id) {
+        const gvxb_band_plan& q = obj_plan.at(id);
+        const Slab& me = slabs.at(id);
         for (int side = 0; side < 2; ++side) {
             if (q.peer[side] < 0) continue;
             Impl* nb = (*group)[static_cast<std::size_t>(q.peer[side])];
@@ -239,8 +348,6 @@ struct BandedSession::Impl {
                       "halo peer copy");
             }
         }
-        check(gvxb_event_record(xctx, ev_xdone), "exchange event");
-        pulled = true;
     }
 
     void wait_exchange() {
@@ -262,6 +369,7 @@ struct BandedSession::Impl {
     }
 
     void launch_standalone() {
+        exchanged.clear();
         for (std::size_t i = 0; i < prog->units.size(); ++i) {
             const bool x = needs_exchange(i);
             if (x) exchange_nccl(i);
@@ -285,9 +393,11 @@ struct BandedSession::Impl {
         if (prog->units.size() != 1)
             throw Error(ErrorCode::UnsupportedKind, "BandedSession::run_host needs a single-group program");
         const dev::Unit& u = prog->units[0];
-        const Slab& in = slabs.at(u.src);
+        if (unit_ins[0].size() != 1)
+            throw Error(ErrorCode::UnsupportedKind, "BandedSession::run_host needs a single-input program");
+        const Slab& in = slabs.at(unit_ins[0][0].first);
         const Slab& out = slabs.at(output);
-        const int R = unit_radius(u);
+        const int R = unit_ins[0][0].second;
         piece = std::max(piece, 1);
         std::vector<std::pair<int, int>> pieces;
         for (int a = band.row0; a < band.row1; a += piece) pieces.emplace_back(a, std::min(band.row1, a + piece));
@@ -428,7 +538,10 @@ int BandedSession::launches_per_run() const {
     int n = 0;
     for (std::size_t i = 0; i < impl_->prog->units.size(); ++i) {
         const gvxb_band_plan& p = impl_->unit_plan[i];
-        n += impl_->needs_exchange(i) ? (p.interior_row1 > p.interior_row0 ? 1 : 0) + p.n_edges : 1;
+        const int per = impl_->prog->units[i].kind == dev::Unit::Kind::Jit
+                            ? static_cast<int>(impl_->prog->units[i].prog.kernels.size())
+                            : 1;
+        n += per * (impl_->has_exchange(i) ? (p.interior_row1 > p.interior_row0 ? 1 : 0) + p.n_edges : 1);
     }
     return n;
 }
@@ -483,6 +596,7 @@ void BandGroup::launch() {
         bool any = false;
         for (auto& b : bands_) {
             b->impl_->pulled = false;
+            if (i == 0) b->impl_->exchanged.clear();
             any = any || b->impl_->needs_exchange(i);
         }
         if (any) {
@@ -491,14 +605,13 @@ void BandGroup::launch() {
                 if (b->impl_->needs_exchange(i)) b->impl_->exchange_peer(i);
         }
         for (auto& b : bands_) b->impl_->run_unit(i, b->impl_->pulled);
-        // the next write of this group's input (a later group or launch) waits
-        // for the neighbours' pulls of it
-        for (auto& b : bands_)
-            for (int side = 0; side < 2; ++side) {
-                const int nb = b->impl_->src_plan[i].peer[side];
-                if (nb < 0) continue;
+        // the next write of this group's inputs (a later group or launch)
+        // waits for the neighbours' pulls of them
+        for (std::size_t g = 0; g < bands_.size(); ++g)
+            for (int nb : {static_cast<int>(g) - 1, static_cast<int>(g) + 1}) {
+                if (nb < 0 || nb >= static_cast<int>(bands_.size())) continue;
                 BandedSession::Impl* o = bands_[static_cast<std::size_t>(nb)]->impl_.get();
-                if (o->pulled) check(gvxb_stream_wait_event(b->impl_->ctx, o->ev_xdone), "exchange ordering");
+                if (o->pulled) check(gvxb_stream_wait_event(bands_[g]->impl_->ctx, o->ev_xdone), "exchange ordering");
             }
     }
 }

@@ -344,78 +344,6 @@ Unit jit_unit(const OperatorNode& n, const VerifiedGraph& vg,
     return u;
 }
 
-/// Producer -> consumer local chain as one JIT unit (jit::lower_local_chain):
-/// the intermediate `mid` stays in shared memory.  Returns false (and leaves
-/// `u` alone) when the pair does not qualify.
-bool chain_unit(const OperatorNode& pn, const OperatorNode& cn, ObjectId mid, const VerifiedGraph& vg,
-                const std::map<ObjectId, std::vector<Value>>& matrices, Unit& u) {
-    if (!pn.abstraction || !cn.abstraction) return false;
-    const ResolvedDesc& md = vg.desc(mid);
-    if (md.kind != ObjKind::Image || !jit::local_chain_fusible(*pn.abstraction, *cn.abstraction, md.format))
-        return false;
-    std::int64_t pr = 0, pw = 0, cr = 0, cw = 0;
-    if (!static_counts(pn, vg, pr, pw) || !static_counts(cn, vg, cr, cw)) return false;
-    Unit pu, cu;
-    auto collect = [&](const OperatorNode& n, Unit& x) {
-        const auto& ps = n.abstraction->signature.params;
-        for (std::size_t i = 0; i < ps.size(); ++i) {
-            const Binding* b = n.binding_for(static_cast<int>(i));
-            const ObjectId id = b ? b->object : kInvalidId;
-            if (ps[i].direction == Direction::Input) {
-                x.in_ids.push_back(id);
-                x.in_slots.push_back(slot_of(vg, id));
-            } else {
-                x.out_ids.push_back(id);
-                x.out_slots.push_back(slot_of(vg, id));
-            }
-        }
-    };
-    collect(pn, pu);
-    collect(cn, cu);
-    if (pu.out_ids.size() != 1 || pu.out_ids[0] != mid || cu.out_ids.empty()) return false;
-    int c_mid = -1;
-    for (std::size_t i = 0; i < cu.in_ids.size(); ++i)
-        if (cu.in_ids[i] == mid) {
-            if (c_mid >= 0) return false; // bound twice
-            c_mid = static_cast<int>(i);
-        }
-    if (c_mid < 0) return false;
-    // one working size: every image either node touches has the intermediate's dims
-    auto same_dims = [&](const std::vector<jit::SlotInfo>& v) {
-        for (const jit::SlotInfo& si : v)
-            if (si.kind == jit::SlotKind::Image && (si.desc.width != md.width || si.desc.height != md.height))
-                return false;
-        return true;
-    };
-    if (!same_dims(pu.in_slots) || !same_dims(cu.in_slots) || !same_dims(cu.out_slots)) return false;
-    u = Unit{};
-    u.kind = Unit::Kind::Jit;
-    u.k = cn.abstraction;
-    u.label = (pn.label.empty() ? pn.kernel : pn.label) + " -> " + (cn.label.empty() ? cn.kernel : cn.label);
-    u.covers = {pn.id, cn.id};
-    u.in_ids = pu.in_ids;
-    u.in_slots = pu.in_slots;
-    for (std::size_t i = 0; i < cu.in_ids.size(); ++i) {
-        u.in_ids.push_back(static_cast<int>(i) == c_mid ? kInvalidId : cu.in_ids[i]);
-        u.in_slots.push_back(cu.in_slots[i]); // the intermediate keeps its image slot info (smem reads)
-    }
-    for (ObjectId id : u.in_ids)
-        if (id != kInvalidId) u.reads.push_back(id);
-    u.out_ids = cu.out_ids;
-    u.out_slots = cu.out_slots;
-    for (ObjectId id : u.out_ids)
-        if (id != kInvalidId) u.writes.push_back(id);
-    u.prog = jit::lower_local_chain(*pn.abstraction, pu.in_slots, matrix_for(pu, vg.context(), matrices),
-                                    slot_of(vg, mid), *cn.abstraction, cu.in_slots, c_mid, cu.out_slots,
-                                    matrix_for(cu, vg.context(), matrices));
-    u.width = md.width;
-    u.height = md.height;
-    u.static_reads = pr + cr;
-    u.static_writes = pw + cw;
-    u.device_counts_reads = false;
-    return true;
-}
-
 /// Generic fused regions (jit::lower_region): maximal convex DAG regions of
 /// the remaining executed point / local nodes over images of one size, each
 /// one kernel with its intermediates in shared memory.  Returns the units
@@ -663,6 +591,14 @@ std::vector<Unit> region_units(const AppGraph& fg, const VerifiedGraph& fused, c
                 std::fprintf(stderr, "[gvx region] %zu nodes not fused: %s\n", mem.size(), e.what());
             continue; // run-time typed parts: per-node kernels
         }
+        // row-band support: rows beyond its output rows each input is read at
+        {
+            int hmax = 0;
+            for (const jit::RegionObject& ro : objs) hmax = std::max(hmax, ro.halo_y);
+            u.prog.in_halo.assign(ins.size(), hmax); // non-staged (multi-channel) inputs: the largest halo
+            for (const jit::RegionObject& ro : objs)
+                if (ro.load >= 0) u.prog.in_halo[static_cast<std::size_t>(ro.load)] = ro.halo_y;
+        }
         u.width = dims[mem.front()->id].first;
         u.height = dims[mem.front()->id].second;
         u.static_reads = reads;
@@ -901,49 +837,6 @@ std::shared_ptr<Program> build_plan(const OptimizedPlan& plan, const std::map<Ob
         }
     }
     for (Unit& u : aot) p->units.push_back(std::move(u));
-    // generic local -> local chains among the remaining executed nodes: a
-    // virtual intermediate written by a local and read only by one local
-    // stays on chip (jit::lower_local_chain).  Opt-in (GVX_LOCAL_CHAINS=1):
-    // the pair kernel moves 4x fewer DRAM bytes but its Value-typed post
-    // bodies run one pixel per thread, and on the corpus pairs it measured
-    // slower than the two per-node kernels (profiles/chain_probe)
-    const bool chains = std::getenv("GVX_LOCAL_CHAINS") != nullptr;
-    if (chains) {
-        std::map<ObjectId, std::vector<ObjectId>> fg_readers; // object -> reading executed nodes
-        std::map<ObjectId, ObjectId> fg_writer;
-        for (const OperatorNode& n : fg.nodes()) {
-            std::set<ObjectId> seen;
-            for (const Binding& b : n.bindings) {
-                if (b.direction == Direction::Input) {
-                    if (seen.insert(b.object).second) fg_readers[b.object].push_back(n.id);
-                } else {
-                    fg_writer[b.object] = n.id;
-                }
-            }
-        }
-        for (ObjectId cid : fg.topo_sort()) {
-            if (covered_fused.count(cid)) continue;
-            const OperatorNode* cn = fg.node(cid);
-            if (!cn || !cn->abstraction || cn->abstraction->kind != AbstractionKind::Local) continue;
-            for (const Binding& b : cn->bindings) {
-                if (b.direction != Direction::Input) continue;
-                const ObjectId mid = b.object;
-                auto w = fg_writer.find(mid);
-                if (w == fg_writer.end() || covered_fused.count(w->second)) continue;
-                const DataObject* mo = base.context().find(mid);
-                if (!mo || !mo->is_virtual) continue;
-                const auto& rs = fg_readers[mid];
-                if (rs.size() != 1 || rs[0] != cid) continue;
-                const OperatorNode* pn = fg.node(w->second);
-                Unit u;
-                if (!pn || !chain_unit(*pn, *cn, mid, fused, matrices, u)) continue;
-                covered_fused.insert(pn->id);
-                covered_fused.insert(cid);
-                p->units.push_back(std::move(u));
-                break;
-            }
-        }
-    }
     {
         std::set<ObjectId> rcov;
         for (Unit& u : region_units(fg, fused, covered_fused, matrices, rcov)) p->units.push_back(std::move(u));
@@ -1205,6 +1098,8 @@ struct DeviceSession::Impl {
         };
         for (std::size_t i = 0; i < u.in_ids.size(); ++i) put(static_cast<int>(i), u.in_ids[i]);
         for (std::size_t o = 0; o < u.out_ids.size(); ++o) put(static_cast<int>(u.in_ids.size() + o), u.out_ids[o]);
+        f[f.size() - 4] = 0;                                  // first output row
+        f[f.size() - 3] = static_cast<std::uint64_t>(u.height); // end row
         f[f.size() - 2] = reinterpret_cast<std::uint64_t>(scr);
         f[f.size() - 1] = np.scratch_bytes_per_frame;
         void* args[] = {f.data()};

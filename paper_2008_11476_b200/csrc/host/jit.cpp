@@ -29,6 +29,8 @@ typedef long long i64;
 typedef unsigned long long u64;
 struct V { int r; i64 i; double f; };
 struct P { u64 f[NFIELDS]; };
+#define ROW0 ((int)p.f[sizeof(p.f) / sizeof(p.f[0]) - 4])
+#define ROW1 ((int)p.f[sizeof(p.f) / sizeof(p.f[0]) - 3])
 __device__ __forceinline__ V vi(i64 x) { V v; v.r = 0; v.i = x; v.f = 0.0; return v; }
 __device__ __forceinline__ V vf(double x) { V v; v.r = 1; v.i = 0; v.f = x; return v; }
 __device__ __forceinline__ double vd(V a) { return a.r ? a.f : __ll2double_rn(a.i); }
@@ -807,10 +809,10 @@ std::string assemble(const Emitter& em, const std::string& body, int nfields) {
 const char* kPixelHead = R"CUDA(
   const int W = (int)p.f[2], H = (int)p.f[3];
   const int px = blockIdx.x * blockDim.x + threadIdx.x;
-  const int py = blockIdx.y * blockDim.y + threadIdx.y;
+  const int py = ROW0 + blockIdx.y * blockDim.y + threadIdx.y;
   const int fr = blockIdx.z;
   u64 rd = 0;
-  const bool live = px < W && py < H;
+  const bool live = px < W && py < ROW1;
 )CUDA";
 
 const char* kStridedHead = R"CUDA(
@@ -829,10 +831,10 @@ constexpr int kCols = 4;
 const char* kPixelHead4 = R"CUDA(
   const int W = (int)p.f[2], H = (int)p.f[3];
   const int px4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  const int py = blockIdx.y * blockDim.y + threadIdx.y;
+  const int py = ROW0 + blockIdx.y * blockDim.y + threadIdx.y;
   const int fr = blockIdx.z;
   u64 rd = 0;
-  const bool live = px4 < W && py < H;
+  const bool live = px4 < W && py < ROW1;
 )CUDA";
 const char* kEachPixel = "#pragma unroll\n    for (int i = 0; i < 4; ++i) { const int px = px4 + i; if (px >= W) break;\n";
 
@@ -902,6 +904,7 @@ NodeProgram lower_point(const AbstractionKernel& k, const std::vector<SlotInfo>&
             b << "  " << em.store(static_cast<int>(o), em.emit_any(*bodies[0]), 0, "px", "py");
         }
     }
+    prog.in_halo.assign(ins.size(), 0);
     KernelSpec ks;
     ks.name = "gvx_point";
     ks.cols = kCols;
@@ -1182,7 +1185,7 @@ NodeProgram lower_local_tiled(const AbstractionKernel& k, const std::vector<Slot
     std::ostringstream src;
     src << "extern \"C\" __global__ void gvx_ltile(const P p) {\n"
         << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
-        << "  const int x0 = (int)blockIdx.x * " << TX * PX << ", y0 = (int)blockIdx.y * " << TY << ";\n"
+        << "  const int x0 = (int)blockIdx.x * " << TX * PX << ", y0 = ROW0 + (int)blockIdx.y * " << TY << ";\n"
         << "  __shared__ " << gty << " gs[" << RW * RH << "];\n"
         << "  for (int ry = threadIdx.y; ry < " << RH << "; ry += " << TY << ")\n"
         << "  for (int rx = threadIdx.x; rx < " << RW << "; rx += " << TX << ") {\n"
@@ -1193,7 +1196,7 @@ NodeProgram lower_local_tiled(const AbstractionKernel& k, const std::vector<Slot
     else
         src << "    if (px < -" << hw << " || py < -" << hh << " || px >= W + " << hw << " || py >= H + " << hh << ") continue;\n";
     src << "    gs[e] = (" << gty << ")(" << gv.c << ");\n  }\n  __syncthreads();\n"
-        << "  const int py = y0 + (int)threadIdx.y;\n  if (py >= H) return;\n"
+        << "  const int py = y0 + (int)threadIdx.y;\n  if (py >= ROW1) return;\n"
         << "#pragma unroll\n  for (int i = 0; i < " << PX << "; ++i) {\n"
         << "    const int px = x0 + (int)threadIdx.x + " << TX << " * i;\n    if (px >= W) break;\n";
     if (undef)
@@ -1201,6 +1204,9 @@ NodeProgram lower_local_tiled(const AbstractionKernel& k, const std::vector<Slot
             << "      " << em.store(0, "v_cast(vi(0), " + std::to_string(type_code(out_t)) + ", 0)", 0, "px", "py")
             << "      continue;\n    }\n";
     src << comb << "    " << em.store(0, pv, 0, "px", "py") << "  }\n  (void)rd;\n}\n";
+    prog.in_halo.assign(ins.size(), 0);
+    for (std::size_t i = 0; i < ins.size(); ++i)
+        if (reads_window(*lk.tap_body, static_cast<int>(i))) prog.in_halo[i] = hh;
     KernelSpec ks;
     ks.name = "gvx_ltile";
     ks.grid = KernelSpec::Grid::Pixels;
@@ -1280,6 +1286,9 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     } else {
         b << "    " << em.store(0, "cmb", 0, "px", "py");
     }
+    prog.in_halo.assign(ins.size(), 0);
+    for (std::size_t i = 0; i < ins.size(); ++i)
+        if (lk.tap_body && reads_window(*lk.tap_body, static_cast<int>(i))) prog.in_halo[i] = hh;
     KernelSpec ks;
     ks.name = "gvx_local";
     ks.cols = kCols;
@@ -1437,81 +1446,6 @@ std::string local_value(Emitter& em, const LocalKernel& lk, const std::vector<Sl
 } // namespace
 } // namespace (lowering helpers)
 
-bool local_chain_fusible(const AbstractionKernel& producer, const AbstractionKernel& consumer, ImageFormat mid) {
-    if (producer.kind != AbstractionKind::Local || consumer.kind != AbstractionKind::Local) return false;
-    const LocalKernel& a = producer.local();
-    const LocalKernel& b = consumer.local();
-    if (a.median3x3 || b.median3x3 || !a.tap_body || !b.tap_body) return false;
-    if (a.boundary == BoundaryMode::Undefined || b.boundary != BoundaryMode::Clamp) return false;
-    if (b.window_w > 7 || b.window_h > 7 || a.window_w > 7 || a.window_h > 7) return false;
-    std::string t, c, l;
-    return storage_of(mid, t, c, l);
-}
-
-NodeProgram lower_local_chain(const AbstractionKernel& producer, const std::vector<SlotInfo>& p_ins,
-                              const std::vector<Value>& p_matrix, const SlotInfo& mid,
-                              const AbstractionKernel& consumer, const std::vector<SlotInfo>& c_ins, int c_mid_slot,
-                              const std::vector<SlotInfo>& c_outs, const std::vector<Value>& c_matrix) {
-    const LocalKernel& pk = producer.local();
-    const LocalKernel& ck = consumer.local();
-    std::string ctype, conv, load;
-    if (!storage_of(mid.desc.format, ctype, conv, load)) throw Error(ErrorCode::BadFormat, "fused chain format");
-    NodeProgram prog;
-    prog.n_inputs = static_cast<int>(p_ins.size() + c_ins.size());
-    prog.n_outputs = static_cast<int>(c_outs.size());
-    prog.dims_from = -1;
-    prog.counts_reads = false; // static windows: the host counts both nodes' reads
-    constexpr int TX = 32, TY = 8;
-    const int RX = ck.window_w / 2, RY = ck.window_h / 2;
-    const int RW = TX + 2 * RX, RH = TY + 2 * RY;
-
-    std::vector<SlotInfo> p_outs{mid};
-    Emitter pe(p_ins, p_outs);
-    pe.local = &pk;
-    pe.mask = pk.mask.empty() ? &p_matrix : &pk.mask;
-    pe.prefix = "P";
-    pe.n_in_total = prog.n_inputs;
-    Emitter ce(c_ins, c_outs);
-    ce.local = &ck;
-    ce.mask = ck.mask.empty() ? &c_matrix : &ck.mask;
-    ce.prefix = "C";
-    ce.slot_base = static_cast<int>(p_ins.size());
-    ce.n_in_total = prog.n_inputs;
-    ce.smem_slot = c_mid_slot;
-    ce.smem_loader = "ld_mid";
-
-    const std::string pbody = local_value(pe, pk, p_ins, *pe.mask, RW);
-    const std::string cbody = local_value(ce, ck, c_ins, *ce.mask, RW);
-    std::ostringstream src;
-    src << "__shared__ " << ctype << " gvx_mid[" << RH * RW << "];\n"
-        << "__device__ __forceinline__ V ld_mid(const P& p, int fr, int x, int y, u64& rd) {\n"
-        << "  const " << ctype << " v = gvx_mid[(y - ((int)blockIdx.y * " << TY << " - " << RY << ")) * " << RW
-        << " + (x - ((int)blockIdx.x * " << TX << " - " << RX << "))];\n  return " << load << ";\n}\n"
-        << "extern \"C\" __global__ void gvx_lchain(const P p) {\n"
-        << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
-        << "  const int x0 = (int)blockIdx.x * " << TX << " - " << RX << ", y0 = (int)blockIdx.y * " << TY << " - "
-        << RY << ";\n  const int rx0 = x0, ry0 = y0;\n"
-        << "  // the intermediate at every (clamped) position the tile's windows read\n"
-        << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << RH * RW
-        << "; e += blockDim.x * blockDim.y) {\n"
-        << "    const int px = clampi(x0 + e % " << RW << ", 0, W - 1), py = clampi(y0 + e / " << RW
-        << ", 0, H - 1);\n"
-        << pbody << "    V sv = pv;\n    gvx_mid[e] = " << conv << ";\n  }\n  __syncthreads();\n"
-        << "  const int px = blockIdx.x * " << TX << " + threadIdx.x, py = blockIdx.y * " << TY << " + threadIdx.y;\n"
-        << "  if (px < W && py < H) {\n"
-        << cbody << "    " << ce.store(0, "pv", 0, "px", "py") << "  }\n}\n";
-    KernelSpec ks;
-    ks.name = "gvx_lchain";
-    ks.block_x = TX;
-    ks.block_y = TY;
-    ks.cols = 1;
-    std::string pre = kPrelude;
-    const std::string key = "NFIELDS";
-    pre.replace(pre.find(key), key.size(), std::to_string(prog.fields()));
-    ks.source = pre + pe.helpers.str() + ce.helpers.str() + src.str();
-    prog.kernels.push_back(std::move(ks));
-    return prog;
-}
 
 namespace {
 
@@ -1917,7 +1851,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     std::ostringstream helpers, body;
     body << "extern \"C\" __global__ void gvx_region(const P p) {\n"
          << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
-         << "  const int tx0 = (int)blockIdx.x * " << TW << ", ty0 = (int)blockIdx.y * " << TH << ";\n";
+         << "  const int tx0 = (int)blockIdx.x * " << TW << ", ty0 = ROW0 + (int)blockIdx.y * " << TH << ";\n";
     for (std::size_t o = 0; o < objs.size(); ++o)
         body << "  __shared__ " << storage_ctype(objs[o].format) << " ro" << o << "["
              << rw(static_cast<int>(o)) * rh(static_cast<int>(o)) << "];\n";
@@ -2053,7 +1987,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         body << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << TW * TH
              << "; e += blockDim.x * blockDim.y) {\n"
              << "    const int ry = e / " << TW << ", rx = e - ry * " << TW << ";\n"
-             << "    const int gx = tx0 + rx, gy = ty0 + ry;\n    if (gx >= W || gy >= H) continue;\n"
+             << "    const int gx = tx0 + rx, gy = ty0 + ry;\n    if (gx >= W || gy >= ROW1) continue;\n"
              << "    " << storage_ctype(objs[o].format) << "* row = (" << storage_ctype(objs[o].format)
              << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2 << "] + (u64)gy * p.f[" << f + 1
              << "]);\n    row[gx] = ro" << o << "[(ry + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))

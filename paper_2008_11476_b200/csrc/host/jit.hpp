@@ -54,7 +54,13 @@ struct NodeProgram {
     std::size_t scratch_bytes_per_frame = 0; ///< device scratch needed
     bool counts_reads = true;
     int dims_from = -1; ///< input slot giving W/H (-1 = output 0)
-    int fields() const { return 5 + 3 * (n_inputs + n_outputs) + 2; }
+    /// Row-band support: rows beyond the output rows each input slot is read
+    /// at (window radius, accumulated halo); empty when the program cannot
+    /// run on a row band (global reductions, scans, scaling, chains).
+    std::vector<int> in_halo;
+    //  ... then [fields-4] first output row, [fields-3] end row (row bands;
+    //  0 / H for a whole image), [fields-2] scratch pointer, [fields-1] stride
+    int fields() const { return 5 + 3 * (n_inputs + n_outputs) + 4; }
 };
 
 /// Lowers one abstraction node.  `ins` / `outs` describe the bound objects
@@ -65,23 +71,6 @@ struct NodeProgram {
 NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
                        const std::vector<SlotInfo>& outs, const std::vector<Value>& matrix_values,
                        bool count_reads = true);
-
-/// Producer -> consumer local pair that lower_local_chain can fuse: generic
-/// tap bodies (no median network), producer border Clamp / Constant, consumer
-/// Clamp, windows <= 7x7, intermediate stored as U8 / U16 / S16 / S32 / F32.
-bool local_chain_fusible(const AbstractionKernel& producer, const AbstractionKernel& consumer, ImageFormat mid);
-
-/// One kernel for local -> local: each 32x8 output tile first evaluates the
-/// producer (cast to the intermediate's storage format, exactly as its store)
-/// at every clamped position the consumer's windows read into shared memory,
-/// then the consumer reads its window over the intermediate from there.  The
-/// parameter block holds the producer's input slots, then the consumer's
-/// (`c_mid_slot` unbound: it is the on-chip intermediate), then the
-/// consumer's outputs.  The host counts both nodes' events statically.
-NodeProgram lower_local_chain(const AbstractionKernel& producer, const std::vector<SlotInfo>& p_ins,
-                              const std::vector<Value>& p_matrix, const SlotInfo& mid,
-                              const AbstractionKernel& consumer, const std::vector<SlotInfo>& c_ins, int c_mid_slot,
-                              const std::vector<SlotInfo>& c_outs, const std::vector<Value>& c_matrix);
 
 /// One node of a fused region (lower_region).
 struct RegionNode {

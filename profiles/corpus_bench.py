@@ -26,7 +26,7 @@ for name in names:
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"graph": name, "error": str(e)[:200]}), flush=True)
         continue
-    row = {"graph": name, "size": [W, H], "frames": F, "local_chains": os.environ.get("GVX_LOCAL_CHAINS", "0")}
+    row = {"graph": name, "size": [W, H], "frames": F, "regions": os.environ.get("GVX_NO_REGIONS") is None}
     for naive in (False, True):
         r = g.bench(naive=naive, frames=F, iters=10)
         px = W * H * F

@@ -51,16 +51,16 @@ def test_corpus_graph_matches_reference(path, gvx):
         assert launches[False] <= launches[True], (path.stem, variant, launches)
 
 
-@pytest.mark.parametrize("stem", ["sobel", "edge_fig1"])
-def test_generic_local_chain_runs_on_chip(stem, gvx, monkeypatch):
-    """Local -> local pairs outside the hand-written groups (Sobel-y feeding
-    Sobel-x + Magnitude, the Gaussian feeding Sobel + Magnitude + Threshold
-    after the reference fuser's merges) run as one NVRTC kernel whose
-    intermediate stays in shared memory, bit-exact with the reference."""
-    monkeypatch.setenv("GVX_LOCAL_CHAINS", "1")  # opt-in pass (see DESIGN.md §3)
+@pytest.mark.parametrize("stem", ["sobel", "harris", "tomasi"])
+def test_generic_regions_fuse_and_match_reference(stem, gvx):
+    """Graphs outside the hand-written groups fuse into generated regions
+    (convex DAG regions of point / local nodes as one kernel,
+    intermediates in shared memory): fewer launches than run_naive, outputs
+    bit-exact with the reference's."""
     gold = GOLDEN[stem]
     g = gvx.GraphFile((REPO / "examples" / f"{stem}.json").read_text())
-    assert " -> " in g.describe(), g.describe()
+    assert "region" in g.describe(), g.describe()
     outs, counters = g.run(naive=False, seed=gold["seed"])
     assert hashlib.sha256(blob(outs)).hexdigest() == gold["sha256"]
-    assert counters["kernel_launches"] == 1
+    _, naive = g.run(naive=True, seed=gold["seed"])
+    assert counters["kernel_launches"] < naive["kernel_launches"]

@@ -32,10 +32,3 @@ def test_reference_expr_and_graph_tests():
 
 def test_cpp_fusion_soundness_and_boundaries():
     _run(REPO / "tests" / "cpp" / "bin" / "test_graphvx")
-
-
-def test_cpp_fusion_soundness_with_local_chains():
-    """The same suite with the opt-in generic local -> local chains: the
-    random DAGs then run their local pairs as single on-chip kernels."""
-    import os
-    _run(REPO / "tests" / "cpp" / "bin" / "test_graphvx", env=dict(os.environ, GVX_LOCAL_CHAINS="1"))
