@@ -1803,19 +1803,69 @@ bool reads_window(const Expr& e, int slot) {
     return false;
 }
 
+namespace {
+bool window_offsets_zero(const Expr& e) {
+    if (e.op == ExprOp::WindowPixel && (e.dx != 0 || e.dy != 0)) return false;
+    for (const ExprPtr* c : {&e.a, &e.b, &e.c})
+        if (*c && !window_offsets_zero(**c)) return false;
+    return true;
+}
+/// A local tap body `mask(dx, dy) * g` or `g` whose g is a computation over
+/// window reads at the tap position alone (a point body the reference fuser
+/// inlined into the taps): g can be tabulated once per position.  Returns g
+/// (and the mask factor, or null) or null when the body does not qualify.
+const Expr* tabulated_g(const LocalKernel& lk, const Expr** mc_out) {
+    *mc_out = nullptr;
+    if (lk.median3x3 || !lk.tap_body) return nullptr;
+    const Expr& t = *lk.tap_body;
+    const Expr* g = &t;
+    const Expr* mc = nullptr;
+    if (t.op == ExprOp::Mul && t.a && t.b) {
+        if (t.a->op == ExprOp::MaskCoef && !uses_op(*t.b, ExprOp::MaskCoef)) mc = t.a.get(), g = t.b.get();
+        else if (t.b->op == ExprOp::MaskCoef && !uses_op(*t.a, ExprOp::MaskCoef)) mc = t.b.get(), g = t.a.get();
+    }
+    if (mc && (mc->dx != 0 || mc->dy != 0)) return nullptr;
+    if (uses_op(*g, ExprOp::MaskCoef) || uses_op(*g, ExprOp::InputPixel) || uses_op(*g, ExprOp::ArrayAt)) return nullptr;
+    if (g->op == ExprOp::WindowPixel || (g->op == ExprOp::Cast && g->a && g->a->op == ExprOp::WindowPixel)) return nullptr;
+    if (!window_offsets_zero(*g)) return nullptr;
+    *mc_out = mc;
+    return g;
+}
+} // namespace
+
 NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector<RegionObject>& objs,
                          const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs) {
     auto unsupported = [](const std::string& why) { return Error(ErrorCode::UnsupportedKind, "region: " + why); };
     for (const RegionObject& o : objs)
         if (!storage_ctype(o.format)) throw unsupported("intermediate format");
+    // nodes whose tap computation is tabulated per position (see tabulated_g)
+    std::vector<bool> tab(nodes.size(), false);
+    static const bool tab_on = std::getenv("GVX_REGION_TAB") != nullptr; // measured slower on the corpus
+    for (std::size_t ni = 0; ni < nodes.size() && tab_on; ++ni) {
+        if (nodes[ni].k->kind != AbstractionKind::Local) continue;
+        const Expr* mc = nullptr;
+        tab[ni] = tabulated_g(nodes[ni].k->local(), &mc) != nullptr;
+    }
+    auto node_halo = [&](std::size_t ni, int& hx, int& hy) {
+        hx = hy = 0;
+        for (int o : nodes[ni].out_obj)
+            if (o >= 0) hx = std::max(hx, objs[static_cast<std::size_t>(o)].halo_x), hy = std::max(hy, objs[static_cast<std::size_t>(o)].halo_y);
+    };
     // tile: 64 x 16 outputs per 256-thread block, halved while the shared
-    // memory of the intermediates exceeds 40 KB
+    // memory of the intermediates (and tabulated taps, 8 bytes each) exceeds 40 KB
     int TW = 64, TH = 16;
     auto smem_bytes = [&] {
         std::size_t b = 0;
         for (const RegionObject& o : objs)
             b += static_cast<std::size_t>(TW + 2 * o.halo_x) * (TH + 2 * o.halo_y) *
                  static_cast<std::size_t>(bytes_per_pixel(o.format));
+        for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
+            if (!tab[ni]) continue;
+            int hx = 0, hy = 0;
+            node_halo(ni, hx, hy);
+            const LocalKernel& lk = nodes[ni].k->local();
+            b += static_cast<std::size_t>(TW + 2 * hx + 2 * (lk.window_w / 2)) * (TH + 2 * hy + 2 * (lk.window_h / 2)) * 8;
+        }
         return b;
     };
     while (smem_bytes() > 40 * 1024 && (TW > 32 || TH > 8)) (TH > 8 ? TH : TW) /= 2;
@@ -1893,6 +1943,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         // in-image entries only (their taps then sit at constant offsets from
         // the entry); out-of-image entries replicate the clamped one below
         std::ostringstream nb;
+        std::string extra_base; // per-entry index of a tabulated tap array
         std::fill(used_obj.begin(), used_obj.end(), false);
         auto put = [&](int o, const Emitter::TV& v) {
             if (v.t != 'd' && orange[static_cast<std::size_t>(o)].t != 'd') {
@@ -1931,6 +1982,60 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
             em.mask = lk.mask.empty() ? &rn.matrix : &lk.mask;
             em.mode = Emitter::Mode::Tap;
             const int hw = lk.window_w / 2, hh = lk.window_h / 2;
+            const Expr* mc = nullptr;
+            const Expr* gexp = tab[ni] ? tabulated_g(lk, &mc) : nullptr;
+            std::vector<Emitter::TV> gtaps;
+            if (gexp) {
+                // g once per position of the node's region + its window radius
+                const int GW = rw(oref) + 2 * hw, GH = rh(oref) + 2 * hh;
+                const std::string gx0 = "(tx0 - " + std::to_string(R.halo_x + hw) + ")",
+                                  gy0 = "(ty0 - " + std::to_string(R.halo_y + hh) + ")";
+                em.mode = Emitter::Mode::Tap;
+                em.tdx = em.tdy = 0;
+                std::fill(used_obj.begin(), used_obj.end(), false);
+                Emitter::TV gv;
+                if (!em.temit(*gexp, gv)) throw unsupported("run-time typed tap computation");
+                const char* gty = gv.t == 'd' ? "double" : gv.t == 'l' ? "i64" : "int";
+                const std::string ga = "gk" + std::to_string(ni);
+                body << "  // node " << ni << " tap computation, tabulated\n"
+                     << "  __shared__ " << gty << " " << ga << "[" << GW * GH << "];\n"
+                     << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << GW * GH
+                     << "; e += blockDim.x * blockDim.y) {\n"
+                     << "    const int ry = e / " << GW << ", rx = e - ry * " << GW << ";\n"
+                     << "    const int px = " << gx0 << " + rx, py = " << gy0 << " + ry;\n";
+                if (lk.boundary == BoundaryMode::Undefined)
+                    body << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
+                else
+                    body << "    if (px < -" << hw << " || py < -" << hh << " || px >= W + " << hw << " || py >= H + "
+                         << hh << ") continue;\n";
+                for (std::size_t o = 0; o < objs.size(); ++o)
+                    if (used_obj[o])
+                        body << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * "
+                             << rw(static_cast<int>(o)) << " + px - tx0 + " << objs[o].halo_x << ";\n";
+                body << "    " << ga << "[e] = (" << gty << ")(" << gv.c << ");\n  }\n  __syncthreads();\n";
+                std::fill(used_obj.begin(), used_obj.end(), false);
+                extra_base = "    const int bG = (py - " + gy0 + ") * " + std::to_string(GW) + " + px - " + gx0 + ";\n";
+                const std::vector<Value>& mask = lk.mask.empty() ? rn.matrix : lk.mask;
+                for (int dy = -hh; dy <= hh; ++dy)
+                    for (int dx = -hw; dx <= hw; ++dx) {
+                        Emitter::TV gt = gv;
+                        gt.c = ga + "[bG + (" + std::to_string(dy * GW + dx) + ")]";
+                        if (!mc) {
+                            gtaps.push_back(gt);
+                            continue;
+                        }
+                        const std::size_t mi = static_cast<std::size_t>((dy + hh) * lk.window_w + dx + hw);
+                        if (mi >= mask.size()) throw unsupported("mask size");
+                        const Emitter::TV cf = Emitter::tvalue(mask[mi]);
+                        if (mask[mi].real || gt.t == 'd') {
+                            gtaps.push_back(Emitter::tdbl("__dmul_rn(" + Emitter::as_dbl(cf) + ", " + Emitter::as_dbl(gt) + ")"));
+                        } else {
+                            const __int128 pr[4] = {cf.lo * gt.lo, cf.lo * gt.hi, cf.hi * gt.lo, cf.hi * gt.hi};
+                            gtaps.push_back(Emitter::tbin_int("*", cf, gt, std::min({pr[0], pr[1], pr[2], pr[3]}),
+                                                              std::max({pr[0], pr[1], pr[2], pr[3]})));
+                        }
+                    }
+            }
             if (lk.boundary == BoundaryMode::Undefined) {
                 Emitter::TV z = Emitter::tint("0", 0, 0);
                 nb << "    if (px < " << hw << " || py < " << hh << " || px >= W - " << hw << " || py >= H - " << hh
@@ -1939,7 +2044,8 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                     if (o >= 0) put(o, z);
                 nb << "      continue;\n    }\n";
             }
-            const std::string taps = typed_taps(em, lk);
+            em.mode = Emitter::Mode::Tap;
+            const std::string taps = gexp ? typed_combine(em, lk, gtaps) : typed_taps(em, lk);
             if (taps.empty()) throw unsupported("run-time typed tap body");
             em.tdx = em.tdy = 0;
             em.mode = Emitter::Mode::Post;
@@ -1959,9 +2065,9 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
              << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
         for (std::size_t o = 0; o < objs.size(); ++o)
             if (used_obj[o])
-                body << "    const int b" << o << " = (ry + " << objs[o].halo_y - R.halo_y << ") * " << rw(static_cast<int>(o))
-                     << " + rx + " << objs[o].halo_x - R.halo_x << ";\n";
-        body << nb.str() << "  }\n  __syncthreads();\n";
+                body << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))
+                     << " + px - tx0 + " << objs[o].halo_x << ";\n";
+        body << extra_base << nb.str() << "  }\n  __syncthreads();\n";
         // out-of-image entries = the entry at the clamped position (border tiles)
         for (int o : rn.out_obj) {
             if (o < 0) continue;
