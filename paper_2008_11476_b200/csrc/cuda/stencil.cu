@@ -631,15 +631,18 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         };
 #pragma unroll
         for (int j = 0; j < K - 1; ++j) row(j, j);
-        for (int O = 0; O < n; O += K) {
+        auto block = [&](int O, auto checked) { // K output rows O .. O+K-1 (O a multiple of K)
 #pragma unroll
             for (int t = 0; t < K; ++t) {
-                if (O + t >= n) break;
-                row(O + t + K - 1, (t + K - 1) % K); // O is a multiple of K
+                if (decltype(checked)::value && O + t >= n) break;
+                row(O + t + K - 1, (t + K - 1) % K);
                 if constexpr (kLoad == 3) emit(vsum((t + K - 1) % K));
-                else emit(acc[t]);                   // output o = O + t
+                else emit(acc[t]); // output o = O + t
             }
-        }
+        };
+        int O = 0;
+        for (; O + K <= n; O += K) block(O, std::false_type{}); // whole blocks: no row checks
+        if (O < n) block(O, std::true_type{});
         if (kMode >= 2 && have_pend) {
             count(pend.e.x, 0);
             count(pend.o.x, 1);
