@@ -1912,9 +1912,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         staged = true;
         const int f = field_in(objs[o].load);
         const char* ct = storage_ctype(objs[o].format);
-        body << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << rw(static_cast<int>(o)) * rh(static_cast<int>(o))
-             << "; e += blockDim.x * blockDim.y) {\n"
-             << "    const int ry = e / " << rw(static_cast<int>(o)) << ", rx = e - ry * " << rw(static_cast<int>(o)) << ";\n"
+        body << "  for (int ry = threadIdx.y; ry < " << (rw(static_cast<int>(o)) * rh(static_cast<int>(o))) / (rw(static_cast<int>(o))) << "; ry += 8)\n" << "  #pragma unroll\n" << "  for (int ix = 0; ix < " << ((rw(static_cast<int>(o))) + 31) / 32 << "; ++ix) {\n" << "    const int rx = threadIdx.x + 32 * ix;\n" << "    if (rx >= " << (rw(static_cast<int>(o))) << ") break;\n" << "    const int e = ry * " << (rw(static_cast<int>(o))) << " + rx;\n"
              << "    const int x = clampi(tx0 - " << objs[o].halo_x << " + rx, 0, W - 1), y = clampi(ty0 - "
              << objs[o].halo_y << " + ry, 0, H - 1);\n"
              << "    ro" << o << "[e] = ((const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
@@ -1999,9 +1997,12 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                 const std::string ga = "gk" + std::to_string(ni);
                 body << "  // node " << ni << " tap computation, tabulated\n"
                      << "  __shared__ " << gty << " " << ga << "[" << GW * GH << "];\n"
-                     << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << GW * GH
-                     << "; e += blockDim.x * blockDim.y) {\n"
-                     << "    const int ry = e / " << GW << ", rx = e - ry * " << GW << ";\n"
+                     << "  for (int ry = threadIdx.y; ry < " << (GW * GH) / (GW) << "; ry += 8)\n"
+                     << "  #pragma unroll\n"
+                     << "  for (int ix = 0; ix < " << ((GW) + 31) / 32 << "; ++ix) {\n"
+                     << "    const int rx = threadIdx.x + 32 * ix;\n"
+                     << "    if (rx >= " << (GW) << ") break;\n"
+                     << "    const int e = ry * " << (GW) << " + rx;\n"
                      << "    const int px = " << gx0 << " + rx, py = " << gy0 << " + ry;\n";
                 if (lk.boundary == BoundaryMode::Undefined)
                     body << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
@@ -2058,9 +2059,12 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
             throw unsupported("node kind");
         }
         body << "  // node " << ni << ": " << k.name << "\n"
-             << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << rw(oref) * rh(oref)
-             << "; e += blockDim.x * blockDim.y) {\n"
-             << "    const int ry = e / " << rw(oref) << ", rx = e - ry * " << rw(oref) << ";\n"
+             << "  for (int ry = threadIdx.y; ry < " << (rw(oref) * rh(oref)) / (rw(oref)) << "; ry += 8)\n"
+             << "  #pragma unroll\n"
+             << "  for (int ix = 0; ix < " << ((rw(oref)) + 31) / 32 << "; ++ix) {\n"
+             << "    const int rx = threadIdx.x + 32 * ix;\n"
+             << "    if (rx >= " << (rw(oref)) << ") break;\n"
+             << "    const int e = ry * " << (rw(oref)) << " + rx;\n"
              << "    const int px = tx0 - " << R.halo_x << " + rx, py = ty0 - " << R.halo_y << " + ry;\n"
              << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
         for (std::size_t o = 0; o < objs.size(); ++o)
@@ -2074,9 +2078,12 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
             const RegionObject& O = objs[static_cast<std::size_t>(o)];
             body << "  if (tx0 - " << O.halo_x << " < 0 || ty0 - " << O.halo_y << " < 0 || tx0 + " << TW + O.halo_x
                  << " > W || ty0 + " << TH + O.halo_y << " > H) {\n"
-                 << "    for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << rw(o) * rh(o)
-                 << "; e += blockDim.x * blockDim.y) {\n"
-                 << "      const int ry = e / " << rw(o) << ", rx = e - ry * " << rw(o) << ";\n"
+                 << "    for (int ry = threadIdx.y; ry < " << (rw(o) * rh(o)) / (rw(o)) << "; ry += 8)\n"
+                 << "    #pragma unroll\n"
+                 << "    for (int ix = 0; ix < " << ((rw(o)) + 31) / 32 << "; ++ix) {\n"
+                 << "      const int rx = threadIdx.x + 32 * ix;\n"
+                 << "      if (rx >= " << (rw(o)) << ") break;\n"
+                 << "      const int e = ry * " << (rw(o)) << " + rx;\n"
                  << "      const int x = tx0 - " << O.halo_x << " + rx, y = ty0 - " << O.halo_y << " + ry;\n"
                  << "      if (x >= 0 && y >= 0 && x < W && y < H) continue;\n"
                  << "      ro" << o << "[e] = ro" << o << "[(clampi(y, 0, H - 1) - ty0 + " << O.halo_y << ") * " << rw(o)
@@ -2090,9 +2097,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     for (std::size_t o = 0; o < objs.size(); ++o) {
         if (objs[o].store < 0) continue;
         const int f = field_in(static_cast<int>(ins.size()) + objs[o].store);
-        body << "  for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < " << TW * TH
-             << "; e += blockDim.x * blockDim.y) {\n"
-             << "    const int ry = e / " << TW << ", rx = e - ry * " << TW << ";\n"
+        body << "  for (int ry = threadIdx.y; ry < " << (TW * TH) / (TW) << "; ry += 8)\n" << "  #pragma unroll\n" << "  for (int ix = 0; ix < " << ((TW) + 31) / 32 << "; ++ix) {\n" << "    const int rx = threadIdx.x + 32 * ix;\n" << "    if (rx >= " << (TW) << ") break;\n" << "    const int e = ry * " << (TW) << " + rx;\n"
              << "    const int gx = tx0 + rx, gy = ty0 + ry;\n    if (gx >= W || gy >= ROW1) continue;\n"
              << "    " << storage_ctype(objs[o].format) << "* row = (" << storage_ctype(objs[o].format)
              << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2 << "] + (u64)gy * p.f[" << f + 1
