@@ -1912,11 +1912,16 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         staged = true;
         const int f = field_in(objs[o].load);
         const char* ct = storage_ctype(objs[o].format);
-        body << "  for (int ry = threadIdx.y; ry < " << (rw(static_cast<int>(o)) * rh(static_cast<int>(o))) / (rw(static_cast<int>(o))) << "; ry += 8)\n" << "  #pragma unroll\n" << "  for (int ix = 0; ix < " << ((rw(static_cast<int>(o))) + 31) / 32 << "; ++ix) {\n" << "    const int rx = threadIdx.x + 32 * ix;\n" << "    if (rx >= " << (rw(static_cast<int>(o))) << ") break;\n" << "    const int e = ry * " << (rw(static_cast<int>(o))) << " + rx;\n"
-             << "    const int x = clampi(tx0 - " << objs[o].halo_x << " + rx, 0, W - 1), y = clampi(ty0 - "
-             << objs[o].halo_y << " + ry, 0, H - 1);\n"
-             << "    ro" << o << "[e] = ((const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
-             << f + 2 << "] + (u64)y * p.f[" << f + 1 << "]))[x];\n  }\n";
+        const int RWo = rw(static_cast<int>(o)), RHo = rh(static_cast<int>(o));
+        // one row pointer per entry row; 32-column blocks unrolled
+        body << "  for (int ry = threadIdx.y; ry < " << RHo << "; ry += 8) {\n"
+             << "    const int y = clampi(ty0 - " << objs[o].halo_y << " + ry, 0, H - 1);\n"
+             << "    const " << ct << "* src = (const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
+             << f + 2 << "] + (u64)y * p.f[" << f + 1 << "]);\n"
+             << "#pragma unroll\n    for (int ix = 0; ix < " << (RWo + 31) / 32 << "; ++ix) {\n"
+             << "      const int rx = threadIdx.x + 32 * ix;\n      if (rx >= " << RWo << ") break;\n"
+             << "      ro" << o << "[ry * " << RWo << " + rx] = src[clampi(tx0 - " << objs[o].halo_x
+             << " + rx, 0, W - 1)];\n    }\n  }\n";
     }
     if (staged) body << "  __syncthreads();\n";
     for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
@@ -2097,12 +2102,15 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     for (std::size_t o = 0; o < objs.size(); ++o) {
         if (objs[o].store < 0) continue;
         const int f = field_in(static_cast<int>(ins.size()) + objs[o].store);
-        body << "  for (int ry = threadIdx.y; ry < " << (TW * TH) / (TW) << "; ry += 8)\n" << "  #pragma unroll\n" << "  for (int ix = 0; ix < " << ((TW) + 31) / 32 << "; ++ix) {\n" << "    const int rx = threadIdx.x + 32 * ix;\n" << "    if (rx >= " << (TW) << ") break;\n" << "    const int e = ry * " << (TW) << " + rx;\n"
-             << "    const int gx = tx0 + rx, gy = ty0 + ry;\n    if (gx >= W || gy >= ROW1) continue;\n"
-             << "    " << storage_ctype(objs[o].format) << "* row = (" << storage_ctype(objs[o].format)
-             << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2 << "] + (u64)gy * p.f[" << f + 1
-             << "]);\n    row[gx] = ro" << o << "[(ry + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))
-             << " + rx + " << objs[o].halo_x << "];\n  }\n";
+        const char* ct = storage_ctype(objs[o].format);
+        body << "  for (int ry = threadIdx.y; ry < " << TH << "; ry += 8) {\n"
+             << "    const int gy = ty0 + ry;\n    if (gy >= ROW1) break;\n"
+             << "    " << ct << "* row = (" << ct << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
+             << "] + (u64)gy * p.f[" << f + 1 << "]);\n"
+             << "#pragma unroll\n    for (int ix = 0; ix < " << TW / 32 << "; ++ix) {\n"
+             << "      const int rx = threadIdx.x + 32 * ix, gx = tx0 + rx;\n      if (gx >= W) break;\n"
+             << "      row[gx] = ro" << o << "[(ry + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o)) << " + rx + "
+             << objs[o].halo_x << "];\n    }\n  }\n";
     }
     body << "  (void)rd;\n}\n";
     KernelSpec ks;
