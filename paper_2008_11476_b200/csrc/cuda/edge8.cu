@@ -83,15 +83,15 @@ __device__ __forceinline__ float e8_sqrt_approx(float x) {
 /// rounded root k*, so k0 = floor(s / 16) (one FFMA2 rounding down into the
 /// magic range) is k* or k* - 1, and k* = k0 + (n > k0 (k0 + 1)).  With
 /// v = 16 k0 + 8, u = v^2 - n64 = 256 (k0 (k0 + 1) - n) is exact (multiples
-/// of 64 below 2^30) and negative exactly when the increment applies; its
-/// sign bit is added to the magic form's low bits (an ALU op).
+/// of 64 below 2^30) and negative exactly when the increment applies.  The
+/// increment is one more packed FMA rounding upward: km - u 2^-21 with
+/// |u| 2^-21 < 1 rounds to km + 1 for u < 0 and to km otherwise (ulp(km) = 1).
 __device__ __forceinline__ float2 e8_round_sqrt16(float2 n64) {
     const float2 s = f2(e8_sqrt_approx(n64.x), e8_sqrt_approx(n64.y));
     const float2 km = __ffma2_rd(s, f2(0.0625f, 0.0625f), f2(8388608.f, 8388608.f)); // 2^23 + k0
     const float2 v = __ffma2_rn(km, f2(16.f, 16.f), f2(-134217720.f, -134217720.f)); // 16 k0 + 8 (2^27 - 8 is exact)
     const float2 u = __ffma2_rn(v, v, f2(-n64.x, -n64.y));
-    return f2(__uint_as_float(__float_as_uint(km.x) + (__float_as_uint(u.x) >> 31)),
-              __uint_as_float(__float_as_uint(km.y) + (__float_as_uint(u.y) >> 31)));
+    return __ffma2_ru(u, f2(-4.76837158203125e-07f, -4.76837158203125e-07f), km); // 2^23 + k*
 }
 
 /// 16-bit lane `hi` of a SWAR word as the float 2^23 + lane (one permute).
