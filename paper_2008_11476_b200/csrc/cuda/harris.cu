@@ -71,7 +71,7 @@ struct HarrisParams {
 struct Q8 {
     float2 v[4];
 };
-/// Source pairs for i = -1 .. 4 at v[i + 1].
+/// Source pairs for i = -1 .. 4 at v[i + 1] (magic floats 2^15 + x).
 struct Raw8 {
     float2 v[6];
 };
@@ -88,6 +88,12 @@ __device__ __forceinline__ Prod3 padd(const Prod3& a, const Prod3& b) {
     return Prod3{q8add(a.xx, b.xx), q8add(a.yy, b.yy), q8add(a.xy, b.xy)};
 }
 __device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
+
+/// 2^15 + byte k of w (the float bit pattern 0x4700bb00; ulp 2^-8): sums of
+/// four of them stay below 2^17 + 2^10, where integers are still exact.
+__device__ __forceinline__ float magic15_byte(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x47000000u, 0x7404u | (static_cast<unsigned>(k) << 4)));
+}
 
 /// The reference's exact expression for one pixel from the exact box sums.
 __device__ __forceinline__ float exact_response(float sxx, float syy, float sxy, double k) {
@@ -210,35 +216,31 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
     // product columns); interior strips run without those selects
     auto body = [&](auto edge_tag) {
         constexpr bool kEdge = decltype(edge_tag)::value;
-        /// Source row j as magic floats 2^23 + x (byte permutes only): pairs
-        /// for i = -1 .. 4.  Every use is a difference of two of them, where
-        /// the 2^23 cancels exactly.
+        /// Source row j as magic floats 2^15 + x (byte permutes only): pairs
+        /// for i = -1 .. 4.  Every use ends in a difference of two rows or
+        /// columns, where the 2^15 terms cancel exactly.
         auto raw_pairs = [&](int j) {
             const uint8_t* row = ring + (j % kHarRing) * kHarSW + off;
             const uint2 lo = lds64(row - 4), hi = lds64(row + 4); // columns c-4 .. c+3, c+4 .. c+11
             Raw8 r;
-            r.v[0] = f2(magic_byte(lo.x, 3), magic_byte(lo.y, 3));
-            r.v[1] = f2(magic_byte(lo.y, 0), magic_byte(hi.x, 0));
-            r.v[2] = f2(magic_byte(lo.y, 1), magic_byte(hi.x, 1));
-            r.v[3] = f2(magic_byte(lo.y, 2), magic_byte(hi.x, 2));
-            r.v[4] = f2(magic_byte(lo.y, 3), magic_byte(hi.x, 3));
-            r.v[5] = f2(magic_byte(hi.x, 0), magic_byte(hi.y, 0));
+            r.v[0] = f2(magic15_byte(lo.x, 3), magic15_byte(lo.y, 3));
+            r.v[1] = f2(magic15_byte(lo.y, 0), magic15_byte(hi.x, 0));
+            r.v[2] = f2(magic15_byte(lo.y, 1), magic15_byte(hi.x, 1));
+            r.v[3] = f2(magic15_byte(lo.y, 2), magic15_byte(hi.x, 2));
+            r.v[4] = f2(magic15_byte(lo.y, 3), magic15_byte(hi.x, 3));
+            r.v[5] = f2(magic15_byte(hi.x, 0), magic15_byte(hi.y, 0));
             return r;
         };
         /// Sobel-x row term D = in(x+1) - in(x-1).
         auto sobel_d = [&](const Raw8& q) {
             return Q8{{sub2(q.v[2], q.v[0]), sub2(q.v[3], q.v[1]), sub2(q.v[4], q.v[2]), sub2(q.v[5], q.v[3])}};
         };
-        /// Sobel-y of the row between source rows j and j-2: vertical
-        /// difference first (the 2^23 cancels exactly), then the 1-2-1
-        /// smoothing across columns.
-        auto sobel_y = [&](const Raw8& q, const Raw8& m) {
-            float2 d[6];
-#pragma unroll
-            for (int i = 0; i < 6; ++i) d[i] = sub2(q.v[i], m.v[i]);
+        /// Horizontal 1-2-1 smoothing S of a source row (values 2^17 + s,
+        /// exact); Sobel-y of row j-1 is S(j) - S(j-2).
+        auto smooth = [&](const Raw8& q) {
             Q8 g;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) g.v[i] = fma2(two, d[i + 1], add2(d[i], d[i + 2]));
+            for (int i = 0; i < 4; ++i) g.v[i] = fma2(two, q.v[i + 1], add2(q.v[i], q.v[i + 2]));
             return g;
         };
         /// Columns beyond W-1 take column W-1's value; at the left border the
@@ -387,14 +389,15 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
         // 2x-unrolled loop renames instead of moving registers.
         struct State {
             Q8 Dp, Qp;   // D(r-1), Q(r-1)
-            Raw8 Raw;    // source pairs of the row this copy last consumed
+            Q8 S;        // smoothing S of the source row this copy last consumed
             Prod3 P, Hp; // P(m-1), H(m-1)
         };
         State A, B;
         {
-            B.Raw = raw_pairs(0); // the copies alternate, so each holds row j-2 when step j reads it
-            A.Raw = raw_pairs(1);
-            const Q8 D0 = sobel_d(B.Raw), D1 = sobel_d(A.Raw);
+            const Raw8 r0 = raw_pairs(0), r1 = raw_pairs(1);
+            B.S = smooth(r0); // the copies alternate, so each holds row j-2 when step j reads it
+            A.S = smooth(r1);
+            const Q8 D0 = sobel_d(r0), D1 = sobel_d(r1);
             A.Qp = q8add(D0, D1);
             A.Dp = D1;
         }
@@ -402,8 +405,11 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
         auto sobel_step = [&](int j, const State& i, State& o) {
             const Raw8 q = raw_pairs(j);
             const Q8 D = sobel_d(q);
-            const Q8 gy = sobel_y(q, o.Raw); // o.Raw = source row j-2
-            o.Raw = q;
+            const Q8 S = smooth(q);
+            Q8 gy;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) gy.v[t] = sub2(S.v[t], o.S.v[t]); // o.S = S of source row j-2
+            o.S = S;
             o.Qp = q8add(i.Dp, D);
             o.Dp = D;
             return products(q8add(i.Qp, o.Qp), gy);
@@ -420,6 +426,17 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
             emit(padd(i.P, Hn));
             o.P = padd(i.Hp, Hn);
             o.Hp = Hn;
+        };
+        /// Two rows: box(o) = P + H1, box(o+1) = Hp + (H1 + H2), and the
+        /// pair sum H1 + H2 is the next P (3 vertical adds per 2 rows).
+        /// The box state stays in A.
+        auto pair_step = [&](int j) {
+            const Prod3 H1 = sobel_step(j, A, B);
+            emit(padd(A.P, H1));
+            const Prod3 H2 = sobel_step(j + 1, B, A);
+            A.P = padd(H1, H2);
+            emit(padd(A.Hp, A.P));
+            A.Hp = H2;
         };
         auto last_step = [&](int j, const State& i, State& o) {
             // product row H clamps to row H-1 at the bottom border
@@ -439,8 +456,7 @@ __global__ void __launch_bounds__(kHarThreads, GVX_HARRIS_MINB) harris_kernel(co
             }
         for (; j + 2 < steps; j += 2) {
             if (j % kHarChunk == 0) next_chunk(j / kHarChunk);
-            full_step(j, A, B);
-            full_step(j + 1, B, A);
+            pair_step(j);
         }
         if (j % kHarChunk == 0) next_chunk(j / kHarChunk);
         if (j + 1 < steps) {
