@@ -129,6 +129,10 @@ class BandGroup;
 /// single-image result bit for bit.  The exchange overlaps the interior rows,
 /// which read owned rows only.  Programs must consist of hand-written
 /// stencil groups over images of one size (Error(UnsupportedKind) otherwise).
+namespace detail {
+struct BandAccess;
+}
+
 class BandedSession {
 public:
     BandedSession(const OptimizedPlan& plan, int rank, int world, void* comm = nullptr, int device = -1,
@@ -163,6 +167,21 @@ public:
     /// host memory (gvxb_host_alloc / gvxb_host_register) DMAs at full rate.
     void run_host(const void* src, std::size_t src_pitch, ObjectId output, void* dst, std::size_t dst_pitch,
                   int piece_rows = 1024);
+    /// Packed host rows of one image (W * bytes-per-pixel per row): the
+    /// input slab's rows, or an output's band rows.  Pageable memory is
+    /// staged through page-locked slots; `drain` (outputs with page-locked
+    /// `host` only) receives a copy of each piece as soon as it has landed.
+    struct HostRows {
+        ObjectId id = kInvalidId;
+        void* host = nullptr;
+        bool page_locked = false;
+        void* drain = nullptr;
+    };
+    /// As run_host for the program's single input and any of its image
+    /// outputs, with pageable or page-locked host rows (host copies of one
+    /// piece overlap the transfers and kernel of the others).  Returns the
+    /// device-counted pixel reads of the execution.
+    long long run_host_rows(const HostRows& input, const std::vector<HostRows>& outputs, int piece_rows = 1024);
     int launches_per_run() const;
     std::string describe() const;
 
@@ -170,6 +189,8 @@ public:
 
 private:
     friend class BandGroup;
+    friend struct detail::BandAccess;
+    BandedSession();
     std::unique_ptr<Impl> impl_;
 };
 

@@ -305,12 +305,18 @@ class ConfigGraph:
         dt = CONFIG_OUTPUT[self.cfg]
         return None if dt is None else np.empty((self.height, self.width), dt)
 
-    def run_host(self, image: np.ndarray, naive: bool = False):
+    def run_host(self, image: np.ndarray, naive: bool = False, out: np.ndarray | None = None):
         """run_plan / run_naive with host buffers.  Returns (result, counters)
-        where result is the output plane, or (hist, mean, stddev) for cfg4."""
+        where result is the output plane (written into `out` when given: a
+        caller reusing one destination array across frames), or (hist, mean,
+        stddev) for cfg4."""
         img = np.ascontiguousarray(image, dtype=np.uint8)
         assert img.shape == (self.height, self.width)
-        out = self.output_array()
+        if out is None:
+            out = self.output_array()
+        else:
+            assert out.shape == (self.height, self.width) and out.dtype == np.dtype(CONFIG_OUTPUT[self.cfg])
+            assert out.flags.c_contiguous
         hist = (ctypes.c_longlong * 256)()
         stats = (ctypes.c_double * 2)()
         counters = (ctypes.c_longlong * 4)()

@@ -166,6 +166,10 @@ int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, l
             if (!g->registered.count(g->input.bytes.data())) // not page-locked: copy up front
                 gvx::dev::parallel_copy(g->input.bytes.data(), in, g->input.bytes.size()), fill.src = nullptr;
         }
+        if (out && g->cfg != 4) { // the caller's destination may be filled piece by piece during the run
+            fill.drain_id = g->cg.outputs.at(0);
+            fill.drain_dst = out;
+        }
         // recycle the previous run's (page-locked) output vectors
         for (auto& [id, b] : g->last.outputs)
             if (b.desc.kind == gvx::ObjKind::Image && !b.bytes.empty()) {
@@ -184,7 +188,7 @@ int gvxc_graph_run_host(gvxc_graph g, int naive, const uint8_t* in, void* out, l
             throw;
         }
         g->input = std::move(slot);
-        copy_outputs(g, r.outputs, out, hist, stats);
+        copy_outputs(g, r.outputs, fill.drained ? nullptr : out, hist, stats);
         if (counters) {
             counters[0] = r.counters.kernel_launches;
             counters[1] = r.counters.pixels_read;

@@ -13,6 +13,7 @@
 // run meanwhile: they read owned rows only).
 #include "graphvx/device.hpp"
 #include "graphvx/error.hpp"
+#include "hostcopy.hpp"
 #include "program.hpp"
 
 #include <algorithm>
@@ -106,6 +107,10 @@ struct BandedSession::Impl {
             if (kv.second.owned) gvxb_free(ctx, kv.second.ptr);
         for (void* e : ev_up) gvxb_event_destroy(e);
         for (void* e : ev_k) gvxb_event_destroy(e);
+        for (void* e : ev_dn) gvxb_event_destroy(e);
+        for (void* e : ev_in_free) gvxb_event_destroy(e);
+        for (void* q : stage_in) gvxb_host_free(q);
+        for (void* q : stage_out) gvxb_host_free(q);
         if (ev_ready) gvxb_event_destroy(ev_ready);
         if (ev_xdone) gvxb_event_destroy(ev_xdone);
         for (gvxb_ctx c : {up, dn, xctx, ctx})
@@ -113,7 +118,12 @@ struct BandedSession::Impl {
     }
 
     void init(const OptimizedPlan& plan, int rank_, int world_, void* comm_, int device_, int frames_) {
-        prog = dev::program_of(plan);
+        init_program(dev::program_of(plan), rank_, world_, comm_, device_, frames_);
+    }
+
+    void init_program(std::shared_ptr<dev::Program> prog_, int rank_, int world_, void* comm_, int device_,
+                      int frames_) {
+        prog = std::move(prog_);
         rank = rank_;
         world = world_;
         frames = std::max(1, frames_);
@@ -430,6 +440,140 @@ struct BandedSession::Impl {
         check(gvxb_sync(ctx), "band compute sync");
     }
 
+    // staging rings of run_host_rows (page-locked, one slot per piece in flight)
+    static constexpr int kSlots = 3;
+    std::vector<void*> stage_in, stage_out; ///< kSlots each (stage_out: kSlots per output)
+    std::size_t stage_in_bytes = 0, stage_out_bytes = 0;
+    std::vector<void*> ev_in_free, ev_dn;
+
+    void* staging(std::vector<void*>& ring, std::size_t& have, std::size_t idx, std::size_t bytes, std::size_t count) {
+        if (have < bytes || ring.size() < count) {
+            check(gvxb_sync(up), "staging sync");
+            check(gvxb_sync(dn), "staging sync");
+            for (void* q : ring) gvxb_host_free(q);
+            ring.assign(count, nullptr);
+            for (void*& q : ring) check(gvxb_host_alloc(bytes, &q), "pinned staging allocation");
+            have = bytes;
+        }
+        return ring[idx];
+    }
+
+    /// run_host for host rows that may be pageable: input rows are copied
+    /// into a page-locked slot (or DMA'd directly when page-locked), output
+    /// rows come back through page-locked slots (or directly), each piece's
+    /// host copies overlapping the DMA and kernel of its neighbours.  `drain`
+    /// (optional, per output) is a second destination filled from a
+    /// page-locked `dst` piece by piece.  Returns the device read counter.
+    long long run_host_rows(const BandedSession::HostRows& in_rows, const std::vector<BandedSession::HostRows>& outs,
+                            int piece) {
+        if (prog->units.size() != 1)
+            throw Error(ErrorCode::UnsupportedKind, "BandedSession::run_host_rows needs a single-group program");
+        const dev::Unit& u = prog->units[0];
+        if (unit_ins[0].size() != 1 || unit_ins[0][0].first != in_rows.id)
+            throw Error(ErrorCode::UnsupportedKind, "BandedSession::run_host_rows needs the program's single input");
+        const Slab& in = slabs.at(in_rows.id);
+        const int R = unit_ins[0][0].second;
+        piece = std::max(piece, 1);
+        std::vector<std::pair<int, int>> pieces;
+        for (int a = band.row0; a < band.row1; a += piece) pieces.emplace_back(a, std::min(band.row1, a + piece));
+        ensure_pipeline(pieces.size());
+        while (ev_dn.size() < pieces.size()) {
+            void* e = nullptr;
+            check(gvxb_event_create(&e), "event");
+            ev_dn.push_back(e);
+        }
+        while (ev_in_free.size() < static_cast<std::size_t>(kSlots)) {
+            void* e = nullptr;
+            check(gvxb_event_create(&e), "event");
+            ev_in_free.push_back(e);
+        }
+        std::vector<const Slab*> oslab;
+        for (const auto& o : outs) oslab.push_back(&slabs.at(o.id));
+        check(gvxb_status_reset(ctx), "status reset");
+        const std::size_t in_row = static_cast<std::size_t>(W) * in.bpp;
+        const std::size_t max_in = static_cast<std::size_t>(piece + 2 * R) * in_row;
+        std::size_t max_out = 0;
+        for (const Slab* o : oslab) max_out = std::max(max_out, static_cast<std::size_t>(piece) * W * o->bpp);
+        const auto* src = static_cast<const std::uint8_t*>(in_rows.host);
+        bool in_used[kSlots] = {false, false, false};
+        std::size_t drained = 0; // pieces whose outputs are in their final host place
+        auto drain = [&](std::size_t j) {
+            const auto [a0, a1] = pieces[j];
+            check(gvxb_event_sync(ev_dn[j]), "piece download wait");
+            for (std::size_t o = 0; o < outs.size(); ++o) {
+                const std::size_t row = static_cast<std::size_t>(W) * oslab[o]->bpp;
+                const std::size_t off = static_cast<std::size_t>(a0 - band.row0) * row, n = (a1 - a0) * row;
+                auto* dst = static_cast<std::uint8_t*>(outs[o].host);
+                if (!outs[o].page_locked) {
+                    const void* slot = stage_out[(j % kSlots) * outs.size() + o];
+                    dev::parallel_copy(dst + off, slot, n);
+                } else if (outs[o].drain) {
+                    dev::parallel_copy(static_cast<std::uint8_t*>(outs[o].drain) + off, dst + off, n);
+                }
+            }
+        };
+        int uploaded = in.row0;
+        const int in_end = in.row0 + in.rows;
+        for (std::size_t k = 0; k < pieces.size(); ++k) {
+            const auto [a0, a1] = pieces[k];
+            const int hi = std::min(in_end, a1 + R);
+            if (hi > uploaded) {
+                const std::size_t n = static_cast<std::size_t>(hi - uploaded);
+                const std::uint8_t* from = src + static_cast<std::size_t>(uploaded - in.row0) * in_row;
+                if (!in_rows.page_locked) {
+                    const int slot = static_cast<int>(k % kSlots);
+                    void* st = staging(stage_in, stage_in_bytes, slot, max_in, kSlots);
+                    if (in_used[slot]) check(gvxb_event_sync(ev_in_free[slot]), "staging wait");
+                    dev::parallel_copy(st, from, n * in_row, /*streaming=*/true);
+                    from = static_cast<const std::uint8_t*>(st);
+                    in_used[slot] = true;
+                }
+                check(gvxb_upload_2d(up, static_cast<char*>(in.ptr) + static_cast<std::int64_t>(uploaded - in.row0) * in.pitch,
+                                     static_cast<std::size_t>(in.pitch), from, in_row, in_row, n),
+                      "band piece upload");
+                if (!in_rows.page_locked) check(gvxb_event_record(up, ev_in_free[k % kSlots]), "event");
+                uploaded = hi;
+            }
+            check(gvxb_event_record(up, ev_up[k]), "event");
+            check(gvxb_stream_wait_event(ctx, ev_up[k]), "event wait");
+            compute(u, a0, a1, ctx);
+            check(gvxb_event_record(ctx, ev_k[k]), "event");
+            check(gvxb_stream_wait_event(dn, ev_k[k]), "event wait");
+            // the slot this piece downloads into was last used by piece k - kSlots
+            while (drained + kSlots <= k) drain(drained++);
+            for (std::size_t o = 0; o < outs.size(); ++o) {
+                const Slab& os = *oslab[o];
+                const std::size_t row = static_cast<std::size_t>(W) * os.bpp;
+                void* to = static_cast<std::uint8_t*>(outs[o].host) + static_cast<std::size_t>(a0 - band.row0) * row;
+                if (!outs[o].page_locked) {
+                    staging(stage_out, stage_out_bytes, 0, max_out, static_cast<std::size_t>(kSlots) * outs.size());
+                    to = stage_out[(k % kSlots) * outs.size() + o];
+                }
+                check(gvxb_download_2d(dn, to, row,
+                                       static_cast<const char*>(os.ptr) + static_cast<std::int64_t>(a0 - os.row0) * os.pitch,
+                                       static_cast<std::size_t>(os.pitch), row, static_cast<std::size_t>(a1 - a0)),
+                      "band piece download");
+            }
+            check(gvxb_event_record(dn, ev_dn[k]), "event");
+            // host copies of older pieces overlap this piece's transfers
+            while (drained + 2 <= k) drain(drained++);
+        }
+        while (drained < pieces.size()) drain(drained++);
+        check(gvxb_sync(ctx), "band compute sync");
+        std::uint32_t status = 0;
+        long long reads = 0;
+        check(gvxb_status_counter_read(ctx, &status, &reads), "device status");
+        if (status & GVXB_STATUS_DIV_BY_ZERO) {
+            gvxb_status_reset(ctx);
+            throw Error(ErrorCode::DivByZero, "division by zero");
+        }
+        if (status & GVXB_STATUS_INDEX_RANGE) {
+            gvxb_status_reset(ctx);
+            throw Error(ErrorCode::ShapeMismatch, "array index out of range");
+        }
+        return reads;
+    }
+
     void synchronize() {
         check(gvxb_sync(ctx), "band sync");
         std::uint32_t status = 0;
@@ -448,7 +592,39 @@ BandedSession::BandedSession(const OptimizedPlan& plan, int rank, int world, voi
     impl_->init(plan, rank, world, comm, device, frames);
 }
 
+BandedSession::BandedSession() : impl_(std::make_unique<Impl>()) {}
+
 BandedSession::~BandedSession() = default;
+
+namespace detail {
+
+/// run_plan's host path for large frames (execute.cpp): a whole-image band
+/// of a program, driven piece by piece from host rows.
+struct BandAccess {
+    static std::unique_ptr<BandedSession> whole_image(std::shared_ptr<dev::Program> prog) {
+        std::unique_ptr<BandedSession> b(new BandedSession());
+        b->impl_->init_program(std::move(prog), 0, 1, nullptr, -1, 1);
+        const auto& ins = b->impl_->unit_ins;
+        if (b->impl_->prog->units.size() != 1 || ins.size() != 1 || ins[0].size() != 1) return nullptr;
+        return b;
+    }
+    static ObjectId input(const BandedSession& b) { return b.impl_->unit_ins[0][0].first; }
+    static long long launches(const BandedSession& b) { return gvxb_launch_count(b.impl_->ctx); }
+    static int height(const BandedSession& b) { return b.impl_->H; }
+};
+
+std::unique_ptr<BandedSession> whole_image_band(std::shared_ptr<dev::Program> prog) {
+    try {
+        return BandAccess::whole_image(std::move(prog));
+    } catch (const Error&) { // not bandable: global operations, run-time scalars, mixed sizes
+        return nullptr;
+    }
+}
+
+ObjectId whole_image_band_input(const BandedSession& b) { return BandAccess::input(b); }
+long long whole_image_band_launches(const BandedSession& b) { return BandAccess::launches(b); }
+
+} // namespace detail
 
 BandLayout BandedSession::layout() const {
     BandLayout l;
@@ -532,6 +708,10 @@ void BandedSession::synchronize() { impl_->synchronize(); }
 void BandedSession::run_host(const void* src, std::size_t src_pitch, ObjectId output, void* dst,
                              std::size_t dst_pitch, int piece_rows) {
     impl_->run_host(src, src_pitch, output, dst, dst_pitch, piece_rows);
+}
+
+long long BandedSession::run_host_rows(const HostRows& input, const std::vector<HostRows>& outputs, int piece_rows) {
+    return impl_->run_host_rows(input, outputs, piece_rows);
 }
 
 int BandedSession::launches_per_run() const {

@@ -1386,7 +1386,31 @@ std::map<ObjectId, const Buffer*> bind_inputs(const VerifiedGraph& vg, const Inp
 struct HostSession {
     std::mutex mu;
     DeviceSession::Impl impl;
+    /// large frames of single-group stencil / point programs: row pieces
+    /// pipelined from host memory (built on first use; null = not eligible)
+    std::unique_ptr<BandedSession> pieces;
+    bool pieces_tried = false;
 };
+
+/// Output rows per piece for the pipelined host path, or 0 to run the frame
+/// whole (small frames: the per-piece transfer and launch overheads win).
+int host_piece_rows(const dev::Program& prog, ObjectId input, int height) {
+    static const char* off = std::getenv("GVX_HOST_PIECES");
+    if (off && off[0] == '0') return 0;
+    const dev::ObjInfo& oi = prog.objects.at(input);
+    const std::size_t bytes =
+        static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format) * static_cast<std::size_t>(height);
+    static const std::size_t min_bytes = [] {
+        const char* e = std::getenv("GVX_HOST_PIECE_MIN_BYTES");
+        return e ? static_cast<std::size_t>(std::atoll(e)) : (std::size_t(1) << 20);
+    }();
+    if (bytes < min_bytes || height < 256) return 0;
+    if (const char* e = std::getenv("GVX_HOST_PIECE_ROWS")) return std::max(16, std::atoi(e));
+    // four pieces: measured best of 2 / 3 / 4 / 6 / 8 / 16 on cfg1, 2, 3 and 5
+    // (the host copies of the pieces are the critical path; each extra piece
+    // adds a wait on its download before its rows can be copied out)
+    return (height + 3) / 4;
+}
 
 /// Device storage is kept per program between synchronous host runs (the
 /// reference allocates per run; reusing it keeps run_plan at copy speed).
@@ -1432,6 +1456,79 @@ ExecutionReport execute(const std::shared_ptr<dev::Program>& prog, const Verifie
     static const bool trace = std::getenv("GVX_TRACE_HOST") != nullptr;
     using clock = std::chrono::steady_clock;
     const auto t0 = clock::now();
+    if (!hs->pieces_tried) {
+        hs->pieces_tried = true;
+        hs->pieces = detail::whole_image_band(prog);
+    }
+    if (hs->pieces) {
+        const ObjectId in_id = detail::whole_image_band_input(*hs->pieces);
+        const int H = prog->objects.at(in_id).desc.height;
+        const int piece = host_piece_rows(*prog, in_id, H);
+        auto bit = bound.find(in_id);
+        if (piece > 0 && bit != bound.end()) {
+            // row pieces: each piece's input rows go up, its kernel runs and its
+            // output rows come down while the host copies of its neighbours run
+            const Buffer& ib = *bit->second;
+            const dev::ObjInfo& ii = prog->objects.at(in_id);
+            const std::size_t in_bytes =
+                static_cast<std::size_t>(ii.desc.width) * bytes_per_pixel(ii.desc.format) * ii.desc.height;
+            if (ib.bytes.size() < in_bytes) throw Error(ErrorCode::ShapeMismatch, "image payload too small", in_id);
+            BandedSession::HostRows in_rows;
+            in_rows.id = in_id;
+            if (fill && fill->id == in_id && fill->src) {
+                in_rows.host = const_cast<std::uint8_t*>(fill->src);
+            } else {
+                in_rows.host = const_cast<std::uint8_t*>(ib.bytes.data());
+                int pinned = 0;
+                gvxb_host_is_pinned(ib.bytes.data(), &pinned);
+                in_rows.page_locked = pinned != 0;
+            }
+            ExecutionReport report;
+            std::vector<BandedSession::HostRows> outs;
+            const AppGraph& g = vg.graph();
+            const Context& gctx = vg.context();
+            for (ObjectId id : g.data()) {
+                const DataObject* o = gctx.find(id);
+                if (!o || o->is_virtual || g.producer(id) == kInvalidId || !prog->objects.count(id)) continue;
+                const dev::ObjInfo& oi = prog->objects.at(id);
+                const std::size_t bytes =
+                    static_cast<std::size_t>(oi.desc.width) * bytes_per_pixel(oi.desc.format) * oi.desc.height;
+                Buffer b;
+                const ResolvedDesc d = vg.resolved().count(id) ? vg.desc(id) : oi.desc;
+                BandedSession::HostRows r;
+                r.id = id;
+                auto pit = out_pool ? out_pool->find(id) : decltype(out_pool->end()){};
+                if (out_pool && pit != out_pool->end() && pit->second.size() == bytes) {
+                    b.desc = d;
+                    b.bytes = std::move(pit->second);
+                    out_pool->erase(pit);
+                    r.page_locked = true;
+                    if (fill && fill->drain_id == id && fill->drain_dst) {
+                        r.drain = fill->drain_dst;
+                        fill->drained = true;
+                    }
+                } else {
+                    b = Buffer::image(d);
+                }
+                b.id = id;
+                Buffer& slot = report.outputs[id] = std::move(b);
+                r.host = slot.bytes.data();
+                outs.push_back(r);
+            }
+            const long long launches0 = detail::whole_image_band_launches(*hs->pieces);
+            const long long dyn = hs->pieces->run_host_rows(in_rows, outs, piece);
+            report.counters.kernel_launches = detail::whole_image_band_launches(*hs->pieces) - launches0;
+            report.counters.pixels_read = dyn;
+            for (const dev::Unit& u : prog->units) {
+                report.counters.pixels_read += u.static_reads;
+                report.counters.pixels_written += u.static_writes;
+            }
+            if (trace)
+                std::fprintf(stderr, "[gvx host] %d-row pieces: %.1f us\n", piece,
+                             std::chrono::duration<double, std::micro>(clock::now() - t0).count());
+            return report;
+        }
+    }
     gvxb_ctx_set_stream(s.ctx, nullptr);
     if (s.scratch.size() != prog->units.size()) s.prepare();
     for (const auto& [id, b] : bound)

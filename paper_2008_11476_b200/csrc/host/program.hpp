@@ -124,6 +124,10 @@ bool static_counts(const OperatorNode& n, const VerifiedGraph& vg, std::int64_t&
 
 } // namespace gvx::dev
 
+namespace gvx {
+class BandedSession;
+}
+
 namespace gvx::detail {
 
 /// Facade-only: the input Buffer `id` is page-locked and still to be filled
@@ -131,7 +135,19 @@ namespace gvx::detail {
 struct HostFill {
     ObjectId id = kInvalidId;
     const std::uint8_t* src = nullptr;
+    /// optional: image output `drain_id` is also copied into `drain_dst`
+    /// during the run (piece by piece); `drained` reports whether it was
+    ObjectId drain_id = kInvalidId;
+    void* drain_dst = nullptr;
+    mutable bool drained = false;
 };
+
+/// A BandedSession over the whole image of a single-group, single-input
+/// stencil / point program (band.cpp), or null when the program cannot run
+/// in row pieces.
+std::unique_ptr<BandedSession> whole_image_band(std::shared_ptr<dev::Program> prog);
+ObjectId whole_image_band_input(const BandedSession& b);
+long long whole_image_band_launches(const BandedSession& b);
 
 /// run_naive / run_plan whose image outputs are downloaded into vectors
 /// taken from `out_pool` (keyed by object id, matching size) when present:
