@@ -1300,150 +1300,6 @@ NodeProgram lower_local(const AbstractionKernel& k, const std::vector<SlotInfo>&
     return prog;
 }
 
-// ------------------------------------------------------- fused local chain
-
-namespace {
-
-/// C type holding a stored pixel of an integer / F32 image format, and the
-/// V -> storage conversion of Emitter::store.
-bool storage_of(ImageFormat f, std::string& ctype, std::string& conv, std::string& load) {
-    switch (f) {
-    case ImageFormat::U8: ctype = "unsigned char"; conv = "(unsigned char)sv.i"; load = "vi((i64)v)"; return true;
-    case ImageFormat::U16: ctype = "unsigned short"; conv = "(unsigned short)sv.i"; load = "vi((i64)v)"; return true;
-    case ImageFormat::S16: ctype = "short"; conv = "(short)sv.i"; load = "vi((i64)v)"; return true;
-    case ImageFormat::S32: ctype = "int"; conv = "(int)sv.i"; load = "vi((i64)v)"; return true;
-    case ImageFormat::F32: ctype = "float"; conv = "(float)vd(sv)"; load = "vf((double)v)"; return true;
-    default: return false;
-    }
-}
-
-/// Integer fast path of one pixel's tap loop (Clamp border, tap body
-/// `window` or `mask * window` with an integer mask whose sums fit int32,
-/// integer source format): typed loads and int32 arithmetic, which equal the
-/// reference's int64 Value arithmetic there.  A window over the chain's
-/// shared-memory intermediate (em.smem_slot) reads the tile (region origin
-/// rx0 / ry0, row length rw).  Returns statements defining `V cmb`, or ""
-/// when the shape does not apply.
-std::string int_tap_single(const LocalKernel& lk, const std::vector<SlotInfo>& ins, const std::vector<Value>& mask,
-                           const Emitter& em, int rw) {
-    if (lk.boundary != BoundaryMode::Clamp || lk.median3x3 || !lk.tap_body) return "";
-    const Expr& t = *lk.tap_body;
-    const Expr* win = nullptr;
-    bool masked = false;
-    if (t.op == ExprOp::WindowPixel) {
-        win = &t;
-    } else if (t.op == ExprOp::Mul && lk.combine == CombineMode::Sum) {
-        if (t.a->op == ExprOp::MaskCoef && t.b->op == ExprOp::WindowPixel) win = t.b.get(), masked = true;
-        if (t.b->op == ExprOp::MaskCoef && t.a->op == ExprOp::WindowPixel) win = t.a.get(), masked = true;
-        const Expr* mc = masked ? (t.a->op == ExprOp::MaskCoef ? t.a.get() : t.b.get()) : nullptr;
-        if (mc && (mc->dx != 0 || mc->dy != 0)) return "";
-    }
-    if (!win || win->channel != Channel::C0 || win->dx != 0 || win->dy != 0) return "";
-    const int slot = win->input;
-    if (slot < 0 || slot >= static_cast<int>(ins.size()) || ins[static_cast<std::size_t>(slot)].kind != SlotKind::Image)
-        return "";
-    std::int64_t lo = 0, hi = 0;
-    if (!int_format_range(ins[static_cast<std::size_t>(slot)].desc.format, lo, hi)) return "";
-    const int ww = lk.window_w, wh = lk.window_h, hw = ww / 2, hh = wh / 2;
-    std::vector<std::int64_t> m(static_cast<std::size_t>(ww * wh), 1);
-    if (masked) {
-        if (mask.size() != m.size()) return "";
-        for (std::size_t i = 0; i < m.size(); ++i) {
-            if (mask[i].real) return "";
-            m[i] = mask[i].i;
-            if (m[i] > 2147483647LL || m[i] < -2147483647LL) return "";
-        }
-    }
-    if (lk.combine == CombineMode::Sum) {
-        std::int64_t bound = 0;
-        for (std::int64_t c : m) {
-            bound += std::llabs(c) * std::max(std::llabs(lo), std::llabs(hi));
-            if (bound > 2147483647LL) return "";
-        }
-    }
-    const char* ctype = "";
-    switch (ins[static_cast<std::size_t>(slot)].desc.format) {
-    case ImageFormat::U8: ctype = "const unsigned char*"; break;
-    case ImageFormat::U16: ctype = "const unsigned short*"; break;
-    case ImageFormat::S16: ctype = "const short*"; break;
-    default: ctype = "const int*"; break;
-    }
-    const bool smem = slot == em.smem_slot;
-    std::ostringstream b;
-    b << "    int cacc;\n";
-    bool first = true;
-    const bool sum = lk.combine == CombineMode::Sum;
-    for (int dy = -hh; dy <= hh; ++dy) {
-        b << "    {\n";
-        if (smem)
-            b << "      const int ry = clampi(py + (" << dy << "), 0, H - 1) - ry0;\n";
-        else
-            b << "      " << ctype << " r = (" << ctype << ")(" << em.in_base(slot) << " + (u64)clampi(py + (" << dy
-              << "), 0, H - 1) * p.f[" << em.fin(slot) + 1 << "]);\n";
-        for (int dx = -hw; dx <= hw; ++dx) {
-            const std::int64_t coef = m[static_cast<std::size_t>((dy + hh) * ww + dx + hw)];
-            if (sum && coef == 0) continue;
-            std::string v = smem ? "(int)gvx_mid[ry * " + std::to_string(rw) + " + clampi(px + (" + std::to_string(dx) +
-                                       "), 0, W - 1) - rx0]"
-                                 : "(int)r[clampi(px + (" + std::to_string(dx) + "), 0, W - 1)]";
-            if (sum && coef != 1) v = "(" + std::to_string(coef) + " * " + v + ")";
-            if (first) b << "      cacc = " << v << ";\n";
-            else if (sum) b << "      cacc += " << v << ";\n";
-            else b << "      cacc = " << (lk.combine == CombineMode::Min ? "min" : "max") << "(cacc, " << v << ");\n";
-            first = false;
-        }
-        b << "    }\n";
-    }
-    if (first) return "";
-    b << "    V cmb = vi((i64)cacc);\n";
-    return b.str();
-}
-
-/// Tap loop + post body of a local node at (px, py): statements defining
-/// `V pv` (the value before its store).  Integer fast path when it applies,
-/// else the Value-typed general path.
-std::string local_value(Emitter& em, const LocalKernel& lk, const std::vector<SlotInfo>& ins,
-                        const std::vector<Value>& mask, int rw) {
-    std::ostringstream b;
-    const int hw = lk.window_w / 2, hh = lk.window_h / 2;
-    const std::string fast = int_tap_single(lk, ins, mask, em, rw);
-    if (!fast.empty()) {
-        em.tdx = em.tdy = 0;
-        em.mode = Emitter::Mode::Post;
-        em.cmb_typed = true;
-        em.cmb_tv = Emitter::tint("cacc", -2147483647LL, 2147483647LL);
-        b << fast << "    V pv = " << (lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb")) << ";\n";
-        return b.str();
-    }
-    em.mode = Emitter::Mode::Tap;
-    const std::string typed = typed_taps(em, lk);
-    if (!typed.empty()) {
-        em.tdx = em.tdy = 0;
-        em.mode = Emitter::Mode::Post;
-        b << typed << "    V pv = " << (lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb")) << ";\n";
-        return b.str();
-    }
-    const char* comb = lk.combine == CombineMode::Sum ? "v_add" : lk.combine == CombineMode::Min ? "v_min" : "v_max";
-    bool first = true;
-    for (int dy = -hh; dy <= hh; ++dy)
-        for (int dx = -hw; dx <= hw; ++dx) {
-            em.tdx = dx;
-            em.tdy = dy;
-            const std::string v = em.emit(*lk.tap_body);
-            if (first) {
-                b << "    V cmb = " << v << ";\n";
-                first = false;
-            } else {
-                b << "    cmb = " << comb << "(cmb, " << v << ");\n";
-            }
-        }
-    em.tdx = em.tdy = 0;
-    em.mode = Emitter::Mode::Post;
-    b << "    V pv = " << (lk.post_body ? em.emit_any(*lk.post_body) : std::string("cmb")) << ";\n";
-    return b.str();
-}
-
-} // namespace
 } // namespace (lowering helpers)
 
 
