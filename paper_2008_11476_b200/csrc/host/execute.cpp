@@ -350,7 +350,8 @@ Unit jit_unit(const OperatorNode& n, const VerifiedGraph& vg,
 /// and the executed nodes they cover; a region that cannot be lowered
 /// (run-time typed bodies, shared memory) falls back to per-node kernels.
 std::vector<Unit> region_units(const AppGraph& fg, const VerifiedGraph& fused, const std::set<ObjectId>& taken,
-                               const std::map<ObjectId, std::vector<Value>>& matrices, std::set<ObjectId>& covered) {
+                               const std::map<ObjectId, std::vector<Value>>& matrices,
+                               const std::map<ObjectId, std::pair<long long, long long>>& known, std::set<ObjectId>& covered) {
     std::vector<Unit> units;
     if (std::getenv("GVX_NO_REGIONS")) return units;
     const Context& ctx = fused.context();
@@ -556,7 +557,10 @@ std::vector<Unit> region_units(const AppGraph& fg, const VerifiedGraph& fused, c
                             ins.push_back(slot_of(fused, id));
                             u.in_ids.push_back(id);
                             u.reads.push_back(id);
-                            objs[static_cast<std::size_t>(obj_index[id])].load = param_of[id];
+                            jit::RegionObject& ro = objs[static_cast<std::size_t>(obj_index[id])];
+                            ro.load = param_of[id];
+                            auto kr = known.find(id);
+                            if (kr != known.end()) ro.ranged = true, ro.lo = kr->second.first, ro.hi = kr->second.second;
                         }
                     } else if (image) {
                         if (!param_of.count(id)) {
@@ -838,8 +842,17 @@ std::shared_ptr<Program> build_plan(const OptimizedPlan& plan, const std::map<Ob
     }
     for (Unit& u : aot) p->units.push_back(std::move(u));
     {
+        // value ranges of images the hand-written groups produce (Sobel of
+        // U8: |g| <= 1020; magnitude <= 1443), narrower than their formats
+        std::map<ObjectId, std::pair<long long, long long>> known;
+        for (const Unit& u : p->units)
+            if (u.kind == Unit::Kind::Edge) {
+                for (int i = 0; i < 2; ++i)
+                    if (u.out[i] != kInvalidId) known[u.out[i]] = {-1020, 1020};
+                if (u.out[2] != kInvalidId) known[u.out[2]] = {0, 1443};
+            }
         std::set<ObjectId> rcov;
-        for (Unit& u : region_units(fg, fused, covered_fused, matrices, rcov)) p->units.push_back(std::move(u));
+        for (Unit& u : region_units(fg, fused, covered_fused, matrices, known, rcov)) p->units.push_back(std::move(u));
         covered_fused.insert(rcov.begin(), rcov.end());
     }
     for (ObjectId nid : fg.topo_sort())

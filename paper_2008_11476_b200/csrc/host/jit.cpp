@@ -115,6 +115,10 @@ __device__ __forceinline__ i64 t_cast_d(double r, i64 lo, i64 hi, int pol) {
   return (lo < 0 && low > (u64)hi) ? (i64)low - (i64)width : (i64)low;
 }
 __device__ __forceinline__ i64 t_sat(i64 x, i64 lo, i64 hi) { return x < lo ? lo : (x > hi ? hi : x); }
+// round half away from zero of x / d (d > 0 a literal): llround(x * fl(1/d))
+// for |x| < 2^51 when d is odd or a power of two (Emitter::temit, Cast)
+__device__ __forceinline__ i64 t_rdiv(i64 x, i64 d) { return x >= 0 ? (2 * x + d) / (2 * d) : -((d - 2 * x) / (2 * d)); }
+__device__ __forceinline__ int t_rdiv32(int x, int d) { return x >= 0 ? (2 * x + d) / (2 * d) : -((d - 2 * x) / (2 * d)); }
 // llround(sqrt((double)n)) for integer 0 <= n < 2^24: fp32 estimate, then
 // the integer correction k* = largest k with k*k - k < n (no n is a half
 // square, so half-away rounding never ties)
@@ -629,6 +633,38 @@ struct Emitter {
                     out = tint("(int)t_sat((i64)t_round_sqrt(" + n.c + "), " + tlit_i(lo) + ", " + tlit_i(hi) + ")",
                                std::max<std::int64_t>(lo, 0), std::min<std::int64_t>(hi, kmax));
                     return true;
+                }
+            }
+            if (pol == 0 && e.a->op == ExprOp::Mul) {
+                // cast(int, x * c) with c = fl(1/d): llround(x * c) is the exact
+                // half-away rounding of x / d when |x| < 2^51 and d is odd or a
+                // power of two (the error stays below the 1/(2d) margin; no ties
+                // for odd d) -- an integer division instead of double arithmetic
+                const Expr* xe = e.a->a.get();
+                const Expr* ce = e.a->b.get();
+                if (xe && ce && xe->op == ExprOp::ConstF) std::swap(xe, ce);
+                TV x;
+                if (xe && ce && ce->op == ExprOp::ConstF && ce->fval > 0 && ce->fval <= 1 && temit(*xe, x) &&
+                    x.t != 'd') {
+                    const double inv = 1.0 / ce->fval;
+                    const long long d = std::llround(inv);
+                    const bool odd_or_pow2 = d >= 1 && ((d & 1) || (d & (d - 1)) == 0);
+                    const __int128 lim = static_cast<__int128>(1) << 51;
+                    if (odd_or_pow2 && d <= (1LL << 30) && 1.0 / static_cast<double>(d) == ce->fval && x.lo > -lim &&
+                        x.hi < lim) {
+                        const bool i32 = 2 * std::max(-x.lo, x.hi) + d < INT32_MAX;
+                        const long long qlo = static_cast<long long>(x.lo / d) - 1, qhi = static_cast<long long>(x.hi / d) + 1;
+                        const std::string q = i32 ? "t_rdiv32((int)(" + x.c + "), " + std::to_string(d) + ")"
+                                                  : "t_rdiv(" + as_i64(x) + ", " + std::to_string(d) + "LL)";
+                        if (qlo >= lo && qhi <= hi) {
+                            out = tint("", qlo, qhi);
+                            out.c = (out.t == 'i' ? "((int)" : "((i64)") + q + ")";
+                        } else {
+                            out = tint("(int)t_sat(" + q + ", " + tlit_i(lo) + ", " + tlit_i(hi) + ")",
+                                       std::max<long long>(lo, qlo), std::min<long long>(hi, qhi));
+                        }
+                        return true;
+                    }
                 }
             }
             if (a.t == 'd') {
@@ -1748,6 +1784,8 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         std::int64_t lo = 0, hi = 0;
         if (objs[o].format == ImageFormat::F32) orange[o].t = 'd';
         else if (int_format_range(objs[o].format, lo, hi)) orange[o].lo = lo, orange[o].hi = hi;
+        if (objs[o].ranged && orange[o].t != 'd' && objs[o].lo >= orange[o].lo && objs[o].hi <= orange[o].hi)
+            orange[o].lo = objs[o].lo, orange[o].hi = objs[o].hi;
     }
     auto otype = [&](int o, TVproto& pr) {
         pr = orange[static_cast<std::size_t>(o)];
@@ -1775,7 +1813,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
              << "    const " << ct << "* src = (const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
              << f + 2 << "] + (u64)y * p.f[" << f + 1 << "]);\n"
              << "#pragma unroll\n    for (int ix = 0; ix < " << (RWo + 31) / 32 << "; ++ix) {\n"
-             << "      const int rx = threadIdx.x + 32 * ix;\n      if (rx >= " << RWo << ") break;\n"
+             << "      const int rx = threadIdx.x + 32 * ix;\n" << (RWo % 32 ? "      if (rx >= " + std::to_string(RWo) + ") break;\n" : std::string())
              << "      ro" << o << "[ry * " << RWo << " + rx] = src[clampi(tx0 - " << objs[o].halo_x
              << " + rx, 0, W - 1)];\n    }\n  }\n";
     }
@@ -1919,20 +1957,31 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         } else {
             throw unsupported("node kind");
         }
-        body << "  // node " << ni << ": " << k.name << "\n"
-             << "  for (int ry = threadIdx.y; ry < " << (rw(oref) * rh(oref)) / (rw(oref)) << "; ry += 8)\n"
-             << "  #pragma unroll\n"
-             << "  for (int ix = 0; ix < " << ((rw(oref)) + 31) / 32 << "; ++ix) {\n"
-             << "    const int rx = threadIdx.x + 32 * ix;\n"
-             << "    if (rx >= " << (rw(oref)) << ") break;\n"
-             << "    const int e = ry * " << (rw(oref)) << " + rx;\n"
-             << "    const int px = tx0 - " << R.halo_x << " + rx, py = ty0 - " << R.halo_y << " + ry;\n"
-             << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
+        // two copies of the entry loop: tiles whose node region lies inside
+        // the image skip the per-entry position test
+        std::ostringstream bases;
         for (std::size_t o = 0; o < objs.size(); ++o)
             if (used_obj[o])
-                body << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))
-                     << " + px - tx0 + " << objs[o].halo_x << ";\n";
-        body << extra_base << nb.str() << "  }\n  __syncthreads();\n";
+                bases << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))
+                      << " + px - tx0 + " << objs[o].halo_x << ";\n";
+        body << "  // node " << ni << ": " << k.name << "\n";
+        for (int border = 0; border < 2; ++border) {
+            if (border == 0)
+                body << "  if (tx0 - " << R.halo_x << " >= 0 && ty0 - " << R.halo_y << " >= 0 && tx0 + " << TW + R.halo_x
+                     << " <= W && ty0 + " << TH + R.halo_y << " <= H) {\n";
+            else
+                body << "  } else {\n";
+            body << "  for (int ry = threadIdx.y; ry < " << rh(oref) << "; ry += 8)\n"
+                 << "  #pragma unroll\n"
+                 << "  for (int ix = 0; ix < " << (rw(oref) + 31) / 32 << "; ++ix) {\n"
+                 << "    const int rx = threadIdx.x + 32 * ix;\n";
+            if (rw(oref) % 32) body << "    if (rx >= " << rw(oref) << ") break;\n";
+            body << "    const int e = ry * " << rw(oref) << " + rx;\n"
+                 << "    const int px = tx0 - " << R.halo_x << " + rx, py = ty0 - " << R.halo_y << " + ry;\n";
+            if (border) body << "    if (px < 0 || py < 0 || px >= W || py >= H) continue;\n";
+            body << bases.str() << extra_base << nb.str() << "  }\n";
+        }
+        body << "  }\n  __syncthreads();\n";
         // out-of-image entries = the entry at the clamped position (border tiles)
         for (int o : rn.out_obj) {
             if (o < 0) continue;

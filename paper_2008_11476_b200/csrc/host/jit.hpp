@@ -90,6 +90,10 @@ struct RegionObject {
     int halo_x = 0, halo_y = 0;
     int store = -1;
     int load = -1; ///< >= 0: an input of the region staged from kernel input slot `load`
+    /// a staged input's values are known to lie in [lo, hi] (its producer's
+    /// range, e.g. Sobel outputs of a U8 image), narrower than its format's
+    bool ranged = false;
+    long long lo = 0, hi = 0;
 };
 
 /// Whether `e` reads input `slot` through a window (WindowPixel).

@@ -80,3 +80,39 @@ def test_edge8_magnitude_rounding_is_exact(tmp_path):
     subprocess.run(["gcc", "-O2", "-ffp-contract=off", str(src), "-o", str(exe), "-lm"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert "bad=0" in out, out
+
+
+def test_reciprocal_cast_is_integer_rounded_division():
+    """The generated code replaces the reference's cast(int, x * fl(1/d))
+    (double multiply, llround: ref:src/expr.cpp binop / cast_value) by the
+    integer half-away division (2|x| + d) / 2d (jit.cpp t_rdiv) when d is
+    odd or a power of two and |x| < 2^51.  Check the claim on boundary and
+    random x for several d, in IEEE double arithmetic (Python floats) with
+    the rounding of the product taken exactly."""
+    import math
+    import random
+    from fractions import Fraction
+
+    def llround(r: float) -> int:  # half away from zero, exact
+        q = Fraction(r)
+        f = math.floor(abs(q) + Fraction(1, 2))
+        return f if q >= 0 else -f
+
+    def rdiv(x: int, d: int) -> int:
+        return (2 * x + d) // (2 * d) if x >= 0 else -((d - 2 * x) // (2 * d))
+
+    rng = random.Random(7)
+    lim = 1 << 51
+    for d in (1, 2, 3, 5, 7, 8, 9, 16, 25, 49, 81, 255, 1023, 4096, 65537):
+        c = 1.0 / d
+        xs = [0, 1, -1, lim - 1, -(lim - 1)]
+        for _ in range(400):
+            k = rng.randrange(-(lim // d), lim // d)
+            for off in (-1, 0, 1):  # around the half-integer quotients k + 1/2 (ties for even d)
+                xs.append(k * d + (d - 1) // 2 + off)
+                xs.append(k * d + d // 2 + off)
+            xs.append(rng.randrange(-lim + 1, lim))
+        for x in xs:
+            if abs(x) >= lim:
+                continue
+            assert llround(float(x) * c) == rdiv(x, d), (x, d)
