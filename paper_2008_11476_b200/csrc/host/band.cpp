@@ -514,6 +514,17 @@ struct BandedSession::Impl {
         };
         int uploaded = in.row0;
         const int in_end = in.row0 + in.rows;
+        // an error leaves no transfer in flight on the caller's host memory
+        struct Quiesce {
+            Impl& s;
+            bool armed = true;
+            ~Quiesce() {
+                if (!armed) return;
+                gvxb_sync(s.up);
+                gvxb_sync(s.dn);
+                gvxb_sync(s.ctx);
+            }
+        } quiesce{*this};
         for (std::size_t k = 0; k < pieces.size(); ++k) {
             const auto [a0, a1] = pieces[k];
             const int hi = std::min(in_end, a1 + R);
@@ -559,7 +570,9 @@ struct BandedSession::Impl {
             while (drained + 2 <= k) drain(drained++);
         }
         while (drained < pieces.size()) drain(drained++);
+        check(gvxb_sync(up), "band upload sync");
         check(gvxb_sync(ctx), "band compute sync");
+        quiesce.armed = false;
         std::uint32_t status = 0;
         long long reads = 0;
         check(gvxb_status_counter_read(ctx, &status, &reads), "device status");

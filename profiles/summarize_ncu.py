@@ -18,21 +18,21 @@ METRICS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "sm__cycles_elapsed.avg.per_second",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
-    "smsp__warps_issue_stalled_math_pipe_throttle_per_warp_active.pct",
-    "smsp__warps_issue_stalled_wait_per_warp_active.pct",
-    "smsp__warps_issue_stalled_short_scoreboard_per_warp_active.pct",
-    "smsp__warps_issue_stalled_long_scoreboard_per_warp_active.pct",
-    "smsp__warps_issue_stalled_barrier_per_warp_active.pct",
-    "smsp__warps_issue_stalled_no_instruction_per_warp_active.pct",
-    "smsp__warps_issue_stalled_not_selected_per_warp_active.pct",
-    "smsp__warps_issue_stalled_selected_per_warp_active.pct",
-    "smsp__warps_issue_stalled_dispatch_stall_per_warp_active.pct",
-    "smsp__warps_issue_stalled_lg_throttle_per_warp_active.pct",
-    "smsp__warps_issue_stalled_mio_throttle_per_warp_active.pct",
-    "smsp__warps_issue_stalled_drain_per_warp_active.pct",
-    "smsp__warps_issue_stalled_sleeping_per_warp_active.pct",
-    "smsp__warps_issue_stalled_branch_resolving_per_warp_active.pct",
-    "smsp__warps_issue_stalled_membar_per_warp_active.pct",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_drain_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio",
     "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
