@@ -379,6 +379,51 @@ TEST_CASE("gpu: row bands of a mixed program (generated + hand-written units) eq
     }
 }
 
+TEST_CASE("gpu: DivByZero and results through the row-piece host path") {
+    GPU_ONLY();
+    // one input, one group, a 1 MB frame: run_naive / run_plan take the
+    // pipelined row-piece path (execute.cpp host_piece_rows)
+    std::vector<SignatureParam> ps(2);
+    ps[0].direction = Direction::Input;
+    ps[0].kind = ObjKind::Image;
+    ps[1].direction = Direction::Output;
+    ps[1].kind = ObjKind::Image;
+    ps[1].formats = {ImageFormat::U8};
+    PointKernel pk;
+    pk.arity = 1;
+    pk.outputs.push_back(PointOutput{{saturate_to(ScalarType::U8, div(const_i(1000), input_pixel(0)))}});
+    auto reg = std::make_shared<KernelRegistry>(KernelRegistry::builtin().clone());
+    reg->add_custom(make_point_kernel("inverse", KernelSignature(ps), pk));
+    Context ctx;
+    ctx.set_registry(reg);
+    AppGraph& g = ctx.create_graph();
+    const int W = 1024, H = 1031;
+    ObjectId a = ctx.create_image(W, H, ImageFormat::U8).id, o = ctx.create_image(W, H, ImageFormat::U8).id;
+    g.note_data(a);
+    g.add_node("inverse", {a, o});
+    VerifiedGraph impl = impl_of(ctx, g);
+    InputMap ok, bad;
+    ok[a] = random_buffer(img_desc(W, H, ImageFormat::U8), 4);
+    for (auto& v : ok[a].bytes) v |= 1;
+    bad = ok;
+    bad[a].bytes[static_cast<std::size_t>(W) * (H - 3) + 17] = 0; // in the last piece
+    const ExecutionReport r1 = run_naive(impl, ok);
+    bool raised = false;
+    try {
+        run_naive(impl, bad);
+    } catch (const Error& e) {
+        raised = e.code() == ErrorCode::DivByZero;
+    }
+    CHECK(raised);
+    const ExecutionReport r2 = run_naive(impl, ok); // the status was cleared
+    CHECK(r2.outputs.at(o).bytes == r1.outputs.at(o).bytes);
+    const auto& in = ok[a].bytes;
+    const auto& out = r1.outputs.at(o).bytes;
+    bool exact = out.size() == in.size();
+    for (std::size_t i = 0; exact && i < in.size(); ++i) exact = out[i] == std::min(255, 1000 / in[i]);
+    CHECK(exact);
+}
+
 TEST_CASE("gpu: runtime division by zero surfaces as DivByZero") {
     GPU_ONLY();
     std::vector<SignatureParam> ps(3);
