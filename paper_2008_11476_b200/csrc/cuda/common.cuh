@@ -55,6 +55,11 @@ inline gvxb_range image_range(const gvxb_image& im) {
 /// write-after-write through any of the ranges.  Returns the value of the
 /// kernel's `pdl_wait` parameter: 1 = must wait for the previous grid.
 int pdl_must_wait(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw);
+/// Whether a launch_tracked of these ranges will overlap the previous
+/// kernel on the stream (programmatic dependent launch without a wait):
+/// overlapped launches hide a grid's tail behind its successor's head, so
+/// the row-ring kernels pick taller bands for them.
+bool launch_overlaps(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw);
 
 /// Launches `fn` on ctx's stream, as a programmatic dependent launch when
 /// the context allows it and the previous stream operation was a tracked

@@ -42,6 +42,8 @@ constexpr int kE8SW = 288;      // ring row bytes: image columns [x_org, x_org +
 constexpr int kE8Chunk = 16;    // rows per TMA chunk
 constexpr int kE8Ring = 2 * kE8Chunk;
 constexpr int kE8THMax = 256;   // band rows: with overlapped launches taller bands win (halo rows amortised; measured 64 -> 256: +1.7% on 16K^2)
+constexpr int kE8THSerial = 64; // band rows when the launch waits for its predecessor: the grid's tail is exposed, so
+                                // shorter bands balance better (measured 16384^2: 211 -> 192 us, 64 x 1080p: +6%)
 
 struct E8Plane {
     int16_t* data;
@@ -430,8 +432,10 @@ int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kE8Threads, 0);
     const long long strips = static_cast<long long>(frames) * ((s.width + kE8Cols - 1) / kE8Cols);
     Edge8Params p;
-    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, kE8THMax,
-                              4);
+    const gvxb_range r[1] = {image_range(s)};
+    const gvxb_range w[3] = {image_range(a->gx), image_range(a->gy), image_range(a->mag)};
+    const int th_max = launch_overlaps(ctx, r, 1, w, 3) ? kE8THMax : kE8THSerial;
+    p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, th_max, 4);
     if (const char* e = std::getenv("GVX_EDGE8_TH")) p.th = std::max(8, std::atoi(e)); // tuning experiments
     CUtensorMap map;
     if (int rc = make_u8_tensor_map(&map, s, kE8SW, kE8Chunk)) return rc;
@@ -448,8 +452,6 @@ int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a) {
     p.gy = plane(a->gy);
     p.mag = plane(a->mag);
     dim3 grid((s.width + kE8Cols - 1) / kE8Cols, (rows + p.th - 1) / p.th, frames);
-    const gvxb_range r[1] = {image_range(s)};
-    const gvxb_range w[3] = {image_range(a->gx), image_range(a->gy), image_range(a->mag)};
     p.pdl_wait = pdl_must_wait(ctx, r, 1, w, 3);
     void* args[] = {&map, &p};
     return launch_tracked(ctx, fn, grid, dim3(kE8Threads), args, 0, r, 1, w, 3, "edge8 kernel");

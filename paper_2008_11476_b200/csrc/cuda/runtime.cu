@@ -59,6 +59,11 @@ int pdl_must_wait(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w
     return 0;
 }
 
+bool launch_overlaps(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw) {
+    const bool allowed = ctx->overlap > 0 || (ctx->overlap < 0 && ctx->stream == ctx->own_stream);
+    return allowed && ctx->prev_kernel && !pdl_must_wait(ctx, r, nr, w, nw);
+}
+
 int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
                    const gvxb_range* r, int nr, const gvxb_range* w, int nw, const char* what) {
     const bool allowed = ctx->overlap > 0 || (ctx->overlap < 0 && ctx->stream == ctx->own_stream);
