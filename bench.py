@@ -354,9 +354,10 @@ def run_frames(args, cfg, rank, world, local_rank):
                                 "output copied to the caller's numpy array, one synchronous call per frame"}
         g2.close()
 
-    # one fused launch per step (F frames in grid.z); cfg4's step also holds
+    # one fused launch per step (F frames in grid.z); a cfg4 batch also holds
     # the scratch-clear and MeanStdDev-finalize micro-kernels (counted in, so
-    # the roofline fraction is a lower bound for the conv/histogram kernel)
+    # the roofline fraction is a lower bound for the conv/histogram kernel;
+    # a single frame is one launch: its last CTA finalizes)
     kernel_ms = ms / args.steps
     if sess.launches() != 1 and cfg != 4:
         kernel_ms = None

@@ -231,6 +231,11 @@ typedef struct gvxb_conv_stats_args {
     int64_t* sumsq;        /* frames int64 scratch (required) */
     gvxb_value* mean;      /* frames, F32-rounded real (may be null) */
     gvxb_value* stddev;    /* frames, F32-rounded real (may be null) */
+    int64_t* work;         /* optional: frames x (bins + 1) int64, zero on entry (allocate zeroed
+                              once; each call leaves it and sum / sumsq zero again): with it a
+                              single frame is one launch (the kernel's last CTA publishes hist /
+                              mean / stddev); without it, or for several frames, a scratch clear
+                              and a finalize kernel bracket the convolution */
 } gvxb_conv_stats_args;
 int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a);
 

@@ -624,7 +624,7 @@ class GvxbConvStatsArgs(ctypes.Structure):
                 ("shift", ctypes.c_int32), ("wrap", ctypes.c_int32), ("bins", ctypes.c_int32),
                 ("offset", ctypes.c_int64), ("range", ctypes.c_int64), ("hist", ctypes.c_void_p),
                 ("sum", ctypes.c_void_p), ("sumsq", ctypes.c_void_p), ("mean", ctypes.c_void_p),
-                ("stddev", ctypes.c_void_p)]
+                ("stddev", ctypes.c_void_p), ("work", ctypes.c_void_p)]
 
 
 def _mask49(mask):
@@ -700,16 +700,23 @@ def stencil_point(device: "Device", img: np.ndarray, mask, div: int, mode: int) 
 
 
 def conv_stats(device: "Device", img: np.ndarray, mask, scale: int, conv_format: int = 2, shift: int = 0,
-               wrap: bool = False, bins: int = 256, offset: int = 0, rng: int = 256):
+               wrap: bool = False, bins: int = 256, offset: int = 0, rng: int = 256, one_launch: bool = False,
+               repeat: int = 1):
     """Host wrapper over gvxb_conv_stats on one U8 frame: returns
-    (converted U8 image, histogram int64[bins], mean, stddev)."""
+    (converted U8 image, histogram int64[bins], mean, stddev).  one_launch:
+    pass zeroed `work` scratch (the single-kernel form); repeat: execute
+    that many times (the scratch must come back zero each time)."""
     c, _ = _load()
     c.gvxb_conv_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(GvxbConvStatsArgs)]
     h, w = img.shape
     pitch = (w + 127) // 128 * 128
     src, conv = device.alloc(pitch * h), device.alloc(pitch * h)
     aux = device.alloc(16 * bins + 64 + 32)
+    work = device.alloc(8 * (bins + 1)) if one_launch else 0
     try:
+        if one_launch:  # zero scratch: the sums and the accumulators
+            device.upload(aux, 16 * bins + 96, np.zeros((1, 16 * bins + 96), np.uint8))
+            device.upload(work, 8 * (bins + 1), np.zeros((1, 8 * (bins + 1)), np.uint8))
         device.upload(src, pitch, np.ascontiguousarray(img, np.uint8))
         a = GvxbConvStatsArgs()
         a.src = GvxbImage(src, pitch, w, h, 0, 1, 0)
@@ -720,7 +727,9 @@ def conv_stats(device: "Device", img: np.ndarray, mask, scale: int, conv_format:
         a.bins, a.offset, a.range = int(bins), int(offset), int(rng)
         a.hist, a.sum, a.sumsq = aux, aux + 16 * bins, aux + 16 * bins + 8
         a.mean, a.stddev = aux + 16 * bins + 16, aux + 16 * bins + 32
-        _check_cuda(c.gvxb_conv_stats(device.h, ctypes.byref(a)))
+        a.work = work or None
+        for _ in range(repeat):
+            _check_cuda(c.gvxb_conv_stats(device.h, ctypes.byref(a)))
         out = np.empty((h, w), np.uint8)
         device.download(out, conv, pitch)
         raw = np.empty(2 * bins + 6, np.int64)
@@ -733,6 +742,8 @@ def conv_stats(device: "Device", img: np.ndarray, mask, scale: int, conv_format:
     finally:
         device.sync()
         device.free(src), device.free(conv), device.free(aux)
+        if work:
+            device.free(work)
 
 
 def band_rows(height: int, world: int, rank: int):

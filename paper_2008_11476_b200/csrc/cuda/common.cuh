@@ -17,6 +17,8 @@ struct gvxb_range {
     uintptr_t lo = 0, hi = 0;
 };
 
+constexpr int kTrackedRanges = 6; // read / write ranges a launch records for the next one's hazard test
+
 struct gvxb_ctx_s {
     int device = 0;
     int sm_count = 148;
@@ -30,7 +32,7 @@ struct gvxb_ctx_s {
     // read / wrote, valid only while nothing else was enqueued after it.
     int overlap = -1; // -1 auto (own stream only), 0 off, 1 on
     bool prev_kernel = false;
-    gvxb_range prev_r[4], prev_w[4];
+    gvxb_range prev_r[kTrackedRanges], prev_w[kTrackedRanges];
     int prev_nr = 0, prev_nw = 0;
 };
 
@@ -38,6 +40,15 @@ namespace gvxb_impl {
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int check_launch(gvxb_ctx ctx, const char* what);
+
+/// Bytes [p, p + n) as a tracked range; empty for a null pointer.
+inline gvxb_range bytes_range(const void* p, size_t n) {
+    gvxb_range r;
+    if (!p || !n) return r;
+    r.lo = reinterpret_cast<uintptr_t>(p);
+    r.hi = r.lo + n;
+    return r;
+}
 
 /// Bytes an image (all its frames) spans; empty for a null image.
 inline gvxb_range image_range(const gvxb_image& im) {

@@ -81,11 +81,11 @@ int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** a
     }
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return cuda_fail(e, what);
-    ctx->prev_nr = nr < 4 ? nr : 4;
-    ctx->prev_nw = nw < 4 ? nw : 4;
+    ctx->prev_nr = nr < kTrackedRanges ? nr : kTrackedRanges;
+    ctx->prev_nw = nw < kTrackedRanges ? nw : kTrackedRanges;
     for (int i = 0; i < ctx->prev_nr; ++i) ctx->prev_r[i] = r[i];
     for (int i = 0; i < ctx->prev_nw; ++i) ctx->prev_w[i] = w[i];
-    ctx->prev_kernel = nr <= 4 && nw <= 4;
+    ctx->prev_kernel = nr <= kTrackedRanges && nw <= kTrackedRanges;
     return check_launch(ctx, what);
 }
 

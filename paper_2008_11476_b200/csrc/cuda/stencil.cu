@@ -144,7 +144,46 @@ struct ConvStatsParams {
     gvxb_value* hist; // frames x bins (integer Value slots)
     unsigned long long* sum;
     unsigned long long* sumsq;
+    // one-launch form: as SepParams::acc (publish_if_last)
+    unsigned long long* acc;
+    int ctas_per_frame;
+    long long npx;
+    gvxb_value* mean;
+    gvxb_value* stddev;
 };
+
+__device__ __forceinline__ void meanstd_of(unsigned long long s1, unsigned long long s2, long long n, gvxb_value* mean,
+                                           gvxb_value* sd);
+
+/// One-launch conv+stats epilogue, called by every thread of a CTA after its
+/// histogram / sum atomics: the frame's last CTA to finish (every CTA fences
+/// its atomics before counting itself done) moves the accumulated histogram
+/// into the output slots, derives MeanStdDev, and leaves the accumulators,
+/// sums and counter zero for the next execution.
+__device__ __forceinline__ void publish_if_last(int frame, int tid, int nt, int bins, unsigned long long* acc_all,
+                                                gvxb_value* hist, unsigned long long* sum, unsigned long long* sumsq,
+                                                int ctas_per_frame, long long npx, gvxb_value* mean, gvxb_value* sd) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    unsigned long long* acc = acc_all + static_cast<int64_t>(frame) * (bins + 1);
+    if (tid == 0) last = atomicAdd(acc + bins, 1ull) == static_cast<unsigned long long>(ctas_per_frame - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (hist) {
+        for (int b = tid; b < bins; b += nt) {
+            gvxb_value& h = hist[static_cast<int64_t>(frame) * bins + b];
+            h.real = 0;
+            h.bits = static_cast<long long>(atomicExch(acc + b, 0ull));
+        }
+    }
+    if (tid == 0) {
+        const unsigned long long t1 = atomicExch(&sum[frame], 0ull), t2 = atomicExch(&sumsq[frame], 0ull);
+        meanstd_of(t1, t2, npx, mean ? mean + frame : nullptr, sd ? sd + frame : nullptr);
+        atomicExch(acc + bins, 0ull);
+    }
+}
 
 template <int K>
 __global__ void __launch_bounds__(kStThreads) conv_stats_kernel(const __grid_constant__ CUtensorMap map,
@@ -236,11 +275,15 @@ __global__ void __launch_bounds__(kStThreads) conv_stats_kernel(const __grid_con
         for (int b = threadIdx.x; b < p.bins; b += blockDim.x) {
             unsigned t = 0;
             for (int w = 0; w < kWarps; ++w) t += hist_smem[w * p.bins + b];
-            if (t)
-                atomicAdd(reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + b].bits),
-                          static_cast<unsigned long long>(t));
+            unsigned long long* slot =
+                p.acc ? p.acc + static_cast<int64_t>(frame) * (p.bins + 1) + b
+                      : reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + b].bits);
+            if (t) atomicAdd(slot, static_cast<unsigned long long>(t));
         }
     }
+    if (p.acc)
+        publish_if_last(frame, static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), p.bins, p.acc, p.hist, p.sum,
+                        p.sumsq, p.ctas_per_frame, p.npx, p.mean, p.stddev);
 }
 
 /// One launch clearing the histogram slots and both per-frame sums.
@@ -258,24 +301,29 @@ __global__ void zero_scratch_kernel(unsigned long long* hist, long long nh, unsi
 /// MeanStdDev finalize, one thread per frame:
 ///   mean = F32((sum * 1.0) / n);  sd = F32(sqrt(max((sumsq * 1.0) / n - m*m, 0.0)))
 /// with m the F32-rounded mean (the reduce_stddev node reads the mean scalar).
+__device__ __forceinline__ void meanstd_of(unsigned long long s1, unsigned long long s2, long long n, gvxb_value* mean,
+                                           gvxb_value* sd) {
+    const double dn = __ll2double_rn(n);
+    const double m = static_cast<double>(
+        __double2float_rn(__ddiv_rn(__dmul_rn(__ll2double_rn(static_cast<long long>(s1)), 1.0), dn)));
+    if (mean) {
+        mean->real = 1;
+        mean->bits = __double_as_longlong(m);
+    }
+    if (sd) {
+        const double ex2 = __ddiv_rn(__dmul_rn(__ll2double_rn(static_cast<long long>(s2)), 1.0), dn);
+        const double var0 = __dsub_rn(ex2, __dmul_rn(m, m));
+        const double var = var0 < 0.0 ? 0.0 : var0; // std::max(var0, 0.0)
+        sd->real = 1;
+        sd->bits = __double_as_longlong(static_cast<double>(__double2float_rn(__dsqrt_rn(var))));
+    }
+}
+
 __global__ void meanstd_finalize_kernel(const unsigned long long* sum, const unsigned long long* sumsq, long long n,
                                         int frames, gvxb_value* mean, gvxb_value* sd) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= frames) return;
-    const double dn = __ll2double_rn(n);
-    const double m = static_cast<double>(
-        __double2float_rn(__ddiv_rn(__dmul_rn(__ll2double_rn(static_cast<long long>(sum[f])), 1.0), dn)));
-    if (mean) {
-        mean[f].real = 1;
-        mean[f].bits = __double_as_longlong(m);
-    }
-    if (sd) {
-        const double ex2 = __ddiv_rn(__dmul_rn(__ll2double_rn(static_cast<long long>(sumsq[f])), 1.0), dn);
-        const double var0 = __dsub_rn(ex2, __dmul_rn(m, m));
-        const double var = var0 < 0.0 ? 0.0 : var0; // std::max(var0, 0.0)
-        sd[f].real = 1;
-        sd[f].bits = __double_as_longlong(static_cast<double>(__double2float_rn(__dsqrt_rn(var))));
-    }
+    meanstd_of(sum[f], sumsq[f], n, mean ? mean + f : nullptr, sd ? sd + f : nullptr);
 }
 
 
@@ -336,6 +384,14 @@ struct SepParams {
     int identity;
     unsigned long long* sum;
     unsigned long long* sumsq;
+    // one-launch form (acc != null): histogram accumulators and a CTA-done
+    // counter per frame, zero on entry; the frame's last CTA publishes the
+    // histogram and MeanStdDev and leaves the scratch zero again
+    unsigned long long* acc; // frames x (bins + 1): bins accumulators, then the counter
+    int ctas_per_frame;
+    long long npx;           // pixels per frame
+    gvxb_value* mean;
+    gvxb_value* stddev;
 };
 
 /// Columns c+j, j = -R .. R+3, of one tile row as pairs P(j) = (c+j, c+j+2).
@@ -495,16 +551,16 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
     __shared__ uint64_t bar;
     extern __shared__ uint4 hist_dyn[]; // kMode 2: [bin][lane][warp] u8 counters
     uint8_t* hist = reinterpret_cast<uint8_t*>(hist_dyn);
+    const int tid = static_cast<int>(threadIdx.x);
+    if (kMode >= 2) { // shared memory only: may overlap the previous grid's tail
+        for (int i = tid; i < kSepHistBytes / 16; i += NT) hist_dyn[i] = make_uint4(0, 0, 0, 0);
+    }
     pdl_prologue(p.pdl_wait);
 
-    const int tid = static_cast<int>(threadIdx.x);
     const int x0 = blockIdx.x * TW;
     const int y0 = p.band.row0 + blockIdx.y * p.th;
     const int n = min(y0 + p.th, p.band.row1) - y0;
     const int frame = blockIdx.z;
-    if (kMode >= 2) {
-        for (int i = tid; i < kSepHistBytes / 16; i += NT) hist_dyn[i] = make_uint4(0, 0, 0, 0);
-    }
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_barrier_init();
@@ -679,8 +735,10 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
                 bin = t / p.range;
             }
             if (bin < 0 || bin >= p.bins) continue; // out of range: skipped (ref:src/execute.cpp:717-724)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + bin].bits),
-                      static_cast<unsigned long long>(cnt));
+            unsigned long long* slot =
+                p.acc ? p.acc + static_cast<int64_t>(frame) * (p.bins + 1) + bin
+                      : reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + bin].bits);
+            atomicAdd(slot, static_cast<unsigned long long>(cnt));
         }
     }
 #pragma unroll
@@ -692,6 +750,9 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         atomicAdd(&p.sum[frame], static_cast<unsigned long long>(s1));
         atomicAdd(&p.sumsq[frame], static_cast<unsigned long long>(s2));
     }
+    if (p.acc)
+        publish_if_last(frame, tid, NT, p.bins, p.acc, p.hist, p.sum, p.sumsq, p.ctas_per_frame, p.npx, p.mean,
+                        p.stddev);
 }
 
 } // namespace gvxd
@@ -808,6 +869,7 @@ int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K,
     CUtensorMap map;
     if (int rc = make_u8_tensor_map(&map, s, sw, p.th + K - 1)) return rc;
     dim3 grid((s.width + tw - 1) / tw, (rows + p.th - 1) / p.th, frames);
+    if (p.acc) p.ctas_per_frame = static_cast<int>(grid.x * grid.y);
     const gvxb_range r[1] = {image_range(s)};
     p.pdl_wait = pdl_must_wait(ctx, r, 1, wr, nw);
     void* args[] = {&map, &p};
@@ -900,7 +962,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
     if (!a->sum || !a->sumsq) return fail(GVXB_ERR_INVALID, "conv_stats: sum scratch required");
     if (a->scale < 1) return fail(GVXB_ERR_INVALID, "conv_stats: scale must be >= 1");
     const int frames = s.frames > 0 ? s.frames : 1;
-    ConvStatsParams p;
+    ConvStatsParams p{};
     p.width = s.width;
     p.height = s.height;
     p.band = Band{0, s.height, s.height, 0, 0};
@@ -921,15 +983,15 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
     p.sumsq = reinterpret_cast<unsigned long long*>(a->sumsq);
     if (a->range == 0 && !p.identity_bins) return fail(GVXB_ERR_DIV_BY_ZERO, "histogram range is zero");
 
-    {
+    auto clear_scratch = [&]() -> int {
         const long long nh = a->hist ? static_cast<long long>(frames) * p.bins * 2 : 0;
         const long long total = nh + 2LL * frames;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 1024));
         untracked_op(ctx);
         zero_scratch_kernel<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<unsigned long long*>(a->hist), nh,
                                                              p.sum, p.sumsq, frames);
-        if (int rc = check_launch(ctx, "conv_stats scratch clear")) return rc;
-    }
+        return check_launch(ctx, "conv_stats scratch clear");
+    };
     cudaError_t e = cudaSuccess;
 
     {
@@ -952,6 +1014,25 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
             sp.sum = p.sum;
             sp.sumsq = p.sumsq;
             void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<2>(a->ksize, sp.clamp255, sp.frac);
+            if (a->work && frames == 1) {
+                // one launch (single frames: one execution per call; a batch
+                // amortises the clear / finalize launches and would pay the
+                // end-of-CTA fence in every CTA instead, measured -7% at 64
+                // frames): the frame's last CTA publishes histogram and statistics
+                // and re-zeroes the scratch; every written range is tracked, so the
+                // next execution waits for this one after its prologue (the
+                // shared-memory histogram clear overlaps this grid's tail)
+                sp.acc = reinterpret_cast<unsigned long long*>(a->work);
+                sp.npx = static_cast<long long>(s.width) * s.height;
+                sp.mean = a->mean;
+                sp.stddev = a->stddev;
+                const size_t fb = static_cast<size_t>(frames) * 8;
+                const gvxb_range w[5] = {image_range(a->converted), bytes_range(a->hist, 2 * fb * p.bins),
+                                         bytes_range(a->work, fb * (p.bins + 1)), bytes_range(a->sum, fb),
+                                         bytes_range(a->sumsq, fb)};
+                return sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2), w, 5);
+            }
+            if (int rc = clear_scratch()) return rc;
             const gvxb_range w[1] = {image_range(a->converted)}; // after the (untracked) scratch clear: waits anyway
             if (int rc = sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2), w, 1))
                 return rc;
@@ -966,6 +1047,16 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
     case 7: fn = reinterpret_cast<void*>(&conv_stats_kernel<7>), sh = kStTH + 6; break;
     default: return fail(GVXB_ERR_UNSUPPORTED, "conv_stats: ksize must be 3, 5 or 7");
     }
+    dim3 grid((s.width + kStTW - 1) / kStTW, (s.height + kStTH - 1) / kStTH, frames);
+    p.acc = frames == 1 ? reinterpret_cast<unsigned long long*>(a->work) : nullptr;
+    if (p.acc) {
+        p.ctas_per_frame = static_cast<int>(grid.x * grid.y);
+        p.npx = static_cast<long long>(s.width) * s.height;
+        p.mean = a->mean;
+        p.stddev = a->stddev;
+    } else if (int rc = clear_scratch()) {
+        return rc;
+    }
     CUtensorMap map;
     if (int rc = make_u8_tensor_map(&map, s, kStSW, sh)) return rc;
     const size_t dyn = sizeof(unsigned) * (kStThreads / 32) * static_cast<size_t>(p.bins);
@@ -973,11 +1064,10 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
         if (e != cudaSuccess) return cuda_fail(e, "conv_stats smem attribute");
     }
-    dim3 grid((s.width + kStTW - 1) / kStTW, (s.height + kStTH - 1) / kStTH, frames);
     void* args[] = {&map, &p};
     untracked_op(ctx);
     e = cudaLaunchKernel(fn, grid, dim3(kStThreads), args, dyn, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "conv_stats kernel launch");
     if (int rc = check_launch(ctx, "conv_stats kernel")) return rc;
-    return meanstd(ctx, a, p, frames, s);
+    return p.acc ? GVXB_OK : meanstd(ctx, a, p, frames, s);
 }

@@ -732,11 +732,14 @@ std::string Program::describe() const {
     return os.str();
 }
 
-int Program::launches_per_run() const {
+int Program::launches_per_run(int frames) const {
     int n = 0;
     for (const Unit& u : units) {
         if (u.kind == Unit::Kind::Jit) n += static_cast<int>(u.prog.kernels.size());
-        else if (u.kind == Unit::Kind::ConvStats) n += (u.out[2] != kInvalidId || u.out[3] != kInvalidId) ? 3 : 2;
+        // conv+stats: one kernel whose last CTA finalizes (single frames), else
+        // scratch clear + kernel (+ MeanStdDev finalize)
+        else if (u.kind == Unit::Kind::ConvStats && frames > 1)
+            n += (u.out[2] != kInvalidId || u.out[3] != kInvalidId) ? 3 : 2;
         else n += 1;
     }
     return n;
@@ -1017,8 +1020,11 @@ struct DeviceSession::Impl {
             const dev::Unit& u = prog->units[i];
             std::size_t bytes = 0;
             if (u.kind == dev::Unit::Kind::Jit) bytes = u.prog.scratch_bytes_per_frame * frames;
-            if (u.kind == dev::Unit::Kind::ConvStats) bytes = 16 * static_cast<std::size_t>(frames);
+            // conv+stats: sum, sumsq and the one-launch accumulators, zero between runs
+            if (u.kind == dev::Unit::Kind::ConvStats)
+                bytes = (16 + 8 * static_cast<std::size_t>(std::max(u.bins, 1) + 1)) * static_cast<std::size_t>(frames);
             if (bytes) dev::check(gvxb_alloc(ctx, bytes, &scratch[i]), "scratch allocation");
+            if (u.kind == dev::Unit::Kind::ConvStats) dev::check(gvxb_memset(ctx, scratch[i], 0, bytes), "scratch clear");
         }
     }
 
@@ -1079,6 +1085,7 @@ struct DeviceSession::Impl {
             a.hist = values(u.out[1]);
             a.sum = static_cast<int64_t*>(scratch[idx]);
             a.sumsq = static_cast<int64_t*>(scratch[idx]) + frames;
+            a.work = static_cast<int64_t*>(scratch[idx]) + 2 * frames;
             a.mean = values(u.out[2]);
             a.stddev = values(u.out[3]);
             dev::check(gvxb_conv_stats(ctx, &a), "gvxb_conv_stats");
@@ -1696,7 +1703,7 @@ Buffer DeviceSession::download(ObjectId id, int frame) {
 }
 
 int DeviceSession::frames() const { return impl_->frames; }
-int DeviceSession::launches_per_run() const { return impl_->prog->launches_per_run(); }
+int DeviceSession::launches_per_run() const { return impl_->prog->launches_per_run(impl_->frames); }
 std::string DeviceSession::describe() const { return impl_->prog->describe(); }
 
 // ------------------------------------------------------------ HostPipeline

@@ -84,7 +84,7 @@ struct Program {
     std::vector<Unit> units;
     std::map<ObjectId, ObjInfo> objects; ///< every object a unit touches
     std::string describe() const;
-    int launches_per_run() const;
+    int launches_per_run(int frames = 1) const;
 };
 
 /// Lowers a verified graph to one JIT unit per node (run_naive).

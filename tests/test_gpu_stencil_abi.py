@@ -59,13 +59,18 @@ CONV = [
 ]
 
 
+@pytest.mark.parametrize("one_launch", [False, True], ids=["clear+finalize", "one-launch"])
 @pytest.mark.parametrize("case", CONV, ids=[c[0] for c in CONV])
-def test_conv_stats_matches_oracle(case, dev, gvx, oracle_mod):
+def test_conv_stats_matches_oracle(case, one_launch, dev, gvx, oracle_mod):
+    """Both forms of gvxb_conv_stats: scratch clear + kernel + finalize, and
+    the single kernel whose last CTA per frame publishes the results (run
+    three times: each run must leave its scratch zero for the next)."""
     name, mask, scale, shift, wrap, bins, offset, rng_ = case
     rng = np.random.default_rng(11)
     for w, h in SIZES:
         img = rng.integers(0, 256, (h, w), dtype=np.uint8)
-        conv, hist, mean, sd = gvx.conv_stats(dev, img, mask, scale, 2, shift, wrap, bins, offset, rng_)
+        conv, hist, mean, sd = gvx.conv_stats(dev, img, mask, scale, 2, shift, wrap, bins, offset, rng_,
+                                              one_launch=one_launch, repeat=3 if one_launch else 1)
         wconv, whist, wmean, wsd = oracle_mod.port_conv_stats(img, mask, scale, -32768, 32767, shift, wrap, bins,
                                                               offset, rng_)
         assert np.array_equal(conv, wconv), f"{name} {w}x{h}: converted image"
