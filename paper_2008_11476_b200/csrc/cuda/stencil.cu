@@ -542,7 +542,7 @@ __device__ __forceinline__ void store4(uint8_t* dp, uint32_t w, int c, int width
 /// kMode 0: U8 stencil output; 1: unsharp chain sat_u8(2x - blur);
 /// 2: Convolve -> ConvertDepth -> per-CTA value histogram; 3: as 2 and also
 /// store the converted image.
-template <int K, int kMode, bool kClamp, int kLoad>
+template <int K, int kMode, bool kClamp, int kLoad, bool kPub = false>
 __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_constant__ CUtensorMap map, SepParams p) {
     constexpr int NT = sep_threads(kMode), TW = 4 * NT, SW = TW + 32;
     constexpr int R = K / 2;
@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
             }
             if (bin < 0 || bin >= p.bins) continue; // out of range: skipped (ref:src/execute.cpp:717-724)
             unsigned long long* slot =
-                p.acc ? p.acc + static_cast<int64_t>(frame) * (p.bins + 1) + bin
-                      : reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + bin].bits);
+                kPub ? p.acc + static_cast<int64_t>(frame) * (p.bins + 1) + bin
+                     : reinterpret_cast<unsigned long long*>(&p.hist[static_cast<int64_t>(frame) * p.bins + bin].bits);
             atomicAdd(slot, static_cast<unsigned long long>(cnt));
         }
     }
@@ -750,7 +750,9 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         atomicAdd(&p.sum[frame], static_cast<unsigned long long>(s1));
         atomicAdd(&p.sumsq[frame], static_cast<unsigned long long>(s2));
     }
-    if (p.acc)
+    // the one-launch form is its own instantiation: a (skipped) epilogue in
+    // the batch kernel cost it 2.4% (measured)
+    if constexpr (kPub)
         publish_if_last(frame, tid, NT, p.bins, p.acc, p.hist, p.sum, p.sumsq, p.ctas_per_frame, p.npx, p.mean,
                         p.stddev);
 }
@@ -837,6 +839,22 @@ void* sep_fn_f(bool clamp, int frac) {
     case 2: return sep_fn<K, M, 2>(clamp);
     case 1: return sep_fn<K, M, 1>(clamp);
     default: return sep_fn<K, M, 0>(clamp);
+    }
+}
+
+/// The one-launch (publishing) conv+stats kernels: modes 2 / 3 with the
+/// fractional-symmetric load (the binomial masks); others run the batch form.
+template <int M>
+void* sep_fn_pub(int k, bool clamp, int frac) {
+    if (frac != 3) return nullptr;
+    switch (k) {
+    case 3: return clamp ? reinterpret_cast<void*>(&sep_kernel<3, M, true, 3, true>)
+                         : reinterpret_cast<void*>(&sep_kernel<3, M, false, 3, true>);
+    case 5: return clamp ? reinterpret_cast<void*>(&sep_kernel<5, M, true, 3, true>)
+                         : reinterpret_cast<void*>(&sep_kernel<5, M, false, 3, true>);
+    case 7: return clamp ? reinterpret_cast<void*>(&sep_kernel<7, M, true, 3, true>)
+                         : reinterpret_cast<void*>(&sep_kernel<7, M, false, 3, true>);
+    default: return nullptr;
     }
 }
 
@@ -1014,7 +1032,8 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
             sp.sum = p.sum;
             sp.sumsq = p.sumsq;
             void* fn = sp.dst ? sep_fn_k<3>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<2>(a->ksize, sp.clamp255, sp.frac);
-            if (a->work && frames == 1) {
+            void* pub = sp.dst ? sep_fn_pub<3>(a->ksize, sp.clamp255, sp.frac) : sep_fn_pub<2>(a->ksize, sp.clamp255, sp.frac);
+            if (a->work && frames == 1 && pub) {
                 // one launch (single frames: one execution per call; a batch
                 // amortises the clear / finalize launches and would pay the
                 // end-of-CTA fence in every CTA instead, measured -7% at 64
@@ -1030,7 +1049,7 @@ extern "C" int gvxb_conv_stats(gvxb_ctx ctx, const gvxb_conv_stats_args* a) {
                 const gvxb_range w[5] = {image_range(a->converted), bytes_range(a->hist, 2 * fb * p.bins),
                                          bytes_range(a->work, fb * (p.bins + 1)), bytes_range(a->sum, fb),
                                          bytes_range(a->sumsq, fb)};
-                return sep_launch(ctx, fn, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2), w, 5);
+                return sep_launch(ctx, pub, s, sp, a->ksize, s.height, kSepHistTH, kSepHistBytes, sep_threads(2), w, 5);
             }
             if (int rc = clear_scratch()) return rc;
             const gvxb_range w[1] = {image_range(a->converted)}; // after the (untracked) scratch clear: waits anyway

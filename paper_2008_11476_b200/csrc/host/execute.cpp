@@ -958,6 +958,7 @@ struct DeviceSession::Impl {
     std::vector<void*> scratch; ///< per unit (JIT reduce scratch, conv sums)
 
     bool owns_ctx = false; ///< ctx created for this storage (destroyed with it)
+    int last_launches = 0; ///< kernels the last DeviceSession::launch enqueued
 
     ~Impl() {
         if (!ctx) return;
@@ -1680,7 +1681,9 @@ void DeviceSession::set_overlap(int mode) { dev::check(gvxb_ctx_set_overlap(impl
 
 void DeviceSession::launch() {
     if (impl_->scratch.size() != impl_->prog->units.size()) impl_->prepare();
+    const std::int64_t n0 = gvxb_launch_count(impl_->ctx);
     impl_->run_all();
+    impl_->last_launches = static_cast<int>(gvxb_launch_count(impl_->ctx) - n0);
 }
 
 void DeviceSession::synchronize() {
@@ -1703,7 +1706,11 @@ Buffer DeviceSession::download(ObjectId id, int frame) {
 }
 
 int DeviceSession::frames() const { return impl_->frames; }
-int DeviceSession::launches_per_run() const { return impl_->prog->launches_per_run(impl_->frames); }
+int DeviceSession::launches_per_run() const {
+    // what the last execution launched (conv+stats picks its one- or
+    // three-launch form in the C-ABI), else the program's estimate
+    return impl_->last_launches > 0 ? impl_->last_launches : impl_->prog->launches_per_run(impl_->frames);
+}
 std::string DeviceSession::describe() const { return impl_->prog->describe(); }
 
 // ------------------------------------------------------------ HostPipeline
