@@ -40,7 +40,7 @@ CONFIG_NAME = {
 }
 # algorithmic HBM bytes per output pixel of the fused program
 ALGO_BYTES = {1: 3, 2: 2, 3: 2, 4: 1, 5: 3}
-KERNEL_NAME = {1: "edge8_kernel", 2: "harris_kernel", 3: "sep_kernel<5,1> (separable stencil, unsharp epilogue)", 4: "sep_kernel<5,2> (separable conv + value histogram)",
+KERNEL_NAME = {1: "edge8_kernel", 2: "harris4_kernel", 3: "sep_kernel<5,1> (separable stencil, unsharp epilogue)", 4: "sep_kernel<5,2> (separable conv + value histogram)",
                5: "edge8_kernel"}
 # frames per launch: each step is one fused launch over a batch of frames; the
 # two rotating batches (inputs + outputs) span >= 4x the 126 MB L2 (SURVEY.md
