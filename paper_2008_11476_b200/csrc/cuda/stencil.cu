@@ -613,6 +613,25 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
         bool have_pend = false;
         auto emit = [&](Q4 acc) {
             if (kMode == 1) {
+#ifndef GVX_SEP_FMNMX_CLAMP
+                // -(1.5*2^23 + b) by round-up of the negated product; the centre
+                // pixels as 1.5*2^23 + x, so 2(1.5*2^23 + x) - (1.5*2^23 + b) =
+                // 1.5*2^23 + y, y = 2x - b in [-255, 510], whose low 16 bits are
+                // y (two's complement); the U8 saturation runs as s16x2 max / min
+                // on two columns per register
+                const Q4 q = sep_neg_quotient(acc, p.qscale, p.qbase, kClamp);
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(crow);
+                auto centre = [&](int k) { return __uint_as_float(__byte_perm(w, 0x4B400000u, 0x7640u | k)); };
+                const float2 two = f2(2.f, 2.f);
+                const float2 ue = fma2(two, f2(centre(0), centre(2)), q.e), uo = fma2(two, f2(centre(1), centre(3)), q.o);
+                uint32_t lo = __byte_perm(__float_as_uint(ue.x), __float_as_uint(uo.x), 0x5410u); // columns c, c+1
+                uint32_t hi = __byte_perm(__float_as_uint(ue.y), __float_as_uint(uo.y), 0x5410u); // columns c+2, c+3
+                asm("max.s16x2 %0, %0, %1;" : "+r"(lo) : "r"(0u));
+                asm("max.s16x2 %0, %0, %1;" : "+r"(hi) : "r"(0u));
+                asm("min.s16x2 %0, %0, %1;" : "+r"(lo) : "r"(0x00FF00FFu));
+                asm("min.s16x2 %0, %0, %1;" : "+r"(hi) : "r"(0x00FF00FFu));
+                store(__byte_perm(lo, hi, 0x6420u));
+#else
                 // -(1.5*2^23 + b) by round-up of the negated product, then
                 // 2(2^23 + x) - (1.5*2^23 + b) = 2^22 + (2x - b), clamped to U8
                 const Q4 q = sep_neg_quotient(acc, p.qscale, p.qbase, kClamp);
@@ -624,6 +643,7 @@ __global__ void __launch_bounds__(sep_threads(kMode)) sep_kernel(const __grid_co
                 re = f2(fminf(fmaxf(re.x, lo), hi), fminf(fmaxf(re.y, lo), hi));
                 ro = f2(fminf(fmaxf(ro.x, lo), hi), fminf(fmaxf(ro.y, lo), hi));
                 store(sep_pack(Q4{add2(re, lift), add2(ro, lift)})); // 1.5*2^23 + y
+#endif
                 crow += SW;
                 drow += p.dst_pitch;
             } else if (kMode == 0) {
