@@ -1751,14 +1751,18 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         for (const RegionObject& o : objs)
             b += static_cast<std::size_t>(TW + 2 * o.halo_x) * (TH + 2 * o.halo_y) *
                  static_cast<std::size_t>(bytes_per_pixel(o.format));
+        std::size_t rs = 0; // the separable row sums share one buffer (nodes run in turn)
         for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
-            if (!tab[ni]) continue;
+            if (nodes[ni].k->kind != AbstractionKind::Local) continue;
             int hx = 0, hy = 0;
             node_halo(ni, hx, hy);
             const LocalKernel& lk = nodes[ni].k->local();
-            b += static_cast<std::size_t>(TW + 2 * hx + 2 * (lk.window_w / 2)) * (TH + 2 * hy + 2 * (lk.window_h / 2)) * 8;
+            if (tab[ni])
+                b += static_cast<std::size_t>(TW + 2 * hx + 2 * (lk.window_w / 2)) * (TH + 2 * hy + 2 * (lk.window_h / 2)) * 8;
+            else
+                rs = std::max(rs, static_cast<std::size_t>(TW + 2 * hx) * (TH + 2 * hy + 2 * (lk.window_h / 2)) * 8);
         }
-        return b;
+        return b + rs;
     };
     while (smem_bytes() > 40 * 1024 && (TW > 32 || TH > 8)) (TH > 8 ? TH : TW) /= 2;
     if (smem_bytes() > 40 * 1024) throw unsupported("intermediates exceed shared memory");
@@ -1818,6 +1822,8 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
              << " + rx, 0, W - 1)];\n    }\n  }\n";
     }
     if (staged) body << "  __syncthreads();\n";
+    std::size_t rs_bytes = 0; // separable row-sum buffer (declared at the top once its size is known)
+    body << "@RSBUF@";
     for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
         const RegionNode& rn = nodes[ni];
         const AbstractionKernel& k = *rn.k;
@@ -1881,6 +1887,14 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
             const int hw = lk.window_w / 2, hh = lk.window_h / 2;
             const Expr* mc = nullptr;
             const Expr* gexp = tab[ni] ? tabulated_g(lk, &mc) : nullptr;
+            bool sep_box = !uses_op(*lk.tap_body, ExprOp::MaskCoef);
+            if (!sep_box) { // a mask whose coefficients are all integer 1
+                const std::vector<Value>& mk = lk.mask.empty() ? rn.matrix : lk.mask;
+                sep_box = mk.size() == static_cast<std::size_t>(lk.window_w * lk.window_h);
+                for (const Value& v : mk) sep_box = sep_box && !v.real && v.i == 1;
+            }
+            static const bool sep_on = std::getenv("GVX_REGION_NOSEP") == nullptr;
+            sep_box = sep_box && sep_on;
             std::vector<Emitter::TV> gtaps;
             if (gexp) {
                 // g once per position of the node's region + its window radius
@@ -1945,7 +1959,64 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                 nb << "      continue;\n    }\n";
             }
             em.mode = Emitter::Mode::Tap;
-            const std::string taps = gexp ? typed_combine(em, lk, gtaps) : typed_taps(em, lk);
+            // separable evaluation of box-like sums (Clamp border, integer taps
+            // whose mask coefficients are all 1, no wrapping): each row of the
+            // window summed once per position into shared memory, then the
+            // rows of the window summed per entry -- w + h - 1 instead of w h
+            // tap evaluations per entry
+            std::string taps;
+            if (!gexp && sep_box && lk.combine == CombineMode::Sum && lk.boundary == BoundaryMode::Clamp && hh > 0) {
+                std::vector<Emitter::TV> row;
+                bool ok = true;
+                std::fill(used_obj.begin(), used_obj.end(), false);
+                for (int dx = -hw; dx <= hw && ok; ++dx) {
+                    em.tdx = dx;
+                    em.tdy = 0;
+                    Emitter::TV t;
+                    ok = em.temit(*lk.tap_body, t) && t.t != 'd';
+                    row.push_back(t);
+                }
+                __int128 lo = 0, hi = 0;
+                for (const Emitter::TV& t : row) lo += t.lo, hi += t.hi;
+                const __int128 tlo = lo * lk.window_h, thi = hi * lk.window_h;
+                ok = ok && tlo >= Emitter::kI64Lo && thi <= Emitter::kI64Hi;
+                if (ok) {
+                    const bool i32 = tlo >= Emitter::kI32Lo && thi <= Emitter::kI32Hi;
+                    const char* ty = i32 ? "int" : "i64";
+                    const int RW = rw(oref), RHs = rh(oref) + 2 * hh;
+                    const std::string rs = "rs" + std::to_string(ni);
+                    std::ostringstream sum;
+                    for (std::size_t k = 0; k < row.size(); ++k)
+                        sum << (k ? " + " : "") << (i32 ? row[k].c : Emitter::as_i64(row[k]));
+                    rs_bytes = std::max(rs_bytes, static_cast<std::size_t>(RW) * RHs * 8);
+                    body << "  // node " << ni << ": window rows summed once per position\n"
+                         << "  " << ty << "* " << rs << " = reinterpret_cast<" << ty << "*>(rsbuf);\n"
+                         << "  for (int ry = threadIdx.y; ry < " << RHs << "; ry += 8)\n"
+                         << "  #pragma unroll\n"
+                         << "  for (int ix = 0; ix < " << (RW + 31) / 32 << "; ++ix) {\n"
+                         << "    const int rx = threadIdx.x + 32 * ix;\n";
+                    if (RW % 32) body << "    if (rx >= " << RW << ") break;\n";
+                    body << "    const int px = tx0 - " << R.halo_x << " + rx, py = ty0 - " << R.halo_y + hh << " + ry;\n";
+                    for (std::size_t o = 0; o < objs.size(); ++o)
+                        if (used_obj[o])
+                            body << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * "
+                                 << rw(static_cast<int>(o)) << " + px - tx0 + " << objs[o].halo_x << ";\n";
+                    body << "    " << rs << "[ry * " << RW << " + rx] = (" << ty << ")(" << sum.str() << ");\n"
+                         << "  }\n  __syncthreads();\n";
+                    // per entry: the window's rows (entry rows ry .. ry + 2 hh of rs)
+                    std::ostringstream cs;
+                    cs << "    " << ty << " cmbt = " << rs << "[(ry + 0) * " << RW << " + rx]";
+                    for (int dy = 1; dy < lk.window_h; ++dy) cs << " + " << rs << "[(ry + " << dy << ") * " << RW << " + rx]";
+                    cs << ";\n    V cmb = vi((i64)cmbt);\n";
+                    taps = cs.str();
+                    Emitter::TV acc = Emitter::tint("cmbt", lo * lk.window_h, hi * lk.window_h);
+                    if (!i32) acc.t = 'l';
+                    em.cmb_typed = true;
+                    em.cmb_tv = acc;
+                    std::fill(used_obj.begin(), used_obj.end(), false);
+                }
+            }
+            if (taps.empty()) taps = gexp ? typed_combine(em, lk, gtaps) : typed_taps(em, lk);
             if (taps.empty()) throw unsupported("run-time typed tap body");
             em.tdx = em.tdy = 0;
             em.mode = Emitter::Mode::Post;
@@ -2028,7 +2099,10 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     std::string pre = kPrelude;
     const std::string key = "NFIELDS";
     pre.replace(pre.find(key), key.size(), std::to_string(prog.fields()));
-    ks.source = pre + helpers.str() + body.str();
+    std::string text = body.str();
+    const std::size_t at = text.find("@RSBUF@");
+    text.replace(at, 7, rs_bytes ? "  __shared__ alignas(8) unsigned char rsbuf[" + std::to_string(rs_bytes) + "];\n" : "");
+    ks.source = pre + helpers.str() + text;
     prog.kernels.push_back(std::move(ks));
     return prog;
 }
