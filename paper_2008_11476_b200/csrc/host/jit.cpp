@@ -1812,7 +1812,8 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         const char* ct = storage_ctype(objs[o].format);
         const int RWo = rw(static_cast<int>(o)), RHo = rh(static_cast<int>(o));
         // one row pointer per entry row; 32-column blocks unrolled
-        body << "  for (int ry = threadIdx.y; ry < " << RHo << "; ry += 8) {\n"
+        body << "#pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (RHo + 7) / 8 << "; ++iy_, ry += 8) {\n"
+             << (RHo % 8 ? "    if (ry >= " + std::to_string(RHo) + ") break;\n" : std::string())
              << "    const int y = clampi(ty0 - " << objs[o].halo_y << " + ry, 0, H - 1);\n"
              << "    const " << ct << "* src = (const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
              << f + 2 << "] + (u64)y * p.f[" << f + 1 << "]);\n"
@@ -1910,9 +1911,10 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                 const std::string ga = "gk" + std::to_string(ni);
                 body << "  // node " << ni << " tap computation, tabulated\n"
                      << "  __shared__ " << gty << " " << ga << "[" << GW * GH << "];\n"
-                     << "  for (int ry = threadIdx.y; ry < " << (GW * GH) / (GW) << "; ry += 8)\n"
+                     << "  #pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (GH + 7) / 8 << "; ++iy_, ry += 8)\n"
                      << "  #pragma unroll\n"
                      << "  for (int ix = 0; ix < " << ((GW) + 31) / 32 << "; ++ix) {\n"
+                     << (GH % 8 ? "    if (ry >= " + std::to_string(GH) + ") break;\n" : std::string())
                      << "    const int rx = threadIdx.x + 32 * ix;\n"
                      << "    if (rx >= " << (GW) << ") break;\n"
                      << "    const int e = ry * " << (GW) << " + rx;\n"
@@ -1991,9 +1993,10 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                     rs_bytes = std::max(rs_bytes, static_cast<std::size_t>(RW) * RHs * 8);
                     body << "  // node " << ni << ": window rows summed once per position\n"
                          << "  " << ty << "* " << rs << " = reinterpret_cast<" << ty << "*>(rsbuf);\n"
-                         << "  for (int ry = threadIdx.y; ry < " << RHs << "; ry += 8)\n"
+                         << "  #pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (RHs + 7) / 8 << "; ++iy_, ry += 8)\n"
                          << "  #pragma unroll\n"
                          << "  for (int ix = 0; ix < " << (RW + 31) / 32 << "; ++ix) {\n"
+                         << (RHs % 8 ? "    if (ry >= " + std::to_string(RHs) + ") break;\n" : std::string())
                          << "    const int rx = threadIdx.x + 32 * ix;\n";
                     if (RW % 32) body << "    if (rx >= " << RW << ") break;\n";
                     body << "    const int px = tx0 - " << R.halo_x << " + rx, py = ty0 - " << R.halo_y + hh << " + ry;\n";
@@ -2042,9 +2045,10 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                      << " <= W && ty0 + " << TH + R.halo_y << " <= H) {\n";
             else
                 body << "  } else {\n";
-            body << "  for (int ry = threadIdx.y; ry < " << rh(oref) << "; ry += 8)\n"
+            body << "  #pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (rh(oref) + 7) / 8 << "; ++iy_, ry += 8)\n"
                  << "  #pragma unroll\n"
                  << "  for (int ix = 0; ix < " << (rw(oref) + 31) / 32 << "; ++ix) {\n"
+                 << (rh(oref) % 8 ? "    if (ry >= " + std::to_string(rh(oref)) + ") break;\n" : std::string())
                  << "    const int rx = threadIdx.x + 32 * ix;\n";
             if (rw(oref) % 32) body << "    if (rx >= " << rw(oref) << ") break;\n";
             body << "    const int e = ry * " << rw(oref) << " + rx;\n"
@@ -2059,9 +2063,10 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
             const RegionObject& O = objs[static_cast<std::size_t>(o)];
             body << "  if (tx0 - " << O.halo_x << " < 0 || ty0 - " << O.halo_y << " < 0 || tx0 + " << TW + O.halo_x
                  << " > W || ty0 + " << TH + O.halo_y << " > H) {\n"
-                 << "    for (int ry = threadIdx.y; ry < " << (rw(o) * rh(o)) / (rw(o)) << "; ry += 8)\n"
+                 << "    #pragma unroll\n    for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (rh(o) + 7) / 8 << "; ++iy_, ry += 8)\n"
                  << "    #pragma unroll\n"
                  << "    for (int ix = 0; ix < " << ((rw(o)) + 31) / 32 << "; ++ix) {\n"
+                 << (rh(o) % 8 ? "      if (ry >= " + std::to_string(rh(o)) + ") break;\n" : std::string())
                  << "      const int rx = threadIdx.x + 32 * ix;\n"
                  << "      if (rx >= " << (rw(o)) << ") break;\n"
                  << "      const int e = ry * " << (rw(o)) << " + rx;\n"
@@ -2079,7 +2084,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         if (objs[o].store < 0) continue;
         const int f = field_in(static_cast<int>(ins.size()) + objs[o].store);
         const char* ct = storage_ctype(objs[o].format);
-        body << "  for (int ry = threadIdx.y; ry < " << TH << "; ry += 8) {\n"
+        body << "#pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (TH + 7) / 8 << "; ++iy_, ry += 8) {\n"
              << "    const int gy = ty0 + ry;\n    if (gy >= ROW1) break;\n"
              << "    " << ct << "* row = (" << ct << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
              << "] + (u64)gy * p.f[" << f + 1 << "]);\n"
