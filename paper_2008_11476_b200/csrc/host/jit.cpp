@@ -117,8 +117,12 @@ __device__ __forceinline__ i64 t_cast_d(double r, i64 lo, i64 hi, int pol) {
 __device__ __forceinline__ i64 t_sat(i64 x, i64 lo, i64 hi) { return x < lo ? lo : (x > hi ? hi : x); }
 // round half away from zero of x / d (d > 0 a literal): llround(x * fl(1/d))
 // for |x| < 2^51 when d is odd or a power of two (Emitter::temit, Cast)
-__device__ __forceinline__ i64 t_rdiv(i64 x, i64 d) { return x >= 0 ? (2 * x + d) / (2 * d) : -((d - 2 * x) / (2 * d)); }
-__device__ __forceinline__ int t_rdiv32(int x, int d) { return x >= 0 ? (2 * x + d) / (2 * d) : -((d - 2 * x) / (2 * d)); }
+__device__ __forceinline__ i64 t_rdiv(i64 x, i64 d) {
+  const i64 q = (i64)((2ull * (u64)(x < 0 ? -x : x) + (u64)d) / (2ull * (u64)d)); return x < 0 ? -q : q;
+}
+__device__ __forceinline__ int t_rdiv32(int x, int d) {
+  const int q = (int)((2u * (unsigned)(x < 0 ? -x : x) + (unsigned)d) / (2u * (unsigned)d)); return x < 0 ? -q : q;
+}
 // llround(sqrt((double)n)) for integer 0 <= n < 2^24: fp32 estimate, then
 // the integer correction k* = largest k with k*k - k < n (no n is a half
 // square, so half-away rounding never ties)
