@@ -1781,7 +1781,16 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     // a node's code reads object o relative to the entry being evaluated:
     // index base b<o> (set per entry) + dy * row length + dx
     std::vector<bool> used_obj(objs.size());
-    auto entry = [&](int o, int dx, int dy) {
+    // point nodes evaluated inside their consumers (see the node loop): the
+    // object's value is its producer's expression at the same entry
+    std::vector<bool> inline_obj(objs.size(), false);
+    std::vector<std::string> inline_code(objs.size());
+    std::vector<std::vector<int>> inline_uses(objs.size());
+    std::function<std::string(int, int, int)> entry = [&](int o, int dx, int dy) -> std::string {
+        if (inline_obj[static_cast<std::size_t>(o)]) {
+            for (int u : inline_uses[static_cast<std::size_t>(o)]) used_obj[static_cast<std::size_t>(u)] = true;
+            return inline_code[static_cast<std::size_t>(o)];
+        }
         used_obj[static_cast<std::size_t>(o)] = true;
         return "ro" + std::to_string(o) + "[b" + std::to_string(o) + " + (" + std::to_string(dy * rw(o) + dx) + ")]";
     };
@@ -1800,13 +1809,39 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         return true;
     };
 
+    // point nodes evaluated inside their consumers (pre-pass: their objects
+    // get no shared memory): outputs read only at the same entry by later
+    // nodes (no halo, not stored), bodies that cannot raise
+    static const bool inline_on = std::getenv("GVX_REGION_NOINLINE") == nullptr;
+    std::vector<bool> inline_node(nodes.size(), false);
+    for (std::size_t ni = 0; ni < nodes.size() && inline_on; ++ni) {
+        const RegionNode& rn = nodes[ni];
+        if (rn.k->kind != AbstractionKind::Point) continue;
+        const PointKernel& pk = rn.k->point();
+        bool ok = false;
+        for (std::size_t j = 0; j < rn.out_obj.size(); ++j) {
+            const int o = rn.out_obj[j];
+            if (o < 0) continue;
+            const RegionObject& O = objs[static_cast<std::size_t>(o)];
+            ok = O.halo_x == 0 && O.halo_y == 0 && O.store < 0 && O.load < 0 && j < pk.outputs.size() &&
+                 pk.outputs[j].channel_bodies.size() == 1 && !uses_op(*pk.outputs[j].channel_bodies[0], ExprOp::Div) &&
+                 !uses_op(*pk.outputs[j].channel_bodies[0], ExprOp::ArrayAt);
+            if (!ok) break;
+        }
+        if (!ok) continue;
+        inline_node[ni] = true;
+        for (int o : rn.out_obj)
+            if (o >= 0) inline_obj[static_cast<std::size_t>(o)] = true;
+    }
+
     std::ostringstream helpers, body;
     body << "extern \"C\" __global__ void gvx_region(const P p) {\n"
          << "  const int W = (int)p.f[2], H = (int)p.f[3];\n  const int fr = blockIdx.z;\n  u64 rd = 0;\n"
          << "  const int tx0 = (int)blockIdx.x * " << TW << ", ty0 = ROW0 + (int)blockIdx.y * " << TH << ";\n";
     for (std::size_t o = 0; o < objs.size(); ++o)
-        body << "  __shared__ " << storage_ctype(objs[o].format) << " ro" << o << "["
-             << rw(static_cast<int>(o)) * rh(static_cast<int>(o)) << "];\n";
+        if (!inline_obj[o])
+            body << "  __shared__ " << storage_ctype(objs[o].format) << " ro" << o << "["
+                 << rw(static_cast<int>(o)) * rh(static_cast<int>(o)) << "];\n";
     // region inputs staged once: entry = input at the CLAMPED position
     bool staged = false;
     for (std::size_t o = 0; o < objs.size(); ++o) {
@@ -1848,6 +1883,48 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                 oref = o;
         if (oref < 0) throw unsupported("node without a region output");
         const RegionObject& R = objs[static_cast<std::size_t>(oref)];
+        // a point node whose outputs are read only at the same entry by later
+        // nodes of the region (no halo, not stored) and whose body cannot
+        // raise (no division / array index) is not given a pass of its own:
+        // its consumers evaluate its expression in place
+        if (inline_node[ni]) {
+            const PointKernel& pk = k.point();
+            bool ok = true;
+            {
+                em.mode = Emitter::Mode::Point;
+                std::vector<std::pair<int, Emitter::TV>> vals;
+                for (std::size_t j = 0; j < rn.out_obj.size() && ok; ++j) {
+                    if (rn.out_obj[j] < 0) continue;
+                    std::fill(used_obj.begin(), used_obj.end(), false);
+                    Emitter::TV v;
+                    ok = em.temit(*pk.outputs[j].channel_bodies[0], v);
+                    if (!ok) break;
+                    const int o = rn.out_obj[j];
+                    std::vector<int> uses;
+                    for (std::size_t u = 0; u < objs.size(); ++u)
+                        if (used_obj[u]) uses.push_back(static_cast<int>(u));
+                    inline_uses[static_cast<std::size_t>(o)] = uses;
+                    vals.push_back({o, v});
+                }
+                if (ok) {
+                    for (auto& [o, v] : vals) {
+                        TVproto& r = orange[static_cast<std::size_t>(o)];
+                        if (v.t != 'd' && r.t != 'd' && v.lo >= r.lo && v.hi <= r.hi)
+                            r.lo = static_cast<long long>(v.lo), r.hi = static_cast<long long>(v.hi);
+                        const ImageFormat f = objs[static_cast<std::size_t>(o)].format;
+                        inline_code[static_cast<std::size_t>(o)] =
+                            f == ImageFormat::F32 ? "((float)" + Emitter::as_dbl(v) + ")"
+                                                  : (v.t == 'd' ? std::string("0")
+                                                                : "((" + std::string(storage_ctype(f)) + ")(" + v.c + "))");
+                    }
+                    body << "  // node " << ni << ": " << k.name << " (evaluated by its consumers)\n";
+                    helpers << em.helpers.str();
+                    std::fill(used_obj.begin(), used_obj.end(), false);
+                    continue;
+                }
+            }
+            throw unsupported("run-time typed point body");
+        }
         // in-image entries only (their taps then sit at constant offsets from
         // the entry); out-of-image entries replicate the clamped one below
         std::ostringstream nb;
@@ -2061,10 +2138,12 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
             body << bases.str() << extra_base << nb.str() << "  }\n";
         }
         body << "  }\n  __syncthreads();\n";
-        // out-of-image entries = the entry at the clamped position (border tiles)
+        // out-of-image entries = the entry at the clamped position (border
+        // tiles); an object without halo is only ever read at in-image entries
         for (int o : rn.out_obj) {
             if (o < 0) continue;
             const RegionObject& O = objs[static_cast<std::size_t>(o)];
+            if (O.halo_x == 0 && O.halo_y == 0) continue;
             body << "  if (tx0 - " << O.halo_x << " < 0 || ty0 - " << O.halo_y << " < 0 || tx0 + " << TW + O.halo_x
                  << " > W || ty0 + " << TH + O.halo_y << " > H) {\n"
                  << "    #pragma unroll\n    for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (rh(o) + 7) / 8 << "; ++iy_, ry += 8)\n"
