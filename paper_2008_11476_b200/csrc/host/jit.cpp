@@ -1776,7 +1776,17 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     prog.n_outputs = static_cast<int>(outs.size());
     prog.dims_from = -1;
     prog.counts_reads = false;
-    auto rw = [&](int o) { return TW + 2 * objs[static_cast<std::size_t>(o)].halo_x; };
+    // staged inputs are laid out from a 16-byte-aligned column origin
+    // (colofs >= halo, in elements) so interior tiles copy them with 16-byte
+    // vector loads and stores; other objects start at their halo
+    static const bool vec_on = std::getenv("GVX_REGION_NOVEC") == nullptr;
+    auto colofs = [&](int o) {
+        const RegionObject& O = objs[static_cast<std::size_t>(o)];
+        const int es = bytes_per_pixel(O.format), per = 16 / std::max(es, 1);
+        if (O.load < 0 || !vec_on || es > 16 || 16 % es) return O.halo_x;
+        return (O.halo_x + per - 1) / per * per;
+    };
+    auto rw = [&](int o) { return TW + 2 * colofs(o); };
     auto rh = [&](int o) { return TH + 2 * objs[static_cast<std::size_t>(o)].halo_y; };
     // a node's code reads object o relative to the entry being evaluated:
     // index base b<o> (set per entry) + dy * row length + dx
@@ -1840,7 +1850,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
          << "  const int tx0 = (int)blockIdx.x * " << TW << ", ty0 = ROW0 + (int)blockIdx.y * " << TH << ";\n";
     for (std::size_t o = 0; o < objs.size(); ++o)
         if (!inline_obj[o])
-            body << "  __shared__ " << storage_ctype(objs[o].format) << " ro" << o << "["
+            body << "  __shared__ alignas(16) " << storage_ctype(objs[o].format) << " ro" << o << "["
                  << rw(static_cast<int>(o)) * rh(static_cast<int>(o)) << "];\n";
     // region inputs staged once: entry = input at the CLAMPED position
     bool staged = false;
@@ -1850,16 +1860,35 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         const int f = field_in(objs[o].load);
         const char* ct = storage_ctype(objs[o].format);
         const int RWo = rw(static_cast<int>(o)), RHo = rh(static_cast<int>(o));
+        const int co = colofs(static_cast<int>(o)), es = bytes_per_pixel(objs[o].format);
+        const bool vec = vec_on && es <= 16 && 16 % es == 0 && (co * es) % 16 == 0 && (TW * es) % 16 == 0;
+        if (vec) {
+            // interior tiles: 16-byte copies of whole padded rows (the origin
+            // column tx0 - co is 16-byte aligned: tx0 is a multiple of 32)
+            const int vrow = RWo * es / 16; // uint4 per row
+            body << "  if (tx0 - " << co << " >= 0 && ty0 - " << objs[o].halo_y << " >= 0 && tx0 + " << TW + co
+                 << " <= W && ty0 + " << TH + objs[o].halo_y << " <= H && ty0 + " << TH << " <= ROW1 && ((p.f[" << f
+                 << "] | p.f[" << f + 1 << "] | p.f[" << f + 2 << "]) & 15) == 0) {\n"
+                 << "    for (int i = threadIdx.y * 32 + threadIdx.x; i < " << vrow * RHo << "; i += 256) {\n"
+                 << "      const int ry = i / " << vrow << ", vx = i - ry * " << vrow << ";\n"
+                 << "      const uint4* src = (const uint4*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
+                 << "] + (u64)(ty0 - " << objs[o].halo_y << " + ry) * p.f[" << f + 1 << "] + (u64)(tx0 - " << co << ") * "
+                 << es << ");\n"
+                 << "      reinterpret_cast<uint4*>(ro" << o << ")[i] = src[vx];\n"
+                 << "    }\n  } else {\n";
+        }
         // one row pointer per entry row; 32-column blocks unrolled
         body << "#pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (RHo + 7) / 8 << "; ++iy_, ry += 8) {\n"
              << (RHo % 8 ? "    if (ry >= " + std::to_string(RHo) + ") break;\n" : std::string())
-             << "    const int y = clampi(ty0 - " << objs[o].halo_y << " + ry, 0, H - 1);\n"
+             << "    const int y = clampi(ty0 - " << objs[o].halo_y << " + ry, max(0, ROW0 - " << objs[o].halo_y
+             << "), min(H, ROW1 + " << objs[o].halo_y << ") - 1);\n"
              << "    const " << ct << "* src = (const " << ct << "*)((const unsigned char*)p.f[" << f << "] + (u64)fr * p.f["
              << f + 2 << "] + (u64)y * p.f[" << f + 1 << "]);\n"
              << "#pragma unroll\n    for (int ix = 0; ix < " << (RWo + 31) / 32 << "; ++ix) {\n"
              << "      const int rx = threadIdx.x + 32 * ix;\n" << (RWo % 32 ? "      if (rx >= " + std::to_string(RWo) + ") break;\n" : std::string())
-             << "      ro" << o << "[ry * " << RWo << " + rx] = src[clampi(tx0 - " << objs[o].halo_x
+             << "      ro" << o << "[ry * " << RWo << " + rx] = src[clampi(tx0 - " << colofs(static_cast<int>(o))
              << " + rx, 0, W - 1)];\n    }\n  }\n";
+        if (vec) body << "  }\n";
     }
     if (staged) body << "  __syncthreads();\n";
     std::size_t rs_bytes = 0; // separable row-sum buffer (declared at the top once its size is known)
@@ -2008,7 +2037,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                 for (std::size_t o = 0; o < objs.size(); ++o)
                     if (used_obj[o])
                         body << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * "
-                             << rw(static_cast<int>(o)) << " + px - tx0 + " << objs[o].halo_x << ";\n";
+                             << rw(static_cast<int>(o)) << " + px - tx0 + " << colofs(static_cast<int>(o)) << ";\n";
                 body << "    " << ga << "[e] = (" << gty << ")(" << gv.c << ");\n  }\n  __syncthreads();\n";
                 std::fill(used_obj.begin(), used_obj.end(), false);
                 extra_base = "    const int bG = (py - " + gy0 + ") * " + std::to_string(GW) + " + px - " + gx0 + ";\n";
@@ -2084,7 +2113,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                     for (std::size_t o = 0; o < objs.size(); ++o)
                         if (used_obj[o])
                             body << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * "
-                                 << rw(static_cast<int>(o)) << " + px - tx0 + " << objs[o].halo_x << ";\n";
+                                 << rw(static_cast<int>(o)) << " + px - tx0 + " << colofs(static_cast<int>(o)) << ";\n";
                     body << "    " << rs << "[ry * " << RW << " + rx] = (" << ty << ")(" << sum.str() << ");\n"
                          << "  }\n  __syncthreads();\n";
                     // per entry: the window's rows (entry rows ry .. ry + 2 hh of rs)
@@ -2118,7 +2147,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         for (std::size_t o = 0; o < objs.size(); ++o)
             if (used_obj[o])
                 bases << "    const int b" << o << " = (py - ty0 + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o))
-                      << " + px - tx0 + " << objs[o].halo_x << ";\n";
+                      << " + px - tx0 + " << colofs(static_cast<int>(o)) << ";\n";
         body << "  // node " << ni << ": " << k.name << "\n";
         for (int border = 0; border < 2; ++border) {
             if (border == 0)
