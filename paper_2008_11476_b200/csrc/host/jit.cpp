@@ -2196,6 +2196,21 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         if (objs[o].store < 0) continue;
         const int f = field_in(static_cast<int>(ins.size()) + objs[o].store);
         const char* ct = storage_ctype(objs[o].format);
+        const int es = bytes_per_pixel(objs[o].format), RWs = rw(static_cast<int>(o));
+        const bool vec = vec_on && es <= 16 && 16 % es == 0 && (objs[o].halo_x * es) % 16 == 0 && (RWs * es) % 16 == 0 &&
+                         (TW * es) % 16 == 0;
+        if (vec) { // interior tiles: 16-byte copies of whole tile rows
+            const int vrow = TW * es / 16;
+            body << "  if (tx0 + " << TW << " <= W && ty0 + " << TH << " <= ROW1 && ((p.f[" << f << "] | p.f[" << f + 1
+                 << "] | p.f[" << f + 2 << "]) & 15) == 0) {\n"
+                 << "    for (int i = threadIdx.y * 32 + threadIdx.x; i < " << vrow * TH << "; i += 256) {\n"
+                 << "      const int ry = i / " << vrow << ", vx = i - ry * " << vrow << ";\n"
+                 << "      uint4* dst = (uint4*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
+                 << "] + (u64)(ty0 + ry) * p.f[" << f + 1 << "] + (u64)tx0 * " << es << ");\n"
+                 << "      dst[vx] = reinterpret_cast<const uint4*>(ro" << o << " + (ry + " << objs[o].halo_y << ") * " << RWs
+                 << " + " << objs[o].halo_x << ")[vx];\n"
+                 << "    }\n  } else {\n";
+        }
         body << "#pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (TH + 7) / 8 << "; ++iy_, ry += 8) {\n"
              << "    const int gy = ty0 + ry;\n    if (gy >= ROW1) break;\n"
              << "    " << ct << "* row = (" << ct << "*)((unsigned char*)p.f[" << f << "] + (u64)fr * p.f[" << f + 2
@@ -2204,6 +2219,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
              << "      const int rx = threadIdx.x + 32 * ix, gx = tx0 + rx;\n      if (gx >= W) break;\n"
              << "      row[gx] = ro" << o << "[(ry + " << objs[o].halo_y << ") * " << rw(static_cast<int>(o)) << " + rx + "
              << objs[o].halo_x << "];\n    }\n  }\n";
+        if (vec) body << "  }\n";
     }
     body << "  (void)rd;\n}\n";
     KernelSpec ks;
