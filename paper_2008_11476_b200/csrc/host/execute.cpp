@@ -455,7 +455,13 @@ std::vector<Unit> region_units(const AppGraph& fg, const VerifiedGraph& fused, c
         for (ObjectId m : S) region_of[m] = static_cast<int>(regions.size()) - 1;
     }
     for (const std::set<ObjectId>& S : regions) {
-        if (S.size() < 2) continue; // merged-away (empty) or single nodes: per-node kernels
+        // merged-away (empty) regions and single point nodes run as per-node
+        // kernels; a single local node takes the region code too (vector
+        // staging and stores, separable box sums: laplacian.json 584 -> 647
+        // Gpx/s); GVX_REGION_NOSINGLE=1 keeps it a per-node kernel
+        static const bool single = std::getenv("GVX_REGION_NOSINGLE") == nullptr;
+        if (S.empty() || (S.size() < 2 && !(single && fg.node(*S.begin())->abstraction->kind == AbstractionKind::Local)))
+            continue;
         // members in topological order
         std::vector<const OperatorNode*> mem;
         for (ObjectId nid : order)
