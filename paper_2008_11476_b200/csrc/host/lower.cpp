@@ -394,6 +394,8 @@ void match_harris(const GraphView& v, std::set<ObjectId>& used, std::vector<Unit
 // ------------------------------------------- linear stencil + points (K3)
 
 void match_stencils(const GraphView& v, std::set<ObjectId>& used, std::vector<Unit>& out) {
+    static const bool off = std::getenv("GVX_NO_K3") != nullptr; // A/B: leave linear stencils to the generic path
+    if (off) return;
     for (const OperatorNode* n : v.nodes) {
         if (used.count(n->id)) continue;
         NodeIO io = io_of(n);
