@@ -1747,9 +1747,14 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         for (int o : nodes[ni].out_obj)
             if (o >= 0) hx = std::max(hx, objs[static_cast<std::size_t>(o)].halo_x), hy = std::max(hy, objs[static_cast<std::size_t>(o)].halo_y);
     };
-    // tile: 64 x 16 outputs per 256-thread block, halved while the shared
-    // memory of the intermediates (and tabulated taps, 8 bytes each) exceeds 40 KB
-    int TW = 64, TH = 16;
+    // tile: halved while the shared memory of the intermediates (and
+    // tabulated taps, 8 bytes each) exceeds 40 KB
+    // 128 x 16 outputs per 256-thread block (measured against 64 x 16 / 64 x 32
+    // / 128 x 8 / 32 x 32: sobel.json 382 -> 431, laplacian.json 646 -> 849
+    // Gpx/s; regions whose intermediates need more shared memory are halved)
+    int TW = 128, TH = 16;
+    if (const char* e = std::getenv("GVX_REGION_TW")) TW = std::max(32, std::atoi(e) / 32 * 32); // tuning experiments
+    if (const char* e = std::getenv("GVX_REGION_TH")) TH = std::max(8, std::atoi(e) / 8 * 8);
     auto smem_bytes = [&] {
         std::size_t b = 0;
         for (const RegionObject& o : objs)
