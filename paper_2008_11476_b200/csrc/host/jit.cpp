@@ -1773,8 +1773,12 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         }
         return b + rs;
     };
-    while (smem_bytes() > 40 * 1024 && (TW > 32 || TH > 8)) (TH > 8 ? TH : TW) /= 2;
-    if (smem_bytes() > 40 * 1024) throw unsupported("intermediates exceed shared memory");
+    static const std::size_t smem_cap = [] {
+        const char* e = std::getenv("GVX_REGION_SMEM_KB"); // tuning experiments
+        return static_cast<std::size_t>(e ? std::atoi(e) : 40) * 1024;
+    }();
+    while (smem_bytes() > smem_cap && (TW > 32 || TH > 8)) (TH > 8 ? TH : TW) /= 2;
+    if (smem_bytes() > std::min<std::size_t>(smem_cap, 46 * 1024)) throw unsupported("intermediates exceed shared memory");
 
     NodeProgram prog;
     prog.n_inputs = static_cast<int>(ins.size());
