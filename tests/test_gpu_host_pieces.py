@@ -63,3 +63,20 @@ def test_pieces_equal_whole_frames(name, size, gvx):
     plan, _ = g.run(naive=False, seed=3)
     naive, _ = g.run(naive=True, seed=3)
     assert plan == naive
+
+
+@pytest.mark.parametrize("name,observe", [("cfg2_harris", ["resp"]), ("cfg1_edge", ["gx", "gy"])])
+def test_pieces_with_observable_intermediates(name, observe, gvx):
+    """Several image outputs (one F32) streamed back piece by piece: the
+    Harris response next to the mask, the edge graph's gx / gy next to the
+    magnitude, against run_naive."""
+    doc = _resize(json.loads((REPO / "examples" / f"{name}.json").read_text()), 2304, 2049)
+    for im in doc["images"]:
+        if im["name"] in observe:
+            im.pop("virtual", None)
+    doc["outputs"] = list(dict.fromkeys(doc["outputs"] + observe))
+    g = gvx.GraphFile(json.dumps(doc))
+    plan, _ = g.run(naive=False, seed=5)
+    naive, _ = g.run(naive=True, seed=5)
+    assert len(plan) == len(doc["outputs"])
+    assert plan == naive
