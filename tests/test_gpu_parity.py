@@ -266,3 +266,41 @@ def test_overlapped_launch_chain_respects_dependences(cfg, gvx, oracle_mod):
         assert np.array_equal(got, want[k]), k
     for p in bufs:
         dev.free(p)
+
+
+STRIP_W = [3, 4, 5, 120, 123, 124, 125, 126, 128, 129, 247, 248, 249, 250, 252, 253, 371, 372, 373, 496, 497]
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("h", [1, 2, 3, 5, 17, 130])
+def test_row_ring_kernels_at_strip_boundaries(cfg, h, gvx, oracle_mod):
+    """The row-ring kernels split the width into strips (harris4: 124
+    columns, 4 per lane; edge8: 248, 8 per lane) whose last one is pulled
+    left and whose border strips clamp: widths around the strip multiples
+    and heights around the ring chunks, against the C restatement."""
+    for w in STRIP_W:
+        img = gvx.random_u8(w, h, 1000 + w + h)
+        got, _ = gvx.ConfigGraph(cfg, w, h).run_host(img)
+        assert np.array_equal(got, oracle_mod.port_run(cfg, img)), (cfg, w, h)
+
+
+def test_eight_column_harris_kernel_stays_exact(gvx):
+    """The 8-column Harris kernel (GVX_HARRIS8=1, the default before
+    harris4) on border-heavy sizes, in a fresh process (the switch is read
+    once), against the C restatement."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.');"
+        "import oracle, paper_2008_11476_b200 as gvx\n"
+        "for w, h in [(5, 3), (247, 19), (248, 130), (253, 7), (3840, 64), (1001, 517)]:\n"
+        "    img = gvx.random_u8(w, h, w * 7 + h)\n"
+        "    g = gvx.ConfigGraph(2, w, h)\n"
+        "    assert 'harris' in g.describe()\n"
+        "    got, _ = g.run_host(img)\n"
+        "    assert np.array_equal(got, oracle.port_run(2, img)), (w, h)\n"
+        "print('ok')\n")
+    env = dict(__import__("os").environ, GVX_HARRIS8="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=str(pathlib.Path(__file__).resolve().parent.parent),
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
