@@ -46,6 +46,11 @@ KERNEL_NAME = {1: "edge8_kernel", 2: "harris4_kernel", 3: "sep_kernel<5,1> (sepa
 # two rotating batches (inputs + outputs) span >= 4x the 126 MB L2 (SURVEY.md
 # §8d), which also amortises the ~20 us fixed cost of a launch (ramp + tail)
 DEFAULT_FRAMES = {1: 64, 2: 32, 3: 8, 4: 64, 5: 1}
+# inputs / outputs rotate over NPOOL buffer sets: a launch may overlap the
+# kernels still running before it only when it touches none of their data
+# (the library's overlap window, runtime.cu launch_tracked), so with NPOOL
+# sets one launch in NPOOL is fully stream-ordered
+NPOOL = 8
 CPU_SAMPLE = {1: (1920, 1080), 2: (3840, 544), 3: (7680, 272), 4: (3840, 544), 5: (16384, 128)}
 
 
@@ -247,7 +252,7 @@ def run_frames(args, cfg, rank, world, local_rank):
         del pipe
         pinned.close()
 
-    for b in range(2):
+    for b in range(NPOOL):
         din = dev.alloc(in_bytes)
         for f in range(F):
             dev.upload(din + f * pitch * h, pitch, np.roll(host[f], b * 13, axis=1))
@@ -262,7 +267,7 @@ def run_frames(args, cfg, rank, world, local_rank):
             sess.bind(1, dout, out_pitch, out_pitch * h)
 
     for i in range(args.warmup):
-        bind(i % 2)
+        bind(i % NPOOL)
         sess.launch()
     sess.sync()
     # correctness spot check of frame 0 of the first batch against the oracle port
@@ -282,7 +287,7 @@ def run_frames(args, cfg, rank, world, local_rank):
         t_end = time.perf_counter() + args.clock_window
         i = 0
         while time.perf_counter() < t_end:
-            bind(i % 2)
+            bind(i % NPOOL)
             sess.launch()
             i += 1
             if i % 50 == 0:
@@ -291,7 +296,7 @@ def run_frames(args, cfg, rank, world, local_rank):
         launches0 = gvx.launch_count()
         dev.record(ev[0])
         for i in range(args.steps):
-            bind(i % 2)
+            bind(i % NPOOL)
             sess.launch()
         dev.record(ev[1])
         dev.sync()
@@ -312,7 +317,7 @@ def run_frames(args, cfg, rank, world, local_rank):
         ofs = out_pitch * h
 
         def bind1(i):
-            b, f = (i // F) % 2, i % F
+            b, f = (i // F) % NPOOL, i % F
             din, dout = pools[b]
             s1.bind(0, din + f * fstride, pitch, fstride)
             if dout is not None:
@@ -333,7 +338,7 @@ def run_frames(args, cfg, rank, world, local_rank):
         single = {"ms_per_frame": round(ms1, 5), "value": round(w * h / (ms1 / 1e3) / 1e6, 1), "unit": "Mpixel/s",
                   "launches_per_frame": s1.launches(), "frames_timed": n1,
                   "note": "one graph execution (one fused launch) per frame, as vxProcessGraph / run_plan "
-                          "execute; inputs rotate over the same two batches"}
+                          "execute; inputs rotate over the same batches"}
         s1.close()
 
     # the drop-in host entry point itself: run_plan(plan, InputMap) on pageable
@@ -420,16 +425,16 @@ def run_banded(args, rank, world, local_rank):
     # uploads only the rows it owns: its halo rows come from the exchange
     img = gvx.random_u8(W, H, 5)
     band.upload(0, img[r0:r1], r0)
-    # results alternate between two output buffers (double buffering, as the
-    # frame configs rotate two batches): consecutive executions then touch
-    # disjoint outputs and may overlap (programmatic dependent launch; only
+    # results rotate over NPOOL output buffers (as the frame configs rotate
+    # their batches): an execution overlaps the ones still running before it
+    # when it touches none of their data (programmatic dependent launch; only
     # this band's work runs on dev.stream)
     band.set_overlap(1)
     out_pitch = (2 * W + 127) // 128 * 128
-    outs = [dev.alloc(out_pitch * (r1 - r0)) for _ in range(2)]
+    outs = [dev.alloc(out_pitch * (r1 - r0)) for _ in range(NPOOL)]
 
     def launch(i):
-        band.bind(1, outs[i % 2], out_pitch, out_pitch * (r1 - r0))
+        band.bind(1, outs[i % NPOOL], out_pitch, out_pitch * (r1 - r0))
         band.launch()
 
     for i in range(args.warmup):
@@ -644,7 +649,7 @@ def main():
             "data": "synthetic (reference random_buffer, seed 5)" if cfg == 5 else
                     "synthetic (reference random_buffer frame + derived frames)",
             "config": {"workload": CONFIG_NAME[cfg], "width": res["w"], "height": res["h"],
-                       "frames_per_step": res["frames"], "l2": "inputs/outputs rotate over 2 batches spanning >= 4x L2"
+                       "frames_per_step": res["frames"], "l2": f"inputs/outputs rotate over {NPOOL} batches spanning >= 4x L2"
                        if cfg != 5 else "16384^2 input > L2",
                        "parallelism": f"{'row bands' if cfg == 5 else 'frame replicas'} x{world}"},
             "e2e": res["e2e"], "roofline": roof, "cpu_baseline": cpu, "clocks": res["clocks"],

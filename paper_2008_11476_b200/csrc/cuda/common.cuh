@@ -17,7 +17,7 @@ struct gvxb_range {
     uintptr_t lo = 0, hi = 0;
 };
 
-constexpr int kTrackedRanges = 6; // read / write ranges a launch records for the next one's hazard test
+constexpr int kTrackedRanges = 16; // read / write ranges of the overlap window (see gvxb_ctx_s)
 
 struct gvxb_ctx_s {
     int device = 0;
@@ -27,13 +27,20 @@ struct gvxb_ctx_s {
     unsigned* status = nullptr;            // GVXB_STATUS_* bits
     unsigned long long* counter = nullptr; // pixel-read events of generated kernels
     int64_t launches = 0;
-    // Programmatic dependent launch between consecutive hand-written kernels
-    // (gvxb_ctx_set_overlap): the ranges the previous kernel on the stream
-    // read / wrote, valid only while nothing else was enqueued after it.
+    // Programmatic dependent launch between hand-written kernels
+    // (gvxb_ctx_set_overlap).  The window holds the ranges read / written by
+    // every kernel that may still be running: the kernels launched since
+    // the last fully stream-ordered launch, all mutually independent (a grid
+    // launched programmatically may finish before its predecessor, so a
+    // later launch must be independent of the whole window to overlap).
+    // Valid only while nothing else was enqueued after the last of them.  A
+    // launch that depends on the window may still overlap it when the window
+    // is a single kernel: its griddepcontrol.wait (pdl_wait) covers it.
     int overlap = -1; // -1 auto (own stream only), 0 off, 1 on
-    bool prev_kernel = false;
+    bool prev_kernel = false; // the window is valid
     gvxb_range prev_r[kTrackedRanges], prev_w[kTrackedRanges];
     int prev_nr = 0, prev_nw = 0;
+    int prev_launches = 0; // kernels in the window
 };
 
 namespace gvxb_impl {

@@ -59,14 +59,34 @@ int pdl_must_wait(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w
     return 0;
 }
 
+namespace {
+int nonempty(const gvxb_range* a, int n) {
+    int k = 0;
+    for (int i = 0; i < n; ++i) k += a[i].lo < a[i].hi ? 1 : 0;
+    return k;
+}
+} // namespace
+
 bool launch_overlaps(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw) {
     const bool allowed = ctx->overlap > 0 || (ctx->overlap < 0 && ctx->stream == ctx->own_stream);
-    return allowed && ctx->prev_kernel && !pdl_must_wait(ctx, r, nr, w, nw);
+    return allowed && ctx->prev_kernel && !pdl_must_wait(ctx, r, nr, w, nw) &&
+           ctx->prev_nr + nonempty(r, nr) <= kTrackedRanges && ctx->prev_nw + nonempty(w, nw) <= kTrackedRanges;
 }
 
+/// A launch independent of every kernel in the window overlaps them
+/// (programmatic dependent launch, pdl_wait = 0) and joins the window; a
+/// launch that depends on a one-kernel window overlaps its tail and waits
+/// for it in the kernel (pdl_wait = 1); any other launch is fully
+/// stream-ordered (it starts after all earlier work completed; its
+/// griddepcontrol.wait is a no-op).  The last two start a new window.
 int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
                    const gvxb_range* r, int nr, const gvxb_range* w, int nw, const char* what) {
     const bool allowed = ctx->overlap > 0 || (ctx->overlap < 0 && ctx->stream == ctx->own_stream);
+    const bool joins = launch_overlaps(ctx, r, nr, w, nw);
+    // dependent on a one-kernel window: overlap its tail and wait for it in
+    // the kernel (the caller passed pdl_wait = 1); the window restarts here
+    const bool waits = !joins && allowed && ctx->prev_kernel && ctx->prev_launches == 1;
+    const bool pdl = joins || waits;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -75,17 +95,23 @@ int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** a
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    if (allowed && ctx->prev_kernel) {
+    if (pdl) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return cuda_fail(e, what);
-    ctx->prev_nr = nr < kTrackedRanges ? nr : kTrackedRanges;
-    ctx->prev_nw = nw < kTrackedRanges ? nw : kTrackedRanges;
-    for (int i = 0; i < ctx->prev_nr; ++i) ctx->prev_r[i] = r[i];
-    for (int i = 0; i < ctx->prev_nw; ++i) ctx->prev_w[i] = w[i];
-    ctx->prev_kernel = nr <= kTrackedRanges && nw <= kTrackedRanges;
+    if (!joins) ctx->prev_nr = ctx->prev_nw = ctx->prev_launches = 0; // a new window
+    if (ctx->prev_nr + nonempty(r, nr) <= kTrackedRanges && ctx->prev_nw + nonempty(w, nw) <= kTrackedRanges) {
+        for (int i = 0; i < nr; ++i)
+            if (r[i].lo < r[i].hi) ctx->prev_r[ctx->prev_nr++] = r[i];
+        for (int i = 0; i < nw; ++i)
+            if (w[i].lo < w[i].hi) ctx->prev_w[ctx->prev_nw++] = w[i];
+        ctx->prev_launches += 1;
+        ctx->prev_kernel = true;
+    } else {
+        ctx->prev_kernel = false; // untrackable: the next launch is stream-ordered
+    }
     return check_launch(ctx, what);
 }
 

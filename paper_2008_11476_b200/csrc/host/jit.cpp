@@ -1729,8 +1729,13 @@ const Expr* tabulated_g(const LocalKernel& lk, const Expr** mc_out) {
 }
 } // namespace
 
-NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector<RegionObject>& objs,
-                         const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs) {
+namespace {
+
+/// One region kernel at a given tile (TW x TH outputs per 256-thread block);
+/// `smem` receives the static shared memory the emitted kernel declares.
+NodeProgram lower_region_at(const std::vector<RegionNode>& nodes, const std::vector<RegionObject>& objs,
+                            const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs, const int TW,
+                            const int TH, std::size_t& smem) {
     auto unsupported = [](const std::string& why) { return Error(ErrorCode::UnsupportedKind, "region: " + why); };
     for (const RegionObject& o : objs)
         if (!storage_ctype(o.format)) throw unsupported("intermediate format");
@@ -1742,44 +1747,6 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         const Expr* mc = nullptr;
         tab[ni] = tabulated_g(nodes[ni].k->local(), &mc) != nullptr;
     }
-    auto node_halo = [&](std::size_t ni, int& hx, int& hy) {
-        hx = hy = 0;
-        for (int o : nodes[ni].out_obj)
-            if (o >= 0) hx = std::max(hx, objs[static_cast<std::size_t>(o)].halo_x), hy = std::max(hy, objs[static_cast<std::size_t>(o)].halo_y);
-    };
-    // tile: halved while the shared memory of the intermediates (and
-    // tabulated taps, 8 bytes each) exceeds 40 KB
-    // 128 x 16 outputs per 256-thread block (measured against 64 x 16 / 64 x 32
-    // / 128 x 8 / 32 x 32: sobel.json 382 -> 431, laplacian.json 646 -> 849
-    // Gpx/s; regions whose intermediates need more shared memory are halved)
-    int TW = 128, TH = 16;
-    if (const char* e = std::getenv("GVX_REGION_TW")) TW = std::max(32, std::atoi(e) / 32 * 32); // tuning experiments
-    if (const char* e = std::getenv("GVX_REGION_TH")) TH = std::max(8, std::atoi(e) / 8 * 8);
-    auto smem_bytes = [&] {
-        std::size_t b = 0;
-        for (const RegionObject& o : objs)
-            b += static_cast<std::size_t>(TW + 2 * o.halo_x) * (TH + 2 * o.halo_y) *
-                 static_cast<std::size_t>(bytes_per_pixel(o.format));
-        std::size_t rs = 0; // the separable row sums share one buffer (nodes run in turn)
-        for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
-            if (nodes[ni].k->kind != AbstractionKind::Local) continue;
-            int hx = 0, hy = 0;
-            node_halo(ni, hx, hy);
-            const LocalKernel& lk = nodes[ni].k->local();
-            if (tab[ni])
-                b += static_cast<std::size_t>(TW + 2 * hx + 2 * (lk.window_w / 2)) * (TH + 2 * hy + 2 * (lk.window_h / 2)) * 8;
-            else
-                rs = std::max(rs, static_cast<std::size_t>(TW + 2 * hx) * (TH + 2 * hy + 2 * (lk.window_h / 2)) * 8);
-        }
-        return b + rs;
-    };
-    static const std::size_t smem_cap = [] {
-        const char* e = std::getenv("GVX_REGION_SMEM_KB"); // tuning experiments
-        return static_cast<std::size_t>(e ? std::atoi(e) : 40) * 1024;
-    }();
-    while (smem_bytes() > smem_cap && (TW > 32 || TH > 8)) (TH > 8 ? TH : TW) /= 2;
-    if (smem_bytes() > std::min<std::size_t>(smem_cap, 46 * 1024)) throw unsupported("intermediates exceed shared memory");
-
     NodeProgram prog;
     prog.n_inputs = static_cast<int>(ins.size());
     prog.n_outputs = static_cast<int>(outs.size());
@@ -1900,6 +1867,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
         if (vec) body << "  }\n";
     }
     if (staged) body << "  __syncthreads();\n";
+    std::size_t tab_bytes = 0;
     std::size_t rs_bytes = 0; // separable row-sum buffer (declared at the top once its size is known)
     body << "@RSBUF@";
     for (std::size_t ni = 0; ni < nodes.size(); ++ni) {
@@ -2028,6 +1996,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                 if (!em.temit(*gexp, gv)) throw unsupported("run-time typed tap computation");
                 const char* gty = gv.t == 'd' ? "double" : gv.t == 'l' ? "i64" : "int";
                 const std::string ga = "gk" + std::to_string(ni);
+                tab_bytes += static_cast<std::size_t>(GW) * GH * (gv.t == 'd' || gv.t == 'l' ? 8 : 4);
                 body << "  // node " << ni << " tap computation, tabulated\n"
                      << "  __shared__ " << gty << " " << ga << "[" << GW * GH << "];\n"
                      << "  #pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (GH + 7) / 8 << "; ++iy_, ry += 8)\n"
@@ -2109,7 +2078,7 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
                     std::ostringstream sum;
                     for (std::size_t k = 0; k < row.size(); ++k)
                         sum << (k ? " + " : "") << (i32 ? row[k].c : Emitter::as_i64(row[k]));
-                    rs_bytes = std::max(rs_bytes, static_cast<std::size_t>(RW) * RHs * 8);
+                    rs_bytes = std::max(rs_bytes, static_cast<std::size_t>(RW) * RHs * (i32 ? 4 : 8));
                     body << "  // node " << ni << ": window rows summed once per position\n"
                          << "  " << ty << "* " << rs << " = reinterpret_cast<" << ty << "*>(rsbuf);\n"
                          << "  #pragma unroll\n  for (int ry = threadIdx.y, iy_ = 0; iy_ < " << (RHs + 7) / 8 << "; ++iy_, ry += 8)\n"
@@ -2241,12 +2210,42 @@ NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector
     std::string pre = kPrelude;
     const std::string key = "NFIELDS";
     pre.replace(pre.find(key), key.size(), std::to_string(prog.fields()));
+    smem = tab_bytes + rs_bytes;
+    for (std::size_t o = 0; o < objs.size(); ++o)
+        if (!inline_obj[o])
+            smem += static_cast<std::size_t>(rw(static_cast<int>(o))) * rh(static_cast<int>(o)) *
+                    static_cast<std::size_t>(bytes_per_pixel(objs[o].format));
     std::string text = body.str();
     const std::size_t at = text.find("@RSBUF@");
     text.replace(at, 7, rs_bytes ? "  __shared__ alignas(8) unsigned char rsbuf[" + std::to_string(rs_bytes) + "];\n" : "");
     ks.source = pre + helpers.str() + text;
     prog.kernels.push_back(std::move(ks));
     return prog;
+}
+
+} // namespace
+
+NodeProgram lower_region(const std::vector<RegionNode>& nodes, const std::vector<RegionObject>& objs,
+                         const std::vector<SlotInfo>& ins, const std::vector<SlotInfo>& outs) {
+    // 128 x 16 outputs per 256-thread block (measured against 64 x 16 / 64 x 32
+    // / 128 x 8 / 32 x 32: sobel.json 382 -> 431, laplacian.json 646 -> 849
+    // Gpx/s), halved while the emitted kernel's shared memory exceeds 36 KB
+    // (harris.json / tomasi.json: 128 x 8 at 22 KB beat 128 x 16 at 38 KB,
+    // 164 vs 160 Gpx/s: more resident blocks)
+    int TW = 128, TH = 16;
+    if (const char* e = std::getenv("GVX_REGION_TW")) TW = std::max(32, std::atoi(e) / 32 * 32); // tuning experiments
+    if (const char* e = std::getenv("GVX_REGION_TH")) TH = std::max(8, std::atoi(e) / 8 * 8);
+    static const std::size_t cap = [] {
+        const char* e = std::getenv("GVX_REGION_SMEM_KB"); // tuning experiments
+        return static_cast<std::size_t>(std::min(e ? std::atoi(e) : 36, 46)) * 1024;
+    }();
+    for (;;) {
+        std::size_t smem = 0;
+        NodeProgram prog = lower_region_at(nodes, objs, ins, outs, TW, TH, smem);
+        if (smem <= cap) return prog;
+        if (TW <= 32 && TH <= 8) throw Error(ErrorCode::UnsupportedKind, "region: intermediates exceed shared memory");
+        (TH > 8 ? TH : TW) /= 2;
+    }
 }
 
 NodeProgram lower_node(const AbstractionKernel& k, const std::vector<SlotInfo>& ins,
