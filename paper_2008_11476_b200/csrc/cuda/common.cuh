@@ -80,8 +80,8 @@ int pdl_must_wait(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w
 bool launch_overlaps(gvxb_ctx ctx, const gvxb_range* r, int nr, const gvxb_range* w, int nw);
 
 /// Launches `fn` on ctx's stream, as a programmatic dependent launch when
-/// the context allows it and the previous stream operation was a tracked
-/// kernel, and records this kernel's ranges for the next one.
+/// the context allows it and the overlap window permits (runtime.cu), and
+/// records this kernel's ranges in the window.
 int launch_tracked(gvxb_ctx ctx, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
                    const gvxb_range* r, int nr, const gvxb_range* w, int nw, const char* what);
 
@@ -90,13 +90,15 @@ inline void untracked_op(gvxb_ctx ctx) { ctx->prev_kernel = false; }
 } // namespace gvxb_impl
 
 namespace gvxd {
-/// Kernel prologue for programmatic dependent launch: let the next grid on
-/// the stream be scheduled as this one's CTAs retire, and, when this grid
-/// may read what the previous one wrote (pdl_wait), wait for it first.  Both
+/// Kernel prologue for programmatic dependent launch: when this grid
+/// depends on the previous one (pdl_wait), wait for it, then let the next
+/// grid on the stream be scheduled as this one's CTAs retire.  Both
 /// are no-ops for a kernel launched without the PDL attribute.
 __device__ __forceinline__ void pdl_prologue(int pdl_wait) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // a waiting grid releases its dependents only after its wait: the next
+    // launch's overlap window then no longer holds the grid waited for
     if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 } // namespace gvxd
 
