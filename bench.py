@@ -50,7 +50,7 @@ DEFAULT_FRAMES = {1: 64, 2: 32, 3: 8, 4: 64, 5: 1}
 # kernels still running before it only when it touches none of their data
 # (the library's overlap window, runtime.cu launch_tracked), so with NPOOL
 # sets one launch in NPOOL is fully stream-ordered
-NPOOL = 8
+NPOOL = 16
 CPU_SAMPLE = {1: (1920, 1080), 2: (3840, 544), 3: (7680, 272), 4: (3840, 544), 5: (16384, 128)}
 
 

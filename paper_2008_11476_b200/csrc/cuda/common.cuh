@@ -17,7 +17,7 @@ struct gvxb_range {
     uintptr_t lo = 0, hi = 0;
 };
 
-constexpr int kTrackedRanges = 16; // read / write ranges of the overlap window (see gvxb_ctx_s)
+constexpr int kTrackedRanges = 32; // read / write ranges of the overlap window (see gvxb_ctx_s)
 
 struct gvxb_ctx_s {
     int device = 0;
