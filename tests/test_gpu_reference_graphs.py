@@ -128,3 +128,18 @@ def test_harris_certified_threshold_matches_reference(k, gvx, oracle_mod):
 
 def blob_of(outs):
     return blob(outs)
+
+
+def test_random_dags_with_interior_tiles_match_reference(gvx, oracle_mod):
+    """Random DAGs at 300 x 70, wide and tall enough for the generated region
+    kernels' interior tiles (16-byte vector staging and stores, no
+    per-entry position tests) next to their border tiles, against the
+    unmodified reference."""
+    ran = 0
+    for seed in range(200, 214):
+        doc = rg.random_dag(seed, 300, 70)
+        if not doc["outputs"]:
+            continue
+        compare(doc, gvx, oracle_mod, seed=seed)
+        ran += 1
+    assert ran >= 10
