@@ -57,6 +57,26 @@ inline gvxb_range bytes_range(const void* p, size_t n) {
     return r;
 }
 
+/// Bytes of buffer rows [first, first + n) of a single-frame image (all of
+/// it for several frames); empty for a null image.  Band launches use it so
+/// kernels on disjoint rows of one buffer count as independent.
+inline gvxb_range rows_range(const gvxb_image& im, int first, int n) {
+    gvxb_range r;
+    if (!im.data || im.height <= 0 || n <= 0) return r;
+    if (im.frames > 1) {
+        const int64_t span = im.frame_stride * (im.frames - 1) + im.pitch * im.height;
+        r.lo = reinterpret_cast<uintptr_t>(im.data);
+        r.hi = r.lo + static_cast<uintptr_t>(span);
+        return r;
+    }
+    first = first < 0 ? 0 : first;
+    const int last = first + n > im.height ? im.height : first + n;
+    if (last <= first) return r;
+    r.lo = reinterpret_cast<uintptr_t>(im.data) + static_cast<uintptr_t>(static_cast<int64_t>(first) * im.pitch);
+    r.hi = reinterpret_cast<uintptr_t>(im.data) + static_cast<uintptr_t>(static_cast<int64_t>(last) * im.pitch);
+    return r;
+}
+
 /// Bytes an image (all its frames) spans; empty for a null image.
 inline gvxb_range image_range(const gvxb_image& im) {
     gvxb_range r;

@@ -432,8 +432,13 @@ int edge8_launch(gvxb_ctx ctx, const gvxb_edge_args* a) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kE8Threads, 0);
     const long long strips = static_cast<long long>(frames) * ((s.width + kE8Cols - 1) / kE8Cols);
     Edge8Params p;
-    const gvxb_range r[1] = {image_range(s)};
-    const gvxb_range w[3] = {image_range(a->gx), image_range(a->gy), image_range(a->mag)};
+    // the rows this launch reads (band rows +- 2, clipped to the slab) and
+    // writes: bands of one buffer on disjoint rows are independent launches
+    const int b0 = a->band.row0, b1 = a->band.row1;
+    const gvxb_range r[1] = {rows_range(s, b0 - 2 - a->band.src_row0, b1 - b0 + 4)};
+    const gvxb_range w[3] = {rows_range(a->gx, b0 - a->band.dst_row0, b1 - b0),
+                             rows_range(a->gy, b0 - a->band.dst_row0, b1 - b0),
+                             rows_range(a->mag, b0 - a->band.dst_row0, b1 - b0)};
     const int th_max = launch_overlaps(ctx, r, 1, w, 3) ? kE8THMax : kE8THSerial;
     p.th = balanced_tile_rows(strips, rows, static_cast<long long>(per_sm > 0 ? per_sm : 1) * ctx->sm_count, th_max, 4);
     if (const char* e = std::getenv("GVX_EDGE8_TH")) p.th = std::max(8, std::atoi(e)); // tuning experiments
