@@ -1,6 +1,6 @@
 """Host-side cost and wall time of banded executions (BandedSession::launch
-through gvx_c.h), outputs alternating between two buffers as bench.py
-does (consecutive executions may overlap): world = 1 on 16384 x H images,
+through gvx_c.h), outputs rotating over PROBE_NOUT (16) buffers as bench.py
+does (an execution overlaps the ones still running when independent of them): world = 1 on 16384 x H images,
 H = one band's share at 1 / 2 / 4 / 8 GPUs.
 Usage: [GVX_EDGE8_TH=n] [PROBE_SINGLE=1] python profiles/band_host_probe.py [WxH ...]"""
 import os
@@ -19,12 +19,13 @@ for W, H in sizes:
     b.upload(0, gvx.random_u8(W, H, 5), 0)
     b.set_overlap(1)
     pitch = (2 * W + 127) // 128 * 128
-    outs = [dev.alloc(pitch * H) for _ in range(2)]
+    nout = int(os.environ.get("PROBE_NOUT", 16))  # rotating outputs, as bench.py (NPOOL)
+    outs = [dev.alloc(pitch * H) for _ in range(nout)]
 
     single = os.environ.get("PROBE_SINGLE") is not None  # one output buffer: every launch waits
 
     def launch(i):
-        b.bind(1, outs[0 if single else i % 2], pitch, pitch * H)
+        b.bind(1, outs[0 if single else i % nout], pitch, pitch * H)
         b.launch()
 
     for i in range(5):
