@@ -853,8 +853,11 @@ extern "C" int gvxb_harris(gvxb_ctx ctx, const gvxb_harris_args* a) {
     p.c_tt = static_cast<float>((c_tt + c_tr / (2.0 * a_tr)) * 1.001);
     p.c0 = static_cast<float>((c_0 + c_tr * a_tr / 2.0) * 1.001 + 1.0);
     dim3 grid((s.width + cols - 1) / cols, (rows + p.th - 1) / p.th, frames);
-    const gvxb_range r[1] = {image_range(s)};
-    const gvxb_range w[2] = {image_range(a->mask), image_range(a->response)};
+    // rows read (band +- 2, within the slab) and written (band rows)
+    const int b0 = a->band.row0, b1 = a->band.row1;
+    const gvxb_range r[1] = {rows_range(s, b0 - 2 - a->band.src_row0, b1 - b0 + 4)};
+    const gvxb_range w[2] = {rows_range(a->mask, b0 - a->band.dst_row0, b1 - b0),
+                             rows_range(a->response, b0 - a->band.dst_row0, b1 - b0)};
     p.pdl_wait = pdl_must_wait(ctx, r, 1, w, 2);
     void* args[] = {&map, &p};
     return launch_tracked(ctx, fn, grid, dim3(kHarThreads), args, 0, r, 1, w, 2, "harris kernel");
