@@ -889,7 +889,7 @@ void* sep_fn_k(int k, bool clamp, int frac) {
 }
 
 int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K, int rows, int th_max, size_t dyn,
-               int ch_threads, const gvxb_range* wr, int nw) {
+               int ch_threads, const gvxb_range* wr, int nw, const gvxb_range* rd = nullptr) {
     using namespace gvxb_impl;
     if (dyn > 0) { // static tile + dynamic histogram exceed the 48 KB default
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
@@ -908,7 +908,7 @@ int sep_launch(gvxb_ctx ctx, void* fn, const gvxb_image& s, SepParams& p, int K,
     if (int rc = make_u8_tensor_map(&map, s, sw, p.th + K - 1)) return rc;
     dim3 grid((s.width + tw - 1) / tw, (rows + p.th - 1) / p.th, frames);
     if (p.acc) p.ctas_per_frame = static_cast<int>(grid.x * grid.y);
-    const gvxb_range r[1] = {image_range(s)};
+    const gvxb_range r[1] = {rd ? *rd : image_range(s)};
     p.pdl_wait = pdl_must_wait(ctx, r, 1, wr, nw);
     void* args[] = {&map, &p};
     return launch_tracked(ctx, fn, grid, dim3(nt), args, dyn, r, 1, wr, nw, "separable stencil kernel");
@@ -949,8 +949,12 @@ extern "C" int gvxb_stencil_point(gvxb_ctx ctx, const gvxb_stencil_args* a) {
             sp.dst_pitch = a->dst.pitch;
             sp.dst_fstride = a->dst.frames > 1 ? a->dst.frame_stride : a->dst.pitch * a->dst.height;
             void* fn = a->mode == 0 ? sep_fn_k<0>(a->ksize, sp.clamp255, sp.frac) : sep_fn_k<1>(a->ksize, sp.clamp255, sp.frac);
-            const gvxb_range w[1] = {image_range(a->dst)};
-            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0, sep_threads(0), w, 1);
+            // the band's rows (plus the K/2 halo read above and below) only, so
+            // launches on disjoint row bands of one buffer stay independent
+            const int b0 = a->band.row0, hk = a->ksize / 2;
+            const gvxb_range rd = rows_range(s, b0 - hk - a->band.src_row0, rows + 2 * hk);
+            const gvxb_range w[1] = {rows_range(a->dst, b0 - a->band.dst_row0, rows)};
+            if (fn) return sep_launch(ctx, fn, s, sp, a->ksize, rows, kSepTHMax, 0, sep_threads(0), w, 1, &rd);
         }
     }
     StencilParams p;
