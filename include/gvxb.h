@@ -122,6 +122,12 @@ int64_t gvxb_total_launch_count(void);
 /* ---- memory and copies ---------------------------------------------------- */
 int gvxb_alloc(gvxb_ctx ctx, size_t bytes, void** dptr);
 int gvxb_free(gvxb_ctx ctx, void* dptr);
+/* Debugging aid (compute-sanitizer stand-in): with GVX_GUARD_ALLOC=1 in the
+ * environment every gvxb_alloc is framed by 4 KB of 0xA5 guard bytes that
+ * gvxb_free checks.  Returns the number of allocations whose guards were
+ * found overwritten (freed ones plus the still-live ones, checked now);
+ * *live (may be null) = allocations still live.  0 without the mode. */
+int64_t gvxb_guard_check(int* live);
 int gvxb_host_alloc(size_t bytes, void** hptr); /* pinned */
 int gvxb_host_free(void* hptr);
 /* Page-lock existing host memory (cudaHostRegister) so copies DMA from/to it

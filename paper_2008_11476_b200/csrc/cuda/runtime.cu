@@ -12,6 +12,7 @@
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -234,16 +235,93 @@ int gvxb_sync(gvxb_ctx ctx) {
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaStreamSynchronize");
 }
 
+// GVX_GUARD_ALLOC=1 (debugging; compute-sanitizer stand-in): every
+// allocation is framed by kGuard bytes of 0xA5 on both sides; gvxb_free
+// synchronizes the device and checks them, counting (and reporting on
+// stderr) each allocation whose guards a kernel overwrote.
+namespace {
+constexpr size_t kGuard = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+struct GuardedAlloc {
+    void* base;
+    size_t bytes;
+};
+std::mutex g_guard_mu;
+std::vector<std::pair<void*, GuardedAlloc>> g_guarded;
+std::atomic<long long> g_guard_violations{0};
+bool guard_mode() {
+    static const bool on = [] {
+        const char* e = std::getenv("GVX_GUARD_ALLOC");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+bool guards_intact(const GuardedAlloc& g) {
+    std::vector<unsigned char> h(kGuard);
+    const unsigned char* base = static_cast<const unsigned char*>(g.base);
+    for (const unsigned char* at : {base, base + kGuard + g.bytes}) {
+        if (cudaMemcpy(h.data(), at, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+        for (unsigned char b : h)
+            if (b != kGuardByte) return false;
+    }
+    return true;
+}
+} // namespace
+
 int gvxb_alloc(gvxb_ctx ctx, size_t bytes, void** p) {
     cudaSetDevice(ctx->device);
+    if (guard_mode()) {
+        const size_t n = (bytes ? bytes : 16), padded = (n + 255) & ~size_t(255);
+        void* base = nullptr;
+        cudaError_t e = cudaMalloc(&base, padded + 2 * kGuard);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+        if ((e = cudaMemset(base, kGuardByte, padded + 2 * kGuard)) != cudaSuccess ||
+            (e = cudaDeviceSynchronize()) != cudaSuccess)
+            return cuda_fail(e, "guard fill");
+        *p = static_cast<char*>(base) + kGuard;
+        std::lock_guard<std::mutex> lk(g_guard_mu);
+        g_guarded.push_back({*p, GuardedAlloc{base, padded}});
+        return GVXB_OK;
+    }
     cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaMalloc");
 }
 
 int gvxb_free(gvxb_ctx ctx, void* p) {
     cudaSetDevice(ctx->device);
+    if (guard_mode() && p) {
+        GuardedAlloc g{nullptr, 0};
+        {
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            for (auto it = g_guarded.begin(); it != g_guarded.end(); ++it)
+                if (it->first == p) {
+                    g = it->second;
+                    g_guarded.erase(it);
+                    break;
+                }
+        }
+        if (g.base) {
+            cudaDeviceSynchronize();
+            if (!guards_intact(g)) {
+                ++g_guard_violations;
+                std::fprintf(stderr, "gvxb: guard bytes around a %zu-byte allocation at %p overwritten\n", g.bytes, p);
+            }
+            cudaError_t e = cudaFree(g.base);
+            return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaFree");
+        }
+    }
     cudaError_t e = cudaFree(p);
     return e == cudaSuccess ? GVXB_OK : cuda_fail(e, "cudaFree");
+}
+
+int64_t gvxb_guard_check(int* live) {
+    long long bad = g_guard_violations.load();
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    if (!g_guarded.empty()) cudaDeviceSynchronize();
+    for (const auto& a : g_guarded)
+        if (!guards_intact(a.second)) ++bad;
+    if (live) *live = static_cast<int>(g_guarded.size());
+    return bad;
 }
 
 int gvxb_host_alloc(size_t bytes, void** p) {
